@@ -1,0 +1,900 @@
+// octmg oracle — TEST INFRASTRUCTURE ONLY.
+//
+// A plain, slow, double-precision CPU implementation of what arXiv 2604.18886
+// ("Matrix-Free Multigrid with Algebraically Consistent Coarsening on Adaptive
+// Octrees") defines: the graded tile octree (Sec. 3), the
+// compact matrix-free Poisson coefficients (Eq. 3), the T-junction
+// stencil (Eqs. 9-12), Galerkin coarsening (Alg. 3), RBGS
+// (L407-409), the FAS-style mu-cycle (Alg. 4), the standard mu-cycle
+// (Alg. 2, used only as an equivalence check on uniform trees) and PCG
+// (Alg. 1).  Readings of silent/ambiguous passages follow SURVEY.md
+// 8(c) and are listed in DESIGN.md "Readings".
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+// reference legs may load this library.  It shares no code, header, table or
+// constant generator with the CUDA path (paper_2604_18886_b200/csrc).
+//
+// Style: cell-centric, global integer coordinates, hash-map tile lookup,
+// everything computed in the order the paper states it.  Loops over cells are
+// OpenMP-parallel only where each output cell is independent; every reduction is
+// a serial sum in cell order, so results do not depend on the thread count.
+//
+// Parity status: every function below is pinned by tests/test_oracle_*.py
+// (see DESIGN.md "Oracle pins"); none is "parity unpinned".
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+enum Kind { K_FLUID = 0, K_DIRICHLET = 1, K_NEUMANN = 2 };
+enum What { L_WALL = 0, L_CELL = 1, L_GHOST = 2, L_UNCOVERED = 3 };
+
+// status codes (same numeric meaning as the ABI's, but defined independently here)
+enum { S_OK = 0, S_INVALID = 1, S_OVERLAP = 2, S_GAP = 3, S_NOT_GRADED = 4, S_BREAKDOWN = 9, S_MAXITER = 10 };
+
+thread_local std::string g_err;
+
+struct Loc {
+  int what;   // L_*
+  int tile;   // CELL: level-l tile; GHOST: coarse leaf tile at l-1
+  int off;    // cell offset within that tile
+};
+
+uint64_t pack3(int64_t i, int64_t j, int64_t k) {
+  return (uint64_t)i | ((uint64_t)j << 21) | ((uint64_t)k << 42);
+}
+
+// Morton interleave, x in the lowest bit of each triple (canonical order, SURVEY c-1).
+uint64_t morton(int64_t i, int64_t j, int64_t k) {
+  uint64_t m = 0;
+  for (int b = 0; b < 21; ++b) {
+    m |= (uint64_t)((i >> b) & 1) << (3 * b);
+    m |= (uint64_t)((j >> b) & 1) << (3 * b + 1);
+    m |= (uint64_t)((k >> b) & 1) << (3 * b + 2);
+  }
+  return m;
+}
+
+struct MG {
+  double alpha = 2.0, beta = 2.0;
+  int mu = 1, nu_pre = 2, nu_post = 2, nu_coarsest = 10;
+};
+
+struct Oracle {
+  int B = 8, B3 = 512;
+  int ext[3] = {1, 1, 1};
+  int wall[6] = {1, 1, 1, 1, 1, 1};  // 1 = Dirichlet wall (p = 0), 0 = Neumann wall
+  int L = 0;                         // finest leaf level
+  int NL = 0, NI = 0, T = 0;
+  std::vector<std::array<int, 4>> tile;  // canonical order: leaves then inners
+  std::vector<std::unordered_map<uint64_t, int>> leafmap, innermap;
+  std::vector<int> nbr, parent, child;
+  std::vector<int> lb, lc, ib, ic;  // per-level leaf/inner segment begin & count
+
+  // inputs and coefficients
+  std::vector<uint8_t> kind;         // leaf cells
+  std::vector<double> w[6];          // leaf cells
+  std::vector<double> c, cm[3];      // all tiles' cells
+  std::unordered_map<uint64_t, std::array<double, 3>> gcoef;  // ghost-cell -face coefficients
+  double alpha = 2.0;
+  bool setup = false;
+
+  // multigrid work arrays (all tiles' cells)
+  std::vector<double> u, b, ustar;
+
+  int levels() const { return L + 1; }
+  int tlev(int t) const { return tile[t][0]; }
+  int64_t dim(int l, int a) const { return (int64_t)ext[a] * B << l; }
+  double hcell(int l) const { return std::ldexp(1.0, -l) / B; }
+
+  int find_tile(int l, int64_t ti, int64_t tj, int64_t tk, bool* is_leaf) const {
+    if (l < 0 || l > L) return -1;
+    uint64_t k = pack3(ti, tj, tk);
+    auto it = leafmap[l].find(k);
+    if (it != leafmap[l].end()) { *is_leaf = true; return it->second; }
+    auto jt = innermap[l].find(k);
+    if (jt != innermap[l].end()) { *is_leaf = false; return jt->second; }
+    return -1;
+  }
+
+  int offset(int64_t X, int64_t Y, int64_t Z) const {
+    return (int)((X % B) + B * (Y % B) + B * B * (Z % B));
+  }
+
+  // What covers the level-l cell position (X,Y,Z): the domain wall, a cell of C_l,
+  // or (ghost) the level-(l-1) leaf cell containing it.
+  Loc locate(int l, int64_t X, int64_t Y, int64_t Z) const {
+    if (X < 0 || Y < 0 || Z < 0 || X >= dim(l, 0) || Y >= dim(l, 1) || Z >= dim(l, 2))
+      return {L_WALL, -1, -1};
+    bool lf;
+    int t = find_tile(l, X / B, Y / B, Z / B, &lf);
+    if (t >= 0) return {L_CELL, t, offset(X, Y, Z)};
+    if (l >= 1) {
+      int64_t x = X >> 1, y = Y >> 1, z = Z >> 1;
+      auto it = leafmap[l - 1].find(pack3(x / B, y / B, z / B));
+      if (it != leafmap[l - 1].end()) return {L_GHOST, it->second, offset(x, y, z)};
+    }
+    return {L_UNCOVERED, -1, -1};
+  }
+
+  // locate() with a shortcut for positions inside tile t (same result, no hash lookup)
+  Loc near(int l, int t, int64_t X, int64_t Y, int64_t Z) const {
+    if (X >= 0 && Y >= 0 && Z >= 0 && X / B == tile[t][1] && Y / B == tile[t][2] && Z / B == tile[t][3])
+      return {L_CELL, t, offset(X, Y, Z)};
+    return locate(l, X, Y, Z);
+  }
+
+  void coords(int t, int off, int64_t* X, int64_t* Y, int64_t* Z) const {
+    *X = (int64_t)tile[t][1] * B + off % B;
+    *Y = (int64_t)tile[t][2] * B + (off / B) % B;
+    *Z = (int64_t)tile[t][3] * B + off / (B * B);
+  }
+
+  size_t idx(int t, int off) const { return (size_t)t * B3 + off; }
+  bool active(size_t i) const { return c[i] != 0.0; }
+  bool loc_active(const Loc& n) const {
+    if (n.what == L_CELL || n.what == L_GHOST) return c[idx(n.tile, n.off)] != 0.0;
+    return false;
+  }
+  uint8_t leaf_kind(size_t i) const { return kind[i]; }
+  double wf(int f, size_t i) const { return w[f][i]; }
+};
+
+// -------------------------------------------------------------------------------------
+// Tree
+// -------------------------------------------------------------------------------------
+int build(Oracle& o, const int32_t* tiles, int64_t n) {
+  if (n <= 0) { g_err = "empty leaf list"; return S_INVALID; }
+  int L = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    int l = tiles[4 * t];
+    if (l < 0 || l > 20) { g_err = "bad level"; return S_INVALID; }
+    L = std::max(L, l);
+    for (int a = 0; a < 3; ++a) {
+      int64_t v = tiles[4 * t + 1 + a];
+      if (v < 0 || v >= ((int64_t)o.ext[a] << l)) { g_err = "tile outside domain"; return S_INVALID; }
+    }
+  }
+  o.L = L;
+  for (int a = 0; a < 3; ++a)
+    if (((int64_t)o.ext[a] * o.B << L) >= (1 << 20)) { g_err = "domain too fine for the oracle"; return S_INVALID; }
+  o.leafmap.assign(L + 1, {});
+  o.innermap.assign(L + 1, {});
+  // leaves, duplicate check
+  for (int64_t t = 0; t < n; ++t) {
+    int l = tiles[4 * t];
+    uint64_t k = pack3(tiles[4 * t + 1], tiles[4 * t + 2], tiles[4 * t + 3]);
+    if (!o.leafmap[l].emplace(k, -1).second) { g_err = "duplicate leaf tile"; return S_OVERLAP; }
+  }
+  // inner tiles = all strict ancestors of leaves
+  for (int64_t t = 0; t < n; ++t) {
+    int l = tiles[4 * t];
+    int64_t i = tiles[4 * t + 1], j = tiles[4 * t + 2], k = tiles[4 * t + 3];
+    for (int m = l - 1; m >= 0; --m) {
+      i >>= 1; j >>= 1; k >>= 1;
+      o.innermap[m].emplace(pack3(i, j, k), -1);
+    }
+  }
+  // overlap: a leaf that is also an ancestor of another leaf
+  for (int l = 0; l <= L; ++l)
+    for (auto& kv : o.leafmap[l])
+      if (o.innermap[l].count(kv.first)) { g_err = "leaf tile overlaps a finer leaf"; return S_OVERLAP; }
+  // gap: total leaf volume equals the domain (exact integer arithmetic)
+  unsigned __int128 vol = 0, dom = (unsigned __int128)o.ext[0] * o.ext[1] * o.ext[2];
+  for (int l = 0; l <= L; ++l) vol += (unsigned __int128)o.leafmap[l].size() << (3 * (L - l));
+  dom <<= 3 * L;
+  if (vol != dom) { g_err = "leaf tiles leave a gap"; return S_GAP; }
+
+  // canonical order: leaves (level L..0, Morton ascending), then inners (same)
+  struct E { int l; int64_t i, j, k; uint64_t m; };
+  auto collect = [&](std::vector<std::unordered_map<uint64_t, int>>& maps) {
+    std::vector<E> v;
+    for (int l = L; l >= 0; --l) {
+      std::vector<E> lv;
+      for (auto& kv : maps[l]) {
+        int64_t i = kv.first & 0x1FFFFF, j = (kv.first >> 21) & 0x1FFFFF, k = (kv.first >> 42) & 0x1FFFFF;
+        lv.push_back({l, i, j, k, morton(i, j, k)});
+      }
+      std::sort(lv.begin(), lv.end(), [](const E& a, const E& b) { return a.m < b.m; });
+      v.insert(v.end(), lv.begin(), lv.end());
+    }
+    return v;
+  };
+  std::vector<E> leaves = collect(o.leafmap), inners = collect(o.innermap);
+  o.NL = (int)leaves.size();
+  o.NI = (int)inners.size();
+  o.T = o.NL + o.NI;
+  o.tile.resize(o.T);
+  o.lb.assign(L + 1, 0); o.lc.assign(L + 1, 0); o.ib.assign(L + 1, 0); o.ic.assign(L + 1, 0);
+  for (int t = 0; t < o.T; ++t) {
+    const E& e = t < o.NL ? leaves[t] : inners[t - o.NL];
+    o.tile[t] = {e.l, (int)e.i, (int)e.j, (int)e.k};
+    auto& mp = t < o.NL ? o.leafmap : o.innermap;
+    mp[e.l][pack3(e.i, e.j, e.k)] = t;
+  }
+  for (int l = L; l >= 0; --l) {
+    o.lb[l] = -1; o.ib[l] = -1;
+  }
+  for (int t = 0; t < o.T; ++t) {
+    int l = o.tile[t][0];
+    if (t < o.NL) { if (o.lb[l] < 0) o.lb[l] = t; o.lc[l]++; }
+    else { if (o.ib[l] < 0) o.ib[l] = t; o.ic[l]++; }
+  }
+  for (int l = 0; l <= L; ++l) { if (o.lb[l] < 0) o.lb[l] = 0; if (o.ib[l] < 0) o.ib[l] = 0; }
+
+  // grading across faces: every face-neighbour position of a leaf at level l
+  // is in C_l or inside a leaf at level l-1.
+  for (int t = 0; t < o.NL; ++t) {
+    int l = o.tile[t][0];
+    for (int f = 0; f < 6; ++f) {
+      int a = f / 2, s = (f & 1) ? 1 : -1;
+      int64_t q[3] = {o.tile[t][1], o.tile[t][2], o.tile[t][3]};
+      q[a] += s;
+      if (q[a] < 0 || q[a] >= ((int64_t)o.ext[a] << l)) continue;
+      bool lf;
+      if (o.find_tile(l, q[0], q[1], q[2], &lf) >= 0) continue;
+      if (l >= 1 && o.leafmap[l - 1].count(pack3(q[0] >> 1, q[1] >> 1, q[2] >> 1))) continue;
+      g_err = "leaf tiles are not 2:1 face graded";
+      return S_NOT_GRADED;
+    }
+  }
+
+  // tables: nbr (>=0 same-level tile, -1 wall, -2-idx ghost with coarse-leaf tile idx),
+  // parent, child (octant dx + 2dy + 4dz)
+  o.nbr.assign((size_t)o.T * 6, -1);
+  o.parent.assign(o.T, -1);
+  o.child.assign((size_t)o.NI * 8, -1);
+  for (int t = 0; t < o.T; ++t) {
+    int l = o.tile[t][0];
+    for (int f = 0; f < 6; ++f) {
+      int a = f / 2, s = (f & 1) ? 1 : -1;
+      int64_t q[3] = {o.tile[t][1], o.tile[t][2], o.tile[t][3]};
+      q[a] += s;
+      if (q[a] < 0 || q[a] >= ((int64_t)o.ext[a] << l)) { o.nbr[6 * t + f] = -1; continue; }
+      bool lf;
+      int nt = o.find_tile(l, q[0], q[1], q[2], &lf);
+      if (nt >= 0) { o.nbr[6 * t + f] = nt; continue; }
+      auto it = l >= 1 ? o.leafmap[l - 1].find(pack3(q[0] >> 1, q[1] >> 1, q[2] >> 1)) : o.leafmap[0].end();
+      if (t < o.NL && l >= 1 && it != o.leafmap[l - 1].end()) { o.nbr[6 * t + f] = -2 - it->second; continue; }
+      g_err = "inner tile without same-level neighbour (not graded)";
+      return S_NOT_GRADED;
+    }
+    if (l >= 1) {
+      auto it = o.innermap[l - 1].find(pack3(o.tile[t][1] >> 1, o.tile[t][2] >> 1, o.tile[t][3] >> 1));
+      o.parent[t] = it->second;
+    }
+    if (t >= o.NL) {
+      for (int d = 0; d < 8; ++d) {
+        bool lf;
+        o.child[8 * (t - o.NL) + d] = o.find_tile(l + 1, 2 * (int64_t)o.tile[t][1] + (d & 1),
+                                                  2 * (int64_t)o.tile[t][2] + ((d >> 1) & 1),
+                                                  2 * (int64_t)o.tile[t][3] + (d >> 2), &lf);
+      }
+    }
+  }
+  return S_OK;
+}
+
+// ghost-cell key: level and 20-bit cell coordinates (build() checks the range)
+uint64_t gkey(int l, int64_t X, int64_t Y, int64_t Z) {
+  return ((uint64_t)l << 60) | ((uint64_t)X << 40) | ((uint64_t)Y << 20) | (uint64_t)Z;
+}
+
+// -------------------------------------------------------------------------------------
+// Leaf coefficients: Eq. 3, cell kinds, T-junction faces
+// (Eqs. 9-10).  kappa = w * h is the face conductance beta*S/h.
+// -------------------------------------------------------------------------------------
+// Fine sub-cells (level l+1) of the inner cell n (level l) that touch cell i across
+// face f of i: the children of n on the side facing i.
+void fine_subcells(const Oracle& o, int l, const Loc& n, int f, std::vector<size_t>& out) {
+  out.clear();
+  int64_t X, Y, Z;
+  o.coords(n.tile, n.off, &X, &Y, &Z);
+  int a = f / 2;
+  int facing = (f & 1) ? 0 : 1;  // neighbour on i's + side -> its children with d_a = 0
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        int d[3] = {dx, dy, dz};
+        if (d[a] != facing) continue;
+        Loc s = o.locate(l + 1, 2 * X + dx, 2 * Y + dy, 2 * Z + dz);
+        // grading guarantees these are leaf cells (inner tile next to a leaf has leaf
+        // children on that face)
+        if (s.what != L_CELL || s.tile >= o.NL) { out.push_back((size_t)-1); continue; }
+        out.push_back(o.idx(s.tile, s.off));
+      }
+}
+
+int assemble(Oracle& o) {
+  const int B3 = o.B3;
+  size_t NC = (size_t)o.T * B3;
+  o.c.assign(NC, 0.0);
+  for (int a = 0; a < 3; ++a) o.cm[a].assign(NC, 0.0);
+  o.gcoef.clear();
+  std::vector<size_t> subs;
+  // pass 1: diagonals of leaf cells from geometry
+  for (int t = 0; t < o.NL; ++t) {
+    int l = o.tlev(t);
+    double h = o.hcell(l);
+    for (int off = 0; off < B3; ++off) {
+      size_t i = o.idx(t, off);
+      if (o.kind[i] != K_FLUID) { o.c[i] = 0.0; continue; }
+      int64_t X, Y, Z;
+      o.coords(t, off, &X, &Y, &Z);
+      double s = 0.0;
+      for (int f = 0; f < 6; ++f) {
+        int a = f / 2, sg = (f & 1) ? 1 : -1;
+        int64_t q[3] = {X, Y, Z};
+        q[a] += sg;
+        Loc n = o.locate(l, q[0], q[1], q[2]);
+        if (n.what == L_WALL) {
+          if (o.wall[f] == 1) s += o.wf(f, i) * h;
+        } else if (n.what == L_CELL && n.tile < o.NL) {
+          size_t j = o.idx(n.tile, n.off);
+          if (o.kind[j] != K_NEUMANN) s += (sg < 0 ? o.wf(f, i) : o.wf(f ^ 1, j)) * h;
+        } else if (n.what == L_CELL) {
+          fine_subcells(o, l, n, f, subs);
+          for (size_t sidx : subs) {
+            if (sidx == (size_t)-1) { g_err = "fine sub-cell is not a leaf"; return S_NOT_GRADED; }
+            if (o.kind[sidx] != K_NEUMANN) s += 0.5 * o.wf(f ^ 1, sidx) * (0.5 * h);
+          }
+        } else if (n.what == L_GHOST) {
+          if (o.kind[o.idx(n.tile, n.off)] != K_NEUMANN) s += o.wf(f, i) * h;
+        } else {
+          g_err = "uncovered neighbour";
+          return S_NOT_GRADED;
+        }
+      }
+      o.c[i] = s;  // a fluid cell with c == 0 is isolated and therefore inactive
+    }
+  }
+  // pass 2: -face off-diagonals and ghost-cell coefficients of the + faces
+  for (int t = 0; t < o.NL; ++t) {
+    int l = o.tlev(t);
+    double h = o.hcell(l);
+    for (int off = 0; off < B3; ++off) {
+      size_t i = o.idx(t, off);
+      if (o.kind[i] == K_NEUMANN) continue;  // all coefficients 0
+      int64_t X, Y, Z;
+      o.coords(t, off, &X, &Y, &Z);
+      for (int a = 0; a < 3; ++a) {
+        int64_t q[3] = {X, Y, Z};
+        q[a] -= 1;
+        int f = 2 * a;
+        Loc n = o.locate(l, q[0], q[1], q[2]);
+        double v = 0.0;
+        if (n.what == L_CELL && n.tile < o.NL) {
+          if (o.kind[o.idx(n.tile, n.off)] != K_NEUMANN) v = -o.wf(f, i) * h;
+        } else if (n.what == L_CELL) {
+          fine_subcells(o, l, n, f, subs);
+          double acc = 0.0;
+          for (size_t sidx : subs)
+            if (o.c[sidx] != 0.0) acc += o.wf(f ^ 1, sidx) * (0.5 * h);
+          v = -0.5 * acc;
+        } else if (n.what == L_GHOST) {
+          if (o.kind[o.idx(n.tile, n.off)] != K_NEUMANN) v = -o.wf(f, i) * h;
+        }
+        o.cm[a][i] = v;
+        // + face toward a ghost: the ghost cell's -face coefficient (c_{6,x-})
+        int64_t p[3] = {X, Y, Z};
+        p[a] += 1;
+        Loc g = o.locate(l, p[0], p[1], p[2]);
+        if (g.what == L_GHOST) {
+          double gv = o.kind[o.idx(g.tile, g.off)] != K_NEUMANN ? -o.wf(f + 1, i) * h : 0.0;
+          o.gcoef[gkey(l, p[0], p[1], p[2])][a] = gv;
+        }
+      }
+    }
+  }
+  return S_OK;
+}
+
+// Alg. 3 with the activity test on the off-diagonal branch (SURVEY c-3 / c-8
+// #3): c^{l-1}_I from the 8 children i = 2I + d at level l.
+void coarsen_level(Oracle& o, int l) {
+  const double al = o.alpha;
+  int lc = l - 1;
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t) {
+    for (int off = 0; off < o.B3; ++off) {
+      int64_t IX, IY, IZ;
+      o.coords(t, off, &IX, &IY, &IZ);
+      double cI = 0.0, cIm[3] = {0.0, 0.0, 0.0};
+      int active_cnt = 0;
+      for (int dz = 0; dz < 2; ++dz)
+        for (int dy = 0; dy < 2; ++dy)
+          for (int dx = 0; dx < 2; ++dx) {
+            int d[3] = {dx, dy, dz};
+            int64_t ch[3] = {2 * IX + dx, 2 * IY + dy, 2 * IZ + dz};
+            Loc ci = o.locate(l, ch[0], ch[1], ch[2]);
+            size_t i = o.idx(ci.tile, ci.off);
+            bool act = o.c[i] != 0.0;
+            if (act) { active_cnt++; cI += o.c[i] / al; }  // diagonal
+            for (int a = 0; a < 3; ++a) {
+              int64_t q[3] = {ch[0], ch[1], ch[2]};
+              q[a] -= 1;
+              Loc nb = o.locate(l, q[0], q[1], q[2]);
+              bool nact = o.loc_active(nb);
+              if (d[a] == 1) {
+                if (act && nact) cI += (2.0 / al) * o.cm[a][i];  // 2 cross terms in the diagonal
+              } else {
+                if (act && nact) cIm[a] += o.cm[a][i] / al;     // non-diagonal
+              }
+            }
+          }
+      size_t I = o.idx(t, off);
+      o.c[I] = active_cnt == 0 ? 0.0 : cI;
+      for (int a = 0; a < 3; ++a) o.cm[a][I] = cIm[a];
+    }
+  }
+}
+
+int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha) {
+  size_t N = (size_t)o.NL * o.B3;
+  o.kind.assign(kind, kind + N);
+  for (int f = 0; f < 6; ++f) {
+    o.w[f].resize(N);
+    for (size_t i = 0; i < N; ++i) o.w[f][i] = w ? (double)w[(size_t)f * N + i] : 1.0;
+  }
+  for (size_t i = 0; i < N; ++i)
+    if (o.kind[i] > 2) { g_err = "bad cell kind"; return S_INVALID; }
+  o.alpha = alpha;
+  int st = assemble(o);
+  if (st) return st;
+  for (int l = o.L; l >= 1; --l) coarsen_level(o, l);
+  o.setup = true;
+  size_t NC = (size_t)o.T * o.B3;
+  o.u.assign(NC, 0.0); o.b.assign(NC, 0.0); o.ustar.assign(NC, 0.0);
+  return S_OK;
+}
+
+// -------------------------------------------------------------------------------------
+// Operators (SURVEY c-4).  Face order x-, x+, y-, y+, z-, z+.
+// -------------------------------------------------------------------------------------
+double coef_plus(const Oracle& o, int l, int a, const Loc& n, int64_t X, int64_t Y, int64_t Z) {
+  if (n.what == L_CELL) return o.cm[a][o.idx(n.tile, n.off)];
+  if (n.what == L_GHOST) {
+    auto it = o.gcoef.find(gkey(l, X, Y, Z));
+    return it == o.gcoef.end() ? 0.0 : it->second[a];
+  }
+  return 0.0;
+}
+
+// mean over the active children of cell i's parent (the 2x2x2 block holding i), values v
+double parent_mean(const Oracle& o, int l, int t, int64_t X, int64_t Y, int64_t Z, const double* v) {
+  double s = 0.0;
+  int n = 0;
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        Loc q = o.near(l, t, (X & ~1LL) + dx, (Y & ~1LL) + dy, (Z & ~1LL) + dz);
+        size_t j = o.idx(q.tile, q.off);
+        if (o.c[j] != 0.0) { s += v[j]; n++; }
+      }
+  return n ? s / n : 0.0;
+}
+
+// mean over the active children (level l+1) of the inner cell n (level l)
+double child_mean(const Oracle& o, int l, const Loc& n, const double* v) {
+  int64_t X, Y, Z;
+  o.coords(n.tile, n.off, &X, &Y, &Z);
+  double s = 0.0;
+  int k = 0;
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        Loc q = o.locate(l + 1, 2 * X + dx, 2 * Y + dy, 2 * Z + dz);
+        size_t j = o.idx(q.tile, q.off);
+        if (o.c[j] != 0.0) { s += v[j]; k++; }
+      }
+  return k ? s / k : 0.0;
+}
+
+// Level operator row (A^l u)_i for a cell i of C_l.  Same-level neighbours use the level
+// value; a ghost uses g = u_i + (u^{l-1}_C - m_P)/2 (Eq. 12), m_P from `snap`; inactive
+// neighbours and walls contribute 0.  `uval` gives same-level/ghost-source values, `snap`
+// the state the ghost reconstruction uses (equal to uval except inside an RBGS pass).
+double level_row(const Oracle& o, int l, int t, int off, const double* uval, const double* snap,
+                 bool skip_diag) {
+  size_t i = o.idx(t, off);
+  int64_t X, Y, Z;
+  o.coords(t, off, &X, &Y, &Z);
+  double s = skip_diag ? 0.0 : o.c[i] * uval[i];
+  double mP = 0.0;
+  bool have_mP = false;
+  for (int f = 0; f < 6; ++f) {
+    int a = f / 2, sg = (f & 1) ? 1 : -1;
+    int64_t q[3] = {X, Y, Z};
+    q[a] += sg;
+    Loc n = o.near(l, t, q[0], q[1], q[2]);
+    double coef = sg < 0 ? o.cm[a][i] : coef_plus(o, l, a, n, q[0], q[1], q[2]);
+    double v = 0.0;
+    if (n.what == L_CELL) {
+      size_t j = o.idx(n.tile, n.off);
+      v = o.c[j] != 0.0 ? uval[j] : 0.0;
+    } else if (n.what == L_GHOST) {
+      size_t C = o.idx(n.tile, n.off);
+      if (o.c[C] != 0.0) {
+        if (!have_mP) { mP = parent_mean(o, l, t, X, Y, Z, snap); have_mP = true; }
+        v = snap[i] + 0.5 * (snap[C] - mP);
+      }
+    }
+    s += coef * v;
+  }
+  return s;
+}
+
+// Composite operator row for a leaf cell (inner neighbour value = mean of its active
+// children; ghost source = the coarse leaf's composite value).
+double composite_row(const Oracle& o, int t, int off, const double* x) {
+  int l = o.tlev(t);
+  size_t i = o.idx(t, off);
+  int64_t X, Y, Z;
+  o.coords(t, off, &X, &Y, &Z);
+  double s = o.c[i] * x[i];
+  for (int f = 0; f < 6; ++f) {
+    int a = f / 2, sg = (f & 1) ? 1 : -1;
+    int64_t q[3] = {X, Y, Z};
+    q[a] += sg;
+    Loc n = o.near(l, t, q[0], q[1], q[2]);
+    double coef = sg < 0 ? o.cm[a][i] : coef_plus(o, l, a, n, q[0], q[1], q[2]);
+    double v = 0.0;
+    if (n.what == L_CELL && n.tile < o.NL) {
+      size_t j = o.idx(n.tile, n.off);
+      v = o.c[j] != 0.0 ? x[j] : 0.0;
+    } else if (n.what == L_CELL) {
+      v = child_mean(o, l, n, x);
+    } else if (n.what == L_GHOST) {
+      size_t C = o.idx(n.tile, n.off);
+      if (o.c[C] != 0.0) v = x[i] + 0.5 * (x[C] - parent_mean(o, l, t, X, Y, Z, x));
+    }
+    s += coef * v;
+  }
+  return s;
+}
+
+void apply_composite(const Oracle& o, const double* x, double* y) {
+  // x, y are leaf vectors (NL*B3); leaf tiles come first in the canonical order, so a
+  // leaf slot is also its all-tile index.
+#pragma omp parallel for schedule(static) if (o.NL >= 256)
+  for (int t = 0; t < o.NL; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t i = o.idx(t, off);
+      y[i] = o.c[i] != 0.0 ? composite_row(o, t, off, x) : 0.0;
+    }
+}
+
+template <class F>
+void for_level_tiles(const Oracle& o, int l, F fn) {
+  std::vector<int> ts;
+  for (int t = o.lb[l]; t < o.lb[l] + o.lc[l]; ++t) ts.push_back(t);
+  for (int t = o.ib[l]; t < o.ib[l] + o.ic[l]; ++t) ts.push_back(t);
+#pragma omp parallel for schedule(static) if (ts.size() >= 256)
+  for (size_t k = 0; k < ts.size(); ++k) fn(ts[k]);
+}
+
+void apply_level(const Oracle& o, int l, const double* u, double* y) {
+  for_level_tiles(o, l, [&](int t) {
+    for (int off = 0; off < o.B3; ++off) {
+      size_t i = o.idx(t, off);
+      y[i] = o.c[i] != 0.0 ? level_row(o, l, t, off, u, u, false) : 0.0;
+    }
+  });
+}
+
+// One red-black Gauss-Seidel colour pass at level l.  Colour = parity of
+// the global level-l cell coordinates (0 = red).  Ghost values and m_P come from the
+// state at the start of the pass (SURVEY c-5 / c-8 #1).
+void rbgs_pass(Oracle& o, int l, int colour, double* u, const double* b) {
+  std::vector<double> snap(u, u + (size_t)o.T * o.B3);
+  for_level_tiles(o, l, [&](int t) {
+    for (int off = 0; off < o.B3; ++off) {
+      int64_t X, Y, Z;
+      o.coords(t, off, &X, &Y, &Z);
+      if (((X + Y + Z) & 1) != colour) continue;
+      size_t i = o.idx(t, off);
+      if (o.c[i] == 0.0) continue;
+      double offd = level_row(o, l, t, off, snap.data(), snap.data(), true);
+      u[i] = (b[i] - offd) / o.c[i];
+    }
+  });
+}
+
+void smooth(Oracle& o, int l, int iters, bool red_first) {
+  for (int k = 0; k < iters; ++k) {
+    rbgs_pass(o, l, red_first ? 0 : 1, o.u.data(), o.b.data());
+    rbgs_pass(o, l, red_first ? 1 : 0, o.u.data(), o.b.data());
+  }
+}
+
+void smooth_coarsest(Oracle& o, const MG& p) {
+  // nu_b split into two opposite-order halves
+  smooth(o, 0, p.nu_coarsest / 2, true);
+  smooth(o, 0, p.nu_coarsest - p.nu_coarsest / 2, false);
+}
+
+void residual(const Oracle& o, int l, std::vector<double>& r) {
+  for_level_tiles(o, l, [&](int t) {
+    for (int off = 0; off < o.B3; ++off) {
+      size_t i = o.idx(t, off);
+      r[i] = o.c[i] != 0.0 ? o.b[i] - level_row(o, l, t, off, o.u.data(), o.u.data(), false) : 0.0;
+    }
+  });
+}
+
+// children of inner cell (t, off) at level l-1, as all-tile indices (octant order)
+void children_of(const Oracle& o, int lc, int t, int off, size_t out[8]) {
+  int64_t X, Y, Z;
+  o.coords(t, off, &X, &Y, &Z);
+  for (int d = 0; d < 8; ++d) {
+    Loc q = o.locate(lc + 1, 2 * X + (d & 1), 2 * Y + ((d >> 1) & 1), 2 * Z + (d >> 2));
+    out[d] = o.idx(q.tile, q.off);
+  }
+}
+
+// Alg. 4, FAS-style mu-cycle, readings SURVEY c-6.
+void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
+  if (l == 0) { smooth_coarsest(o, p); return; }
+  smooth(o, l, p.nu_pre, true);                  // pre-smoothing (R,B)
+  residual(o, l, r);                             // r^l = b^l - A^l u^l
+  int lc = l - 1;
+  // u*_I = Avg(u^l) over active children; u^{l-1}_I := u*_I  (inner cells of level l-1)
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t ch[8];
+      children_of(o, lc, t, off, ch);
+      double s = 0.0;
+      int n = 0;
+      for (int d = 0; d < 8; ++d)
+        if (o.c[ch[d]] != 0.0) { s += o.u[ch[d]]; n++; }
+      size_t I = o.idx(t, off);
+      o.ustar[I] = n ? s / n : 0.0;
+      o.u[I] = o.ustar[I];
+    }
+  // b^{l-1}_I = beta R r^l + (A^{l-1} u^{l-1})_I  on inner rows; leaf(l-1) rows keep b
+  std::vector<double> Au((size_t)o.T * o.B3, 0.0);
+  apply_level(o, lc, o.u.data(), Au.data());
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t ch[8];
+      children_of(o, lc, t, off, ch);
+      double rs = 0.0;
+      for (int d = 0; d < 8; ++d)
+        if (o.c[ch[d]] != 0.0) rs += r[ch[d]];
+      size_t I = o.idx(t, off);
+      o.b[I] = p.beta * (rs / p.alpha) + Au[I];
+    }
+  for (int k = 0; k < p.mu; ++k) fas(o, lc, p, r);
+  // prolongation of the update u^{l-1} - u* (no beta)
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t ch[8];
+      children_of(o, lc, t, off, ch);
+      size_t I = o.idx(t, off);
+      double corr = o.u[I] - o.ustar[I];
+      for (int d = 0; d < 8; ++d)
+        if (o.c[ch[d]] != 0.0) o.u[ch[d]] += corr;
+    }
+  smooth(o, l, p.nu_post, false);                // post-smoothing (B,R)
+}
+
+// Alg. 2, standard mu-cycle with beta at prolongation.  Only meaningful on
+// uniform trees (no leaves below the finest level); used as an equivalence check.
+void mucycle_std(Oracle& o, int l, const MG& p, std::vector<double>& r) {
+  if (l == 0) { smooth_coarsest(o, p); return; }
+  smooth(o, l, p.nu_pre, true);
+  residual(o, l, r);
+  int lc = l - 1;
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t ch[8];
+      children_of(o, lc, t, off, ch);
+      double rs = 0.0;
+      for (int d = 0; d < 8; ++d)
+        if (o.c[ch[d]] != 0.0) rs += r[ch[d]];
+      size_t I = o.idx(t, off);
+      o.b[I] = rs / p.alpha;  // R r
+      o.u[I] = 0.0;
+    }
+  for (int k = 0; k < p.mu; ++k) mucycle_std(o, lc, p, r);
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t ch[8];
+      children_of(o, lc, t, off, ch);
+      size_t I = o.idx(t, off);
+      for (int d = 0; d < 8; ++d)
+        if (o.c[ch[d]] != 0.0) o.u[ch[d]] += p.beta * o.u[I];
+    }
+  smooth(o, l, p.nu_post, false);
+}
+
+// M(r): u^l := 0 for all l; b^l[leaf(l)] := r; cycle from the finest level; z := u[leaves]
+void precond(Oracle& o, const MG& p, const double* rin, double* z, bool fas_form) {
+  size_t NC = (size_t)o.T * o.B3, N = (size_t)o.NL * o.B3;
+  std::fill(o.u.begin(), o.u.end(), 0.0);
+  std::fill(o.b.begin(), o.b.end(), 0.0);
+  std::fill(o.ustar.begin(), o.ustar.end(), 0.0);
+  for (size_t i = 0; i < N; ++i) o.b[i] = o.c[i] != 0.0 ? rin[i] : 0.0;
+  std::vector<double> r(NC, 0.0);
+  if (fas_form) fas(o, o.L, p, r); else mucycle_std(o, o.L, p, r);
+  for (size_t i = 0; i < N; ++i) z[i] = o.u[i];
+}
+
+double dot(const Oracle& o, const double* a, const double* b) {
+  size_t N = (size_t)o.NL * o.B3;
+  double s = 0.0;
+  for (size_t i = 0; i < N; ++i)
+    if (o.c[i] != 0.0) s += a[i] * b[i];
+  return s;
+}
+
+void project_mean(const Oracle& o, double* r) {
+  size_t N = (size_t)o.NL * o.B3;
+  double s = 0.0;
+  size_t n = 0;
+  for (size_t i = 0; i < N; ++i)
+    if (o.c[i] != 0.0) { s += r[i]; n++; }
+  if (!n) return;
+  double m = s / (double)n;
+  for (size_t i = 0; i < N; ++i)
+    if (o.c[i] != 0.0) r[i] -= m;
+}
+
+bool pure_neumann(const Oracle& o) {
+  for (int f = 0; f < 6; ++f) if (o.wall[f] == 1) return false;
+  for (uint8_t k : o.kind) if (k == K_DIRICHLET) return false;
+  return true;
+}
+
+// Alg. 1, readings SURVEY c-7 / c-8 #11-12.
+int pcg(Oracle& o, const MG& p, int precond_kind, const double* bin, double* x, double rtol,
+        int max_iters, int nullspace, int* iters_out, double* relres_out, double* bnorm_out,
+        double* hist, int hcap) {
+  size_t N = (size_t)o.NL * o.B3;
+  bool ns = nullspace < 0 ? pure_neumann(o) : nullspace == 1;
+  std::vector<double> r(N), z(N), pv(N), q(N);
+  for (size_t i = 0; i < N; ++i) { x[i] = 0.0; r[i] = o.c[i] != 0.0 ? bin[i] : 0.0; }
+  if (ns) project_mean(o, r.data());
+  double bn = std::sqrt(dot(o, r.data(), r.data()));
+  *bnorm_out = bn;
+  *iters_out = 0;
+  *relres_out = 0.0;
+  if (bn == 0.0) return S_OK;
+  auto M = [&](const double* rr, double* zz) {
+    if (precond_kind == 0) { for (size_t i = 0; i < N; ++i) zz[i] = o.c[i] != 0.0 ? rr[i] : 0.0; }
+    else precond(o, p, rr, zz, precond_kind == 1);
+  };
+  M(r.data(), z.data());
+  pv = z;
+  double rho = dot(o, r.data(), z.data());
+  int k = 0;
+  while (true) {
+    apply_composite(o, pv.data(), q.data());
+    double sigma = dot(o, pv.data(), q.data());
+    if (!(sigma > 0.0)) { *iters_out = k; return S_BREAKDOWN; }
+    double alpha = rho / sigma;
+    for (size_t i = 0; i < N; ++i) { x[i] += alpha * pv[i]; r[i] -= alpha * q[i]; }
+    if (ns) project_mean(o, r.data());
+    k++;
+    double rn = std::sqrt(dot(o, r.data(), r.data()));
+    if (k - 1 < hcap) hist[k - 1] = rn / bn;
+    *iters_out = k;
+    *relres_out = rn / bn;
+    if (rn <= rtol * bn) return S_OK;
+    if (k >= max_iters) return S_MAXITER;
+    M(r.data(), z.data());
+    double rho2 = dot(o, r.data(), z.data());
+    double beta = rho2 / rho;
+    rho = rho2;
+    for (size_t i = 0; i < N; ++i) pv[i] = z[i] + beta * pv[i];
+  }
+}
+
+MG mg_from(const double* prm) {
+  MG p;
+  if (prm) {
+    p.alpha = prm[0]; p.beta = prm[1]; p.mu = (int)prm[2]; p.nu_pre = (int)prm[3];
+    p.nu_post = (int)prm[4]; p.nu_coarsest = (int)prm[5];
+  }
+  return p;
+}
+
+}  // namespace
+
+// ======================================================================================
+// C API (ctypes; see oracle/oracle.py)
+// ======================================================================================
+extern "C" {
+
+const char* orc_last_error() { return g_err.c_str(); }
+
+void* orc_create(int B, const int32_t* ext, const int32_t* wall, const int32_t* tiles, int64_t n,
+                 int32_t* status) {
+  auto* o = new Oracle();
+  if (B != 2 && B != 4 && B != 8) { g_err = "B must be 2, 4 or 8"; *status = S_INVALID; delete o; return nullptr; }
+  o->B = B;
+  o->B3 = B * B * B;
+  for (int a = 0; a < 3; ++a) o->ext[a] = ext[a];
+  for (int f = 0; f < 6; ++f) o->wall[f] = wall[f];
+  int st = build(*o, tiles, n);
+  *status = st;
+  if (st) { delete o; return nullptr; }
+  return o;
+}
+
+void orc_destroy(void* h) { delete (Oracle*)h; }
+
+// out: [L, NL, NI, T, then for l = 0..L: leaf_begin, leaf_count, inner_begin, inner_count]
+void orc_info(void* h, int64_t* out) {
+  auto* o = (Oracle*)h;
+  out[0] = o->L; out[1] = o->NL; out[2] = o->NI; out[3] = o->T;
+  for (int l = 0; l <= o->L; ++l) {
+    out[4 + 4 * l] = o->lb[l]; out[5 + 4 * l] = o->lc[l];
+    out[6 + 4 * l] = o->ib[l]; out[7 + 4 * l] = o->ic[l];
+  }
+}
+
+void orc_tables(void* h, int32_t* tiles, int32_t* nbr, int32_t* parent, int32_t* child) {
+  auto* o = (Oracle*)h;
+  for (int t = 0; t < o->T; ++t)
+    for (int a = 0; a < 4; ++a) tiles[4 * t + a] = o->tile[t][a];
+  std::memcpy(nbr, o->nbr.data(), sizeof(int32_t) * o->nbr.size());
+  std::memcpy(parent, o->parent.data(), sizeof(int32_t) * o->parent.size());
+  if (o->NI) std::memcpy(child, o->child.data(), sizeof(int32_t) * o->child.size());
+}
+
+int32_t orc_setup(void* h, const uint8_t* kind, const float* w, double alpha) {
+  return setup(*(Oracle*)h, kind, w, alpha);
+}
+
+// out: T*B3*4 doubles (c, cxm, cym, czm) per cell in all-tile order
+void orc_coefs(void* h, double* out) {
+  auto* o = (Oracle*)h;
+  size_t NC = (size_t)o->T * o->B3;
+  for (size_t i = 0; i < NC; ++i) {
+    out[4 * i] = o->c[i];
+    for (int a = 0; a < 3; ++a) out[4 * i + 1 + a] = o->cm[a][i];
+  }
+}
+
+// ghost cell (level, X, Y, Z): its -face coefficients; returns 1 if such a ghost exists
+int32_t orc_ghost_coef(void* h, int32_t l, int64_t X, int64_t Y, int64_t Z, double* out) {
+  auto* o = (Oracle*)h;
+  auto it = o->gcoef.find(gkey(l, X, Y, Z));
+  if (it == o->gcoef.end()) return 0;
+  for (int a = 0; a < 3; ++a) out[a] = it->second[a];
+  return 1;
+}
+
+void orc_apply(void* h, const double* x, double* y) { apply_composite(*(Oracle*)h, x, y); }
+
+void orc_apply_level(void* h, int32_t l, const double* u, double* y) {
+  apply_level(*(Oracle*)h, l, u, y);
+}
+
+void orc_rbgs_pass(void* h, int32_t l, int32_t colour, double* u, const double* b) {
+  rbgs_pass(*(Oracle*)h, l, colour, u, b);
+}
+
+// prm: [alpha, beta, mu, nu_pre, nu_post, nu_coarsest]; form: 1 = Alg. 4 (FAS), 0 = Alg. 2
+void orc_vcycle(void* h, const double* prm, const double* r, double* z, int32_t form) {
+  precond(*(Oracle*)h, mg_from(prm), r, z, form == 1);
+}
+
+// precond_kind: 0 identity, 1 FAS mu-cycle (Alg. 4), 2 standard mu-cycle (Alg. 2)
+int32_t orc_pcg(void* h, const double* prm, int32_t precond_kind, const double* b, double* x,
+                double rtol, int32_t max_iters, int32_t nullspace, int32_t* iters, double* relres,
+                double* bnorm, double* hist, int32_t hcap) {
+  int it = 0;
+  int st = pcg(*(Oracle*)h, mg_from(prm), precond_kind, b, x, rtol, max_iters, nullspace, &it,
+               relres, bnorm, hist, hcap);
+  *iters = it;
+  return st;
+}
+
+}  // extern "C"
