@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark: full PCG-MG solve throughput (leaf cells / s to relative residual 1e-6).
+
+One "step" = one complete octmg_pcg_solve (Alg. 1 with the FAS mu-cycle preconditioner,
+every PCG iteration until ||r|| <= 1e-6 ||r0||) on the workload BASELINE.json's metric is
+quoted on: config 2, uniform 256^3 (16.78M leaf cells) with the paper's Sec. 5.3 setup
+(Table 1 was measured on it).  Inputs are resident in HBM before
+the timed region; setup (tree, coefficients, Galerkin hierarchy) is outside it, as in
+Table 1 (reading #14).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+N > 1 (torchrun): every rank solves its own instance (replicas),
+value = total cells / max-over-ranks time, "scaling": "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "full PCG-MG solve cells/sec to 1e-6 rel residual; HBM GB/s vs peak"
+WORKLOADS = {
+    "cfg2_uniform256": "BASELINE config 2: uniform 256^3 sinusoidal Poisson, paper Sec. 5.3 setup "
+                       "(outermost cell layer Neumann, null-space projection), V-cycle mu=1, rtol 1e-6",
+    "cfg1_octant": "BASELINE config 1: 16^3 base + one refined octant (7680 leaves), Dirichlet walls",
+    "cfg3_sphere": "BASELINE config 3: sphere band l0=4..7 (60.1M leaves), paper Sec. 5.3 setup",
+    "uniform128": "uniform 128^3 (paper Table 1 uniform (4-4)), Sec. 5.3 setup",
+    "tank_mid": "cut-cell tank, sphere obstacle r=0.3, levels 3..5, W-cycle mu=2",
+}
+CPU_SAMPLE = "uniform64"  # same recipe as cfg2 at 64^3: the bounded oracle sample
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2_uniform256")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rtol", type=float, default=1e-6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(seconds: float):
+    """The fp64 oracle as it stands, on the host cores, on a bounded sample of the same
+    workload recipe (64^3): repeated full solves to 1e-6 for >= `seconds`."""
+    from octgen import make_config
+    from oracle.oracle import Oracle
+    cfg = make_config(CPU_SAMPLE)
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    o.setup(cfg["kind"], cfg["w"])
+    b = cfg["b"].astype(np.float64)
+    n, t0, iters = 0, time.perf_counter(), 0
+    while True:
+        r = o.pcg(b, rtol=1e-6, mu=cfg["mu"])
+        n += 1
+        iters = r["iters"]
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": n * o.N / el, "unit": "cells/s", "cores": cores, "kind": "oracle",
+            "sample": f"{CPU_SAMPLE} (64^3, same recipe as cfg2): {n} full fp64 solves to 1e-6 "
+                      f"({iters} PCG iterations each) in {el:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from octgen import make_config
+    from oracle.oracle import Oracle
+    cfg = make_config(CPU_SAMPLE)
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    o.setup(cfg["kind"], cfg["w"])
+    b = cfg["b"].astype(np.float64)
+    for _ in range(args.warmup):
+        o.pcg(b, rtol=args.rtol, mu=cfg["mu"])
+    t0 = time.perf_counter()
+    iters = 0
+    for _ in range(args.steps):
+        iters = o.pcg(b, rtol=args.rtol, mu=cfg["mu"])["iters"]
+    el = time.perf_counter() - t0
+    value = args.steps * o.N / el
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {"metric": METRIC, "value": value, "unit": "cells/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS.get(args.config, args.config),
+                       "reference_sample": f"{CPU_SAMPLE}: 64^3 instance of the same recipe per step",
+                       "leaf_cells": o.N, "iters": iters},
+            "cpu_baseline": {"value": value, "unit": "cells/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{CPU_SAMPLE} per step, {args.steps} steps"},
+            "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def traffic_from_profiles(config):
+    """ncu dram bytes per launch of the dominant kernel, from the committed summary."""
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(config)
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    import paper_2604_18886_b200 as om
+    from octgen import make_config
+    assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
+
+    cfg = make_config(args.config)
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    kind = torch.from_numpy(cfg["kind"]).to(dev)
+    frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(dev)
+    h = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
+    b_host = torch.from_numpy(cfg["b"]).pin_memory()
+    b = b_host.to(dev)
+    x = torch.zeros_like(b)
+    x_host = torch.empty_like(b_host).pin_memory()
+    N = tree.N
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timing --------------------------------------------------------
+    for _ in range(args.warmup):
+        rep = h.pcg_solve(b, x, rtol=args.rtol)
+    torch.cuda.synchronize()
+    barrier()
+    sampler = ClockSampler(dev.index)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    launches = 0
+    iters = []
+    for _ in range(args.steps):
+        rep = h.pcg_solve(b, x, rtol=args.rtol)
+        launches += rep["kernel_launches"]
+        iters.append(rep["iters"])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = world * N / (ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers --------------------------
+    for _ in range(max(1, args.warmup)):
+        b.copy_(b_host, non_blocking=True)
+        h.pcg_solve(b, x, rtol=args.rtol)
+        x_host.copy_(x, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        b.copy_(b_host, non_blocking=True)
+        h.pcg_solve(b, x, rtol=args.rtol)
+        x_host.copy_(x, non_blocking=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+
+    # ---- per-kernel device time (profiling pass: events around every launch) -----------
+    h.profile(True)
+    for _ in range(2):
+        h.pcg_solve(b, x, rtol=args.rtol)
+    prof = h.profile_read()
+    h.profile(False)
+    dom = max((k for k in prof if prof[k]["launches"]), key=lambda k: prof[k]["ms"])
+    tot_ms = sum(v["ms"] for v in prof.values())
+    d = prof[dom]
+    achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    solve_bytes = sum(v["bytes"] for v in prof.values()) / 2
+    traffic = traffic_from_profiles(args.config)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS.get(args.config, args.config), "name": args.config,
+                       "leaf_cells": N, "levels": tree.levels, "mu": cfg["mu"], "rtol": args.rtol,
+                       "pcg_iters": iters[-1], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "working set > 126 MB L2 (coefficient store alone %.0f MB); no flush"
+                             % (tree.T * 512 * 16 / 1e6)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "share_of_step": d["ms"] / tot_ms if tot_ms else None,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+            "model_gbs_solve": solve_bytes / (ms * 1e-3) / 1e9,
+            "kernels": {k: {"ms_per_solve": v["ms"] / 2, "launches_per_solve": v["launches"] // 2,
+                            "gbs": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] else None}
+                        for k, v in prof.items() if v["launches"]},
+            "e2e": {"value": world * N / (ms_e2e * 1e-3), "unit": "cells/s", "h2d_bytes_per_step": 4 * N,
+                    "d2h_bytes_per_step": 4 * N, "ms_per_step": ms_e2e},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "paper_context": "RTX 4090: uniform (5-5) 256^3 = 2.41e8 cells/s (Table 1, P:L1797, M = 2^20)",
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

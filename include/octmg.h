@@ -1,0 +1,190 @@
+/*
+ * octmg.h — C ABI of the B200-native (sm_100a) matrix-free multigrid-preconditioned CG
+ * solver for  -div(beta grad p) = b  on graded adaptive octrees with cut cells.
+ *
+ * Method: arXiv 2604.18886 (Wang, Sun, Zhu), "Matrix-Free Multigrid with Algebraically
+ * Consistent Coarsening on Adaptive Octrees".  Citations "P:Lnnn" are lines of that
+ * paper's PAPER.md (section / equation / algorithm named beside each).
+ *
+ * Conventions
+ *  - Tiles are 8x8x8 cells.  At tile level l the domain has ext[a] * 2^l tiles
+ *    along axis a and the cell edge is h_l = 2^-l / 8 in units of a level-0 tile.
+ *  - Leaf-slot order (all user vectors): leaf tiles sorted by (level descending, Morton
+ *    key ascending; Morton interleaves bits with x in the lowest bit of each triple), then
+ *    cells x + 8y + 64z within a tile.  octmg_tree_export(OCTMG_EXPORT_TILES) returns that
+ *    order; slot = tile_index * 512 + cell.
+ *  - Face order: x-, x+, y-, y+, z-, z+.
+ *  - Right-hand side convention: A p = b with A ~ -div(beta grad) * V (volume-integrated,
+ *    symmetric-positive sign), Eq. 1-3.  For div(beta grad p) = f pass
+ *    b_i = -f_i V_i.
+ *  - Vectors are fp32 device arrays; dot products accumulate in fp64.
+ *  - Ownership: the library owns every internal device allocation; caller buffers are
+ *    borrowed for the duration of a call.  All device work is issued on the caller's
+ *    stream; calls are asynchronous unless stated otherwise.  A handle is not
+ *    thread-safe (one call at a time).
+ *  - Errors: every entry point returns an octmg_status; octmg_last_error() gives a
+ *    thread-local message.  No C++ exception crosses the ABI.  A failed call leaves no
+ *    handle allocated.
+ */
+#ifndef OCTMG_H
+#define OCTMG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t without including the CUDA headers; NULL = legacy default stream. */
+typedef struct CUstream_st* octmg_stream;
+
+typedef enum {
+  OCTMG_OK = 0,
+  OCTMG_E_INVALID = 1,     /* bad argument, level or coordinate out of range            */
+  OCTMG_E_OVERLAP = 2,     /* duplicate leaf tiles, or a leaf that contains another     */
+  OCTMG_E_GAP = 3,         /* leaf tiles do not cover the domain                        */
+  OCTMG_E_NOT_GRADED = 4,  /* two face-adjacent leaves differ by > 1 level     */
+  OCTMG_E_OOM = 5,         /* device allocation failed                                  */
+  OCTMG_E_CUDA = 6,        /* any other CUDA runtime error                              */
+  OCTMG_E_NCCL = 7,        /* reserved (multi-GPU)                                      */
+  OCTMG_E_NONFINITE = 8,   /* non-finite value in b or in a PCG scalar                  */
+  OCTMG_E_BREAKDOWN = 9,   /* p.Ap <= 0 in PCG; the last good iterate is kept           */
+  OCTMG_E_MAXITER = 10     /* not converged within max_iters (report.converged = 0)     */
+} octmg_status;
+
+/* Thread-local description of the last failure (never NULL). */
+const char* octmg_last_error(void);
+/* Library version string. */
+const char* octmg_version(void);
+
+typedef struct octmg_tree octmg_tree;
+typedef struct octmg_hier octmg_hier;
+
+/* A LEAF tile: level l and tile coordinates (i, j, k) at that level. */
+typedef struct {
+  int32_t level, i, j, k;
+} octmg_tile;
+
+typedef struct {
+  int32_t ext[3];      /* domain size in level-0 tiles; (1,1,1) = unit cube              */
+  uint8_t wall_bc[6];  /* per domain face x-,x+,y-,y+,z-,z+: 0 Neumann, 1 Dirichlet p=0
+                          at the centre of a virtual wall cell of the boundary cell's
+                          size (P:L328-330 ghost-fluid Dirichlet)                         */
+  int32_t grade_repair;/* must be 0: ungraded input is rejected with NOT_GRADED          */
+  int32_t rank, nranks;/* must be 0, 1 (single GPU in this release)                      */
+  void* nccl_comm;     /* must be NULL                                                   */
+} octmg_tree_desc;
+
+/*
+ * Build the octree tables on the GPU from the host list of leaf tiles (P:L548-550,
+ * "recompute the six same-level neighbors for each tile"): validates range,
+ * overlap, coverage (exact integer volume) and 2:1 face grading; sorts tiles into the
+ * canonical order; derives inner tiles (all strict ancestors of leaves), per-level
+ * segments, the 6-neighbour table (>= 0 same-level tile, -1 domain wall, -2 - c when the
+ * neighbour position is a ghost whose coarse leaf tile is c), parent and child tables.
+ * leaf_tiles_host: n entries, any order, host memory (copied).  Synchronises `stream`.
+ */
+octmg_status octmg_build_tree(const octmg_tree_desc* desc, const octmg_tile* leaf_tiles_host,
+                              int64_t n, octmg_stream stream, octmg_tree** out);
+
+#define OCTMG_MAX_LEVELS 16
+typedef struct {
+  int32_t levels;          /* L + 1 (level 0 .. L, L = finest leaf level)                 */
+  int32_t n_leaf_tiles;    /* NL; leaf tiles are tile indices [0, NL)                     */
+  int32_t n_inner_tiles;   /* NI; inner tiles are tile indices [NL, NL + NI)              */
+  int64_t n_leaf_cells;    /* NL * 512 = length of every user vector                      */
+  int32_t leaf_begin[OCTMG_MAX_LEVELS], leaf_count[OCTMG_MAX_LEVELS];
+  int32_t inner_begin[OCTMG_MAX_LEVELS], inner_count[OCTMG_MAX_LEVELS];
+  int32_t n_ghost_layers;  /* T-junction (+face toward a ghost) coefficient layers        */
+} octmg_tree_info;
+octmg_status octmg_tree_info_get(const octmg_tree* tree, octmg_tree_info* out);
+
+/* Copy canonical tables to host (bit-exact contract; int32):
+ *  TILES  (NL+NI) x 4 (level,i,j,k)   NBR (NL+NI) x 6   PARENT (NL+NI) (-1 at level 0)
+ *  CHILD  NI x 8 (octant dx + 2dy + 4dz)                 bytes must equal the size. */
+enum { OCTMG_EXPORT_TILES = 0, OCTMG_EXPORT_NBR = 1, OCTMG_EXPORT_PARENT = 2, OCTMG_EXPORT_CHILD = 3 };
+octmg_status octmg_tree_export(const octmg_tree* tree, int32_t what, void* host_dst, size_t bytes);
+
+typedef struct {
+  float alpha;          /* restriction scaling, R = P^T / alpha; 2   */
+  float beta;           /* overshoot, applied at restriction (Alg. 4 line 10); 2   */
+  int32_t mu;           /* cycle index: 1 V-cycle, 2 W-cycle                   */
+  int32_t nu_pre;       /* RBGS iterations (red+black) before coarsening: 2        */
+  int32_t nu_post;      /* RBGS iterations after (opposite colour order): 2                 */
+  int32_t nu_coarsest;  /* RBGS iterations at level 0, two opposite-order halves: 10        */
+} octmg_mg_params;
+
+/*
+ * Assemble the compact matrix-free coefficients (c, c_x-, c_y-, c_z-) of every leaf cell
+ * (Eq. 3; ghost-fluid kinds; T-junction faces, Eqs. 9-10,
+ * P:L641-648) and coarsen every inner cell bottom-up with Alg. 3 (with the
+ * activity test on the off-diagonal branch so that it equals R A P over fluid DOFs).
+ *  kind:      device u8[N], 0 fluid, 1 Dirichlet (p = 0), 2 Neumann (solid)
+ *  face_beta: device f32[6][N] or NULL (= 1): beta on each face of each leaf cell
+ *  face_frac: device f32[6][N] or NULL (= 1): fluid area fraction S / h^2 of each face
+ *  Face conductance kappa = beta * frac * h.  Authority: the +side cell's -face entry on
+ *  same-level faces, the fine side's entries on T-junction faces, the cell's own entry
+ *  on domain faces.  params: NULL = defaults above.  Inputs are read during the call only.
+ */
+octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const float* face_beta,
+                                   const float* face_frac, const octmg_mg_params* params,
+                                   octmg_stream stream, octmg_hier** out);
+
+/* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
+ * in tile order.  Synchronises `stream` of the last call. */
+octmg_status octmg_hier_export_coefs(const octmg_hier* h, float* host_dst, size_t bytes);
+
+/* y = A x, the composite operator over all leaf cells (T-junction ghosts, Eq. 12,
+ * P:L661-665; inner neighbour value = mean of its active children).  x, y are
+ * device f32[N]; y is 0 on inactive cells; x's inactive entries are ignored. */
+octmg_status octmg_apply(octmg_hier* h, const float* x, float* y, octmg_stream stream);
+
+/* u = M b: one FAS-style mu-cycle (Alg. 4) from a zero initial guess.
+ * b, u are device f32[N]; b's inactive entries are ignored; u is 0 on inactive cells. */
+octmg_status octmg_vcycle(octmg_hier* h, const float* b, float* u, octmg_stream stream);
+
+typedef struct {
+  double rtol;          /* stop when ||r||_2 <= rtol * ||r_0||_2 (active cells); 1e-6    */
+  int32_t max_iters;    /* 200                                                            */
+  int32_t nullspace;    /* -1 auto (no Dirichlet wall or cell), 0 off, 1 project residual
+                           to zero mean after Alg. 1 lines 4 and 11              */
+} octmg_solve_params;
+
+typedef struct {
+  int32_t iters;        /* PCG iterations performed (= A applications = M applications)  */
+  int32_t converged;
+  double rel_residual;  /* ||r_k|| / ||r_0|| (recursive residual)                         */
+  double bnorm;         /* ||r_0||                                                        */
+  int32_t status;       /* octmg_status of the solve                                      */
+  double* history;      /* optional host array: relative residual after each iteration   */
+  int32_t history_cap;
+  int64_t kernel_launches; /* device kernels launched by this solve (graph nodes counted) */
+} octmg_solve_report;
+
+/*
+ * Alg. 1: x0 = 0, r0 = b (masked to active cells, projected if nullspace),
+ * z = M r, CG recurrences with fp64 scalars kept on the device; one 8-byte device->host
+ * read per iteration for the stopping test.  b (read-only) and x (overwritten) are
+ * device f32[N].  Synchronises `stream` before returning.  report may be NULL.
+ */
+octmg_status octmg_pcg_solve(octmg_hier* h, const float* b, float* x, const octmg_solve_params* params,
+                             octmg_solve_report* report, octmg_stream stream);
+
+/* Per-kernel-class device time of the work issued since the last reset while profiling
+ * is on (CUDA events bracketing each launch on the launch stream; CUDA-graph replay is
+ * disabled while profiling), with the launch count and the ALGORITHMIC bytes those
+ * launches must move at minimum (e.g. 28 B per cell for an RBGS
+ * pass: read u, b, the 16-byte coefficient record, write u).  names/ms/counts/bytes:
+ * arrays of cap entries (any may be NULL); *n = number of classes.  Synchronises. */
+octmg_status octmg_profile_enable(octmg_hier* h, int32_t on);
+octmg_status octmg_profile_read(octmg_hier* h, const char** names, double* ms, int64_t* counts,
+                                double* bytes, int32_t cap, int32_t* n);
+
+void octmg_hier_destroy(octmg_hier* h);
+void octmg_tree_destroy(octmg_tree* tree);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCTMG_H */

@@ -1,0 +1,7 @@
+"""B200-native (sm_100a) matrix-free multigrid-preconditioned CG on adaptive octrees
+(arXiv 2604.18886).  The compute path is liboctmg.so (hand-written CUDA); this package is
+its build script and a thin ctypes binding."""
+from .octmg import (  # noqa: F401
+    Tree, Hierarchy, OctmgError, octmg_build_tree, octmg_setup_hierarchy, octmg_apply, octmg_vcycle,
+    octmg_pcg_solve, version, lib, ABI_SYMBOLS,
+)

@@ -1,0 +1,233 @@
+// Internal declarations of the octmg CUDA library (sm_100a).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/octmg.h"
+
+namespace octmg {
+
+constexpr int TB = 8;          // tile edge
+constexpr int TB3 = 512;       // cells per tile
+constexpr int MAXL = OCTMG_MAX_LEVELS - 1;
+constexpr int KEY_LEVEL_SHIFT = 58;  // key = (MAXL - level) << 58 | morton(i,j,k) (19 bits/axis)
+
+// ------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------
+void set_error(const std::string& msg);
+octmg_status cuda_status(cudaError_t e, const char* what);
+
+#define OCTMG_CUDA(call)                                                   \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) return ::octmg::cuda_status(e_, #call);         \
+  } while (0)
+
+#define OCTMG_TRY(call)                                                    \
+  do {                                                                     \
+    octmg_status s_ = (call);                                              \
+    if (s_ != OCTMG_OK) return s_;                                         \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// Tree (device tables + host metadata)
+// ------------------------------------------------------------------------------------
+struct Tree {
+  int ext[3] = {1, 1, 1};
+  uint8_t wall[6] = {1, 1, 1, 1, 1, 1};
+  int L = 0;
+  int NL = 0, NI = 0, T = 0;
+  int lb[MAXL + 1] = {}, lc[MAXL + 1] = {}, ib[MAXL + 1] = {}, ic[MAXL + 1] = {};
+  int n_glayers = 0;
+  // device
+  uint64_t* leaf_keys = nullptr;   // [NL] sorted
+  uint64_t* inner_keys = nullptr;  // [NI] sorted
+  int4* tile = nullptr;            // [T] (level, i, j, k)
+  int* nbr = nullptr;              // [T*6]
+  int* parent = nullptr;           // [T]
+  int* child = nullptr;            // [NI*8]
+  int* glayer = nullptr;           // [NL*3] layer index of the +x/+y/+z ghost face, or -1
+  std::vector<void*> allocs;
+  ~Tree();
+};
+
+// A field over all tiles, stored as a leaf part and an inner part (either may alias a
+// caller / PCG vector).  Tile t's 512 cells start at leaf + t*512 (t < NL) or
+// inner + (t-NL)*512.
+struct Fld {
+  float* leaf;
+  float* inner;
+};
+
+__device__ __forceinline__ float* tptr(const Fld& f, int t, int NL) {
+  return t < NL ? f.leaf + (size_t)t * TB3 : f.inner + (size_t)(t - NL) * TB3;
+}
+
+// PCG scalars, device resident (fp64)
+struct Scalars {
+  double rho;      // (r, z)
+  double sigma;    // (p, Ap)
+  double alpha;
+  double beta;
+  double rr;       // ||r||^2 (after projection if enabled)
+  double rsum;     // sum of r over active cells (null-space projection)
+  double mean;     // projection mean
+  double n_active; // number of active leaf cells
+  int flags;       // bit0: breakdown (sigma <= 0 or non-finite); bit1: non-finite rho/alpha
+  int pad;
+};
+
+// Kernel classes for profiling
+enum KClass {
+  KC_PASS = 0, KC_PASS_ZERO, KC_PASS_FAS, KC_PASS_PROLONG, KC_RESTRICT, KC_COARSEST,
+  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_COUNT
+};
+extern const char* kclass_name[KC_COUNT];
+
+struct Hier;
+
+// launch helpers implemented in kernels.cu
+struct PassArgs {
+  const int4* tile;
+  const int* nbr;
+  const int* parent;
+  const float4* coef;
+  const float* glayer_val;
+  const int* glayer;
+  Fld uin, uout;        // level-l buffers (read / write)
+  Fld ucoarse;          // level-(l-1) rest buffer (ghost sources, prolongation)
+  const float* ustar;   // inner-indexed u* (prolongation)
+  Fld b;                // leaf = PCG residual r, inner = FAS rhs
+  int NL;
+  int loff, nl, ioff, ni;
+  int colour;
+};
+
+enum PassMode { PM_PLAIN = 0, PM_ZERO = 1, PM_FAS = 2, PM_PROLONG = 3 };
+
+void launch_pass(int mode, const PassArgs& a, cudaStream_t s);
+
+struct RestrictArgs {
+  const int4* tile;
+  const int* nbr;
+  const int* parent;
+  const float4* coef;
+  const float* glayer_val;
+  const int* glayer;
+  Fld u;                // level l (rest buffer)
+  Fld ucoarse;          // level l-1 (rest buffer): receives u* on inner cells
+  float* ustar;         // inner-indexed
+  Fld b;                // level l rhs: leaf = r, inner = FAS rhs; receives beta * R r
+  float bscale;         // beta (overshoot at restriction, Alg. 4 line 10)
+  float alpha_div;      // alpha (R = P^T / alpha)
+  int NL;
+  int loff, nl, ioff, ni;
+};
+void launch_restrict(const RestrictArgs& a, cudaStream_t s);
+
+struct ApplyArgs {
+  const int4* tile;
+  const int* nbr;
+  const int* child;
+  const float4* coef;
+  const float* glayer_val;
+  const int* glayer;
+  const float* z;       // direction source (user x for octmg_apply)
+  const float* pold;    // previous p (nullptr: beta = 0)
+  float* pnew;          // written p = z + beta p (nullptr: not written)
+  float* q;             // A p
+  double* partial;      // per-tile fp64 partial of p.q (nullptr: no dot)
+  unsigned* counter;
+  Scalars* sc;          // beta read from here; sigma/alpha written by the last block
+  int NL;
+  int use_beta;
+};
+void launch_apply(const ApplyArgs& a, cudaStream_t s);
+
+// vector kernels (PCG)
+void launch_init(const float* b, const float4* coef, float* r, float* x, int64_t n, double* partial,
+                 unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
+void launch_update(float* x, float* r, const float* p, const float* q, int64_t n, double* partial,
+                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
+void launch_project(float* r, const float4* coef, int64_t n, double* partial, unsigned* counter,
+                    Scalars* sc, cudaStream_t s, int grid);
+void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, unsigned* counter,
+                   Scalars* sc, int first, cudaStream_t s, int grid);
+void launch_mask_copy(const float* src, const float4* coef, float* dst, int64_t n, cudaStream_t s);
+
+// setup kernels (setup.cu)
+struct SetupArgs;
+octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
+                                 cudaStream_t s);
+octmg_status coarsen_all(Hier& h, cudaStream_t s);
+
+// tree build (tree.cu)
+octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, int64_t n, cudaStream_t s,
+                        Tree* t);
+
+// ------------------------------------------------------------------------------------
+// Hierarchy (coefficients + multigrid work buffers + PCG state)
+// ------------------------------------------------------------------------------------
+struct Op {
+  int kind;   // 0 pass, 1 restrict, 2 memset
+  int level;
+  int mode;
+  int colour;
+  int in_buf, out_buf;
+};
+
+struct Hier {
+  Tree* tree = nullptr;
+  octmg_mg_params prm{};
+  float4* coef = nullptr;        // [T*512] (c, cxm, cym, czm)
+  float* glayer_val = nullptr;   // [n_glayers*64]
+  // multigrid buffers
+  float* z = nullptr;            // [NL*512] leaf part of u (buffer A) = M output
+  float* zB = nullptr;           // [NL*512] leaf part of buffer B
+  float* uinA = nullptr;         // [NI*512]
+  float* uinB = nullptr;
+  float* binner = nullptr;       // [NI*512]
+  float* ustar = nullptr;        // [NI*512]
+  float* r = nullptr;            // [NL*512] PCG residual = leaf part of the cycle rhs
+  // PCG
+  float* p0 = nullptr;
+  float* p1 = nullptr;
+  float* q = nullptr;
+  double* partial = nullptr;     // reduction partials
+  size_t n_partial = 0;
+  unsigned* counter = nullptr;   // last-block counters (one per reduction slot)
+  Scalars* sc = nullptr;         // device scalars
+  Scalars* sc_host = nullptr;    // pinned mirror
+  double n_active = 0;
+  int any_dirichlet = 0;
+  // schedule of one preconditioner application
+  std::vector<Op> ops;
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int64_t launches = 0;
+  // profiling
+  bool profiling = false;
+  struct Ev { int cls; double bytes; cudaEvent_t a, b; };
+  std::vector<Ev> events;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+  double prof_ms[KC_COUNT] = {};
+  int64_t prof_cnt[KC_COUNT] = {};
+  double prof_bytes[KC_COUNT] = {};
+  std::vector<void*> allocs;
+  ~Hier();
+};
+
+}  // namespace octmg
+
+struct octmg_tree {
+  octmg::Tree t;
+};
+struct octmg_hier {
+  octmg::Hier h;
+};

@@ -1,0 +1,270 @@
+// Coefficient setup: leaf assembly (Eq. 3; ghost-fluid kinds P:L318-337;
+// T-junction faces Eqs. 9-10) and Galerkin coarsening (Alg. 3)
+// of the compact record (c, c_x-, c_y-, c_z-) held as one float4 per cell.
+#include "octmg_internal.cuh"
+
+namespace octmg {
+
+namespace {
+
+enum { NB_WALL = 0, NB_LEAF = 1, NB_INNER = 2, NB_GHOST = 3 };
+enum { KF = 0, KD = 1, KN = 2 };
+
+struct NbRef {
+  int what, tile, off;
+};
+
+__device__ __forceinline__ int loff(int x, int y, int z) { return x + 8 * y + 64 * z; }
+
+// neighbour of cell (x,y,z) of tile t (tile coords tv) across face f
+__device__ __forceinline__ NbRef nb_ref(const int* nbr, int4 tv, int t, int NL, int x, int y, int z, int f) {
+  int a = f >> 1, s = (f & 1) ? 1 : -1;
+  int c[3] = {x, y, z};
+  c[a] += s;
+  if (c[a] >= 0 && c[a] < 8) return {t < NL ? NB_LEAF : NB_INNER, t, loff(c[0], c[1], c[2])};
+  int n = nbr[6 * t + f];
+  if (n == -1) return {NB_WALL, -1, -1};
+  if (n >= 0) {
+    c[a] &= 7;
+    return {n < NL ? NB_LEAF : NB_INNER, n, loff(c[0], c[1], c[2])};
+  }
+  // ghost: the level-(l-1) leaf cell containing the fine neighbour position
+  int g[3] = {tv.y * 8 + x, tv.z * 8 + y, tv.w * 8 + z};
+  g[a] += s;
+  return {NB_GHOST, -2 - n, loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7)};
+}
+
+struct WIn {
+  const float* beta;  // [6][N] or null
+  const float* frac;  // [6][N] or null
+  size_t N;
+  __device__ __forceinline__ float w(int f, size_t i) const {
+    float v = 1.0f;
+    if (beta) v = beta[(size_t)f * N + i];
+    if (frac) v = beta ? v * frac[(size_t)f * N + i] : frac[(size_t)f * N + i];
+    return v;
+  }
+};
+
+// the 4 fine sub-cells (leaf cells at level l+1) of the inner cell nb that touch the
+// fine-to-coarse face f of our cell; order dz, dy, dx as in the oracle
+__device__ __forceinline__ void fine_subs(const int* child, int NL, const NbRef& nb, int f, size_t out[4]) {
+  int xn = nb.off & 7, yn = (nb.off >> 3) & 7, zn = nb.off >> 6;
+  int ct = child[8 * (nb.tile - NL) + (xn >> 2) + 2 * (yn >> 2) + 4 * (zn >> 2)];
+  int a = f >> 1;
+  int facing = (f & 1) ? 0 : 1;
+  int k = 0;
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        int d[3] = {dx, dy, dz};
+        if (d[a] != facing) continue;
+        out[k++] = (size_t)ct * TB3 + loff((2 * xn + dx) & 7, (2 * yn + dy) & 7, (2 * zn + dz) & 7);
+      }
+}
+
+struct AsmArgs {
+  const int4* tile;
+  const int* nbr;
+  const int* child;
+  const int* glayer;
+  const uint8_t* kind;
+  WIn w;
+  float4* coef;
+  float* glayer_val;
+  int NL;
+  uint8_t wall[6];
+};
+
+// pass 1: diagonal of every leaf cell from geometry (SURVEY c-2)
+__global__ __launch_bounds__(256) void k_assemble_diag(AsmArgs a) {
+  int t = blockIdx.x;
+  int4 tv = a.tile[t];
+  float h = ldexpf(1.0f, -tv.x) * 0.125f;
+  for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
+    int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    size_t i = (size_t)t * TB3 + off;
+    float c = 0.0f;
+    if (a.kind[i] == KF) {
+      for (int f = 0; f < 6; ++f) {
+        NbRef nb = nb_ref(a.nbr, tv, t, a.NL, x, y, z, f);
+        if (nb.what == NB_WALL) {
+          if (a.wall[f]) c += a.w.w(f, i) * h;
+        } else if (nb.what == NB_LEAF) {
+          size_t j = (size_t)nb.tile * TB3 + nb.off;
+          if (a.kind[j] != KN) c += ((f & 1) ? a.w.w(f ^ 1, j) : a.w.w(f, i)) * h;
+        } else if (nb.what == NB_INNER) {
+          size_t sub[4];
+          fine_subs(a.child, a.NL, nb, f, sub);
+          for (int k = 0; k < 4; ++k)
+            if (a.kind[sub[k]] != KN) c += 0.5f * a.w.w(f ^ 1, sub[k]) * (0.5f * h);
+        } else {
+          size_t C = (size_t)nb.tile * TB3 + nb.off;
+          if (a.kind[C] != KN) c += a.w.w(f, i) * h;
+        }
+      }
+    }
+    a.coef[i] = make_float4(c, 0.f, 0.f, 0.f);
+  }
+}
+
+// pass 2: -face off-diagonals and the +face ghost-layer coefficients
+__global__ __launch_bounds__(256) void k_assemble_offdiag(AsmArgs a) {
+  int t = blockIdx.x;
+  int4 tv = a.tile[t];
+  float h = ldexpf(1.0f, -tv.x) * 0.125f;
+  for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
+    int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    size_t i = (size_t)t * TB3 + off;
+    if (a.kind[i] == KN) continue;  // Neumann: all-zero record (already zero)
+    float cm[3];
+    for (int ax = 0; ax < 3; ++ax) {
+      int f = 2 * ax;
+      NbRef nb = nb_ref(a.nbr, tv, t, a.NL, x, y, z, f);
+      float v = 0.0f;
+      if (nb.what == NB_LEAF) {
+        if (a.kind[(size_t)nb.tile * TB3 + nb.off] != KN) v = -a.w.w(f, i) * h;
+      } else if (nb.what == NB_INNER) {
+        size_t sub[4];
+        fine_subs(a.child, a.NL, nb, f, sub);
+        float acc = 0.0f;
+        for (int k = 0; k < 4; ++k)
+          if (a.coef[sub[k]].x != 0.0f) acc += a.w.w(f ^ 1, sub[k]) * (0.5f * h);
+        v = -0.5f * acc;
+      } else if (nb.what == NB_GHOST) {
+        if (a.kind[(size_t)nb.tile * TB3 + nb.off] != KN) v = -a.w.w(f, i) * h;
+      }
+      cm[ax] = v;
+      // +face toward a ghost: coefficient of the ghost cell's -face (c_{6,x-})
+      int cc[3] = {x, y, z};
+      if (cc[ax] == 7) {
+        int gl = a.glayer[3 * t + ax];
+        if (gl >= 0) {
+          NbRef g = nb_ref(a.nbr, tv, t, a.NL, x, y, z, f + 1);
+          float gv = a.kind[(size_t)g.tile * TB3 + g.off] != KN ? -a.w.w(f + 1, i) * h : 0.0f;
+          int p = ax == 0 ? y + 8 * z : (ax == 1 ? x + 8 * z : x + 8 * y);
+          a.glayer_val[(size_t)gl * 64 + p] = gv;
+        }
+      }
+    }
+    float4 r = a.coef[i];
+    r.y = cm[0]; r.z = cm[1]; r.w = cm[2];
+    a.coef[i] = r;
+  }
+}
+
+struct CoarsenArgs {
+  const int4* tile;
+  const int* nbr;
+  const int* child;
+  float4* coef;
+  int NL;
+  int toff;  // first inner tile of level l-1
+  float alpha;
+};
+
+__device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
+
+// Alg. 3 with the activity test on the off-diagonal branch (SURVEY c-3)
+__global__ __launch_bounds__(256) void k_coarsen(CoarsenArgs a) {
+  int P = a.toff + blockIdx.x;
+  const int* ch8 = a.child + 8 * (P - a.NL);
+  for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
+    int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    int ct = ch8[(x >> 2) + 2 * (y >> 2) + 4 * (z >> 2)];
+    int4 ctv = a.tile[ct];
+    float cI = 0.0f, cIm[3] = {0.f, 0.f, 0.f};
+    int cnt = 0;
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          int d[3] = {dx, dy, dz};
+          int cx[3] = {(2 * x + dx) & 7, (2 * y + dy) & 7, (2 * z + dz) & 7};
+          float4 ci = a.coef[(size_t)ct * TB3 + loff(cx[0], cx[1], cx[2])];
+          bool act = ci.x != 0.0f;
+          if (act) { cnt++; cI += ci.x / a.alpha; }
+          for (int ax = 0; ax < 3; ++ax) {
+            if (d[ax] == 1) {
+              int sx[3] = {cx[0], cx[1], cx[2]};
+              sx[ax] -= 1;
+              bool sact = a.coef[(size_t)ct * TB3 + loff(sx[0], sx[1], sx[2])].x != 0.0f;
+              if (act && sact) cI += (2.0f / a.alpha) * comp(ci, ax);
+            } else {
+              NbRef nb = nb_ref(a.nbr, ctv, ct, a.NL, cx[0], cx[1], cx[2], 2 * ax);
+              bool nact = nb.what != NB_WALL && a.coef[(size_t)nb.tile * TB3 + nb.off].x != 0.0f;
+              if (act && nact) cIm[ax] += comp(ci, ax) / a.alpha;
+            }
+          }
+        }
+    a.coef[(size_t)P * TB3 + off] = make_float4(cnt ? cI : 0.0f, cIm[0], cIm[1], cIm[2]);
+  }
+}
+
+__global__ void k_count_active(const float4* coef, int64_t n, unsigned long long* cnt) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += coef[i].x != 0.0f;
+  for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
+__global__ void k_any_dirichlet(const uint8_t* kind, int64_t n, int* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (kind[i] == KD) { *flag = 1; return; }
+}
+
+}  // namespace
+
+octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
+                                 cudaStream_t s) {
+  Tree& T = *h.tree;
+  AsmArgs a;
+  a.tile = T.tile;
+  a.nbr = T.nbr;
+  a.child = T.child;
+  a.glayer = T.glayer;
+  a.kind = kind;
+  a.w = WIn{fbeta, ffrac, (size_t)T.NL * TB3};
+  a.coef = h.coef;
+  a.glayer_val = h.glayer_val;
+  a.NL = T.NL;
+  for (int f = 0; f < 6; ++f) a.wall[f] = T.wall[f];
+  if (T.n_glayers) OCTMG_CUDA(cudaMemsetAsync(h.glayer_val, 0, (size_t)T.n_glayers * 64 * sizeof(float), s));
+  k_assemble_diag<<<T.NL, 256, 0, s>>>(a);
+  k_assemble_offdiag<<<T.NL, 256, 0, s>>>(a);
+  OCTMG_CUDA(cudaGetLastError());
+  // active leaf-cell count and whether any Dirichlet kind exists (null-space auto)
+  unsigned long long* d_cnt;
+  int* d_flag;
+  OCTMG_CUDA(cudaMallocAsync(&d_cnt, sizeof(unsigned long long) + sizeof(int) * 2, s));
+  d_flag = (int*)(d_cnt + 1);
+  OCTMG_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) + sizeof(int) * 2, s));
+  int64_t N = (int64_t)T.NL * TB3;
+  k_count_active<<<592, 256, 0, s>>>(h.coef, N, d_cnt);
+  k_any_dirichlet<<<592, 256, 0, s>>>(kind, N, d_flag);
+  unsigned long long cnt = 0;
+  int flag = 0;
+  OCTMG_CUDA(cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+  OCTMG_CUDA(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  OCTMG_CUDA(cudaFreeAsync(d_cnt, s));
+  OCTMG_CUDA(cudaStreamSynchronize(s));
+  h.n_active = (double)cnt;
+  int wall_d = 0;
+  for (int f = 0; f < 6; ++f) wall_d |= T.wall[f];
+  h.any_dirichlet = flag || wall_d;
+  return OCTMG_OK;
+}
+
+octmg_status coarsen_all(Hier& h, cudaStream_t s) {
+  Tree& T = *h.tree;
+  for (int l = T.L; l >= 1; --l) {
+    int lc = l - 1;
+    if (T.ic[lc] == 0) continue;
+    CoarsenArgs a{T.tile, T.nbr, T.child, h.coef, T.NL, T.ib[lc], h.prm.alpha};
+    k_coarsen<<<T.ic[lc], 256, 0, s>>>(a);
+  }
+  OCTMG_CUDA(cudaGetLastError());
+  return OCTMG_OK;
+}
+
+}  // namespace octmg

@@ -1,0 +1,245 @@
+"""Thin ctypes binding of the C ABI in include/octmg.h (argument marshalling only).
+
+Every step of the solver runs in liboctmg.so (hand-written CUDA for sm_100a).  There is
+no CPU fallback: if the shared object is missing, loading fails loudly.  PyTorch supplies
+device memory (tensor.data_ptr()) and the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from ._build import LIB
+
+STATUS = {0: "OK", 1: "INVALID", 2: "OVERLAP", 3: "GAP", 4: "NOT_GRADED", 5: "OOM", 6: "CUDA",
+          7: "NCCL", 8: "NONFINITE", 9: "BREAKDOWN", 10: "MAXITER"}
+MAX_LEVELS = 16
+
+
+class OctmgError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = STATUS.get(status, status)
+        super().__init__(f"octmg {self.status}: {msg}")
+
+
+class TreeDesc(C.Structure):
+    _fields_ = [("ext", C.c_int32 * 3), ("wall_bc", C.c_uint8 * 6), ("grade_repair", C.c_int32),
+                ("rank", C.c_int32), ("nranks", C.c_int32), ("nccl_comm", C.c_void_p)]
+
+
+class TreeInfo(C.Structure):
+    _fields_ = [("levels", C.c_int32), ("n_leaf_tiles", C.c_int32), ("n_inner_tiles", C.c_int32),
+                ("n_leaf_cells", C.c_int64),
+                ("leaf_begin", C.c_int32 * MAX_LEVELS), ("leaf_count", C.c_int32 * MAX_LEVELS),
+                ("inner_begin", C.c_int32 * MAX_LEVELS), ("inner_count", C.c_int32 * MAX_LEVELS),
+                ("n_ghost_layers", C.c_int32)]
+
+
+class MGParams(C.Structure):
+    _fields_ = [("alpha", C.c_float), ("beta", C.c_float), ("mu", C.c_int32), ("nu_pre", C.c_int32),
+                ("nu_post", C.c_int32), ("nu_coarsest", C.c_int32)]
+
+
+class SolveParams(C.Structure):
+    _fields_ = [("rtol", C.c_double), ("max_iters", C.c_int32), ("nullspace", C.c_int32)]
+
+
+class SolveReport(C.Structure):
+    _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
+                ("bnorm", C.c_double), ("status", C.c_int32), ("history", C.POINTER(C.c_double)),
+                ("history_cap", C.c_int32), ("kernel_launches", C.c_int64)]
+
+
+EXPORT_TILES, EXPORT_NBR, EXPORT_PARENT, EXPORT_CHILD = 0, 1, 2, 3
+
+# every symbol include/octmg.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_tree_info_get",
+               "octmg_tree_export", "octmg_setup_hierarchy", "octmg_hier_export_coefs", "octmg_apply",
+               "octmg_vcycle", "octmg_pcg_solve", "octmg_profile_enable", "octmg_profile_read",
+               "octmg_hier_destroy", "octmg_tree_destroy"]
+
+_lib = None
+
+
+def lib():
+    """Load liboctmg.so (built by __graft_entry__.build()); raise if it is absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB)
+        P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
+        L.octmg_last_error.restype = C.c_char_p
+        L.octmg_version.restype = C.c_char_p
+        L.octmg_build_tree.argtypes = [C.POINTER(TreeDesc), P, I64, P, C.POINTER(P)]
+        L.octmg_tree_info_get.argtypes = [P, C.POINTER(TreeInfo)]
+        L.octmg_tree_export.argtypes = [P, I32, P, C.c_size_t]
+        L.octmg_setup_hierarchy.argtypes = [P, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
+        L.octmg_hier_export_coefs.argtypes = [P, P, C.c_size_t]
+        L.octmg_apply.argtypes = [P, P, P, P]
+        L.octmg_vcycle.argtypes = [P, P, P, P]
+        L.octmg_pcg_solve.argtypes = [P, P, P, C.POINTER(SolveParams), C.POINTER(SolveReport), P]
+        L.octmg_profile_enable.argtypes = [P, I32]
+        L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
+        L.octmg_hier_destroy.argtypes = [P]
+        L.octmg_tree_destroy.argtypes = [P]
+        for name in ABI_SYMBOLS[2:12]:
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st):
+    if st != 0:
+        raise OctmgError(st, lib().octmg_last_error().decode())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if hasattr(stream, "cuda_stream"):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(stream)
+
+
+def _ptr(t):
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def version() -> str:
+    return lib().octmg_version().decode()
+
+
+class Tree:
+    """octmg_build_tree: graded leaf tiles (host int array (n,4): level,i,j,k)."""
+
+    def __init__(self, tiles, ext=(1, 1, 1), wall_bc=(1, 1, 1, 1, 1, 1), stream=None):
+        t = np.ascontiguousarray(np.asarray(tiles, dtype=np.int32).reshape(-1, 4))
+        d = TreeDesc()
+        for a in range(3):
+            d.ext[a] = int(ext[a])
+        for f in range(6):
+            d.wall_bc[f] = int(wall_bc[f])
+        d.grade_repair, d.rank, d.nranks, d.nccl_comm = 0, 0, 1, None
+        h = C.c_void_p()
+        _check(lib().octmg_build_tree(C.byref(d), t.ctypes.data_as(C.c_void_p), len(t), _stream(stream),
+                                      C.byref(h)))
+        self._h = h
+        info = TreeInfo()
+        _check(lib().octmg_tree_info_get(self._h, C.byref(info)))
+        self.levels = info.levels
+        self.L = info.levels - 1
+        self.NL = info.n_leaf_tiles
+        self.NI = info.n_inner_tiles
+        self.T = self.NL + self.NI
+        self.N = int(info.n_leaf_cells)
+        self.leaf_begin = np.array(info.leaf_begin[:self.levels])
+        self.leaf_count = np.array(info.leaf_count[:self.levels])
+        self.inner_begin = np.array(info.inner_begin[:self.levels])
+        self.inner_count = np.array(info.inner_count[:self.levels])
+        self.n_ghost_layers = info.n_ghost_layers
+
+    def export(self, what):
+        shape = {EXPORT_TILES: (self.T, 4), EXPORT_NBR: (self.T, 6), EXPORT_PARENT: (self.T,),
+                 EXPORT_CHILD: (self.NI, 8)}[what]
+        out = np.zeros(shape, dtype=np.int32)
+        _check(lib().octmg_tree_export(self._h, what, out.ctypes.data_as(C.c_void_p), out.nbytes))
+        return out
+
+    def tables(self):
+        return dict(tiles=self.export(EXPORT_TILES), nbr=self.export(EXPORT_NBR),
+                    parent=self.export(EXPORT_PARENT), child=self.export(EXPORT_CHILD))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().octmg_tree_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+class Hierarchy:
+    """octmg_setup_hierarchy + the solver calls.  Device tensors (torch, cuda) in and out."""
+
+    def __init__(self, tree: Tree, kind, face_beta=None, face_frac=None, alpha=2.0, beta=2.0, mu=1,
+                 nu_pre=2, nu_post=2, nu_coarsest=10, stream=None):
+        self.tree = tree
+        p = MGParams(alpha, beta, mu, nu_pre, nu_post, nu_coarsest)
+        h = C.c_void_p()
+        _check(lib().octmg_setup_hierarchy(tree._h, _ptr(kind), _ptr(face_beta), _ptr(face_frac), C.byref(p),
+                                           _stream(stream), C.byref(h)))
+        self._h = h
+        self.N = tree.N
+
+    def apply(self, x, y, stream=None):
+        _check(lib().octmg_apply(self._h, _ptr(x), _ptr(y), _stream(stream)))
+
+    def vcycle(self, b, u, stream=None):
+        _check(lib().octmg_vcycle(self._h, _ptr(b), _ptr(u), _stream(stream)))
+
+    def pcg_solve(self, b, x, rtol=1e-6, max_iters=200, nullspace=-1, history_cap=256, stream=None,
+                  raise_on_error=True):
+        prm = SolveParams(rtol, max_iters, nullspace)
+        hist = (C.c_double * max(history_cap, 1))()
+        rep = SolveReport()
+        rep.history = C.cast(hist, C.POINTER(C.c_double))
+        rep.history_cap = history_cap
+        st = lib().octmg_pcg_solve(self._h, _ptr(b), _ptr(x), C.byref(prm), C.byref(rep), _stream(stream))
+        out = dict(iters=rep.iters, converged=bool(rep.converged), rel_residual=rep.rel_residual,
+                   bnorm=rep.bnorm, status=STATUS.get(st, st), kernel_launches=int(rep.kernel_launches),
+                   history=np.array(hist[:min(rep.iters, history_cap)]))
+        if raise_on_error and st not in (0, 10):
+            _check(st)
+        return out
+
+    def export_coefs(self):
+        out = np.zeros((self.tree.T * 512, 4), dtype=np.float32)
+        _check(lib().octmg_hier_export_coefs(self._h, out.ctypes.data_as(C.c_void_p), out.nbytes))
+        return out
+
+    def profile(self, on: bool):
+        _check(lib().octmg_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self):
+        cap = 32
+        names = (C.c_char_p * cap)()
+        ms = (C.c_double * cap)()
+        cnt = (C.c_int64 * cap)()
+        byt = (C.c_double * cap)()
+        n = C.c_int32()
+        _check(lib().octmg_profile_read(self._h, C.cast(names, C.c_void_p), C.cast(ms, C.c_void_p),
+                                        C.cast(cnt, C.c_void_p), C.cast(byt, C.c_void_p), cap, C.byref(n)))
+        return {names[k].decode(): dict(ms=ms[k], launches=int(cnt[k]), bytes=byt[k]) for k in range(n.value)}
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().octmg_hier_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+# C-ABI names as module-level functions (same names as include/octmg.h)
+def octmg_build_tree(tiles, ext=(1, 1, 1), wall_bc=(1, 1, 1, 1, 1, 1), stream=None) -> Tree:
+    return Tree(tiles, ext, wall_bc, stream)
+
+
+def octmg_setup_hierarchy(tree, kind, face_beta=None, face_frac=None, stream=None, **mg) -> Hierarchy:
+    return Hierarchy(tree, kind, face_beta, face_frac, stream=stream, **mg)
+
+
+def octmg_apply(h: Hierarchy, x, y, stream=None):
+    h.apply(x, y, stream)
+
+
+def octmg_vcycle(h: Hierarchy, b, u, stream=None):
+    h.vcycle(b, u, stream)
+
+
+def octmg_pcg_solve(h: Hierarchy, b, x, **kw):
+    return h.pcg_solve(b, x, **kw)

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Bars (BASELINE north_star): tree/neighbour/level tables bit-exact; coefficients
+within fp32 rounding; apply <= 1e-5 relative L2; solution <= 1e-5 relative L2 at relative
+residual 1e-6 with iteration counts within +-1."""
+import numpy as np
+import pytest
+
+from octgen import make_config, sphere_band_tiles, uniform_tiles, canonical_order, octant_tiles
+from oracle.oracle import Oracle
+from tests.helpers import random_graded_tree
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def om():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2604_18886_b200._build import build_library
+    build_library()
+    import paper_2604_18886_b200 as m
+    return m
+
+
+DEV = "cuda:0"
+SMALL = ["cfg1_octant", "uniform32", "sphere_small", "sphere_small_dir", "tank_small"]
+
+
+def _setup(om, cfg, **mg):
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    kind = torch.from_numpy(cfg["kind"]).to(DEV)
+    frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(DEV)
+    h = om.Hierarchy(tree, kind, face_frac=frac, mu=mg.pop("mu", cfg["mu"]), **mg)
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    o.setup(cfg["kind"], cfg["w"])
+    return tree, h, o
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---------------------------------------------------------------------------------------
+# tree: bit-exact
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", SMALL + ["cfg3_sphere"])
+def test_tree_tables_bit_exact(om, name):
+    cfg = make_config(name, with_fields=False)
+    t = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    g, r = t.tables(), o.tables()
+    for k in ("tiles", "nbr", "parent", "child"):
+        assert np.array_equal(g[k], r[k]), k
+    assert (t.L, t.NL, t.NI) == (o.L, o.NL, o.NI)
+    assert np.array_equal(t.leaf_count, o.leaf_count) and np.array_equal(t.inner_count, o.inner_count)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_tree_random_graded_bit_exact(om, seed):
+    rng = np.random.default_rng(seed)
+    tiles = random_graded_tree(rng, 1, 4, 0.3)
+    tiles = tiles[rng.permutation(len(tiles))]  # any input order
+    g = om.Tree(tiles).tables()
+    r = Oracle(tiles).tables()
+    for k in g:
+        assert np.array_equal(g[k], r[k]), k
+
+
+def test_tree_table1_sphere_5_7(om):
+    t = sphere_band_tiles(5, 2, r=0.25)
+    g = om.Tree(t)
+    assert g.NL == 79080
+    assert np.array_equal(g.export(1), Oracle(t).tables()["nbr"])
+
+
+def test_tree_error_classes(om):
+    t = uniform_tiles(1)
+    cases = [(t[1:], "GAP"), (np.concatenate([t, t[:1]]), "OVERLAP"),
+             (np.concatenate([t, [[0, 0, 0, 0]]]), "OVERLAP"),
+             (sphere_band_tiles(3, 2, r=0.25, repair=False), "NOT_GRADED")]
+    bad = t.copy()
+    bad[0, 1] = 5
+    cases.append((bad, "INVALID"))
+    for tiles, st in cases:
+        with pytest.raises(om.OctmgError) as e:
+            om.Tree(tiles)
+        assert e.value.status == st
+
+
+# ---------------------------------------------------------------------------------------
+# coefficients and operator
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", SMALL)
+def test_coefficients_match_oracle(om, name):
+    cfg = make_config(name)
+    tree, h, o = _setup(om, cfg)
+    g = h.export_coefs().astype(np.float64)
+    r = o.coefs()
+    scale = np.abs(r).max(axis=1, keepdims=True) + 1e-30
+    err = np.abs(g - r) / scale
+    assert err.max() <= 2e-6, (name, err.max(), np.unravel_index(err.argmax(), err.shape))
+    # activity decisions identical
+    assert np.array_equal(g[:, 0] != 0, r[:, 0] != 0)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_coefficients_random_masks_weights(om, seed):
+    rng = np.random.default_rng(seed)
+    tiles = random_graded_tree(rng, 1, 3, 0.35)
+    N = len(tiles) * 512
+    kind = rng.choice([0, 1, 2], size=N, p=[0.8, 0.1, 0.1]).astype(np.uint8)
+    beta = (0.1 + rng.random((6, N))).astype(np.float32)
+    frac = rng.random((6, N)).astype(np.float32)
+    walls = tuple(int(v) for v in rng.integers(0, 2, size=6))
+    tree = om.Tree(tiles, wall_bc=walls)
+    h = om.Hierarchy(tree, torch.from_numpy(kind).to(DEV), torch.from_numpy(beta).to(DEV),
+                     torch.from_numpy(frac).to(DEV))
+    o = Oracle(tiles, wall_bc=walls)
+    o.setup(kind, (beta * frac).astype(np.float32))
+    g, r = h.export_coefs().astype(np.float64), o.coefs()
+    scale = np.abs(r).max(axis=1, keepdims=True) + 1e-30
+    assert (np.abs(g - r) / scale).max() <= 5e-6
+    x = rng.standard_normal(o.N).astype(np.float32)
+    y = torch.zeros(o.N, device=DEV)
+    h.apply(torch.from_numpy(x).to(DEV), y)
+    assert _rel(y.cpu().numpy().astype(np.float64), o.apply(x.astype(np.float64))) <= 1e-5
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_apply_matches_oracle(om, name):
+    cfg = make_config(name)
+    tree, h, o = _setup(om, cfg)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(o.N).astype(np.float32)
+    y = torch.zeros(o.N, device=DEV)
+    h.apply(torch.from_numpy(x).to(DEV), y)
+    ref = o.apply(x.astype(np.float64))
+    assert _rel(y.cpu().numpy().astype(np.float64), ref) <= 1e-5
+
+
+# ---------------------------------------------------------------------------------------
+# preconditioner and solve
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("mu", [1, 2])
+def test_vcycle_matches_oracle(om, name, mu):
+    cfg = make_config(name)
+    tree, h, o = _setup(om, cfg, mu=mu)
+    rng = np.random.default_rng(2)
+    r = rng.standard_normal(o.N).astype(np.float32)
+    u = torch.zeros(o.N, device=DEV)
+    h.vcycle(torch.from_numpy(r).to(DEV), u)
+    ref = o.vcycle(r.astype(np.float64), mu=mu)
+    assert _rel(u.cpu().numpy().astype(np.float64), ref) <= 1e-5
+
+
+@pytest.mark.parametrize("name", SMALL + ["uniform64", "tank_mid"])
+def test_pcg_matches_oracle(om, name):
+    cfg = make_config(name)
+    tree, h, o = _setup(om, cfg)
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    x = torch.zeros_like(b)
+    rep = h.pcg_solve(b, x, rtol=1e-6)
+    ref = o.pcg(cfg["b"].astype(np.float64), rtol=1e-6, mu=cfg["mu"])
+    assert rep["converged"] and ref["status"] == "OK"
+    assert abs(rep["iters"] - ref["iters"]) <= 1, (rep["iters"], ref["iters"])
+    xg = x.cpu().numpy().astype(np.float64)
+    xr = ref["x"]
+    if cfg["bc"] == "neumann_layer":  # unique up to a constant (SURVEY c-8 #19)
+        act = o.coefs()[:o.N, 0] != 0
+        xg = xg - xg[act].mean() * act
+        xr = xr - xr[act].mean() * act
+    assert _rel(xg, xr) <= 1e-5, _rel(xg, xr)
+
+
+def test_pcg_random_rhs_and_deterministic(om):
+    cfg = make_config("sphere_small_dir", rhs="random", seed=3)
+    tree, h, o = _setup(om, cfg)
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    x1, x2 = torch.zeros_like(b), torch.zeros_like(b)
+    r1 = h.pcg_solve(b, x1, rtol=1e-6)
+    r2 = h.pcg_solve(b, x2, rtol=1e-6)
+    assert torch.equal(x1, x2) and r1["history"].tolist() == r2["history"].tolist()
+    ref = o.pcg(cfg["b"].astype(np.float64), rtol=1e-6)
+    assert abs(r1["iters"] - ref["iters"]) <= 1
+    assert _rel(x1.cpu().numpy().astype(np.float64), ref["x"]) <= 1e-5
+
+
+def test_pcg_edge_cases(om):
+    cfg = make_config("cfg1_octant")
+    tree, h, o = _setup(om, cfg)
+    b = torch.zeros(o.N, device=DEV)
+    x = torch.full_like(b, 7.0)
+    rep = h.pcg_solve(b, x)
+    assert rep["iters"] == 0 and rep["converged"] and torch.count_nonzero(x) == 0
+    bad = torch.from_numpy(cfg["b"]).to(DEV)
+    bad[5] = float("nan")
+    with pytest.raises(om.OctmgError) as e:
+        h.pcg_solve(bad, x)
+    assert e.value.status == "NONFINITE"
+    rep = h.pcg_solve(torch.from_numpy(cfg["b"]).to(DEV), x, rtol=1e-12, max_iters=2)
+    assert rep["status"] == "MAXITER" and rep["iters"] == 2 and not rep["converged"]
+
+
+def test_single_tile_tree(om):
+    t = uniform_tiles(0)
+    tree = om.Tree(t)
+    assert (tree.L, tree.NL, tree.NI) == (0, 1, 0)
+    h = om.Hierarchy(tree, torch.zeros(512, dtype=torch.uint8, device=DEV))
+    b = torch.ones(512, device=DEV)
+    x = torch.zeros_like(b)
+    rep = h.pcg_solve(b, x, rtol=1e-6)
+    o = Oracle(t)
+    o.setup()
+    ref = o.pcg(np.ones(512), rtol=1e-6)
+    assert abs(rep["iters"] - ref["iters"]) <= 1
+    assert _rel(x.cpu().numpy().astype(np.float64), ref["x"]) <= 1e-5
+
+
+# ---------------------------------------------------------------------------------------
+# full-size configuration timed by bench.py (BASELINE config 2, uniform 256^3)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.slow
+def test_full_size_cfg2_parity(om):
+    cfg = make_config("cfg2_uniform256")
+    tree, h, o = _setup(om, cfg)
+    # sampled apply outputs: the full apply is cheap for the oracle too
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal(o.N).astype(np.float32)
+    y = torch.zeros(o.N, device=DEV)
+    h.apply(torch.from_numpy(x).to(DEV), y)
+    assert _rel(y.cpu().numpy().astype(np.float64), o.apply(x.astype(np.float64))) <= 1e-5
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    xg = torch.zeros_like(b)
+    rep = h.pcg_solve(b, xg, rtol=1e-6)
+    ref = o.pcg(cfg["b"].astype(np.float64), rtol=1e-6)
+    assert abs(rep["iters"] - ref["iters"]) <= 1
+    act = o.coefs()[:o.N, 0] != 0
+    a = xg.cpu().numpy().astype(np.float64)
+    a = a - a[act].mean() * act
+    r = ref["x"] - ref["x"][act].mean() * act
+    assert _rel(a, r) <= 1e-5
