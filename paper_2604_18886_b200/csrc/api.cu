@@ -1,5 +1,6 @@
 // C-ABI entry points (include/octmg.h), hierarchy management, the unrolled mu-cycle
 // schedule (captured once into a CUDA graph) and the PCG driver (Alg. 1).
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -17,9 +18,9 @@ octmg_status cuda_status(cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? OCTMG_E_OOM : OCTMG_E_CUDA;
 }
 
-const char* kclass_name[KC_COUNT] = {"rbgs_pass", "rbgs_pass_zero", "rbgs_pass_fas", "rbgs_pass_prolong",
-                                     "residual_restrict", "coarsest", "apply", "pcg_update", "dot_rz",
-                                     "project", "init", "setup", "memset"};
+const char* kclass_name[KC_COUNT] = {"smooth_pre_restrict", "smooth_post_prolong", "coarsest", "fas_rhs",
+                                     "smooth_coarse_levels", "apply", "pcg_update", "dot_rz", "project",
+                                     "init", "setup", "memset"};
 
 template <class T>
 static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
@@ -49,53 +50,171 @@ Hier::~Hier() {
 // ------------------------------------------------------------------------------------
 namespace {
 
+enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
+
+inline int stage_desc(int colour, int mode) { return colour | (mode << 1); }
+
+// Tiles of each level in rank order (slab-major: z, then Morton of (x, y)) and the lag D =
+// 1 + the largest rank gap between same-level face neighbours (host, once per hierarchy).
+octmg_status build_orders(Hier& h) {
+  const Tree& T = *h.tree;
+  std::vector<int4> tile(T.T);
+  std::vector<int> nbr((size_t)T.T * 6);
+  OCTMG_CUDA(cudaMemcpy(tile.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
+  OCTMG_CUDA(cudaMemcpy(nbr.data(), T.nbr, sizeof(int) * 6 * T.T, cudaMemcpyDeviceToHost));
+  auto m2 = [](uint32_t x, uint32_t y) {
+    uint64_t m = 0;
+    for (int b = 0; b < 21; ++b) m |= ((uint64_t)((x >> b) & 1) << (2 * b)) | ((uint64_t)((y >> b) & 1) << (2 * b + 1));
+    return m;
+  };
+  std::vector<int> order;
+  order.reserve(T.T);
+  std::vector<int> rank(T.T, -1);
+  for (int l = 0; l <= T.L; ++l) {
+    std::vector<int> ts;
+    for (int t = T.lb[l]; t < T.lb[l] + T.lc[l]; ++t) ts.push_back(t);
+    for (int t = T.ib[l]; t < T.ib[l] + T.ic[l]; ++t) ts.push_back(t);
+    std::sort(ts.begin(), ts.end(), [&](int a, int b) {
+      if (tile[a].w != tile[b].w) return tile[a].w < tile[b].w;
+      return m2(tile[a].y, tile[a].z) < m2(tile[b].y, tile[b].z);
+    });
+    h.lvl_order_off[l] = (int)order.size();
+    h.lvl_n[l] = (int)ts.size();
+    for (size_t r = 0; r < ts.size(); ++r) rank[ts[r]] = (int)r;
+    order.insert(order.end(), ts.begin(), ts.end());
+    int D = 1;
+    for (int t : ts)
+      for (int f = 0; f < 6; ++f) {
+        int n = nbr[6 * (size_t)t + f];
+        if (n >= 0) D = std::max(D, rank[n] - rank[t] + 1);
+      }
+    h.lvl_D[l] = D;
+  }
+  int* d;
+  OCTMG_CUDA(cudaMalloc(&d, sizeof(int) * std::max<size_t>(order.size(), 1)));
+  h.allocs.push_back(d);
+  OCTMG_CUDA(cudaMemcpy(d, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
+  h.order = d;
+  return OCTMG_OK;
+}
+
+// issue order of the (stage, rank) items of a level: by key = rank + stage * D
+int get_list(Hier& h, int level, int S) {
+  for (size_t k = 0; k < h.lists.size(); ++k)
+    if (h.lists[k].level == level && h.lists[k].nstages == S) return (int)k;
+  const int n = h.lvl_n[level], D = h.lvl_D[level];
+  std::vector<int> items;
+  items.reserve((size_t)n * S);
+  for (int64_t key = 0; key < n + (int64_t)(S - 1) * D; ++key)
+    for (int s = S - 1; s >= 0; --s) {
+      int64_t r = key - (int64_t)s * D;
+      if (r >= 0 && r < n) items.push_back((s << 24) | (int)r);
+    }
+  ItemList L{level, S, nullptr, (int)items.size()};
+  if (cudaMalloc(&L.items, sizeof(int) * std::max<size_t>(items.size(), 1)) != cudaSuccess) return -1;
+  h.allocs.push_back(L.items);
+  cudaMemcpy(L.items, items.data(), sizeof(int) * items.size(), cudaMemcpyHostToDevice);
+  h.lists.push_back(L);
+  return (int)h.lists.size() - 1;
+}
+
 struct Builder {
   Hier& h;
-  int cur[MAXL + 1];
-  void pass(int l, int colour, int mode) {
-    Op op{0, l, mode, colour, cur[l], 1 - cur[l]};
+  int epoch = 1;
+  int counters = 0;
+  bool ok = true;
+  void smooth(int l, const std::vector<int>& st) {
+    Op op{};
+    op.kind = 0;
+    op.level = l;
+    op.list = get_list(h, l, (int)st.size());
+    if (op.list < 0) ok = false;
+    op.epoch = epoch;
+    epoch += (int)st.size() + 1;
+    op.counter = counters++;
+    op.nstages = (int)st.size();
+    for (size_t k = 0; k < st.size(); ++k) op.stage[k] = st[k];
     h.ops.push_back(op);
-    cur[l] = 1 - cur[l];
   }
-  void smooth(int l, int iters, bool red_first, int first_mode) {
+  // colour passes of `iters` RBGS iterations, red first or black first
+  static void passes(std::vector<int>& st, int iters, bool red_first) {
     for (int k = 0; k < iters; ++k) {
-      pass(l, red_first ? 0 : 1, k == 0 ? first_mode : PM_PLAIN);
-      pass(l, red_first ? 1 : 0, PM_PLAIN);
+      st.push_back(stage_desc(red_first ? 0 : 1, SM_PLAIN));
+      st.push_back(stage_desc(red_first ? 1 : 0, SM_PLAIN));
     }
   }
-  // fas_first: this is the first of the mu calls from level l+1, so the first pre-smoothing
-  // pass forms the inner rows' FAS right-hand side
+  static void first_two(std::vector<int>& st, int m1, int m2) {
+    st[0] = (st[0] & 1) | (m1 << 1);
+    st[1] = (st[1] & 1) | (m2 << 1);
+  }
+  // Alg. 4 at level l; fas_first: first of the mu calls from level l+1 (forms the FAS rhs)
   void fas(int l, bool fas_first) {
-    const int L = h.tree->L;
-    int first_mode = l == L ? PM_ZERO : (fas_first ? PM_FAS : PM_PLAIN);
+    const Tree& T = *h.tree;
+    if (l < T.L && fas_first && T.ic[l] > 0) {
+      Op op{};
+      op.kind = 1;
+      op.level = l;
+      h.ops.push_back(op);
+    }
+    std::vector<int> st;
     if (l == 0) {
       int nb = h.prm.nu_coarsest;
-      smooth(0, nb / 2, true, first_mode);
-      smooth(0, nb - nb / 2, false, nb / 2 == 0 ? first_mode : PM_PLAIN);
+      passes(st, nb / 2, true);
+      passes(st, nb - nb / 2, false);
+      if (l == T.L) first_two(st, SM_ZERO1, SM_ZERO2);
+      smooth(0, st);
       return;
     }
-    smooth(l, h.prm.nu_pre, true, first_mode);
-    h.ops.push_back(Op{1, l, 0, 0, cur[l], cur[l]});
+    passes(st, h.prm.nu_pre, true);
+    if (l == T.L) first_two(st, SM_ZERO1, SM_ZERO2);
+    st.push_back(stage_desc(0, SM_RESTRICT));
+    smooth(l, st);
     for (int k = 0; k < h.prm.mu; ++k) fas(l - 1, k == 0);
-    smooth(l, h.prm.nu_post, false, PM_PROLONG);
+    std::vector<int> post;
+    passes(post, h.prm.nu_post, false);
+    first_two(post, SM_PRO1, SM_PRO2);
+    smooth(l, post);
   }
 };
 
-void build_schedule(Hier& h) {
+octmg_status build_schedule(Hier& h) {
   h.ops.clear();
-  Builder b{h, {}};
+  OCTMG_TRY(build_orders(h));
+  Builder b{h};
   const Tree& T = *h.tree;
-  if (T.NL > T.lc[T.L]) h.ops.push_back(Op{2, 0, 0, 0, 0, 0});  // zero coarse leaves
+  Op reset{};
+  reset.kind = 3;
+  h.ops.push_back(reset);
+  if (T.NL > T.lc[T.L]) {
+    Op z{};
+    z.kind = 2;
+    h.ops.push_back(z);  // coarse leaves start the cycle at 0
+  }
   b.fas(T.L, false);
+  if (!b.ok) { set_error("item list allocation failed"); return OCTMG_E_OOM; }
+  h.n_counters = b.counters;
+  int* d;
+  OCTMG_CUDA(cudaMalloc(&d, sizeof(int) * ((size_t)T.T + h.n_counters + 1)));
+  h.allocs.push_back(d);
+  h.flags = d;
+  h.counters = d + T.T;
+  OCTMG_CUDA(cudaMemset(d, 0, sizeof(int) * ((size_t)T.T + h.n_counters + 1)));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, smooth_kernel_ptr(), 256, 0);
+  h.smooth_grid = sms * std::max(per, 1);
+  return OCTMG_OK;
 }
 
 int64_t schedule_kernels(const Hier& h) {
   int64_t n = 0;
-  for (const Op& op : h.ops) n += op.kind != 2;
+  for (const Op& op : h.ops) n += op.kind <= 1;
   return n;
 }
 
-Fld buf(const Hier& h, int which) { return which == 0 ? Fld{h.z, h.uinA} : Fld{h.zB, h.uinB}; }
+Fld ubuf(const Hier& h) { return Fld{h.z, h.uinA}; }
 
 cudaEvent_t next_event(Hier& h) {
   if (h.event_next == h.event_pool.size()) {
@@ -126,6 +245,11 @@ struct ProfScope {
 
 void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   const Tree& T = *h.tree;
+  if (op.kind == 3) {
+    ProfScope ps(h, KC_MEMSET, s, 4.0 * ((double)T.T + h.n_counters));
+    cudaMemsetAsync(h.flags, 0, sizeof(int) * ((size_t)T.T + h.n_counters), s);
+    return;
+  }
   if (op.kind == 2) {
     size_t first = (size_t)T.lc[T.L] * TB3;
     ProfScope ps(h, KC_MEMSET, s, 4.0 * ((double)T.NL * TB3 - first));
@@ -133,34 +257,42 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     return;
   }
   const int l = op.level;
-  if (op.kind == 0) {
-    PassArgs a;
-    a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
-    a.glayer = T.glayer;
-    a.uin = buf(h, op.in_buf); a.uout = buf(h, op.out_buf); a.ucoarse = buf(h, 0);
-    a.ustar = h.ustar; a.b = Fld{h.r, h.binner}; a.NL = T.NL;
-    a.loff = T.lb[l]; a.nl = T.lc[l]; a.ioff = T.ib[l]; a.ni = T.ic[l];
-    a.colour = op.colour;
-    int cls = op.mode == PM_ZERO ? KC_PASS_ZERO : op.mode == PM_FAS ? KC_PASS_FAS
-            : op.mode == PM_PROLONG ? KC_PASS_PROLONG : (l == 0 ? KC_COARSEST : KC_PASS);
-    // algorithmic bytes per cell: read u, b, 16-byte record, write u (zero mode: no u read);
-    // FAS: + write of the inner rows' b; prolong: + u^{l-1}, u* per parent (1 B/cell)
-    double cells = (double)(a.nl + a.ni) * TB3;
-    double bytes = cells * (op.mode == PM_ZERO ? 24.0 : 28.0);
-    if (op.mode == PM_FAS) bytes += 4.0 * a.ni * TB3;
-    if (op.mode == PM_PROLONG) bytes += cells * 1.0;
-    ProfScope ps(h, cls, s, bytes);
-    launch_pass(op.mode, a, s);
-  } else {
-    RestrictArgs a;
-    a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
-    a.glayer = T.glayer; a.u = buf(h, 0); a.ucoarse = buf(h, 0); a.ustar = h.ustar;
-    a.b = Fld{h.r, h.binner}; a.bscale = h.prm.beta; a.alpha_div = h.prm.alpha; a.NL = T.NL;
-    a.loff = T.lb[l]; a.nl = T.lc[l]; a.ioff = T.ib[l]; a.ni = T.ic[l];
-    // read u, b, record (24 B/cell) + write u, u*, b of the parent (12 B per 8 cells)
-    ProfScope ps(h, KC_RESTRICT, s, (double)(a.nl + a.ni) * TB3 * 25.5);
-    launch_restrict(a, s);
+  SmoothArgs a;
+  a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
+  a.glayer = T.glayer; a.u = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar; a.b = Fld{h.r, h.binner};
+  a.beta = h.prm.beta; a.alpha = h.prm.alpha; a.NL = T.NL;
+  a.order = h.order + h.lvl_order_off[l];
+  a.n = h.lvl_n[l];
+  a.first_tile = T.ib[l];
+  a.flags = h.flags;
+  a.epoch = op.epoch;
+  a.has_prolong = 0;
+  if (op.kind == 1) {
+    a.items = nullptr; a.nstages = 0; a.counter = nullptr;
+    // read u, b, record; write b (inner cells of the level)
+    ProfScope ps(h, KC_FASRHS, s, 28.0 * T.ic[l] * TB3);
+    launch_fasrhs(a, T.ic[l], s);
+    return;
   }
+  const ItemList& L = h.lists[op.list];
+  a.items = L.items;
+  a.nstages = op.nstages;
+  a.counter = h.counters + op.counter;
+  bool restrict_ = false;
+  for (int k = 0; k < op.nstages; ++k) {
+    a.stage[k] = op.stage[k];
+    if ((op.stage[k] >> 1) == SM_PRO1) a.has_prolong = 1;
+    if ((op.stage[k] >> 1) == SM_RESTRICT) restrict_ = true;
+  }
+  // algorithmic bytes of the launch: every cell's u, b and 16-byte record read once and u
+  // written once (28 B/cell); restriction adds the parents' u, u*, b (1.5 B/cell),
+  // prolongation the parents' u, u* (1 B/cell)
+  double cells = (double)a.n * TB3;
+  double bytes = cells * 28.0 + (restrict_ ? 1.5 * cells : 0.0) + (a.has_prolong ? 1.0 * cells : 0.0);
+  int cls = l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : (a.has_prolong ? KC_SMOOTH_POST : KC_SMOOTH_PRE));
+  int grid = (int)std::min<int64_t>(h.smooth_grid, (int64_t)L.n_items);
+  ProfScope ps(h, cls, s, bytes);
+  launch_smooth(a, grid, s);
 }
 
 octmg_status run_M(Hier& h, cudaStream_t s) {
@@ -269,9 +401,7 @@ octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const 
   if ((st = halloc(h.allocs, &h.coef, (size_t)T.T * TB3))) return fail(st);
   if ((st = halloc(h.allocs, &h.glayer_val, (size_t)T.n_glayers * 64))) return fail(st);
   if ((st = halloc(h.allocs, &h.z, NLc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.zB, NLc))) return fail(st);
   if ((st = halloc(h.allocs, &h.uinA, NIc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.uinB, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.binner, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.ustar, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.r, NLc))) return fail(st);
@@ -289,14 +419,14 @@ octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const 
   }
   cudaError_t e = cudaMemsetAsync(h.counter, 0, 16 * sizeof(unsigned), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(h.uinA, 0, NIc * sizeof(float) + 0, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h.uinB, 0, NIc * sizeof(float), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h.zB, 0, NLc * sizeof(float), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h.z, 0, NLc * sizeof(float), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(h.sc, 0, sizeof(Scalars), s);
   if (e != cudaSuccess) return fail(cuda_status(e, "memset"));
   if ((st = assemble_leaf_coefs(h, kind, face_beta, face_frac, s))) return fail(st);
   if ((st = coarsen_all(h, s))) return fail(st);
-  build_schedule(h);
   e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(cuda_status(e, "setup"));
+  if ((st = build_schedule(h))) return fail(st);
   if (e != cudaSuccess) return fail(cuda_status(e, "setup"));
   *out = hh;
   return OCTMG_OK;

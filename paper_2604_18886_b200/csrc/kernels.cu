@@ -63,18 +63,6 @@ __device__ __forceinline__ void set_plus_coef(TileSmem& S, int a, const int halo
   else S.cz[scz_idx(halo[0], halo[1], 8)] = v;
 }
 
-__device__ __forceinline__ float offdiag(const TileSmem& S, int x, int y, int z) {
-  int iu = su_idx(x, y, z);
-  float s = 0.0f;
-  s = fmaf(S.cx[scx_idx(x, y, z)], S.u[iu - 1], s);
-  s = fmaf(S.cx[scx_idx(x + 1, y, z)], S.u[iu + 1], s);
-  s = fmaf(S.cy[scy_idx(x, y, z)], S.u[iu - 10], s);
-  s = fmaf(S.cy[scy_idx(x, y + 1, z)], S.u[iu + 10], s);
-  s = fmaf(S.cz[scz_idx(x, y, z)], S.u[iu - 100], s);
-  s = fmaf(S.cz[scz_idx(x, y, z + 1)], S.u[iu + 100], s);
-  return s;
-}
-
 __device__ __forceinline__ float rowsum(const TileSmem& S, int x, int y, int z, float c) {
   // c*u first, then faces x-, x+, y-, y+, z-, z+ (the oracle's order)
   int iu = su_idx(x, y, z);
@@ -88,185 +76,6 @@ __device__ __forceinline__ float rowsum(const TileSmem& S, int x, int y, int z, 
   return s;
 }
 
-__device__ __forceinline__ int pcell_of(int4 tv, int x, int y, int z) {
-  return loff(((tv.y & 1) << 2) + (x >> 1), ((tv.z & 1) << 2) + (y >> 1), ((tv.w & 1) << 2) + (z >> 1));
-}
-
-// ------------------------------------------------------------------------------------
-// Level-l staging: own tile values (optionally prolongation-corrected), coefficients,
-// halos with on-the-fly ghosts.  Used by the RBGS pass and the residual/restrict kernel.
-// ------------------------------------------------------------------------------------
-template <int MODE>
-__device__ __forceinline__ void stage_level(TileSmem& S, const PassArgs& a, int t, float& u0, float& u1,
-                                            float4& q0, float4& q1) {
-  const int tid = threadIdx.x;
-  if (tid < 6) {
-    int n = a.nbr[6 * t + tid];
-    S.nb[tid] = n;
-    if (MODE == PM_PROLONG && n >= 0) { S.ntv[tid] = a.tile[n]; S.npar[tid] = a.parent[n]; }
-  }
-  if (tid == 6) S.tv = a.tile[t];
-  if (tid == 7) S.par = a.parent[t];
-  const int x2 = tid & 3, y = (tid >> 2) & 7, z = tid >> 5, x0 = 2 * x2;
-  const int off0 = loff(x0, y, z);
-  const float4* cf = a.coef + (size_t)t * TB3;
-  q0 = cf[off0];
-  q1 = cf[off0 + 1];
-  if (MODE == PM_ZERO) {
-    u0 = 0.0f; u1 = 0.0f;
-  } else {
-    float2 uu = *reinterpret_cast<const float2*>(tptr(a.uin, t, a.NL) + off0);
-    u0 = uu.x; u1 = uu.y;
-  }
-  __syncthreads();  // S.tv, S.par, S.nb visible
-  if (MODE == PM_PROLONG) {
-    int pc = pcell_of(S.tv, x0, y, z);
-    float corr = tptr(a.ucoarse, S.par, a.NL)[pc] - a.ustar[(size_t)(S.par - a.NL) * TB3 + pc];
-    if (q0.x != 0.0f) u0 += corr;
-    if (q1.x != 0.0f) u1 += corr;
-  }
-  S.u[su_idx(x0, y, z)] = u0;
-  S.u[su_idx(x0 + 1, y, z)] = u1;
-  S.c[off0] = q0.x;
-  S.c[off0 + 1] = q1.x;
-  S.cx[scx_idx(x0, y, z)] = q0.y;
-  S.cx[scx_idx(x0 + 1, y, z)] = q1.y;
-  S.cy[scy_idx(x0, y, z)] = q0.z;
-  S.cy[scy_idx(x0 + 1, y, z)] = q1.z;
-  S.cz[scz_idx(x0, y, z)] = q0.w;
-  S.cz[scz_idx(x0 + 1, y, z)] = q1.w;
-  __syncthreads();
-  if (MODE == PM_ZERO) {
-    // every value is zero at the first pass of a cycle (u = 0, coarse leaves = 0): the halo
-    // values vanish; only the +face coefficients would be read, against zero values.
-    for (int w = tid; w < 384; w += NT) {
-      int f = w >> 6, p = w & 7, q = (w >> 3) & 7;
-      int own[3], src[3], halo[3];
-      face_cells(f, p, q, own, src, halo);
-      S.u[su_idx(halo[0], halo[1], halo[2])] = 0.0f;
-      if (f & 1) set_plus_coef(S, f >> 1, halo, 0.0f);
-    }
-    __syncthreads();
-    return;
-  }
-  for (int w = tid; w < 384; w += NT) {
-    int f = w >> 6, p = w & 7, q = (w >> 3) & 7;
-    int own[3], src[3], halo[3];
-    face_cells(f, p, q, own, src, halo);
-    int a_ = f >> 1;
-    int n = S.nb[f];
-    float v = 0.0f, cplus = 0.0f;
-    if (n >= 0) {
-      int so = loff(src[0], src[1], src[2]);
-      v = tptr(a.uin, n, a.NL)[so];
-      if ((f & 1) || MODE == PM_PROLONG) {
-        float4 r = a.coef[(size_t)n * TB3 + so];
-        cplus = comp(r, a_);
-        if (MODE == PM_PROLONG && r.x != 0.0f) {
-          int P = S.npar[f];
-          int pc = pcell_of(S.ntv[f], src[0], src[1], src[2]);
-          v += tptr(a.ucoarse, P, a.NL)[pc] - a.ustar[(size_t)(P - a.NL) * TB3 + pc];
-        }
-      }
-    } else if (n <= -2) {
-      int C = -2 - n;
-      int g0 = S.tv.y * 8 + halo[0], g1 = S.tv.z * 8 + halo[1], g2 = S.tv.w * 8 + halo[2];
-      int co = loff((g0 >> 1) & 7, (g1 >> 1) & 7, (g2 >> 1) & 7);
-      if (a.coef[(size_t)C * TB3 + co].x != 0.0f) {
-        float uc = tptr(a.ucoarse, C, a.NL)[co];
-        float ub = S.u[su_idx(own[0], own[1], own[2])];
-        v = ub + 0.5f * (uc - block_mean(S, own));
-      }
-      if (f & 1) cplus = a.glayer_val[(size_t)a.glayer[3 * t + a_] * 64 + p + 8 * q];
-    }
-    S.u[su_idx(halo[0], halo[1], halo[2])] = v;
-    if (f & 1) set_plus_coef(S, a_, halo, cplus);
-  }
-  __syncthreads();
-}
-
-// One red-black Gauss-Seidel colour pass at level l, snapshot ghosts
-// (SURVEY c-5).  Reads uin, writes every cell of uout.  MODE: plain, zero (first pass of
-// the cycle at the finest level), FAS (first pre-smoothing pass of a coarse visit: the
-// inner rows' rhs b = beta R r + A u* is formed here, Alg. 4 line 10), prolong (first
-// post-smoothing pass: u += P(u^{l-1} - u*) applied while staging, Alg. 4 line 15).
-template <int MODE>
-__global__ __launch_bounds__(NT) void k_pass(PassArgs a) {
-  __shared__ TileSmem S;
-  const int blk = blockIdx.x;
-  const int t = blk < a.nl ? a.loff + blk : a.ioff + blk - a.nl;
-  float u0, u1;
-  float4 q0, q1;
-  stage_level<MODE>(S, a, t, u0, u1, q0, q1);
-  const int tid = threadIdx.x;
-  const int x2 = tid & 3, y = (tid >> 2) & 7, z = tid >> 5, x0 = 2 * x2;
-  const int off0 = loff(x0, y, z);
-  float b0, b1;
-  if (t < a.NL) {
-    float2 bb = *reinterpret_cast<const float2*>(a.b.leaf + (size_t)t * TB3 + off0);
-    b0 = bb.x; b1 = bb.y;
-  } else {
-    float* bi = a.b.inner + (size_t)(t - a.NL) * TB3 + off0;
-    float2 bb = *reinterpret_cast<const float2*>(bi);
-    b0 = bb.x; b1 = bb.y;
-    if (MODE == PM_FAS) {
-      b0 = q0.x != 0.0f ? b0 + rowsum(S, x0, y, z, q0.x) : 0.0f;
-      b1 = q1.x != 0.0f ? b1 + rowsum(S, x0 + 1, y, z, q1.x) : 0.0f;
-      *reinterpret_cast<float2*>(bi) = make_float2(b0, b1);
-    }
-  }
-  // the thread's cell of this colour
-  const int sel = (a.colour + y + z) & 1;  // 0: x0, 1: x0+1
-  const int xc = x0 + sel;
-  const float cc = sel ? q1.x : q0.x;
-  const float bc = sel ? b1 : b0;
-  float unew = sel ? u1 : u0;
-  if (cc != 0.0f) unew = (bc - offdiag(S, xc, y, z)) / cc;
-  float o0 = sel ? u0 : unew, o1 = sel ? unew : u1;
-  *reinterpret_cast<float2*>(tptr(a.uout, t, a.NL) + off0) = make_float2(o0, o1);
-}
-
-// r = b - A^l u on the tile; then per parent cell (inner, level l-1): u* = mean of active
-// children (Avg, Alg. 4 line 9), u^{l-1} := u*, b^{l-1} := beta * (R r) (R = P^T/alpha),
-// the FAS pass at level l-1 adds A^{l-1} u* (Alg. 4 line 10).  Fused as in P:L891.
-__global__ __launch_bounds__(NT) void k_restrict(RestrictArgs ra) {
-  __shared__ TileSmem S;
-  __shared__ float sr[512];
-  PassArgs a;
-  a.tile = ra.tile; a.nbr = ra.nbr; a.parent = ra.parent; a.coef = ra.coef; a.glayer_val = ra.glayer_val;
-  a.glayer = ra.glayer; a.uin = ra.u; a.uout = ra.u; a.ucoarse = ra.ucoarse; a.ustar = ra.ustar; a.b = ra.b;
-  a.NL = ra.NL;
-  const int blk = blockIdx.x;
-  const int t = blk < ra.nl ? ra.loff + blk : ra.ioff + blk - ra.nl;
-  float u0, u1;
-  float4 q0, q1;
-  stage_level<PM_PLAIN>(S, a, t, u0, u1, q0, q1);
-  const int tid = threadIdx.x;
-  const int x2 = tid & 3, y = (tid >> 2) & 7, z = tid >> 5, x0 = 2 * x2;
-  const int off0 = loff(x0, y, z);
-  const float* bp = tptr(ra.b, t, ra.NL) + off0;
-  float2 bb = *reinterpret_cast<const float2*>(bp);
-  sr[off0] = q0.x != 0.0f ? bb.x - rowsum(S, x0, y, z, q0.x) : 0.0f;
-  sr[off0 + 1] = q1.x != 0.0f ? bb.y - rowsum(S, x0 + 1, y, z, q1.x) : 0.0f;
-  __syncthreads();
-  if (tid < 64) {
-    int bx = (tid & 3) * 2, by = ((tid >> 2) & 3) * 2, bz = (tid >> 4) * 2;
-    float su = 0.0f, rs = 0.0f;
-    int n = 0;
-    for (int dz = 0; dz < 2; ++dz)
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-          int o = loff(bx + dx, by + dy, bz + dz);
-          if (S.c[o] != 0.0f) { n++; su += S.u[su_idx(bx + dx, by + dy, bz + dz)]; rs += sr[o]; }
-        }
-    float us = n ? su / (float)n : 0.0f;
-    int P = S.par;
-    int pc = pcell_of(S.tv, bx, by, bz);
-    tptr(ra.ucoarse, P, ra.NL)[pc] = us;
-    ra.ustar[(size_t)(P - ra.NL) * TB3 + pc] = us;
-    ra.b.inner[(size_t)(P - ra.NL) * TB3 + pc] = ra.bscale * (rs / ra.alpha_div);
-  }
-}
 
 // ------------------------------------------------------------------------------------
 // Composite operator (PCG q = A p with p = z + beta p fused, and the p.q dot)
@@ -521,22 +330,6 @@ __global__ void k_mask_copy(const float* src, const float4* coef, float* dst, in
 }
 
 }  // namespace
-
-void launch_pass(int mode, const PassArgs& a, cudaStream_t s) {
-  int grid = a.nl + a.ni;
-  if (grid == 0) return;
-  switch (mode) {
-    case PM_ZERO: k_pass<PM_ZERO><<<grid, NT, 0, s>>>(a); break;
-    case PM_FAS: k_pass<PM_FAS><<<grid, NT, 0, s>>>(a); break;
-    case PM_PROLONG: k_pass<PM_PROLONG><<<grid, NT, 0, s>>>(a); break;
-    default: k_pass<PM_PLAIN><<<grid, NT, 0, s>>>(a); break;
-  }
-}
-
-void launch_restrict(const RestrictArgs& a, cudaStream_t s) {
-  int grid = a.nl + a.ni;
-  if (grid) k_restrict<<<grid, NT, 0, s>>>(a);
-}
 
 void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   if (a.NL == 0) return;

@@ -84,7 +84,7 @@ struct Scalars {
 
 // Kernel classes for profiling
 enum KClass {
-  KC_PASS = 0, KC_PASS_ZERO, KC_PASS_FAS, KC_PASS_PROLONG, KC_RESTRICT, KC_COARSEST,
+  KC_SMOOTH_PRE = 0, KC_SMOOTH_POST, KC_COARSEST, KC_FASRHS, KC_SMOOTH_COARSE,
   KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_COUNT
 };
 extern const char* kclass_name[KC_COUNT];
@@ -92,44 +92,6 @@ extern const char* kclass_name[KC_COUNT];
 struct Hier;
 
 // launch helpers implemented in kernels.cu
-struct PassArgs {
-  const int4* tile;
-  const int* nbr;
-  const int* parent;
-  const float4* coef;
-  const float* glayer_val;
-  const int* glayer;
-  Fld uin, uout;        // level-l buffers (read / write)
-  Fld ucoarse;          // level-(l-1) rest buffer (ghost sources, prolongation)
-  const float* ustar;   // inner-indexed u* (prolongation)
-  Fld b;                // leaf = PCG residual r, inner = FAS rhs
-  int NL;
-  int loff, nl, ioff, ni;
-  int colour;
-};
-
-enum PassMode { PM_PLAIN = 0, PM_ZERO = 1, PM_FAS = 2, PM_PROLONG = 3 };
-
-void launch_pass(int mode, const PassArgs& a, cudaStream_t s);
-
-struct RestrictArgs {
-  const int4* tile;
-  const int* nbr;
-  const int* parent;
-  const float4* coef;
-  const float* glayer_val;
-  const int* glayer;
-  Fld u;                // level l (rest buffer)
-  Fld ucoarse;          // level l-1 (rest buffer): receives u* on inner cells
-  float* ustar;         // inner-indexed
-  Fld b;                // level l rhs: leaf = r, inner = FAS rhs; receives beta * R r
-  float bscale;         // beta (overshoot at restriction, Alg. 4 line 10)
-  float alpha_div;      // alpha (R = P^T / alpha)
-  int NL;
-  int loff, nl, ioff, ni;
-};
-void launch_restrict(const RestrictArgs& a, cudaStream_t s);
-
 struct ApplyArgs {
   const int4* tile;
   const int* nbr;
@@ -160,6 +122,36 @@ void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, u
                    Scalars* sc, int first, cudaStream_t s, int grid);
 void launch_mask_copy(const float* src, const float4* coef, float* dst, int64_t n, cudaStream_t s);
 
+// persistent wavefront smoother (smooth.cu)
+constexpr int MAX_STAGES = 48;
+struct SmoothArgs {
+  const int4* tile;
+  const int* nbr;
+  const int* parent;
+  const float4* coef;
+  const float* glayer_val;
+  const int* glayer;
+  Fld u;                // in-place level values (all levels share the buffer)
+  const float* ustar;   // inner-indexed u* (prolongation)
+  float* ustar_w;       // inner-indexed u* output (restrict stage)
+  Fld b;                // leaf = PCG residual r, inner = FAS rhs
+  float beta, alpha;
+  int NL;
+  const int* order;     // tiles of the level in rank order (slab-major)
+  const int* items;     // (stage << 24) | rank, issue order
+  int n;                // tiles in the level
+  int nstages;
+  int first_tile;       // k_fasrhs: first inner tile of the level
+  int has_prolong;
+  int* flags;           // per-tile stage completion (epoch + s + 1)
+  int* counter;         // work counter of this launch
+  int epoch;
+  int stage[MAX_STAGES];  // bit0 colour, bits1.. mode
+};
+void launch_smooth(const SmoothArgs& a, int grid, cudaStream_t s);
+const void* smooth_kernel_ptr();
+void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
+
 // setup kernels (setup.cu)
 struct SetupArgs;
 octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
@@ -174,11 +166,19 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
 // Hierarchy (coefficients + multigrid work buffers + PCG state)
 // ------------------------------------------------------------------------------------
 struct Op {
-  int kind;   // 0 pass, 1 restrict, 2 memset
+  int kind;    // 0 smooth launch, 1 FAS rhs, 2 zero coarse leaves, 3 reset flags/counters
   int level;
-  int mode;
-  int colour;
-  int in_buf, out_buf;
+  int list;    // index of the stage list (level, nstages) in Hier::lists
+  int epoch;
+  int counter;
+  int nstages;
+  int stage[MAX_STAGES];
+};
+
+struct ItemList {
+  int level, nstages;
+  int* items;   // device
+  int n_items;
 };
 
 struct Hier {
@@ -187,10 +187,8 @@ struct Hier {
   float4* coef = nullptr;        // [T*512] (c, cxm, cym, czm)
   float* glayer_val = nullptr;   // [n_glayers*64]
   // multigrid buffers
-  float* z = nullptr;            // [NL*512] leaf part of u (buffer A) = M output
-  float* zB = nullptr;           // [NL*512] leaf part of buffer B
-  float* uinA = nullptr;         // [NI*512]
-  float* uinB = nullptr;
+  float* z = nullptr;            // [NL*512] leaf part of the cycle's u (in place) = M output
+  float* uinA = nullptr;         // [NI*512] inner part of u
   float* binner = nullptr;       // [NI*512]
   float* ustar = nullptr;        // [NI*512]
   float* r = nullptr;            // [NL*512] PCG residual = leaf part of the cycle rhs
@@ -207,6 +205,16 @@ struct Hier {
   int any_dirichlet = 0;
   // schedule of one preconditioner application
   std::vector<Op> ops;
+  std::vector<ItemList> lists;
+  int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
+  int lvl_order_off[MAXL + 1] = {};
+  int lvl_n[MAXL + 1] = {};
+  int lvl_D[MAXL + 1] = {};
+  int* inner_order = nullptr;    // not used (inner tiles are contiguous)
+  int* flags = nullptr;          // [T]
+  int* counters = nullptr;       // [n_counters]
+  int n_counters = 0;
+  int smooth_grid = 0;
   cudaGraphExec_t graph = nullptr;
   cudaStream_t graph_stream = nullptr;
   int64_t launches = 0;
