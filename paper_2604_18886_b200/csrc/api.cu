@@ -1,6 +1,7 @@
 // C-ABI entry points (include/octmg.h), hierarchy management, the unrolled mu-cycle
 // schedule (captured once into a CUDA graph) and the PCG driver (Alg. 1).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -18,9 +19,9 @@ octmg_status cuda_status(cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? OCTMG_E_OOM : OCTMG_E_CUDA;
 }
 
-const char* kclass_name[KC_COUNT] = {"smooth_pre_restrict", "smooth_post_prolong", "coarsest", "fas_rhs",
-                                     "smooth_coarse_levels", "apply", "pcg_update", "dot_rz", "project",
-                                     "init", "setup", "memset"};
+const char* kclass_name[KC_COUNT] = {"rbgs_pass", "prolong", "residual_restrict", "coarsest",
+                                     "fas_rhs", "coarse_levels", "apply", "pcg_update", "dot_rz", "project",
+                                     "init", "setup", "memset", "coarse_subcycle"};
 
 template <class T>
 static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
@@ -54,14 +55,12 @@ enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RE
 
 inline int stage_desc(int colour, int mode) { return colour | (mode << 1); }
 
-// Tiles of each level in rank order (slab-major: z, then Morton of (x, y)) and the lag D =
-// 1 + the largest rank gap between same-level face neighbours (host, once per hierarchy).
+// Tiles of each level in rank order (slab-major: z, then Morton of (x, y)), so that the
+// consecutive tiles of a CTA's run share faces (host, once per hierarchy).
 octmg_status build_orders(Hier& h) {
   const Tree& T = *h.tree;
   std::vector<int4> tile(T.T);
-  std::vector<int> nbr((size_t)T.T * 6);
   OCTMG_CUDA(cudaMemcpy(tile.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
-  OCTMG_CUDA(cudaMemcpy(nbr.data(), T.nbr, sizeof(int) * 6 * T.T, cudaMemcpyDeviceToHost));
   auto m2 = [](uint32_t x, uint32_t y) {
     uint64_t m = 0;
     for (int b = 0; b < 21; ++b) m |= ((uint64_t)((x >> b) & 1) << (2 * b)) | ((uint64_t)((y >> b) & 1) << (2 * b + 1));
@@ -69,7 +68,6 @@ octmg_status build_orders(Hier& h) {
   };
   std::vector<int> order;
   order.reserve(T.T);
-  std::vector<int> rank(T.T, -1);
   for (int l = 0; l <= T.L; ++l) {
     std::vector<int> ts;
     for (int t = T.lb[l]; t < T.lb[l] + T.lc[l]; ++t) ts.push_back(t);
@@ -80,15 +78,7 @@ octmg_status build_orders(Hier& h) {
     });
     h.lvl_order_off[l] = (int)order.size();
     h.lvl_n[l] = (int)ts.size();
-    for (size_t r = 0; r < ts.size(); ++r) rank[ts[r]] = (int)r;
     order.insert(order.end(), ts.begin(), ts.end());
-    int D = 1;
-    for (int t : ts)
-      for (int f = 0; f < 6; ++f) {
-        int n = nbr[6 * (size_t)t + f];
-        if (n >= 0) D = std::max(D, rank[n] - rank[t] + 1);
-      }
-    h.lvl_D[l] = D;
   }
   int* d;
   OCTMG_CUDA(cudaMalloc(&d, sizeof(int) * std::max<size_t>(order.size(), 1)));
@@ -98,119 +88,70 @@ octmg_status build_orders(Hier& h) {
   return OCTMG_OK;
 }
 
-// issue order of the (stage, rank) items of a level: by key = rank + stage * D
-int get_list(Hier& h, int level, int S) {
-  for (size_t k = 0; k < h.lists.size(); ++k)
-    if (h.lists[k].level == level && h.lists[k].nstages == S) return (int)k;
-  const int n = h.lvl_n[level], D = h.lvl_D[level];
-  std::vector<int> items;
-  items.reserve((size_t)n * S);
-  for (int64_t key = 0; key < n + (int64_t)(S - 1) * D; ++key)
-    for (int s = S - 1; s >= 0; --s) {
-      int64_t r = key - (int64_t)s * D;
-      if (r >= 0 && r < n) items.push_back((s << 24) | (int)r);
-    }
-  ItemList L{level, S, nullptr, (int)items.size()};
-  if (cudaMalloc(&L.items, sizeof(int) * std::max<size_t>(items.size(), 1)) != cudaSuccess) return -1;
-  h.allocs.push_back(L.items);
-  cudaMemcpy(L.items, items.data(), sizeof(int) * items.size(), cudaMemcpyHostToDevice);
-  h.lists.push_back(L);
-  return (int)h.lists.size() - 1;
-}
-
 struct Builder {
   Hier& h;
-  int epoch = 1;
-  int counters = 0;
-  bool ok = true;
-  void smooth(int l, const std::vector<int>& st) {
-    Op op{};
-    op.kind = 0;
-    op.level = l;
-    op.list = get_list(h, l, (int)st.size());
-    if (op.list < 0) ok = false;
-    op.epoch = epoch;
-    epoch += (int)st.size() + 1;
-    op.counter = counters++;
-    op.nstages = (int)st.size();
-    for (size_t k = 0; k < st.size(); ++k) op.stage[k] = st[k];
-    h.ops.push_back(op);
-  }
-  // colour passes of `iters` RBGS iterations, red first or black first
-  static void passes(std::vector<int>& st, int iters, bool red_first) {
+  void stage(int l, int desc) { h.ops.push_back(Op{0, l, desc}); }
+  void passes(int l, int iters, bool red_first, int m1, int m2) {
     for (int k = 0; k < iters; ++k) {
-      st.push_back(stage_desc(red_first ? 0 : 1, SM_PLAIN));
-      st.push_back(stage_desc(red_first ? 1 : 0, SM_PLAIN));
+      stage(l, stage_desc(red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN));
+      stage(l, stage_desc(red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN));
     }
-  }
-  static void first_two(std::vector<int>& st, int m1, int m2) {
-    st[0] = (st[0] & 1) | (m1 << 1);
-    st[1] = (st[1] & 1) | (m2 << 1);
   }
   // Alg. 4 at level l; fas_first: first of the mu calls from level l+1 (forms the FAS rhs)
   void fas(int l, bool fas_first) {
     const Tree& T = *h.tree;
-    if (l < T.L && fas_first && T.ic[l] > 0) {
-      Op op{};
-      op.kind = 1;
-      op.level = l;
-      h.ops.push_back(op);
-    }
-    std::vector<int> st;
-    if (l == 0) {
-      int nb = h.prm.nu_coarsest;
-      passes(st, nb / 2, true);
-      passes(st, nb - nb / 2, false);
-      if (l == T.L) first_two(st, SM_ZERO1, SM_ZERO2);
-      smooth(0, st);
+    if (l <= h.sub_K) {  // the rest of the cycle runs on chip in one CTA
+      h.ops.push_back(Op{4, l, fas_first ? 1 : 0});
       return;
     }
-    passes(st, h.prm.nu_pre, true);
-    if (l == T.L) first_two(st, SM_ZERO1, SM_ZERO2);
-    st.push_back(stage_desc(0, SM_RESTRICT));
-    smooth(l, st);
+    if (l < T.L && fas_first && T.ic[l] > 0) h.ops.push_back(Op{1, l, 0});
+    const bool finest = l == T.L;
+    if (l == 0) {
+      int nb = h.prm.nu_coarsest;
+      int h1 = nb / 2;
+      passes(0, h1, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN);
+      bool z = finest && h1 == 0;
+      passes(0, nb - h1, false, z ? SM_ZERO1 : SM_PLAIN, z ? SM_ZERO2 : SM_PLAIN);
+      return;
+    }
+    passes(l, h.prm.nu_pre, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN);
+    stage(l, stage_desc(0, SM_RESTRICT));
     for (int k = 0; k < h.prm.mu; ++k) fas(l - 1, k == 0);
-    std::vector<int> post;
-    passes(post, h.prm.nu_post, false);
-    first_two(post, SM_PRO1, SM_PRO2);
-    smooth(l, post);
+    h.ops.push_back(Op{3, l, 0});  // prolongation u += P(u^{l-1} - u*), in place
+    passes(l, h.prm.nu_post, false, SM_PLAIN, SM_PLAIN);
   }
 };
 
 octmg_status build_schedule(Hier& h) {
   h.ops.clear();
   OCTMG_TRY(build_orders(h));
-  Builder b{h};
-  const Tree& T = *h.tree;
-  Op reset{};
-  reset.kind = 3;
-  h.ops.push_back(reset);
-  if (T.NL > T.lc[T.L]) {
-    Op z{};
-    z.kind = 2;
-    h.ops.push_back(z);  // coarse leaves start the cycle at 0
-  }
-  b.fas(T.L, false);
-  if (!b.ok) { set_error("item list allocation failed"); return OCTMG_E_OOM; }
-  h.n_counters = b.counters;
-  int* d;
-  OCTMG_CUDA(cudaMalloc(&d, sizeof(int) * ((size_t)T.T + h.n_counters + 1)));
-  h.allocs.push_back(d);
-  h.flags = d;
-  h.counters = d + T.T;
-  OCTMG_CUDA(cudaMemset(d, 0, sizeof(int) * ((size_t)T.T + h.n_counters + 1)));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, smooth_kernel_ptr(), 256, 0);
   h.smooth_grid = sms * std::max(per, 1);
+  const char* pk = getenv("OCTMG_PASS_KERNEL");
+  h.pass_kernel = (pk && std::string(pk) == "stage") ? 1 : 0;
+  const char* pc = getenv("OCTMG_PASS_CPT");
+  h.pass_cpt = pc ? std::max(1, std::min(2, atoi(pc))) : 2;
+  const Tree& T = *h.tree;
+  const char* sc = getenv("OCTMG_SUBCYCLE");
+  h.sub_K = -1;
+  if (!(sc && std::string(sc) == "0"))
+    for (int l = 0; l <= std::min(T.L, subcycle_max_level()); ++l) {
+      if (h.lvl_n[l] > subcycle_max_tiles()) break;
+      h.sub_K = l;
+    }
+  if (T.NL > T.lc[T.L]) h.ops.push_back(Op{2, 0, 0});  // coarse leaves start the cycle at 0
+  Builder b{h};
+  b.fas(T.L, false);
   return OCTMG_OK;
 }
 
 int64_t schedule_kernels(const Hier& h) {
   int64_t n = 0;
-  for (const Op& op : h.ops) n += op.kind <= 1;
+  for (const Op& op : h.ops) n += op.kind != 2;
   return n;
 }
 
@@ -245,11 +186,6 @@ struct ProfScope {
 
 void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   const Tree& T = *h.tree;
-  if (op.kind == 3) {
-    ProfScope ps(h, KC_MEMSET, s, 4.0 * ((double)T.T + h.n_counters));
-    cudaMemsetAsync(h.flags, 0, sizeof(int) * ((size_t)T.T + h.n_counters), s);
-    return;
-  }
   if (op.kind == 2) {
     size_t first = (size_t)T.lc[T.L] * TB3;
     ProfScope ps(h, KC_MEMSET, s, 4.0 * ((double)T.NL * TB3 - first));
@@ -264,35 +200,40 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.order = h.order + h.lvl_order_off[l];
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
-  a.flags = h.flags;
-  a.epoch = op.epoch;
-  a.has_prolong = 0;
+  a.stage[0] = op.stage;
+  if (op.kind == 4) {
+    ProfScope ps(h, KC_SUBCYCLE, s, 0.0);
+    launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, s);
+    return;
+  }
+  if (op.kind == 3) {
+    // read u, record; write u (8 + 16 B/cell) + the parents' u, u* (1 B/cell)
+    ProfScope ps(h, KC_PROLONG, s, 25.0 * a.n * TB3);
+    launch_prolong(a, s);
+    return;
+  }
   if (op.kind == 1) {
-    a.items = nullptr; a.nstages = 0; a.counter = nullptr;
+    a.run = 1;
     // read u, b, record; write b (inner cells of the level)
     ProfScope ps(h, KC_FASRHS, s, 28.0 * T.ic[l] * TB3);
     launch_fasrhs(a, T.ic[l], s);
     return;
   }
-  const ItemList& L = h.lists[op.list];
-  a.items = L.items;
-  a.nstages = op.nstages;
-  a.counter = h.counters + op.counter;
-  bool restrict_ = false;
-  for (int k = 0; k < op.nstages; ++k) {
-    a.stage[k] = op.stage[k];
-    if ((op.stage[k] >> 1) == SM_PRO1) a.has_prolong = 1;
-    if ((op.stage[k] >> 1) == SM_RESTRICT) restrict_ = true;
-  }
-  // algorithmic bytes of the launch: every cell's u, b and 16-byte record read once and u
-  // written once (28 B/cell); restriction adds the parents' u, u*, b (1.5 B/cell),
-  // prolongation the parents' u, u* (1 B/cell)
-  double cells = (double)a.n * TB3;
-  double bytes = cells * 28.0 + (restrict_ ? 1.5 * cells : 0.0) + (a.has_prolong ? 1.0 * cells : 0.0);
-  int cls = l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : (a.has_prolong ? KC_SMOOTH_POST : KC_SMOOTH_PRE));
-  int grid = (int)std::min<int64_t>(h.smooth_grid, (int64_t)L.n_items);
+  const int mode = op.stage >> 1;
+  a.run = (a.n + h.smooth_grid - 1) / h.smooth_grid;
+  const int grid = (a.n + a.run - 1) / a.run;
+  // algorithmic bytes per cell of the level: colour pass = read u, b, 16-byte record, write
+  // u (28 B; 24 B when u is known zero); restrict = read u, b, record (24 B) + the parents'
+  // u, u*, b (1.5 B); prolongation-fused passes read the parents' u, u* (+1 B)
+  const double cells = (double)a.n * TB3;
+  double bytes = cells * (mode == SM_RESTRICT ? 25.5 : (mode == SM_ZERO1 ? 24.0 : 28.0));
+  if (mode == SM_PRO1 || mode == SM_PRO2) bytes += cells;
+  int cls = mode == SM_RESTRICT ? KC_RESTRICT
+          : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
   ProfScope ps(h, cls, s, bytes);
-  launch_smooth(a, grid, s);
+  if (h.pass_kernel == 1) launch_smooth(a, grid, s);
+  else if (mode == SM_RESTRICT) launch_restrict_direct(a, s);
+  else launch_pass_direct(a, s, a.n >= 1024 ? h.pass_cpt : 1);
 }
 
 octmg_status run_M(Hier& h, cudaStream_t s) {
@@ -400,6 +341,7 @@ octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const 
   auto fail = [&](octmg_status e) { delete hh; return e; };
   if ((st = halloc(h.allocs, &h.coef, (size_t)T.T * TB3))) return fail(st);
   if ((st = halloc(h.allocs, &h.glayer_val, (size_t)T.n_glayers * 64))) return fail(st);
+  if ((st = halloc(h.allocs, &h.act, NLc / 32))) return fail(st);
   if ((st = halloc(h.allocs, &h.z, NLc))) return fail(st);
   if ((st = halloc(h.allocs, &h.uinA, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.binner, NIc))) return fail(st);
@@ -424,6 +366,7 @@ octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const 
   if (e != cudaSuccess) return fail(cuda_status(e, "memset"));
   if ((st = assemble_leaf_coefs(h, kind, face_beta, face_frac, s))) return fail(st);
   if ((st = coarsen_all(h, s))) return fail(st);
+  launch_build_mask(h.coef, (int64_t)NLc, h.act, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail(cuda_status(e, "setup"));
   if ((st = build_schedule(h))) return fail(st);
@@ -455,8 +398,10 @@ octmg_status octmg_apply(octmg_hier* hh, const float* x, float* y, octmg_stream 
   if (!hh || !x || !y) { set_error("null argument"); return OCTMG_E_INVALID; }
   Hier& h = hh->h;
   cudaStream_t s = (cudaStream_t)stream;
+  // mask the caller's x to the active cells (the operator kernel relies on zeros there)
+  launch_mask_copy(x, h.act, h.p1, (int64_t)h.tree->NL * TB3, s);
   ApplyArgs a = apply_args(h);
-  a.z = x;
+  a.z = h.p1;
   a.q = y;
   {
     ProfScope ps(h, KC_APPLY, s, (double)h.tree->NL * TB3 * 24.0);  // read x, record; write y
@@ -472,7 +417,7 @@ octmg_status octmg_vcycle(octmg_hier* hh, const float* b, float* u, octmg_stream
   Hier& h = hh->h;
   cudaStream_t s = (cudaStream_t)stream;
   size_t N = (size_t)h.tree->NL * TB3;
-  launch_mask_copy(b, h.coef, h.r, (int64_t)N, s);
+  launch_mask_copy(b, h.act, h.r, (int64_t)N, s);
   OCTMG_TRY(run_M(h, s));
   OCTMG_CUDA(cudaMemcpyAsync(u, h.z, N * sizeof(float), cudaMemcpyDeviceToDevice, s));
   OCTMG_CUDA(cudaGetLastError());
@@ -513,13 +458,13 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   hs->n_active = h.n_active;
   OCTMG_CUDA(cudaMemcpyAsync(&h.sc->n_active, &hs->n_active, sizeof(double), cudaMemcpyHostToDevice, s));
   {
-    ProfScope ps(h, KC_INIT, s, (double)N * 28.0);  // read b, record; write r, x
-    launch_init(b, h.coef, h.r, x, N, h.partial, h.counter, h.sc, s, G);
+    ProfScope ps(h, KC_INIT, s, (double)N * 12.125);  // read b, mask; write r, x
+    launch_init(b, h.act, h.r, x, N, h.partial, h.counter, h.sc, s, G);
   }
   h.launches++;
   if (ns) {
-    ProfScope ps(h, KC_PROJECT, s, (double)N * 24.0);  // read r, record; write r
-    launch_project(h.r, h.coef, N, h.partial, h.counter + 1, h.sc, s, G);
+    ProfScope ps(h, KC_PROJECT, s, (double)N * 8.125);  // read r, mask; write r
+    launch_project(h.r, h.act, N, h.partial, h.counter + 1, h.sc, s, G);
     h.launches++;
   }
   OCTMG_TRY(fetch());
@@ -556,8 +501,8 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     }
     h.launches += 2;
     if (ns) {
-      ProfScope ps(h, KC_PROJECT, s, (double)N * 24.0);
-      launch_project(h.r, h.coef, N, h.partial, h.counter + 1, h.sc, s, G);
+      ProfScope ps(h, KC_PROJECT, s, (double)N * 8.125);
+      launch_project(h.r, h.act, N, h.partial, h.counter + 1, h.sc, s, G);
       h.launches++;
     }
     OCTMG_CUDA(cudaGetLastError());

@@ -1,0 +1,157 @@
+// Sync-light tile kernels (sm_100a): RBGS colour pass, residual + restriction + Avg,
+// prolongation.  One CTA of 256 threads per 8^3 tile; each thread gathers the 7-point
+// stencil of its cell(s) directly through L1/L2 (in-tile neighbours are L1 hits of the
+// CTA's own loads; face neighbours come from the adjacent tiles via the cached neighbour
+// table).  No shared-memory staging: every load of a cell is independent and
+// in flight at once.  Ghost values are reconstructed per access (Eq. 12, P:L661-665,
+// P:L880-882) from the pass-start snapshot.
+#include "stencil.cuh"
+
+namespace octmg {
+
+namespace {
+
+constexpr int NT = 256;
+
+// RBGS colour pass, in place.  MODE: PLAIN, ZERO1 (first pass of the cycle:
+// all values zero), ZERO2 (second pass: own-colour cells still zero).  CPT colour cells per
+// thread (CPT = 2: the second cell is 4 z-layers up), NT/CPT threads per tile CTA.
+template <int MODE, int CPT>
+__global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_direct(SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  const int colour = a.stage[0] & 1;
+  const int j = threadIdx.x;
+  const int y = (j >> 2) & 7, z0 = j >> 5;
+  float* ut = tptr(a.u, t, a.NL);
+  const float* bt = tptr(a.b, t, a.NL);
+  const bool ghost = MODE != SM_ZERO1 && has_ghost(a, t);
+  float unew[CPT];
+  bool act[CPT];
+  int offs[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int z = z0 + k * (8 / CPT);
+    const int x = 2 * (j & 3) + ((colour + y + z) & 1);
+    const int off = loff(x, y, z);
+    offs[k] = off;
+    const float4 q = __ldg(a.coef + (size_t)t * TB3 + off);
+    const float b = __ldg(bt + off);
+    act[k] = q.x != 0.0f;
+    unew[k] = 0.0f;
+    if (act[k]) {
+      if (MODE == SM_ZERO1) {
+        unew[k] = b / q.x;
+      } else {
+        float ui = 0.0f, mP = 0.0f;
+        if (ghost) {
+          ui = MODE == SM_ZERO2 ? 0.0f : __ldg(ut + off);
+          mP = block_mean<MODE == SM_ZERO2>(a, t, x, y, z, colour);
+        }
+        unew[k] = (b - face_sum<MODE == SM_ZERO2>(a, t, x, y, z, q, ui, mP, colour, 0.0f)) / q.x;
+      }
+    }
+  }
+  __syncthreads();  // every pass-start read of this tile precedes the in-place writes
+#pragma unroll
+  for (int k = 0; k < CPT; ++k)
+    if (act[k] || MODE == SM_ZERO1 || MODE == SM_ZERO2) ut[offs[k]] = unew[k];
+}
+
+// Residual r = b - A^l u and, per parent (inner, level l-1): u* = mean of the active
+// children (Avg, Alg. 4 line 9), u^{l-1} := u*, b^{l-1} := beta * (R r), R = P^T / alpha
+// (Alg. 4 lines 8-10; "residual computation and restriction step are fused").
+// Thread layout: lanes of one 2x2x2 block are 4 apart in a warp (bits 2,3 = y&1, z&1), so
+// block sums are two xor-shuffles.
+__global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  const int j = threadIdx.x;
+  const int x2 = j & 3;
+  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
+  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
+  const int x0 = 2 * x2;
+  const size_t base = (size_t)t * TB3;
+  const int off0 = loff(x0, y, z);
+  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float2 uu = *reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0);
+  const float2 bb = *reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0);
+  __shared__ float su_t[TB3];
+  su_t[off0] = uu.x;
+  su_t[off0 + 1] = uu.y;
+  // active u sum / count of the block (also the ghost m_P of its cells)
+  float su = (q0.x != 0.0f ? uu.x : 0.0f) + (q1.x != 0.0f ? uu.y : 0.0f);
+  int na = (q0.x != 0.0f) + (q1.x != 0.0f);
+  su += __shfl_xor_sync(0xffffffffu, su, 4);
+  na += __shfl_xor_sync(0xffffffffu, na, 4);
+  su += __shfl_xor_sync(0xffffffffu, su, 8);
+  na += __shfl_xor_sync(0xffffffffu, na, 8);
+  const float mP = na ? su / (float)na : 0.0f;
+  __syncthreads();
+  float r0 = 0.0f, r1 = 0.0f;
+  if (q0.x != 0.0f) r0 = bb.x - face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, q0.x * uu.x, su_t);
+  if (q1.x != 0.0f) r1 = bb.y - face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, q1.x * uu.y, su_t);
+  float rs = r0 + r1;
+  rs += __shfl_xor_sync(0xffffffffu, rs, 4);
+  rs += __shfl_xor_sync(0xffffffffu, rs, 8);
+  if (((j >> 2) & 3) == 0) {
+    const int4 tv = __ldg(a.tile + t);
+    const int P = __ldg(a.parent + t);
+    const int pc = pcell_of(tv, x0, y, z);
+    const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
+    a.u.inner[pi] = mP;
+    a.ustar_w[pi] = mP;
+    a.b.inner[pi] = a.beta * (rs / a.alpha);
+  }
+}
+
+// Prolongation of the coarse update, in place: u_i += u^{l-1}_P - u*_P for every active
+// cell (Alg. 4 line 15; no beta).  4 cells per thread (float4).
+__global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  const int j = threadIdx.x;  // cells 4j .. 4j+3: x0 = 4*(j&1), y = (j>>1)&7, z = j>>4
+  const int x0 = 4 * (j & 1), y = (j >> 1) & 7, z = j >> 4;
+  const int4 tv = __ldg(a.tile + t);
+  const int P = __ldg(a.parent + t);
+  const size_t base = (size_t)t * TB3;
+  float4* up = reinterpret_cast<float4*>(tptr(a.u, t, a.NL) + loff(x0, y, z));
+  float4 u = *up;
+  const float* uc = tptr(a.u, P, a.NL);
+  const float* us = a.ustar + (size_t)(P - a.NL) * TB3;
+  const int pc0 = pcell_of(tv, x0, y, z), pc1 = pcell_of(tv, x0 + 2, y, z);
+  const float c0 = __ldg(uc + pc0) - __ldg(us + pc0), c1 = __ldg(uc + pc1) - __ldg(us + pc1);
+  const float4 q0 = __ldg(a.coef + base + loff(x0, y, z)), q1 = __ldg(a.coef + base + loff(x0 + 1, y, z));
+  const float4 q2 = __ldg(a.coef + base + loff(x0 + 2, y, z)), q3 = __ldg(a.coef + base + loff(x0 + 3, y, z));
+  if (q0.x != 0.0f) u.x += c0;
+  if (q1.x != 0.0f) u.y += c0;
+  if (q2.x != 0.0f) u.z += c1;
+  if (q3.x != 0.0f) u.w += c1;
+  *up = u;
+}
+
+}  // namespace
+
+template <int CPT>
+static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s) {
+  const int grid = a.n;
+  switch (mode) {
+    case SM_ZERO1: k_pass_direct<SM_ZERO1, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+    case SM_ZERO2: k_pass_direct<SM_ZERO2, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+    default: k_pass_direct<SM_PLAIN, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+  }
+}
+
+void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt) {
+  if (a.n == 0) return;
+  const int mode = a.stage[0] >> 1;
+  if (cpt == 2) launch_pass_cpt<2>(a, mode, s);
+  else launch_pass_cpt<1>(a, mode, s);
+}
+
+void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s) {
+  if (a.n) k_restrict_direct<<<a.n, NT, 0, s>>>(a);
+}
+
+void launch_prolong(const SmoothArgs& a, cudaStream_t s) {
+  if (a.n) k_prolong<<<a.n, 128, 0, s>>>(a);
+}
+
+}  // namespace octmg

@@ -1,8 +1,8 @@
-// Hot-path kernels (sm_100a).  One CTA per 8^3 tile: the tile's values are
-// staged in shared memory with a one-cell halo ("10x10x10 working region");
-// ghost values are reconstructed on the fly at halo load (Eq. 12);
-// coefficient records are float4 (c, c_x-, c_y-, c_z-) read with 128-bit loads and the
-// +face coefficients come from the neighbour record or the ghost layer.
+// PCG kernels (sm_100a): the composite operator fused with p = z + beta p and the fp64 p.q
+// reduction, and the vector updates / dots.  One CTA per 8^3 tile for the operator; the
+// stencil is gathered directly through L1/L2 (see direct.cu); coefficient records are
+// float4 (c, c_x-, c_y-, c_z-) and the +face coefficient comes from the neighbour record or
+// the ghost layer.
 #include "octmg_internal.cuh"
 
 namespace octmg {
@@ -11,80 +11,9 @@ namespace {
 
 constexpr int NT = 256;  // threads per tile CTA; thread -> cells (2*x2, y, z), (2*x2+1, y, z)
 
-__device__ __forceinline__ int su_idx(int x, int y, int z) { return (z + 1) * 100 + (y + 1) * 10 + (x + 1); }
-__device__ __forceinline__ int scx_idx(int x, int y, int z) { return (z * 8 + y) * 9 + x; }   // x in 0..8
-__device__ __forceinline__ int scy_idx(int x, int y, int z) { return (z * 9 + y) * 8 + x; }   // y in 0..8
-__device__ __forceinline__ int scz_idx(int x, int y, int z) { return (z * 8 + y) * 8 + x; }   // z in 0..8
 __device__ __forceinline__ int loff(int x, int y, int z) { return x + 8 * y + 64 * z; }
 __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
 
-struct TileSmem {
-  float u[1000];
-  float cx[576];
-  float cy[576];
-  float cz[576];
-  float c[512];
-  int nb[6];
-  int4 tv;
-  int4 ntv[6];     // neighbour tile coords (prolongation parity)
-  int npar[6];     // neighbour tile parents
-  int par;
-};
-
-// own boundary cell adjacent to halo item (f, p, q) and the source cell in the neighbour
-__device__ __forceinline__ void face_cells(int f, int p, int q, int own[3], int src[3], int halo[3]) {
-  int a = f >> 1, s = f & 1;
-  int o[3];
-  if (a == 0) { o[0] = s ? 7 : 0; o[1] = p; o[2] = q; }
-  else if (a == 1) { o[0] = p; o[1] = s ? 7 : 0; o[2] = q; }
-  else { o[0] = p; o[1] = q; o[2] = s ? 7 : 0; }
-  for (int k = 0; k < 3; ++k) { own[k] = o[k]; src[k] = o[k]; halo[k] = o[k]; }
-  src[a] = s ? 0 : 7;
-  halo[a] = s ? 8 : -1;
-}
-
-// mean of the active cells of the 2x2x2 block (parent's children) holding own cell o
-__device__ __forceinline__ float block_mean(const TileSmem& S, const int o[3]) {
-  int bx = o[0] & ~1, by = o[1] & ~1, bz = o[2] & ~1;
-  float s = 0.0f;
-  int n = 0;
-  for (int dz = 0; dz < 2; ++dz)
-    for (int dy = 0; dy < 2; ++dy)
-      for (int dx = 0; dx < 2; ++dx) {
-        int off = loff(bx + dx, by + dy, bz + dz);
-        if (S.c[off] != 0.0f) { s += S.u[su_idx(bx + dx, by + dy, bz + dz)]; n++; }
-      }
-  return n ? s / (float)n : 0.0f;
-}
-
-__device__ __forceinline__ void set_plus_coef(TileSmem& S, int a, const int halo[3], float v) {
-  if (a == 0) S.cx[scx_idx(8, halo[1], halo[2])] = v;
-  else if (a == 1) S.cy[scy_idx(halo[0], 8, halo[2])] = v;
-  else S.cz[scz_idx(halo[0], halo[1], 8)] = v;
-}
-
-__device__ __forceinline__ float rowsum(const TileSmem& S, int x, int y, int z, float c) {
-  // c*u first, then faces x-, x+, y-, y+, z-, z+ (the oracle's order)
-  int iu = su_idx(x, y, z);
-  float s = c * S.u[iu];
-  s = fmaf(S.cx[scx_idx(x, y, z)], S.u[iu - 1], s);
-  s = fmaf(S.cx[scx_idx(x + 1, y, z)], S.u[iu + 1], s);
-  s = fmaf(S.cy[scy_idx(x, y, z)], S.u[iu - 10], s);
-  s = fmaf(S.cy[scy_idx(x, y + 1, z)], S.u[iu + 10], s);
-  s = fmaf(S.cz[scz_idx(x, y, z)], S.u[iu - 100], s);
-  s = fmaf(S.cz[scz_idx(x, y, z + 1)], S.u[iu + 100], s);
-  return s;
-}
-
-
-// ------------------------------------------------------------------------------------
-// Composite operator (PCG q = A p with p = z + beta p fused, and the p.q dot)
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ float dir_val(const ApplyArgs& a, float beta, size_t i) {
-  float v = a.z[i];
-  if (a.pold) v = fmaf(beta, a.pold[i], v);
-  return v;
-}
 
 __device__ __forceinline__ double block_reduce_d(double v, double* sred) {
   for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -120,89 +49,115 @@ __device__ __forceinline__ bool last_block_sum(double mine, double* partial, uns
   return threadIdx.x == 0;
 }
 
+// direction value p = z + beta p_old of cell i; z and p_old are zero on inactive cells (the
+// cycle never writes them, octmg_apply masks its input first), so no activity test
+__device__ __forceinline__ float pval(const ApplyArgs& a, float beta, size_t i) {
+  float v = __ldg(a.z + i);
+  if (a.pold) v = fmaf(beta, __ldg(a.pold + i), v);
+  return v;
+}
+
+// Composite operator row: same-level leaf neighbours give their value, a
+// same-level inner neighbour the mean of its active children (all leaves), a ghost
+// g = p_i + (p_C - m_P)/2 (Eq. 12), walls 0.  Face order x-, x+, y-, y+, z-, z+.
+__device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta, int t, int x, int y, int z,
+                                                 const float4& q, float pi, float mP, float s0, const float* sp) {
+  const size_t base = (size_t)t * TB3;
+  const int c[3] = {x, y, z};
+  float s = s0;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
+    int nc[3] = {c[0], c[1], c[2]};
+    nc[ax] += sg;
+    float v = 0.0f, cf = (f & 1) ? 0.0f : comp(q, ax);
+    if (nc[ax] >= 0 && nc[ax] < 8) {
+      const int no = loff(nc[0], nc[1], nc[2]);
+      if (f & 1) cf = comp(__ldg(a.coef + base + no), ax);
+      v = sp[no];  // this tile's p, staged in shared memory
+    } else {
+      const int n = __ldg(a.nbr + 6 * t + f);
+      nc[ax] &= 7;
+      const int no = loff(nc[0], nc[1], nc[2]);
+      if (n >= 0) {
+        if (f & 1) cf = comp(__ldg(a.coef + (size_t)n * TB3 + no), ax);
+        if (n < a.NL) {
+          v = pval(a, beta, (size_t)n * TB3 + no);
+        } else {
+          const int ct = __ldg(a.child + 8 * (n - a.NL) + (nc[0] >> 2) + 2 * (nc[1] >> 2) + 4 * (nc[2] >> 2));
+          float sm = 0.0f;
+          int k = 0;
+          for (int dz = 0; dz < 2; ++dz)
+            for (int dy = 0; dy < 2; ++dy)
+              for (int dx = 0; dx < 2; ++dx) {
+                const size_t ci = (size_t)ct * TB3 + loff((2 * nc[0] + dx) & 7, (2 * nc[1] + dy) & 7, (2 * nc[2] + dz) & 7);
+                if (__ldg(a.coef + ci).x != 0.0f) { sm += pval(a, beta, ci); k++; }
+              }
+          v = k ? sm / (float)k : 0.0f;
+        }
+      } else if (n <= -2) {
+        if (f & 1)
+          cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 +
+                     (ax == 0 ? y + 8 * z : (ax == 1 ? x + 8 * z : x + 8 * y)));
+        const int C = -2 - n;
+        const int4 tv = __ldg(a.tile + t);
+        int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
+        g[ax] += sg;
+        const size_t ci = (size_t)C * TB3 + loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
+        if (__ldg(a.coef + ci).x != 0.0f) v = pi + 0.5f * (pval(a, beta, ci) - mP);
+      }
+    }
+    s = fmaf(cf, v, s);
+  }
+  return s;
+}
+
+// q = A p with p = z + beta p_old formed on the fly (and stored), plus the fp64 partial of
+// p.q with a deterministic last-block reduction that sets sigma and alpha = rho / sigma
+// (Alg. 1 lines 9-10; fp64 dots P:L1233).  Thread layout as the restriction: the
+// four lanes of a 2x2x2 block are xor 4 / xor 8 apart (ghost m_P by shuffles).
 template <bool DOT>
-__global__ __launch_bounds__(NT) void k_apply(ApplyArgs a) {
-  __shared__ TileSmem S;
+__global__ __launch_bounds__(NT, 6) void k_apply(ApplyArgs a) {
   __shared__ double sred[NT / 32];
   const int t = blockIdx.x;
-  const int tid = threadIdx.x;
+  const int j = threadIdx.x;
+  const int x2 = j & 3;
+  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
+  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
+  const int x0 = 2 * x2;
   const float beta = (a.use_beta && a.pold) ? (float)a.sc->beta : 0.0f;
-  if (tid < 6) S.nb[tid] = a.nbr[6 * t + tid];
-  if (tid == 6) S.tv = a.tile[t];
-  const int x2 = tid & 3, y = (tid >> 2) & 7, z = tid >> 5, x0 = 2 * x2;
-  const int off0 = loff(x0, y, z);
   const size_t base = (size_t)t * TB3;
-  float4 q0 = a.coef[base + off0], q1 = a.coef[base + off0 + 1];
-  float p0v, p1v;
+  const int off0 = loff(x0, y, z);
+  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  float p0 = 0.0f, p1 = 0.0f;
   {
-    float2 zz = *reinterpret_cast<const float2*>(a.z + base + off0);
-    p0v = zz.x; p1v = zz.y;
+    float2 zz = __ldg(reinterpret_cast<const float2*>(a.z + base + off0));
+    p0 = zz.x; p1 = zz.y;
     if (a.pold) {
-      float2 pp = *reinterpret_cast<const float2*>(a.pold + base + off0);
-      p0v = fmaf(beta, pp.x, p0v);
-      p1v = fmaf(beta, pp.y, p1v);
+      float2 pp = __ldg(reinterpret_cast<const float2*>(a.pold + base + off0));
+      p0 = fmaf(beta, pp.x, p0);
+      p1 = fmaf(beta, pp.y, p1);
     }
-    if (q0.x == 0.0f) p0v = 0.0f;
-    if (q1.x == 0.0f) p1v = 0.0f;
+    if (q0.x == 0.0f) p0 = 0.0f;
+    if (q1.x == 0.0f) p1 = 0.0f;
   }
-  if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0v, p1v);
-  S.u[su_idx(x0, y, z)] = p0v;
-  S.u[su_idx(x0 + 1, y, z)] = p1v;
-  S.c[off0] = q0.x;
-  S.c[off0 + 1] = q1.x;
-  S.cx[scx_idx(x0, y, z)] = q0.y;
-  S.cx[scx_idx(x0 + 1, y, z)] = q1.y;
-  S.cy[scy_idx(x0, y, z)] = q0.z;
-  S.cy[scy_idx(x0 + 1, y, z)] = q1.z;
-  S.cz[scz_idx(x0, y, z)] = q0.w;
-  S.cz[scz_idx(x0 + 1, y, z)] = q1.w;
+  if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0, p1);
+  __shared__ float sp[TB3];
+  sp[off0] = p0;
+  sp[off0 + 1] = p1;
+  float su = p0 + p1;
+  int na = (q0.x != 0.0f) + (q1.x != 0.0f);
+  su += __shfl_xor_sync(0xffffffffu, su, 4);
+  na += __shfl_xor_sync(0xffffffffu, na, 4);
+  su += __shfl_xor_sync(0xffffffffu, su, 8);
+  na += __shfl_xor_sync(0xffffffffu, na, 8);
+  const float mP = na ? su / (float)na : 0.0f;
   __syncthreads();
-  for (int w = tid; w < 384; w += NT) {
-    int f = w >> 6, p = w & 7, q = (w >> 3) & 7;
-    int own[3], src[3], halo[3];
-    face_cells(f, p, q, own, src, halo);
-    int ax = f >> 1;
-    int n = S.nb[f];
-    float v = 0.0f, cplus = 0.0f;
-    if (n >= 0) {
-      int so = loff(src[0], src[1], src[2]);
-      float4 r = a.coef[(size_t)n * TB3 + so];
-      cplus = comp(r, ax);
-      if (n < a.NL) {
-        if (r.x != 0.0f) v = dir_val(a, beta, (size_t)n * TB3 + so);
-      } else {
-        // inner same-level neighbour: mean of its active children (all leaves)
-        int ct = a.child[8 * (n - a.NL) + (src[0] >> 2) + 2 * (src[1] >> 2) + 4 * (src[2] >> 2)];
-        float s = 0.0f;
-        int k = 0;
-        for (int dz = 0; dz < 2; ++dz)
-          for (int dy = 0; dy < 2; ++dy)
-            for (int dx = 0; dx < 2; ++dx) {
-              size_t ci = (size_t)ct * TB3 +
-                          loff((2 * src[0] + dx) & 7, (2 * src[1] + dy) & 7, (2 * src[2] + dz) & 7);
-              if (a.coef[ci].x != 0.0f) { s += dir_val(a, beta, ci); k++; }
-            }
-        v = k ? s / (float)k : 0.0f;
-      }
-    } else if (n <= -2) {
-      int C = -2 - n;
-      int g0 = S.tv.y * 8 + halo[0], g1 = S.tv.z * 8 + halo[1], g2 = S.tv.w * 8 + halo[2];
-      size_t ci = (size_t)C * TB3 + loff((g0 >> 1) & 7, (g1 >> 1) & 7, (g2 >> 1) & 7);
-      if (a.coef[ci].x != 0.0f) {
-        float pc = dir_val(a, beta, ci);
-        v = S.u[su_idx(own[0], own[1], own[2])] + 0.5f * (pc - block_mean(S, own));
-      }
-      if (f & 1) cplus = a.glayer_val[(size_t)a.glayer[3 * t + ax] * 64 + p + 8 * q];
-    }
-    S.u[su_idx(halo[0], halo[1], halo[2])] = v;
-    if (f & 1) set_plus_coef(S, ax, halo, cplus);
-  }
-  __syncthreads();
-  float r0 = q0.x != 0.0f ? rowsum(S, x0, y, z, q0.x) : 0.0f;
-  float r1 = q1.x != 0.0f ? rowsum(S, x0 + 1, y, z, q1.x) : 0.0f;
+  const float r0 = q0.x != 0.0f ? composite_faces(a, beta, t, x0, y, z, q0, p0, mP, q0.x * p0, sp) : 0.0f;
+  const float r1 = q1.x != 0.0f ? composite_faces(a, beta, t, x0 + 1, y, z, q1, p1, mP, q1.x * p1, sp) : 0.0f;
   *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
   if (DOT) {
-    double d = (double)p0v * (double)r0 + (double)p1v * (double)r1;
+    double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
     double tot;
     double bs = block_reduce_d(d, sred);
     if (last_block_sum(bs, a.partial, a.counter, gridDim.x, &tot, sred)) {
@@ -217,17 +172,19 @@ __global__ __launch_bounds__(NT) void k_apply(ApplyArgs a) {
 // ------------------------------------------------------------------------------------
 // PCG vector kernels (grid-stride over float4, fixed grid => deterministic partials)
 // ------------------------------------------------------------------------------------
-__device__ __forceinline__ bool active_of(const float4* coef, int64_t i) { return coef[i].x != 0.0f; }
+// activity nibble of the 4 cells of float4 index i (bit k = cell 4i+k active; mask bit per cell)
+__device__ __forceinline__ unsigned act4(const uint32_t* act, int64_t i) { return (act[i >> 3] >> ((i & 7) * 4)) & 0xFu; }
 
-__global__ __launch_bounds__(256) void k_init(const float* b, const float4* coef, float* r, float* x, int64_t n4,
+__global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n4,
                                               double* partial, unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   double s2 = 0.0, s1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 v = reinterpret_cast<const float4*>(b)[i];
     float m[4] = {v.x, v.y, v.z, v.w};
+    const unsigned am = act4(act, i);
     for (int k = 0; k < 4; ++k) {
-      if (!active_of(coef, 4 * i + k)) m[k] = 0.0f;
+      if (!((am >> k) & 1u)) m[k] = 0.0f;
       s2 += (double)m[k] * m[k];
       s1 += (double)m[k];
     }
@@ -283,7 +240,7 @@ __global__ __launch_bounds__(256) void k_update(float* x, float* r, const float*
 }
 
 // null-space projection r -= mean_active(r), recomputes ||r||^2
-__global__ __launch_bounds__(256) void k_project(float* r, const float4* coef, int64_t n4, double* partial,
+__global__ __launch_bounds__(256) void k_project(float* r, const uint32_t* act, int64_t n4, double* partial,
                                                  unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   const float m = (float)(sc->rsum / sc->n_active);
@@ -291,8 +248,9 @@ __global__ __launch_bounds__(256) void k_project(float* r, const float4* coef, i
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 v = reinterpret_cast<float4*>(r)[i];
     float e[4] = {v.x, v.y, v.z, v.w};
+    const unsigned am = act4(act, i);
     for (int k = 0; k < 4; ++k) {
-      if (active_of(coef, 4 * i + k)) e[k] -= m;
+      if ((am >> k) & 1u) e[k] -= m;
       s2 += (double)e[k] * e[k];
     }
     reinterpret_cast<float4*>(r)[i] = make_float4(e[0], e[1], e[2], e[3]);
@@ -324,9 +282,18 @@ __global__ __launch_bounds__(256) void k_dot_rz(const float* r, const float* z, 
   }
 }
 
-__global__ void k_mask_copy(const float* src, const float4* coef, float* dst, int64_t n) {
+__global__ void k_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = coef[i].x != 0.0f ? src[i] : 0.0f;
+    dst[i] = ((act[i >> 5] >> (i & 31)) & 1u) ? src[i] : 0.0f;
+}
+
+// activity bitmask of the leaf cells (bit i%32 of word i/32: c_i != 0)
+__global__ void k_build_mask(const float4* coef, int64_t nwords, uint32_t* act) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = 0;
+    for (int k = 0; k < 32; ++k) m |= (coef[32 * w + k].x != 0.0f ? 1u : 0u) << k;
+    act[w] = m;
+  }
 }
 
 }  // namespace
@@ -337,24 +304,27 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   else k_apply<false><<<a.NL, NT, 0, s>>>(a);
 }
 
-void launch_init(const float* b, const float4* coef, float* r, float* x, int64_t n, double* partial,
+void launch_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n, double* partial,
                  unsigned* counter, Scalars* sc, cudaStream_t s, int grid) {
-  k_init<<<grid, 256, 0, s>>>(b, coef, r, x, n / 4, partial, counter, sc);
+  k_init<<<grid, 256, 0, s>>>(b, act, r, x, n / 4, partial, counter, sc);
 }
 void launch_update(float* x, float* r, const float* p, const float* q, int64_t n, double* partial,
                    unsigned* counter, Scalars* sc, cudaStream_t s, int grid) {
   k_update<<<grid, 256, 0, s>>>(x, r, p, q, n / 4, partial, counter, sc);
 }
-void launch_project(float* r, const float4* coef, int64_t n, double* partial, unsigned* counter, Scalars* sc,
+void launch_project(float* r, const uint32_t* act, int64_t n, double* partial, unsigned* counter, Scalars* sc,
                     cudaStream_t s, int grid) {
-  k_project<<<grid, 256, 0, s>>>(r, coef, n / 4, partial, counter, sc);
+  k_project<<<grid, 256, 0, s>>>(r, act, n / 4, partial, counter, sc);
 }
 void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, unsigned* counter, Scalars* sc,
                    int first, cudaStream_t s, int grid) {
   k_dot_rz<<<grid, 256, 0, s>>>(r, z, n / 4, partial, counter, sc, first);
 }
-void launch_mask_copy(const float* src, const float4* coef, float* dst, int64_t n, cudaStream_t s) {
-  k_mask_copy<<<592, 256, 0, s>>>(src, coef, dst, n);
+void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s) {
+  k_mask_copy<<<592, 256, 0, s>>>(src, act, dst, n);
+}
+void launch_build_mask(const float4* coef, int64_t n, uint32_t* act, cudaStream_t s) {
+  k_build_mask<<<592, 256, 0, s>>>(coef, n / 32, act);
 }
 
 }  // namespace octmg

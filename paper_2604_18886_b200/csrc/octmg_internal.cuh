@@ -84,8 +84,8 @@ struct Scalars {
 
 // Kernel classes for profiling
 enum KClass {
-  KC_SMOOTH_PRE = 0, KC_SMOOTH_POST, KC_COARSEST, KC_FASRHS, KC_SMOOTH_COARSE,
-  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_COUNT
+  KC_PASS = 0, KC_PROLONG, KC_RESTRICT, KC_COARSEST, KC_FASRHS, KC_SMOOTH_COARSE,
+  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_COUNT
 };
 extern const char* kclass_name[KC_COUNT];
 
@@ -112,18 +112,18 @@ struct ApplyArgs {
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
 // vector kernels (PCG)
-void launch_init(const float* b, const float4* coef, float* r, float* x, int64_t n, double* partial,
+void launch_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n, double* partial,
                  unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
 void launch_update(float* x, float* r, const float* p, const float* q, int64_t n, double* partial,
                    unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
-void launch_project(float* r, const float4* coef, int64_t n, double* partial, unsigned* counter,
+void launch_project(float* r, const uint32_t* act, int64_t n, double* partial, unsigned* counter,
                     Scalars* sc, cudaStream_t s, int grid);
 void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, unsigned* counter,
                    Scalars* sc, int first, cudaStream_t s, int grid);
-void launch_mask_copy(const float* src, const float4* coef, float* dst, int64_t n, cudaStream_t s);
+void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);
+void launch_build_mask(const float4* coef, int64_t n, uint32_t* act, cudaStream_t s);
 
-// persistent wavefront smoother (smooth.cu)
-constexpr int MAX_STAGES = 48;
+// smoother stage kernels (smooth.cu)
 struct SmoothArgs {
   const int4* tile;
   const int* nbr;
@@ -131,26 +131,29 @@ struct SmoothArgs {
   const float4* coef;
   const float* glayer_val;
   const int* glayer;
-  Fld u;                // in-place level values (all levels share the buffer)
+  Fld u;                // in-place cycle values (all levels share the buffer)
   const float* ustar;   // inner-indexed u* (prolongation)
   float* ustar_w;       // inner-indexed u* output (restrict stage)
   Fld b;                // leaf = PCG residual r, inner = FAS rhs
   float beta, alpha;
   int NL;
   const int* order;     // tiles of the level in rank order (slab-major)
-  const int* items;     // (stage << 24) | rank, issue order
   int n;                // tiles in the level
-  int nstages;
+  int run;              // tiles per CTA
   int first_tile;       // k_fasrhs: first inner tile of the level
-  int has_prolong;
-  int* flags;           // per-tile stage completion (epoch + s + 1)
-  int* counter;         // work counter of this launch
-  int epoch;
-  int stage[MAX_STAGES];  // bit0 colour, bits1.. mode
+  int stage[1];         // bit0 colour, bits1.. mode
 };
 void launch_smooth(const SmoothArgs& a, int grid, cudaStream_t s);
 const void* smooth_kernel_ptr();
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
+void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
+void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s);
+void launch_prolong(const SmoothArgs& a, cudaStream_t s);
+int subcycle_max_tiles();
+int subcycle_max_level();
+void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
+                     const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
+                     cudaStream_t s);
 
 // setup kernels (setup.cu)
 struct SetupArgs;
@@ -166,25 +169,16 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
 // Hierarchy (coefficients + multigrid work buffers + PCG state)
 // ------------------------------------------------------------------------------------
 struct Op {
-  int kind;    // 0 smooth launch, 1 FAS rhs, 2 zero coarse leaves, 3 reset flags/counters
+  int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle
   int level;
-  int list;    // index of the stage list (level, nstages) in Hier::lists
-  int epoch;
-  int counter;
-  int nstages;
-  int stage[MAX_STAGES];
-};
-
-struct ItemList {
-  int level, nstages;
-  int* items;   // device
-  int n_items;
+  int stage;   // bit0 colour, bits1.. mode (SM_*)
 };
 
 struct Hier {
   Tree* tree = nullptr;
   octmg_mg_params prm{};
   float4* coef = nullptr;        // [T*512] (c, cxm, cym, czm)
+  uint32_t* act = nullptr;       // [NL*512/32] activity bitmask of the leaf cells
   float* glayer_val = nullptr;   // [n_glayers*64]
   // multigrid buffers
   float* z = nullptr;            // [NL*512] leaf part of the cycle's u (in place) = M output
@@ -205,16 +199,13 @@ struct Hier {
   int any_dirichlet = 0;
   // schedule of one preconditioner application
   std::vector<Op> ops;
-  std::vector<ItemList> lists;
   int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
-  int lvl_D[MAXL + 1] = {};
-  int* inner_order = nullptr;    // not used (inner tiles are contiguous)
-  int* flags = nullptr;          // [T]
-  int* counters = nullptr;       // [n_counters]
-  int n_counters = 0;
-  int smooth_grid = 0;
+  int smooth_grid = 0;           // resident CTAs of the stage kernel (one wave)
+  int pass_kernel = 0;           // 0 direct (sync-light), 1 staged pipeline (OCTMG_PASS_KERNEL)
+  int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
+  int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   cudaGraphExec_t graph = nullptr;
   cudaStream_t graph_stream = nullptr;
   int64_t launches = 0;

@@ -1,22 +1,22 @@
-// Persistent wavefront smoother (sm_100a): one launch runs a whole smoothing phase of a
-// level — several red-black Gauss-Seidel colour passes and optionally the
-// fused residual + restriction + Avg of Alg. 4 lines 8-9 ("fused into one
-// kernel") — in place.
+// Smoother stage kernel (sm_100a): one launch = one stage over all tiles of a level — a
+// red-black Gauss-Seidel colour pass done IN PLACE, or the fused residual +
+// restriction + Avg of Alg. 4 lines 8-9 ("fused into one kernel").
+// An in-place colour-c pass is race-free: it reads only colour-(1-c) cells of other tiles
+// (the face neighbours of its colour-c cells) and its own tile, and writes only its own
+// colour-c cells; ghost values use the pass-start snapshot of the own tile (SURVEY c-5).
 //
-// Work items are (stage s, tile t).  Tiles of the level are ranked slab by slab (z, then
-// Morton in x,y) and items are issued in order of rank + s*D, D = 1 + the largest rank
-// gap between face neighbours, so every item's producers come earlier in the stream.
-// CTAs claim items with an atomic counter; an item (s, t) waits until stage s-1 is done
-// on t and its six same-level neighbours (per-tile flags, release/acquire), which orders
-// both the read-after-write and the write-after-read of the in-place colour passes, so
-// the result equals the sequential pass-by-pass order bit for bit.  Consecutive stages of
-// a slab run while the slab is still in L2, so HBM sees ~one read of (u, b, coefficients)
-// per launch instead of one per pass.  The next item's coefficient record (8 KB) and
-// right-hand side (2 KB) are prefetched by TMA bulk copies (cp.async.bulk + mbarrier)
-// while the current item computes.
+// Each CTA walks a contiguous run of tiles of the level in slab-major rank order (z, then
+// Morton of (x, y), so consecutive tiles share faces) with a two-deep software pipeline:
+// while tile i is computed, TMA bulk copies (cp.async.bulk + mbarrier) bring tile i+1's
+// u (2 KB), coefficient record (8 KB) and right-hand side (2 KB) into the other shared
+// buffer, and its face halos / ghost sources / prolongation parents are loaded into
+// registers.  The run length is sized so the grid is one wave of resident CTAs.
 #include "octmg_internal.cuh"
 
 namespace octmg {
+
+// stage descriptor: bit0 colour, bits 1..3 mode
+enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
 
 namespace {
 
@@ -50,14 +50,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 struct Meta {
   int4 tv;
@@ -71,12 +63,12 @@ struct Meta {
 struct Smem {
   float4 coef[2][512];
   float b[2][512];
-  float u[1000];
-  float cp[3][64];  // +face coefficients of the neighbour layer (x+, y+, z+)
-  float r[512];     // residual (restrict stage)
-  Meta meta[2];
+  float ub[2][512];  // own u (bulk copy)
+  float u[1000];     // own u + halo, the pass-start snapshot
+  float cp[3][64];   // +face coefficients of the neighbour layer (x+, y+, z+)
+  float r[512];      // residual (restrict stage)
+  Meta meta[3];
   uint64_t bar[2];
-  int item[2];
 };
 
 __device__ __forceinline__ void face_cells(int f, int p, int q, int own[3], int src[3], int halo[3]) {
@@ -147,154 +139,149 @@ __device__ __forceinline__ void load_meta(Meta& m, const SmoothArgs& a, int t, b
   }
 }
 
-__device__ __forceinline__ void issue_static(Smem& S, int buf, const SmoothArgs& a, int t) {
-  // one elected thread: coefficient record (8 KB) + right-hand side (2 KB) of tile t
-  mbar_expect_tx(&S.bar[buf], TB3 * 16 + TB3 * 4);
+__device__ __forceinline__ void issue_tile(Smem& S, int buf, const SmoothArgs& a, int t, bool with_u) {
+  // one elected thread: coefficient record (8 KB) + right-hand side (2 KB) + u (2 KB)
+  mbar_expect_tx(&S.bar[buf], TB3 * 16 + TB3 * 4 + (with_u ? TB3 * 4 : 0));
   bulk_g2s(&S.coef[buf][0], a.coef + (size_t)t * TB3, TB3 * 16, &S.bar[buf]);
   bulk_g2s(&S.b[buf][0], tptr(a.b, t, a.NL), TB3 * 4, &S.bar[buf]);
+  if (with_u) bulk_g2s(&S.ub[buf][0], tptr(a.u, t, a.NL), TB3 * 4, &S.bar[buf]);
+}
+
+// halo sources of one tile held in registers between prefetch and staging
+struct Halo {
+  float v[2], c[2], uc[2];
+  int kind[2];  // 0 zero, 1 value, 2 ghost (uc = coarse value)
+  float corr;   // prolongation correction of the thread's own cells
+};
+
+__device__ __forceinline__ void load_halo(Halo& H, const Meta& M, const SmoothArgs& a, int mode) {
+  const int tid = threadIdx.x;
+  const int x2 = tid & 3, y = (tid >> 2) & 7, z = tid >> 5, x0 = 2 * x2;
+  H.corr = 0.0f;
+  if (mode == SM_PRO1 || mode == SM_PRO2) {
+    int pc = pcell_of(M.tv, x0, y, z);
+    H.corr = __ldcg(tptr(a.u, M.par, a.NL) + pc) - a.ustar[(size_t)(M.par - a.NL) * TB3 + pc];
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    H.v[k] = 0.0f; H.c[k] = 0.0f; H.uc[k] = 0.0f; H.kind[k] = 0;
+    int w = tid + k * NT;
+    if (w >= 384) break;
+    int f = w >> 6, p = w & 7, q = (w >> 3) & 7;
+    int own[3], src[3], halo[3];
+    face_cells(f, p, q, own, src, halo);
+    int n = M.nb[f];
+    if (n >= 0) {
+      int so = loff(src[0], src[1], src[2]);
+      if (mode != SM_ZERO1) {
+        H.v[k] = __ldcg(tptr(a.u, n, a.NL) + so);
+        H.kind[k] = 1;
+      }
+      if ((f & 1) || mode == SM_PRO1) {
+        float4 r = a.coef[(size_t)n * TB3 + so];
+        H.c[k] = comp(r, f >> 1);
+        if (mode == SM_PRO1 && r.x != 0.0f) {
+          int P = M.npar[f];
+          int pc = pcell_of(M.ntv[f], src[0], src[1], src[2]);
+          H.v[k] += __ldcg(tptr(a.u, P, a.NL) + pc) - a.ustar[(size_t)(P - a.NL) * TB3 + pc];
+        }
+      }
+    } else if (n <= -2) {
+      int C = -2 - n;
+      int g0 = M.tv.y * 8 + halo[0], g1 = M.tv.z * 8 + halo[1], g2 = M.tv.w * 8 + halo[2];
+      int co = loff((g0 >> 1) & 7, (g1 >> 1) & 7, (g2 >> 1) & 7);
+      if (mode != SM_ZERO1 && a.coef[(size_t)C * TB3 + co].x != 0.0f) {
+        H.uc[k] = __ldcg(tptr(a.u, C, a.NL) + co);
+        H.kind[k] = 2;
+      }
+      if (f & 1) H.c[k] = a.glayer_val[(size_t)M.gl[f >> 1] * 64 + p + 8 * q];
+    }
+  }
 }
 
 }  // namespace
 
-// stage descriptor: bit0 colour, bits 1..3 mode
-enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
-
-__global__ __launch_bounds__(NT, 6) void k_smooth(SmoothArgs a) {
+__global__ __launch_bounds__(NT, 7) void k_stage(SmoothArgs a) {
   __shared__ __align__(128) Smem S;
   const int tid = threadIdx.x;
   const int x2 = tid & 3, y = (tid >> 2) & 7, z = tid >> 5, x0 = 2 * x2;
   const int off0 = loff(x0, y, z);
-  const int total = a.n * a.nstages;
-  const bool any_prolong = a.has_prolong;
+  const int desc = a.stage[0];
+  const int colour = desc & 1, mode = desc >> 1;
+  const bool pro = mode == SM_PRO1;
+  const int r0 = blockIdx.x * a.run;
+  const int r1 = min(a.n, r0 + a.run);
+  if (r0 >= r1) return;
   if (tid == 0) {
     mbar_init(&S.bar[0]);
     mbar_init(&S.bar[1]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    int it = atomicAdd(a.counter, 1);
-    S.item[0] = it;
-    if (it < total) issue_static(S, 0, a, a.order[a.items[it] & 0xFFFFFF]);
+    issue_tile(S, 0, a, a.order[r0], mode != SM_ZERO1);
+  }
+  if (tid >= 32 && tid < 40) {
+    load_meta(S.meta[0], a, a.order[r0], pro);
+    if (r0 + 1 < r1) load_meta(S.meta[1], a, a.order[r0 + 1], pro);
   }
   __syncthreads();
-  if (tid >= 32 && tid < 40 && S.item[0] < total) load_meta(S.meta[0], a, a.order[a.items[S.item[0]] & 0xFFFFFF], any_prolong);
+  Halo H, Hn;
+  load_halo(H, S.meta[0], a, mode);
   uint32_t phase[2] = {0u, 0u};
-  int cur = 0;
-  while (true) {
-    const int it = S.item[cur];
-    if (it >= total) break;
-    const int packed = a.items[it];
-    const int s = packed >> 24;
-    const int t = a.order[packed & 0xFFFFFF];
-    const int desc = a.stage[s];
-    const int colour = desc & 1, mode = desc >> 1;
-    // claim and prefetch the next item; wait for this item's producers
-    if (tid == 0) {
-      int nx = atomicAdd(a.counter, 1);
-      S.item[cur ^ 1] = nx;
-      if (nx < total) {
+  for (int i = r0; i < r1; ++i) {
+    const int k = i - r0;
+    const int cur = k & 1;
+    const Meta& M = S.meta[k % 3];
+    const int t = a.order[i];
+    // (b) prefetch tile i+1 (its buffers were freed by the sync that ended tile i-1)
+    if (i + 1 < r1) {
+      if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_static(S, cur ^ 1, a, a.order[a.items[nx] & 0xFFFFFF]);
+        issue_tile(S, cur ^ 1, a, a.order[i + 1], mode != SM_ZERO1);
       }
-      if (s > 0) {
-        const int need = a.epoch + s;
-        while (ld_acquire(a.flags + t) < need) __nanosleep(32);
-        for (int f = 0; f < 6; ++f) {
-          int n = a.nbr[6 * t + f];
-          if (n >= 0)
-            while (ld_acquire(a.flags + n) < need) __nanosleep(32);
-        }
-      }
+      load_halo(Hn, S.meta[(k + 1) % 3], a, mode);
+      if (i + 2 < r1 && tid >= 32 && tid < 40) load_meta(S.meta[(k + 2) % 3], a, a.order[i + 2], pro);
     }
-    __syncthreads();  // (1) producers done, next item published, meta[cur] visible
-    const Meta& M = S.meta[cur];
-    if (tid >= 32 && tid < 40 && S.item[cur ^ 1] < total)
-      load_meta(S.meta[cur ^ 1], a, a.order[a.items[S.item[cur ^ 1]] & 0xFFFFFF], any_prolong);
-    // own values
-    float u0 = 0.0f, u1 = 0.0f;
-    if (mode != SM_ZERO1) {
-      float2 uu = __ldcg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
-      u0 = uu.x; u1 = uu.y;
-    }
-    float corr = 0.0f;
-    if (mode == SM_PRO1 || mode == SM_PRO2) {
-      int pc = pcell_of(M.tv, x0, y, z);
-      corr = __ldcg(tptr(a.u, M.par, a.NL) + pc) - a.ustar[(size_t)(M.par - a.NL) * TB3 + pc];
-    }
-    // halo loads (values in registers until the own tile is in shared memory)
-    float hv[2] = {0.0f, 0.0f}, hc[2] = {0.0f, 0.0f}, huc[2] = {0.0f, 0.0f};
-    int hkind[2] = {0, 0};  // 0 zero, 1 value, 2 ghost (huc = coarse value)
-    for (int k = 0; k < 2; ++k) {
-      int w = tid + k * NT;
-      if (w >= 384) break;
-      int f = w >> 6, p = w & 7, q = (w >> 3) & 7;
-      int own[3], src[3], halo[3];
-      face_cells(f, p, q, own, src, halo);
-      int n = M.nb[f];
-      if (n >= 0) {
-        int so = loff(src[0], src[1], src[2]);
-        if (mode != SM_ZERO1) {
-          hv[k] = __ldcg(tptr(a.u, n, a.NL) + so);
-          hkind[k] = 1;
-        }
-        if ((f & 1) || mode == SM_PRO1) {
-          float4 r = a.coef[(size_t)n * TB3 + so];
-          hc[k] = comp(r, f >> 1);
-          if (mode == SM_PRO1 && r.x != 0.0f) {
-            int P = M.npar[f];
-            int pc = pcell_of(M.ntv[f], src[0], src[1], src[2]);
-            hv[k] += __ldcg(tptr(a.u, P, a.NL) + pc) - a.ustar[(size_t)(P - a.NL) * TB3 + pc];
-          }
-        }
-      } else if (n <= -2) {
-        int C = -2 - n;
-        int g0 = M.tv.y * 8 + halo[0], g1 = M.tv.z * 8 + halo[1], g2 = M.tv.w * 8 + halo[2];
-        int co = loff((g0 >> 1) & 7, (g1 >> 1) & 7, (g2 >> 1) & 7);
-        if (mode != SM_ZERO1 && a.coef[(size_t)C * TB3 + co].x != 0.0f) {
-          huc[k] = __ldcg(tptr(a.u, C, a.NL) + co);
-          hkind[k] = 2;
-        }
-        if (f & 1) hc[k] = a.glayer_val[(size_t)M.gl[f >> 1] * 64 + p + 8 * q];
-      }
-    }
+    // (c) own values: snapshot of this pass with the stage's transforms
     mbar_wait(&S.bar[cur], phase[cur]);
     phase[cur] ^= 1u;
     const float4 q0 = S.coef[cur][off0], q1 = S.coef[cur][off0 + 1];
-    // stage-specific transforms of the own values (snapshot of this pass)
+    float u0 = 0.0f, u1 = 0.0f;
+    if (mode != SM_ZERO1) { u0 = S.ub[cur][off0]; u1 = S.ub[cur][off0 + 1]; }
     if (mode == SM_PRO1) {
-      if (q0.x != 0.0f) u0 += corr;
-      if (q1.x != 0.0f) u1 += corr;
+      if (q0.x != 0.0f) u0 += H.corr;
+      if (q1.x != 0.0f) u1 += H.corr;
     } else if (mode == SM_PRO2 || mode == SM_ZERO2) {
-      const int selc = (colour + y + z) & 1;  // which of the two cells has this pass's colour
+      const int selc = (colour + y + z) & 1;
       float& uc = selc ? u1 : u0;
       const float qc = selc ? q1.x : q0.x;
       if (mode == SM_ZERO2) uc = 0.0f;
-      else if (qc != 0.0f) uc += corr;
+      else if (qc != 0.0f) uc += H.corr;
     }
     S.u[su_idx(x0, y, z)] = u0;
     S.u[su_idx(x0 + 1, y, z)] = u1;
-    __syncthreads();  // (2) own tile values in shared memory
-    for (int k = 0; k < 2; ++k) {
-      int w = tid + k * NT;
+    __syncthreads();  // own snapshot visible (ghosts need it)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      int w = tid + kk * NT;
       if (w >= 384) break;
       int f = w >> 6, p = w & 7, q = (w >> 3) & 7;
       int own[3], src[3], halo[3];
       face_cells(f, p, q, own, src, halo);
-      float v = hv[k];
-      if (hkind[k] == 2) v = S.u[su_idx(own[0], own[1], own[2])] + 0.5f * (huc[k] - block_mean(S, cur, own));
-      else if (hkind[k] == 0) v = 0.0f;
+      float v = H.v[kk];
+      if (H.kind[kk] == 2) v = S.u[su_idx(own[0], own[1], own[2])] + 0.5f * (H.uc[kk] - block_mean(S, cur, own));
+      else if (H.kind[kk] == 0) v = 0.0f;
       S.u[su_idx(halo[0], halo[1], halo[2])] = v;
-      if (f & 1) S.cp[f >> 1][p + 8 * q] = hc[k];
+      if (f & 1) S.cp[f >> 1][p + 8 * q] = H.c[kk];
     }
-    __syncthreads();  // (3) halo in shared memory
+    __syncthreads();  // halo visible
     if (mode != SM_RESTRICT) {
       const int sel = (colour + y + z) & 1;
       const int xc = x0 + sel;
       const float cc = sel ? q1.x : q0.x;
       if (cc != 0.0f) {
         float bc = S.b[cur][off0 + sel];
-        float unew = (bc - faces(S, cur, xc, y, z, 0.0f)) / cc;
-        tptr(a.u, t, a.NL)[off0 + sel] = unew;
-      } else if (mode == SM_ZERO2 || mode == SM_ZERO1) {
-        tptr(a.u, t, a.NL)[off0 + sel] = 0.0f;  // inactive cells stay 0 (memory held old data)
+        tptr(a.u, t, a.NL)[off0 + sel] = (bc - faces(S, cur, xc, y, z, 0.0f)) / cc;
+      } else if (mode == SM_ZERO1 || mode == SM_ZERO2) {
+        tptr(a.u, t, a.NL)[off0 + sel] = 0.0f;  // memory may hold a previous cycle's data
       }
     } else {
       // r = b - A^l u; per parent: u* = mean of active children, u^{l-1} := u*,
@@ -321,12 +308,8 @@ __global__ __launch_bounds__(NT, 6) void k_smooth(SmoothArgs a) {
         a.b.inner[pi] = a.beta * (rs / a.alpha);
       }
     }
-    __syncthreads();  // (4) all writes of this item issued; buffers of `cur` free
-    if (tid == 0) {
-      __threadfence();
-      st_release(a.flags + t, a.epoch + s + 1);
-    }
-    cur ^= 1;
+    H = Hn;
+    __syncthreads();  // buffers of `cur`, S.u and meta slot k%3 free for reuse
   }
 }
 
@@ -370,10 +353,10 @@ __global__ __launch_bounds__(NT) void k_fasrhs(SmoothArgs a) {
   *reinterpret_cast<float2*>(bi) = make_float2(b0, b1);
 }
 
-const void* smooth_kernel_ptr() { return (const void*)k_smooth; }
+const void* smooth_kernel_ptr() { return (const void*)k_stage; }
 
 void launch_smooth(const SmoothArgs& a, int grid, cudaStream_t s) {
-  k_smooth<<<grid, NT, 0, s>>>(a);
+  k_stage<<<grid, NT, 0, s>>>(a);
 }
 
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s) {

@@ -1,0 +1,106 @@
+// Per-cell stencil helpers shared by the tile kernels (direct.cu) and the on-chip coarse
+// sub-cycle (subcycle.cu).  Cell (x,y,z) of tile t at the tile's level; coefficient record
+// float4 (c, c_x-, c_y-, c_z-); face order x-, x+, y-, y+, z-, z+ (the oracle's).
+// NC: values may be read through the non-coherent path (true when no thread of the kernel
+// writes them before they are read); false inside the sub-cycle kernel, which reads values
+// its own threads wrote earlier in the launch.
+#pragma once
+#include "octmg_internal.cuh"
+
+namespace octmg {
+
+enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
+
+template <bool NC>
+__device__ __forceinline__ float ldv(const float* p) {
+  if (NC) return __ldg(p);
+  return *p;
+}
+
+__device__ __forceinline__ int loff(int x, int y, int z) { return x + 8 * y + 64 * z; }
+__device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
+__device__ __forceinline__ int pcell_of(int4 tv, int x, int y, int z) {
+  return loff(((tv.y & 1) << 2) + (x >> 1), ((tv.z & 1) << 2) + (y >> 1), ((tv.w & 1) << 2) + (z >> 1));
+}
+
+// face term sum (x-, x+, y-, y+, z-, z+ order, the oracle's) for cell (x,y,z) of tile t at
+// its level, values from u; ghosts use ui (the cell's snapshot value) and mP (mean of the
+// active cells of its parent block) — only evaluated if the tile has a ghost face.
+// ZERO_OWN: cells of `colour` read as 0 (first black pass of a cycle).
+template <bool ZERO_OWN, bool NC = true>
+__device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int y, int z, const float4& q,
+                                          float ui, float mP, int colour, float s0, const float* su = nullptr) {
+  const size_t base = (size_t)t * TB3;
+  const float* ut = tptr(a.u, t, a.NL);
+  const int c[3] = {x, y, z};
+  float s = s0;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
+    int nc[3] = {c[0], c[1], c[2]};
+    nc[ax] += sg;
+    float v = 0.0f, cf = (f & 1) ? 0.0f : comp(q, ax);
+    if (nc[ax] >= 0 && nc[ax] < 8) {
+      const int no = loff(nc[0], nc[1], nc[2]);
+      v = su ? su[no] : ldv<NC>(ut + no);  // su: this tile's values staged in shared memory
+      if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
+      if (f & 1) cf = comp(__ldg(a.coef + base + no), ax);
+    } else {
+      const int n = __ldg(a.nbr + 6 * t + f);
+      nc[ax] &= 7;
+      const int no = loff(nc[0], nc[1], nc[2]);
+      if (n >= 0) {
+        v = ldv<NC>(tptr(a.u, n, a.NL) + no);
+        if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
+        if (f & 1) cf = comp(__ldg(a.coef + (size_t)n * TB3 + no), ax);
+      } else if (n <= -2) {
+        if (f & 1)
+          cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 +
+                     (ax == 0 ? y + 8 * z : (ax == 1 ? x + 8 * z : x + 8 * y)));
+        const int C = -2 - n;
+        const int4 tv = __ldg(a.tile + t);
+        int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
+        g[ax] += sg;
+        const int co = loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
+        if (__ldg(a.coef + (size_t)C * TB3 + co).x != 0.0f) {
+          const float uc = ZERO_OWN ? 0.0f : ldv<NC>(tptr(a.u, C, a.NL) + co);
+          v = ui + 0.5f * (uc - mP);
+        }
+      }
+    }
+    s = fmaf(cf, v, s);
+  }
+  return s;
+}
+
+__device__ __forceinline__ bool has_ghost(const SmoothArgs& a, int t) {
+  bool g = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) g |= __ldg(a.nbr + 6 * t + f) <= -2;
+  return g;
+}
+
+// mean of the active cells of the 2x2x2 block holding (x,y,z) (pass-start values)
+template <bool ZERO_OWN, bool NC = true>
+__device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, int y, int z, int colour) {
+  const size_t base = (size_t)t * TB3;
+  const float* ut = tptr(a.u, t, a.NL);
+  float sm = 0.0f;
+  int nn = 0;
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const int bx = (x & ~1) + dx, by = (y & ~1) + dy, bz = (z & ~1) + dz;
+        const int bo = loff(bx, by, bz);
+        if (__ldg(a.coef + base + bo).x != 0.0f) {
+          float bv = ldv<NC>(ut + bo);
+          if (ZERO_OWN && ((bx + by + bz) & 1) == colour) bv = 0.0f;
+          sm += bv;
+          nn++;
+        }
+      }
+  return nn ? sm / (float)nn : 0.0f;
+}
+
+
+}  // namespace octmg
