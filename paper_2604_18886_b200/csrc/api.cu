@@ -21,7 +21,8 @@ octmg_status cuda_status(cudaError_t e, const char* what) {
 
 const char* kclass_name[KC_COUNT] = {"rbgs_pass", "prolong", "residual_restrict", "coarsest",
                                      "fas_rhs", "coarse_levels", "apply", "pcg_update", "dot_rz", "project",
-                                     "init", "setup", "memset", "coarse_subcycle"};
+                                     "init", "setup", "memset", "coarse_subcycle", "rbgs_fused_iteration",
+                                     "copy_level"};
 
 template <class T>
 static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
@@ -92,6 +93,16 @@ struct Builder {
   Hier& h;
   void stage(int l, int desc) { h.ops.push_back(Op{0, l, desc}); }
   void passes(int l, int iters, bool red_first, int m1, int m2) {
+    if (h.rb_fused) {  // one launch per RB iteration, ping-pong A -> B -> A ...
+      int cur = 0;
+      for (int k = 0; k < iters; ++k) {
+        const int zero = (k == 0 && m1 == SM_ZERO1) ? 2 : 0;
+        h.ops.push_back(Op{5, l, (red_first ? 0 : 1) | zero, cur, 1 - cur});
+        cur = 1 - cur;
+      }
+      if (cur == 1) h.ops.push_back(Op{6, l, 0, 1, 0});  // odd count: back to the rest buffer
+      return;
+    }
     for (int k = 0; k < iters; ++k) {
       stage(l, stage_desc(red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN));
       stage(l, stage_desc(red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN));
@@ -133,6 +144,10 @@ octmg_status build_schedule(Hier& h) {
   h.smooth_grid = sms * std::max(per, 1);
   const char* pk = getenv("OCTMG_PASS_KERNEL");
   h.pass_kernel = (pk && std::string(pk) == "stage") ? 1 : 0;
+  const char* rbv = getenv("OCTMG_RB");
+  // default: one launch per colour pass; OCTMG_RB=fused selects the fused RB iteration
+  // (parity-tested, currently slower: see DESIGN.md "Fused red-black")
+  h.rb_fused = (rbv && std::string(rbv) == "fused") ? 1 : ((rbv && std::string(rbv) == "fused_noshell") ? 2 : 0);
   const char* pc = getenv("OCTMG_PASS_CPT");
   h.pass_cpt = pc ? std::max(1, std::min(2, atoi(pc))) : 2;
   const Tree& T = *h.tree;
@@ -155,7 +170,7 @@ int64_t schedule_kernels(const Hier& h) {
   return n;
 }
 
-Fld ubuf(const Hier& h) { return Fld{h.z, h.uinA}; }
+Fld ubuf(const Hier& h, int which = 0) { return which == 0 ? Fld{h.z, h.uinA} : Fld{h.zB, h.uinB}; }
 
 cudaEvent_t next_event(Hier& h) {
   if (h.event_next == h.event_pool.size()) {
@@ -195,12 +210,29 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   const int l = op.level;
   SmoothArgs a;
   a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
-  a.glayer = T.glayer; a.u = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar; a.b = Fld{h.r, h.binner};
+  a.glayer = T.glayer; a.u = ubuf(h); a.u2 = ubuf(h, 1); a.uc = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar;
+  a.b = Fld{h.r, h.binner};
   a.beta = h.prm.beta; a.alpha = h.prm.alpha; a.NL = T.NL;
   a.order = h.order + h.lvl_order_off[l];
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
   a.stage[0] = op.stage;
+  if (op.kind == 5) {
+    a.u = ubuf(h, op.in_buf);
+    a.u2 = ubuf(h, op.out_buf);
+    a.stage[0] = op.stage & 1;
+    // one HBM pass per RB iteration: read u, b, 16-byte record, write u (28 B/cell)
+    ProfScope ps(h, l < T.L ? KC_SMOOTH_COARSE : KC_RBFUSED, s, 28.0 * a.n * TB3);
+    launch_rb_fused(a, (op.stage & 2) != 0, s, h.rb_fused != 2);
+    return;
+  }
+  if (op.kind == 6) {
+    a.u = ubuf(h, op.in_buf);
+    a.u2 = ubuf(h, op.out_buf);
+    ProfScope ps(h, KC_COPY, s, 8.0 * a.n * TB3);
+    launch_copy_level(a, s);
+    return;
+  }
   if (op.kind == 4) {
     ProfScope ps(h, KC_SUBCYCLE, s, 0.0);
     launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, s);
@@ -344,6 +376,8 @@ octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const 
   if ((st = halloc(h.allocs, &h.act, NLc / 32))) return fail(st);
   if ((st = halloc(h.allocs, &h.z, NLc))) return fail(st);
   if ((st = halloc(h.allocs, &h.uinA, NIc))) return fail(st);
+  if ((st = halloc(h.allocs, &h.zB, NLc))) return fail(st);
+  if ((st = halloc(h.allocs, &h.uinB, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.binner, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.ustar, NIc))) return fail(st);
   if ((st = halloc(h.allocs, &h.r, NLc))) return fail(st);
@@ -499,7 +533,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       ProfScope ps(h, KC_UPDATE, s, (double)N * 24.0);  // read x, r, p, q; write x, r
       launch_update(x, h.r, pcur, h.q, N, h.partial, h.counter + 4, h.sc, s, G);
     }
-    h.launches += 2;
+    h.launches += 3;  // apply, finish_sigma, update
     if (ns) {
       ProfScope ps(h, KC_PROJECT, s, (double)N * 8.125);
       launch_project(h.r, h.act, N, h.partial, h.counter + 1, h.sc, s, G);

@@ -114,7 +114,7 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
   const size_t base = (size_t)t * TB3;
   float4* up = reinterpret_cast<float4*>(tptr(a.u, t, a.NL) + loff(x0, y, z));
   float4 u = *up;
-  const float* uc = tptr(a.u, P, a.NL);
+  const float* uc = tptr(a.uc, P, a.NL);
   const float* us = a.ustar + (size_t)(P - a.NL) * TB3;
   const int pc0 = pcell_of(tv, x0, y, z), pc1 = pcell_of(tv, x0 + 2, y, z);
   const float c0 = __ldg(uc + pc0) - __ldg(us + pc0), c1 = __ldg(uc + pc1) - __ldg(us + pc1);

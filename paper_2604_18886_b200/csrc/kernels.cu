@@ -157,15 +157,27 @@ __global__ __launch_bounds__(NT, 6) void k_apply(ApplyArgs a) {
   const float r1 = q1.x != 0.0f ? composite_faces(a, beta, t, x0 + 1, y, z, q1, p1, mP, q1.x * p1, sp) : 0.0f;
   *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
   if (DOT) {
+    // per-tile fp64 partial; k_finish_sigma sums them in tile order (no per-CTA fence)
     double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
-    double tot;
     double bs = block_reduce_d(d, sred);
-    if (last_block_sum(bs, a.partial, a.counter, gridDim.x, &tot, sred)) {
-      Scalars* sc = a.sc;
-      sc->sigma = tot;
-      if (!(tot > 0.0) || !isfinite(tot)) { sc->flags |= 1; sc->alpha = 0.0; }
-      else sc->alpha = sc->rho / tot;
-    }
+    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
+  }
+}
+
+// sigma = p.q from the per-tile partials (fixed order => deterministic), alpha = rho / sigma
+__global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, int n, Scalars* sc) {
+  __shared__ double sred[32];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) s += partial[k];
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sred[w];
+    sc->sigma = tot;
+    if (!(tot > 0.0) || !isfinite(tot)) { sc->flags |= 1; sc->alpha = 0.0; }
+    else sc->alpha = sc->rho / tot;
   }
 }
 
@@ -300,8 +312,12 @@ __global__ void k_build_mask(const float4* coef, int64_t nwords, uint32_t* act) 
 
 void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   if (a.NL == 0) return;
-  if (a.partial) k_apply<true><<<a.NL, NT, 0, s>>>(a);
-  else k_apply<false><<<a.NL, NT, 0, s>>>(a);
+  if (a.partial) {
+    k_apply<true><<<a.NL, NT, 0, s>>>(a);
+    k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.NL, a.sc);
+  } else {
+    k_apply<false><<<a.NL, NT, 0, s>>>(a);
+  }
 }
 
 void launch_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n, double* partial,

@@ -85,7 +85,7 @@ struct Scalars {
 // Kernel classes for profiling
 enum KClass {
   KC_PASS = 0, KC_PROLONG, KC_RESTRICT, KC_COARSEST, KC_FASRHS, KC_SMOOTH_COARSE,
-  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_COUNT
+  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_RBFUSED, KC_COPY, KC_COUNT
 };
 extern const char* kclass_name[KC_COUNT];
 
@@ -131,7 +131,9 @@ struct SmoothArgs {
   const float4* coef;
   const float* glayer_val;
   const int* glayer;
-  Fld u;                // in-place cycle values (all levels share the buffer)
+  Fld u;                // level values read (in place: also written)
+  Fld u2;               // fused RB iteration: output buffer of the ping-pong pair
+  Fld uc;               // rest buffer of every level (ghost sources, prolongation parents)
   const float* ustar;   // inner-indexed u* (prolongation)
   float* ustar_w;       // inner-indexed u* output (restrict stage)
   Fld b;                // leaf = PCG residual r, inner = FAS rhs
@@ -149,6 +151,8 @@ void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s);
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
+void launch_rb_fused(const SmoothArgs& a, bool zero, cudaStream_t s, bool shell = true);
+void launch_copy_level(const SmoothArgs& a, cudaStream_t s);
 int subcycle_max_tiles();
 int subcycle_max_level();
 void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
@@ -169,9 +173,11 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
 // Hierarchy (coefficients + multigrid work buffers + PCG state)
 // ------------------------------------------------------------------------------------
 struct Op {
-  int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle
+  int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle,
+               // 5 fused RB iteration, 6 copy level buffer in -> out
   int level;
-  int stage;   // bit0 colour, bits1.. mode (SM_*)
+  int stage;   // bit0 colour, bits1.. mode (SM_*); kind 5: bit0 first colour, bit1 zero
+  int in_buf = 0, out_buf = 0;
 };
 
 struct Hier {
@@ -181,8 +187,10 @@ struct Hier {
   uint32_t* act = nullptr;       // [NL*512/32] activity bitmask of the leaf cells
   float* glayer_val = nullptr;   // [n_glayers*64]
   // multigrid buffers
-  float* z = nullptr;            // [NL*512] leaf part of the cycle's u (in place) = M output
-  float* uinA = nullptr;         // [NI*512] inner part of u
+  float* z = nullptr;            // [NL*512] leaf part of the cycle's u (buffer A) = M output
+  float* uinA = nullptr;         // [NI*512] inner part of u (buffer A)
+  float* zB = nullptr;           // [NL*512] buffer B (fused RB ping-pong)
+  float* uinB = nullptr;         // [NI*512]
   float* binner = nullptr;       // [NI*512]
   float* ustar = nullptr;        // [NI*512]
   float* r = nullptr;            // [NL*512] PCG residual = leaf part of the cycle rhs
@@ -206,6 +214,7 @@ struct Hier {
   int pass_kernel = 0;           // 0 direct (sync-light), 1 staged pipeline (OCTMG_PASS_KERNEL)
   int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
+  int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes
   cudaGraphExec_t graph = nullptr;
   cudaStream_t graph_stream = nullptr;
   int64_t launches = 0;

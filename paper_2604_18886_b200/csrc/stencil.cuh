@@ -63,7 +63,7 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
         g[ax] += sg;
         const int co = loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
         if (__ldg(a.coef + (size_t)C * TB3 + co).x != 0.0f) {
-          const float uc = ZERO_OWN ? 0.0f : ldv<NC>(tptr(a.u, C, a.NL) + co);
+          const float uc = ZERO_OWN ? 0.0f : ldv<NC>(tptr(a.uc, C, a.NL) + co);
           v = ui + 0.5f * (uc - mP);
         }
       }

@@ -154,7 +154,7 @@ __device__ void sc_prolong(const SubArgs& A, int l) {
     const int4 tv = __ldg(a.tile + t);
     const int P = __ldg(a.parent + t);
     const int pc = pcell_of(tv, off & 7, (off >> 3) & 7, off >> 6);
-    tptr(a.u, t, a.NL)[off] += tptr(a.u, P, a.NL)[pc] - a.ustar[(size_t)(P - a.NL) * TB3 + pc];
+    tptr(a.u, t, a.NL)[off] += tptr(a.uc, P, a.NL)[pc] - a.ustar[(size_t)(P - a.NL) * TB3 + pc];
   }
   __syncthreads();
 }

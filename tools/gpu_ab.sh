@@ -1,10 +1,13 @@
-# A/B of the direct pass: colour cells per thread
-for C in 1 2; do
-  echo "== cpt $C"
-  OCTMG_PASS_CPT=$C BENCH_ALLOW_SHORT=1 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$C.json 2> gpurun_out/bench_$C.err
-  python - "$C" <<'PY'
+# A/B: fused RB iterations vs per-colour passes; then GPU parity with the default
+for V in fused_noshell split; do
+  echo "== $V"
+  OCTMG_RB=$V BENCH_ALLOW_SHORT=1 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$V.json 2> gpurun_out/bench_$V.err
+  python - "$V" <<'PY'
 import json, sys
-d = json.loads(open('gpurun_out/bench_%s.json' % sys.argv[1]).read().strip().splitlines()[-1])
+try:
+    d = json.loads(open('gpurun_out/bench_%s.json' % sys.argv[1]).read().strip().splitlines()[-1])
+except Exception:
+    print(open('gpurun_out/bench_%s.err' % sys.argv[1]).read()[-2000:]); raise SystemExit
 print('value %.3e ms %.3f iters %s' % (d['value'], d['ms_per_step'], d['config']['pcg_iters']))
 for k, v in d['kernels'].items(): print('  %-22s %8.3f ms  n=%4d  %s GB/s' % (k, v['ms_per_solve'], v['launches_per_solve'], v['gbs'] and round(v['gbs'])))
 PY
