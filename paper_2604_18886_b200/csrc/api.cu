@@ -136,14 +136,6 @@ struct Builder {
 octmg_status build_schedule(Hier& h) {
   h.ops.clear();
   OCTMG_TRY(build_orders(h));
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, smooth_kernel_ptr(), 256, 0);
-  h.smooth_grid = sms * std::max(per, 1);
-  const char* pk = getenv("OCTMG_PASS_KERNEL");
-  h.pass_kernel = (pk && std::string(pk) == "stage") ? 1 : 0;
   const char* rbv = getenv("OCTMG_RB");
   // default: one launch per colour pass; OCTMG_RB=fused selects the fused RB iteration
   // (parity-tested, currently slower: see DESIGN.md "Fused red-black")
@@ -245,15 +237,12 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     return;
   }
   if (op.kind == 1) {
-    a.run = 1;
     // read u, b, record; write b (inner cells of the level)
     ProfScope ps(h, KC_FASRHS, s, 28.0 * T.ic[l] * TB3);
     launch_fasrhs(a, T.ic[l], s);
     return;
   }
   const int mode = op.stage >> 1;
-  a.run = (a.n + h.smooth_grid - 1) / h.smooth_grid;
-  const int grid = (a.n + a.run - 1) / a.run;
   // algorithmic bytes per cell of the level: colour pass = read u, b, 16-byte record, write
   // u (28 B; 24 B when u is known zero); restrict = read u, b, record (24 B) + the parents'
   // u, u*, b (1.5 B); prolongation-fused passes read the parents' u, u* (+1 B)
@@ -263,8 +252,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   int cls = mode == SM_RESTRICT ? KC_RESTRICT
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
   ProfScope ps(h, cls, s, bytes);
-  if (h.pass_kernel == 1) launch_smooth(a, grid, s);
-  else if (mode == SM_RESTRICT) launch_restrict_direct(a, s);
+  if (mode == SM_RESTRICT) launch_restrict_direct(a, s);
   else launch_pass_direct(a, s, a.n >= 1024 ? h.pass_cpt : 1);
 }
 

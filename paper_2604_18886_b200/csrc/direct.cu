@@ -127,7 +127,30 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
   *up = u;
 }
 
+// FAS right-hand side of the inner rows of a coarse level (Alg. 4 line 10):
+// b_I = beta R r (already in b) + (A^{l-1} u*)_I, with u* in u (inner rows) and the current
+// u of the leaf rows.  Inner tiles never border a ghost (grading), so no reconstruction.
+__global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
+  const int t = a.first_tile + blockIdx.x;
+  const int j = threadIdx.x;
+  const int y = (j >> 2) & 7, z = j >> 5, x0 = 2 * (j & 3);
+  const int off0 = loff(x0, y, z);
+  const size_t base = (size_t)t * TB3;
+  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float2 uu = __ldg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
+  float2* bp = reinterpret_cast<float2*>(a.b.inner + (size_t)(t - a.NL) * TB3 + off0);
+  const float2 bb = *bp;
+  float2 out;
+  out.x = q0.x != 0.0f ? bb.x + face_sum<false>(a, t, x0, y, z, q0, 0.0f, 0.0f, 0, q0.x * uu.x) : 0.0f;
+  out.y = q1.x != 0.0f ? bb.y + face_sum<false>(a, t, x0 + 1, y, z, q1, 0.0f, 0.0f, 0, q1.x * uu.y) : 0.0f;
+  *bp = out;
+}
+
 }  // namespace
+
+void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s) {
+  if (ninner > 0) k_fasrhs<<<ninner, NT, 0, s>>>(a);
+}
 
 template <int CPT>
 static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s) {

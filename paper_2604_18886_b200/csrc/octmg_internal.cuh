@@ -123,7 +123,7 @@ void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, u
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);
 void launch_build_mask(const float4* coef, int64_t n, uint32_t* act, cudaStream_t s);
 
-// smoother stage kernels (smooth.cu)
+// smoother kernels (direct.cu, rbfused.cu, subcycle.cu)
 struct SmoothArgs {
   const int4* tile;
   const int* nbr;
@@ -141,12 +141,9 @@ struct SmoothArgs {
   int NL;
   const int* order;     // tiles of the level in rank order (slab-major)
   int n;                // tiles in the level
-  int run;              // tiles per CTA
   int first_tile;       // k_fasrhs: first inner tile of the level
   int stage[1];         // bit0 colour, bits1.. mode
 };
-void launch_smooth(const SmoothArgs& a, int grid, cudaStream_t s);
-const void* smooth_kernel_ptr();
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s);
@@ -210,8 +207,6 @@ struct Hier {
   int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
-  int smooth_grid = 0;           // resident CTAs of the stage kernel (one wave)
-  int pass_kernel = 0;           // 0 direct (sync-light), 1 staged pipeline (OCTMG_PASS_KERNEL)
   int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes

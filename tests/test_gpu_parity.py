@@ -241,3 +241,25 @@ def test_full_size_cfg2_parity(om):
     a = a - a[act].mean() * act
     r = ref["x"] - ref["x"][act].mean() * act
     assert _rel(a, r) <= 1e-5
+
+
+# ---------------------------------------------------------------------------------------
+# alternative schedules selected at setup (same semantics, must match the oracle too)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("env", [{"OCTMG_RB": "fused"}, {"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"}])
+@pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
+def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = make_config(name)
+    tree, h, o = _setup(om, cfg)
+    rng = np.random.default_rng(11)
+    r = rng.standard_normal(o.N).astype(np.float32)
+    u = torch.zeros(o.N, device=DEV)
+    h.vcycle(torch.from_numpy(r).to(DEV), u)
+    ref = o.vcycle(r.astype(np.float64), mu=cfg["mu"])
+    assert _rel(u.cpu().numpy().astype(np.float64), ref) <= 1e-5
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    x = torch.zeros_like(b)
+    rep = h.pcg_solve(b, x, rtol=1e-6)
+    assert abs(rep["iters"] - o.pcg(cfg["b"].astype(np.float64), rtol=1e-6, mu=cfg["mu"])["iters"]) <= 1

@@ -1,7 +1,7 @@
 # quick GPU check: smoke, GPU parity tests (not slow), short bench
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
 timeout 900 python -m pytest tests -x -q -m "gpu and not slow" 2>&1 | tail -25
-BENCH_ALLOW_SHORT=1 timeout 600 python bench.py --steps 5 --warmup 3 --cpu-seconds 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
+BENCH_ALLOW_SHORT=1 timeout 600 python bench.py --steps 20 --warmup 3 --cpu-seconds 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
 python - <<'PY'
 import json
 try:
