@@ -252,8 +252,11 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   int cls = mode == SM_RESTRICT ? KC_RESTRICT
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
   ProfScope ps(h, cls, s, bytes);
-  if (mode == SM_RESTRICT) launch_restrict_direct(a, s);
-  else launch_pass_direct(a, s, a.n >= 1024 ? h.pass_cpt : 1);
+  if (mode == SM_RESTRICT) {
+    launch_restrict_direct(a, s);
+  } else {
+    launch_pass_direct(a, s, a.n >= 1024 ? h.pass_cpt : 1);
+  }
 }
 
 octmg_status run_M(Hier& h, cudaStream_t s) {

@@ -75,8 +75,11 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
   const float2 uu = *reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0);
   const float2 bb = *reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0);
   __shared__ float su_t[TB3];
+  __shared__ float scm[3][TB3];
   su_t[off0] = uu.x;
   su_t[off0 + 1] = uu.y;
+  scm[0][off0] = q0.y; scm[1][off0] = q0.z; scm[2][off0] = q0.w;
+  scm[0][off0 + 1] = q1.y; scm[1][off0 + 1] = q1.z; scm[2][off0 + 1] = q1.w;
   // active u sum / count of the block (also the ghost m_P of its cells)
   float su = (q0.x != 0.0f ? uu.x : 0.0f) + (q1.x != 0.0f ? uu.y : 0.0f);
   int na = (q0.x != 0.0f) + (q1.x != 0.0f);
@@ -87,8 +90,8 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
   const float mP = na ? su / (float)na : 0.0f;
   __syncthreads();
   float r0 = 0.0f, r1 = 0.0f;
-  if (q0.x != 0.0f) r0 = bb.x - face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, q0.x * uu.x, su_t);
-  if (q1.x != 0.0f) r1 = bb.y - face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, q1.x * uu.y, su_t);
+  if (q0.x != 0.0f) r0 = bb.x - face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, q0.x * uu.x, su_t, scm);
+  if (q1.x != 0.0f) r1 = bb.y - face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, q1.x * uu.y, su_t, scm);
   float rs = r0 + r1;
   rs += __shfl_xor_sync(0xffffffffu, rs, 4);
   rs += __shfl_xor_sync(0xffffffffu, rs, 8);

@@ -61,7 +61,8 @@ __device__ __forceinline__ float pval(const ApplyArgs& a, float beta, size_t i) 
 // same-level inner neighbour the mean of its active children (all leaves), a ghost
 // g = p_i + (p_C - m_P)/2 (Eq. 12), walls 0.  Face order x-, x+, y-, y+, z-, z+.
 __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta, int t, int x, int y, int z,
-                                                 const float4& q, float pi, float mP, float s0, const float* sp) {
+                                                 const float4& q, float pi, float mP, float s0, const float* sp,
+                                                 const float (*scm)[TB3]) {
   const size_t base = (size_t)t * TB3;
   const int c[3] = {x, y, z};
   float s = s0;
@@ -73,8 +74,8 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
     float v = 0.0f, cf = (f & 1) ? 0.0f : comp(q, ax);
     if (nc[ax] >= 0 && nc[ax] < 8) {
       const int no = loff(nc[0], nc[1], nc[2]);
-      if (f & 1) cf = comp(__ldg(a.coef + base + no), ax);
-      v = sp[no];  // this tile's p, staged in shared memory
+      if (f & 1) cf = scm[ax][no];  // this tile's -face coefficients, staged (SoA)
+      v = sp[no];                   // this tile's p, staged in shared memory
     } else {
       const int n = __ldg(a.nbr + 6 * t + f);
       nc[ax] &= 7;
@@ -117,7 +118,7 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
 // (Alg. 1 lines 9-10; fp64 dots P:L1233).  Thread layout as the restriction: the
 // four lanes of a 2x2x2 block are xor 4 / xor 8 apart (ghost m_P by shuffles).
 template <bool DOT>
-__global__ __launch_bounds__(NT, 6) void k_apply(ApplyArgs a) {
+__global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
   __shared__ double sred[NT / 32];
   const int t = blockIdx.x;
   const int j = threadIdx.x;
@@ -143,8 +144,11 @@ __global__ __launch_bounds__(NT, 6) void k_apply(ApplyArgs a) {
   }
   if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0, p1);
   __shared__ float sp[TB3];
+  __shared__ float scm[3][TB3];
   sp[off0] = p0;
   sp[off0 + 1] = p1;
+  scm[0][off0] = q0.y; scm[1][off0] = q0.z; scm[2][off0] = q0.w;
+  scm[0][off0 + 1] = q1.y; scm[1][off0 + 1] = q1.z; scm[2][off0 + 1] = q1.w;
   float su = p0 + p1;
   int na = (q0.x != 0.0f) + (q1.x != 0.0f);
   su += __shfl_xor_sync(0xffffffffu, su, 4);
@@ -153,8 +157,8 @@ __global__ __launch_bounds__(NT, 6) void k_apply(ApplyArgs a) {
   na += __shfl_xor_sync(0xffffffffu, na, 8);
   const float mP = na ? su / (float)na : 0.0f;
   __syncthreads();
-  const float r0 = q0.x != 0.0f ? composite_faces(a, beta, t, x0, y, z, q0, p0, mP, q0.x * p0, sp) : 0.0f;
-  const float r1 = q1.x != 0.0f ? composite_faces(a, beta, t, x0 + 1, y, z, q1, p1, mP, q1.x * p1, sp) : 0.0f;
+  const float r0 = q0.x != 0.0f ? composite_faces(a, beta, t, x0, y, z, q0, p0, mP, q0.x * p0, sp, scm) : 0.0f;
+  const float r1 = q1.x != 0.0f ? composite_faces(a, beta, t, x0 + 1, y, z, q1, p1, mP, q1.x * p1, sp, scm) : 0.0f;
   *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
   if (DOT) {
     // per-tile fp64 partial; k_finish_sigma sums them in tile order (no per-CTA fence)

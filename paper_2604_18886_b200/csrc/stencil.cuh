@@ -29,7 +29,8 @@ __device__ __forceinline__ int pcell_of(int4 tv, int x, int y, int z) {
 // ZERO_OWN: cells of `colour` read as 0 (first black pass of a cycle).
 template <bool ZERO_OWN, bool NC = true>
 __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int y, int z, const float4& q,
-                                          float ui, float mP, int colour, float s0, const float* su = nullptr) {
+                                          float ui, float mP, int colour, float s0, const float* su = nullptr,
+                                          const float (*scm)[TB3] = nullptr) {
   const size_t base = (size_t)t * TB3;
   const float* ut = tptr(a.u, t, a.NL);
   const int c[3] = {x, y, z};
@@ -44,7 +45,7 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
       const int no = loff(nc[0], nc[1], nc[2]);
       v = su ? su[no] : ldv<NC>(ut + no);  // su: this tile's values staged in shared memory
       if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
-      if (f & 1) cf = comp(__ldg(a.coef + base + no), ax);
+      if (f & 1) cf = scm ? scm[ax][no] : comp(__ldg(a.coef + base + no), ax);  // scm: staged SoA
     } else {
       const int n = __ldg(a.nbr + 6 * t + f);
       nc[ax] &= 7;
@@ -104,3 +105,4 @@ __device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, i
 
 
 }  // namespace octmg
+
