@@ -72,8 +72,10 @@ typedef struct {
                           at the centre of a virtual wall cell of the boundary cell's
                           size (P:L328-330 ghost-fluid Dirichlet)                         */
   int32_t grade_repair;/* must be 0: ungraded input is rejected with NOT_GRADED          */
-  int32_t rank, nranks;/* must be 0, 1 (single GPU in this release)                      */
-  void* nccl_comm;     /* must be NULL                                                   */
+  int32_t rank, nranks;/* this process's rank and the number of ranks (1 = single GPU)    */
+  void* nccl_comm;     /* ncclComm_t over the nranks GPUs (octmg_nccl_comm_init), or NULL
+                          when nranks == 1.  The leaf-tile list is replicated on all ranks;
+                          the partition is deterministic.                    */
 } octmg_tree_desc;
 
 /*
@@ -130,6 +132,32 @@ typedef struct {
 octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const float* face_beta,
                                    const float* face_frac, const octmg_mg_params* params,
                                    octmg_stream stream, octmg_hier** out);
+
+/*
+ * Partitioned hierarchy of `nparts` parts living in this process on the current device
+ * ("loopback" transport: halo exchanges are device copies between the parts).  Same
+ * partition, schedule and kernels as an nparts-rank NCCL job; used to test the
+ * distributed path on one GPU.  Vectors passed to the solver calls are global leaf-slot
+ * vectors; each part reads/writes its owned cells.
+ */
+octmg_status octmg_setup_hierarchy_loopback(octmg_tree* tree, int32_t nparts, const uint8_t* kind,
+                                            const float* face_beta, const float* face_frac,
+                                            const octmg_mg_params* params, octmg_stream stream,
+                                            octmg_hier** out);
+
+/* Partition of part `part` (0 for an NCCL rank): partition level lg (levels < lg are
+ * replicated), rank, nranks, and per level the owned leaf tiles [begin, begin+count). */
+octmg_status octmg_partition_info(const octmg_hier* h, int32_t part, int32_t* lg, int32_t* rank,
+                                  int32_t* nranks, int32_t* own_leaf_begin, int32_t* own_leaf_count);
+
+/* NCCL bootstrap for a multi-GPU job (libnccl.so.2 is loaded on first use): rank 0 calls
+ * octmg_nccl_unique_id (128 bytes), broadcasts it (e.g. via torch.distributed), every rank
+ * calls octmg_nccl_comm_init on its device.  The solver calls of an nranks > 1 hierarchy
+ * are collective: every rank must issue them in the same order.  Each rank's output
+ * vectors hold its owned cells. */
+octmg_status octmg_nccl_unique_id(void* out128);
+octmg_status octmg_nccl_comm_init(int32_t rank, int32_t nranks, const void* id128, void** comm);
+void octmg_nccl_comm_destroy(void* comm);
 
 /* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
  * in tile order.  Synchronises `stream` of the last call. */

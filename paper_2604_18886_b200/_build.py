@@ -12,8 +12,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "liboctmg.so")
-SOURCES = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
-HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "octmg.h")]
+SOURCES = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")) + glob.glob(os.path.join(HERE, "csrc", "*.cpp")))
+HEADERS = sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(os.path.join(HERE, "csrc", "*.h"))) + [os.path.join(ROOT, "include", "octmg.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "550,128"]
 
@@ -29,7 +29,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if force or _stale():
         nvcc = os.environ.get("NVCC", "nvcc")
         tmp = LIB + ".tmp%d" % os.getpid()
-        cmd = [nvcc] + NVCC_FLAGS + ["-o", tmp] + SOURCES
+        cmd = [nvcc] + NVCC_FLAGS + ["-o", tmp] + SOURCES + ["-ldl"]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -5,7 +5,9 @@
 #include <cstdio>
 #include <cstring>
 
+#include "comm.h"
 #include "octmg_internal.cuh"
+#include "partition.h"
 
 namespace octmg {
 
@@ -40,11 +42,17 @@ static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
 }
 
 Hier::~Hier() {
-  if (graph) cudaGraphExecDestroy(graph);
-  if (graph_stream) cudaStreamDestroy(graph_stream);
   for (auto e : event_pool) cudaEventDestroy(e);
   for (void* p : allocs) cudaFree(p);
   if (sc_host) cudaFreeHost(sc_host);
+}
+
+Group::~Group() {
+  if (graph) cudaGraphExecDestroy(graph);
+  if (graph_stream) cudaStreamDestroy(graph_stream);
+  for (Hier* h : parts) delete h;
+  delete comm;
+  delete plan;
 }
 
 // ------------------------------------------------------------------------------------
@@ -71,8 +79,8 @@ octmg_status build_orders(Hier& h) {
   order.reserve(T.T);
   for (int l = 0; l <= T.L; ++l) {
     std::vector<int> ts;
-    for (int t = T.lb[l]; t < T.lb[l] + T.lc[l]; ++t) ts.push_back(t);
-    for (int t = T.ib[l]; t < T.ib[l] + T.ic[l]; ++t) ts.push_back(t);
+    for (int t = h.own_lb[l]; t < h.own_lb[l] + h.own_lc[l]; ++t) ts.push_back(t);
+    for (int t = h.own_ib[l]; t < h.own_ib[l] + h.own_ic[l]; ++t) ts.push_back(t);
     std::sort(ts.begin(), ts.end(), [&](int a, int b) {
       if (tile[a].w != tile[b].w) return tile[a].w < tile[b].w;
       return m2(tile[a].y, tile[a].z) < m2(tile[b].y, tile[b].z);
@@ -90,17 +98,30 @@ octmg_status build_orders(Hier& h) {
 }
 
 struct Builder {
-  Hier& h;
-  void stage(int l, int desc) { h.ops.push_back(Op{0, l, desc}); }
+  Group& g;
+  Hier& h;  // part 0 (every part has the same schedule)
+  void push(const Op& op) { g.ops.push_back(op); }
+  void xchg(int l) {  // halo exchange of level l after a kernel changed it
+    if (h.nranks > 1 && l >= h.lg) push(Op{7, l, 0});
+  }
+  void stage(int l, int desc) {
+    push(Op{0, l, desc});
+    if ((desc >> 1) == SM_RESTRICT) {
+      if (h.nranks > 1 && l == h.lg && l >= 1) push(Op{8, l - 1, 0});  // parents -> all ranks
+      else xchg(l - 1);
+    } else {
+      xchg(l);
+    }
+  }
   void passes(int l, int iters, bool red_first, int m1, int m2) {
     if (h.rb_fused) {  // one launch per RB iteration, ping-pong A -> B -> A ...
       int cur = 0;
       for (int k = 0; k < iters; ++k) {
         const int zero = (k == 0 && m1 == SM_ZERO1) ? 2 : 0;
-        h.ops.push_back(Op{5, l, (red_first ? 0 : 1) | zero, cur, 1 - cur});
+        push(Op{5, l, (red_first ? 0 : 1) | zero, cur, 1 - cur});
         cur = 1 - cur;
       }
-      if (cur == 1) h.ops.push_back(Op{6, l, 0, 1, 0});  // odd count: back to the rest buffer
+      if (cur == 1) push(Op{6, l, 0, 1, 0});  // odd count: back to the rest buffer
       return;
     }
     for (int k = 0; k < iters; ++k) {
@@ -112,10 +133,10 @@ struct Builder {
   void fas(int l, bool fas_first) {
     const Tree& T = *h.tree;
     if (l <= h.sub_K) {  // the rest of the cycle runs on chip in one CTA
-      h.ops.push_back(Op{4, l, fas_first ? 1 : 0});
+      push(Op{4, l, fas_first ? 1 : 0});
       return;
     }
-    if (l < T.L && fas_first && T.ic[l] > 0) h.ops.push_back(Op{1, l, 0});
+    if (l < T.L && fas_first && T.ic[l] > 0) push(Op{1, l, 0});
     const bool finest = l == T.L;
     if (l == 0) {
       int nb = h.prm.nu_coarsest;
@@ -128,18 +149,18 @@ struct Builder {
     passes(l, h.prm.nu_pre, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN);
     stage(l, stage_desc(0, SM_RESTRICT));
     for (int k = 0; k < h.prm.mu; ++k) fas(l - 1, k == 0);
-    h.ops.push_back(Op{3, l, 0});  // prolongation u += P(u^{l-1} - u*), in place
+    push(Op{3, l, 0});  // prolongation u += P(u^{l-1} - u*), in place
+    xchg(l);
     passes(l, h.prm.nu_post, false, SM_PLAIN, SM_PLAIN);
   }
 };
 
-octmg_status build_schedule(Hier& h) {
-  h.ops.clear();
-  OCTMG_TRY(build_orders(h));
+void read_env(Hier& h) {
   const char* rbv = getenv("OCTMG_RB");
   // default: one launch per colour pass; OCTMG_RB=fused selects the fused RB iteration
   // (parity-tested, currently slower: see DESIGN.md "Fused red-black")
   h.rb_fused = (rbv && std::string(rbv) == "fused") ? 1 : ((rbv && std::string(rbv) == "fused_noshell") ? 2 : 0);
+  if (h.nranks > 1) h.rb_fused = 0;  // the partitioned schedule exchanges after every pass
   const char* pc = getenv("OCTMG_PASS_CPT");
   h.pass_cpt = pc ? std::max(1, std::min(2, atoi(pc))) : 2;
   const Tree& T = *h.tree;
@@ -148,18 +169,29 @@ octmg_status build_schedule(Hier& h) {
   if (!(sc && std::string(sc) == "0"))
     for (int l = 0; l <= std::min(T.L, subcycle_max_level()); ++l) {
       if (h.lvl_n[l] > subcycle_max_tiles()) break;
+      if (h.nranks > 1 && l >= h.lg) break;  // only replicated levels run on chip
       h.sub_K = l;
     }
-  if (T.NL > T.lc[T.L]) h.ops.push_back(Op{2, 0, 0});  // coarse leaves start the cycle at 0
-  Builder b{h};
+}
+
+octmg_status build_schedule(Group& g) {
+  g.ops.clear();
+  for (Hier* p : g.parts) {
+    OCTMG_TRY(build_orders(*p));
+    read_env(*p);
+  }
+  Hier& h = *g.parts[0];
+  const Tree& T = *h.tree;
+  if (T.NL > T.lc[T.L]) g.ops.push_back(Op{2, 0, 0});  // coarse leaves start the cycle at 0
+  Builder b{g, h};
   b.fas(T.L, false);
   return OCTMG_OK;
 }
 
-int64_t schedule_kernels(const Hier& h) {
+int64_t schedule_kernels(const Group& g) {
   int64_t n = 0;
-  for (const Op& op : h.ops) n += op.kind != 2;
-  return n;
+  for (const Op& op : g.ops) n += op.kind != 2 && op.kind != 7 && op.kind != 8;
+  return n * (int64_t)g.parts.size();
 }
 
 Fld ubuf(const Hier& h, int which = 0) { return which == 0 ? Fld{h.z, h.uinA} : Fld{h.zB, h.uinB}; }
@@ -237,9 +269,10 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     return;
   }
   if (op.kind == 1) {
-    // read u, b, record; write b (inner cells of the level)
-    ProfScope ps(h, KC_FASRHS, s, 28.0 * T.ic[l] * TB3);
-    launch_fasrhs(a, T.ic[l], s);
+    // read u, b, record; write b (inner cells of the level, this part's)
+    a.first_tile = h.own_ib[l];
+    ProfScope ps(h, KC_FASRHS, s, 28.0 * h.own_ic[l] * TB3);
+    launch_fasrhs(a, h.own_ic[l], s);
     return;
   }
   const int mode = op.stage >> 1;
@@ -259,26 +292,50 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   }
 }
 
-octmg_status run_M(Hier& h, cudaStream_t s) {
-  if (h.profiling) {
-    for (const Op& op : h.ops) launch_op(h, op, s);
+std::vector<Fld> ubufs(const Group& g) {
+  std::vector<Fld> f;
+  for (const Hier* h : g.parts) f.push_back(ubuf(*h));
+  return f;
+}
+
+octmg_status launch_ops(Group& g, cudaStream_t s) {
+  for (const Op& op : g.ops) {
+    if (op.kind == 7) OCTMG_TRY(g.comm->exchange(g, op.level, 0, ubufs(g), s));
+    else if (op.kind == 8) OCTMG_TRY(g.comm->bcast_parents(g, s));
+    else
+      for (Hier* h : g.parts) launch_op(*h, op, s);
+  }
+  return OCTMG_OK;
+}
+
+bool profiling(const Group& g) { return g.parts[0]->profiling; }
+
+octmg_status run_M(Group& g, cudaStream_t s) {
+  if (profiling(g)) {
+    OCTMG_TRY(launch_ops(g, s));
     OCTMG_CUDA(cudaGetLastError());
-    h.launches += schedule_kernels(h);
+    g.launches += schedule_kernels(g);
     return OCTMG_OK;
   }
-  if (!h.graph) {
-    if (!h.graph_stream) OCTMG_CUDA(cudaStreamCreateWithFlags(&h.graph_stream, cudaStreamNonBlocking));
-    cudaGraph_t g;
-    OCTMG_CUDA(cudaStreamBeginCapture(h.graph_stream, cudaStreamCaptureModeThreadLocal));
-    for (const Op& op : h.ops) launch_op(h, op, h.graph_stream);
-    cudaError_t e = cudaStreamEndCapture(h.graph_stream, &g);
+  if (!g.graph) {
+    if (!g.graph_stream) OCTMG_CUDA(cudaStreamCreateWithFlags(&g.graph_stream, cudaStreamNonBlocking));
+    cudaGraph_t gr;
+    OCTMG_CUDA(cudaStreamBeginCapture(g.graph_stream, cudaStreamCaptureModeThreadLocal));
+    octmg_status st = launch_ops(g, g.graph_stream);
+    cudaError_t e = cudaStreamEndCapture(g.graph_stream, &gr);
+    if (st != OCTMG_OK) return st;
     if (e != cudaSuccess) return cuda_status(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&h.graph, g, 0);
-    cudaGraphDestroy(g);
+    e = cudaGraphInstantiate(&g.graph, gr, 0);
+    cudaGraphDestroy(gr);
     if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate");
   }
-  OCTMG_CUDA(cudaGraphLaunch(h.graph, s));
-  h.launches += schedule_kernels(h);
+  OCTMG_CUDA(cudaGraphLaunch(g.graph, s));
+  g.launches += schedule_kernels(g);
+  return OCTMG_OK;
+}
+
+octmg_status allreduce(Group& g, int first, int count, cudaStream_t s) {
+  if (g.comm) return g.comm->allreduce(g, first, count, s);
   return OCTMG_OK;
 }
 
@@ -341,68 +398,233 @@ octmg_status octmg_tree_export(const octmg_tree* tree, int32_t what, void* host_
   return OCTMG_OK;
 }
 
+}  // extern "C"
+
+namespace octmg {
+namespace {
+
+// allocate and assemble one part (every part holds the full replicated coefficient set)
+octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* fbeta, const float* ffrac,
+                        const octmg_mg_params& prm, cudaStream_t s) {
+  h.tree = tree;
+  h.prm = prm;
+  const Tree& T = *tree;
+  size_t NLc = (size_t)T.NL * TB3, NIc = (size_t)T.NI * TB3;
+  OCTMG_TRY(halloc(h.allocs, &h.coef, (size_t)T.T * TB3));
+  OCTMG_TRY(halloc(h.allocs, &h.glayer_val, (size_t)T.n_glayers * 64));
+  OCTMG_TRY(halloc(h.allocs, &h.act, NLc / 32));
+  OCTMG_TRY(halloc(h.allocs, &h.z, NLc));
+  OCTMG_TRY(halloc(h.allocs, &h.uinA, NIc));
+  OCTMG_TRY(halloc(h.allocs, &h.zB, NLc));
+  OCTMG_TRY(halloc(h.allocs, &h.uinB, NIc));
+  OCTMG_TRY(halloc(h.allocs, &h.binner, NIc));
+  OCTMG_TRY(halloc(h.allocs, &h.ustar, NIc));
+  OCTMG_TRY(halloc(h.allocs, &h.r, NLc));
+  OCTMG_TRY(halloc(h.allocs, &h.p0, NLc));
+  OCTMG_TRY(halloc(h.allocs, &h.p1, NLc));
+  OCTMG_TRY(halloc(h.allocs, &h.q, NLc));
+  h.n_partial = std::max<size_t>((size_t)T.NL, 2 * (size_t)vec_grid()) + 16;
+  OCTMG_TRY(halloc(h.allocs, &h.partial, h.n_partial));
+  OCTMG_TRY(halloc(h.allocs, &h.counter, 16));
+  OCTMG_TRY(halloc(h.allocs, &h.sc, 1));
+  if (cudaMallocHost(&h.sc_host, sizeof(Scalars)) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("pinned allocation failed");
+    return OCTMG_E_OOM;
+  }
+  OCTMG_CUDA(cudaMemsetAsync(h.counter, 0, 16 * sizeof(unsigned), s));
+  OCTMG_CUDA(cudaMemsetAsync(h.uinA, 0, NIc * sizeof(float), s));
+  OCTMG_CUDA(cudaMemsetAsync(h.z, 0, NLc * sizeof(float), s));
+  OCTMG_CUDA(cudaMemsetAsync(h.p0, 0, NLc * sizeof(float), s));
+  OCTMG_CUDA(cudaMemsetAsync(h.p1, 0, NLc * sizeof(float), s));
+  OCTMG_CUDA(cudaMemsetAsync(h.sc, 0, sizeof(Scalars), s));
+  OCTMG_TRY(assemble_leaf_coefs(h, kind, fbeta, ffrac, s));
+  OCTMG_TRY(coarsen_all(h, s));
+  launch_build_mask(h.coef, (int64_t)NLc, h.act, s);
+  OCTMG_CUDA(cudaStreamSynchronize(s));
+  Scalars init{};
+  init.n_active = h.n_active;
+  OCTMG_CUDA(cudaMemcpy(h.sc, &init, sizeof(Scalars), cudaMemcpyHostToDevice));
+  return OCTMG_OK;
+}
+
+uint64_t morton3h(uint32_t i, uint32_t j, uint32_t k) {
+  uint64_t m = 0;
+  for (int b = 0; b < 21; ++b)
+    m |= ((uint64_t)((i >> b) & 1) << (3 * b)) | ((uint64_t)((j >> b) & 1) << (3 * b + 1)) |
+         ((uint64_t)((k >> b) & 1) << (3 * b + 2));
+  return m;
+}
+
+octmg_status plan_input(const Tree& T, PartInput& in) {
+  in.L = T.L; in.NL = T.NL; in.NI = T.NI;
+  in.lb = T.lb; in.lc = T.lc; in.ib = T.ib; in.ic = T.ic;
+  in.tiles4.resize((size_t)T.T * 4);
+  in.nbr.resize((size_t)T.T * 6);
+  in.parent.resize(T.T);
+  in.child.resize((size_t)T.NI * 8);
+  OCTMG_CUDA(cudaMemcpy(in.tiles4.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
+  OCTMG_CUDA(cudaMemcpy(in.nbr.data(), T.nbr, sizeof(int) * 6 * T.T, cudaMemcpyDeviceToHost));
+  OCTMG_CUDA(cudaMemcpy(in.parent.data(), T.parent, sizeof(int) * T.T, cudaMemcpyDeviceToHost));
+  if (T.NI) OCTMG_CUDA(cudaMemcpy(in.child.data(), T.child, sizeof(int) * 8 * T.NI, cudaMemcpyDeviceToHost));
+  in.morton.resize(T.T);
+  for (int t = 0; t < T.T; ++t) in.morton[t] = morton3h(in.tiles4[4 * t + 1], in.tiles4[4 * t + 2], in.tiles4[4 * t + 3]);
+  return OCTMG_OK;
+}
+
+// owned tile ranges of part h (contiguous per level by construction of the partition)
+octmg_status set_ownership(Hier& h, const PartPlan* P) {
+  const Tree& T = *h.tree;
+  std::vector<int> tiles;
+  for (int l = 0; l <= T.L; ++l) {
+    auto range = [&](int b, int c, int* ob, int* oc) -> bool {
+      if (!P || l < P->lg) { *ob = b; *oc = c; return true; }
+      int first = -1, cnt = 0;
+      for (int t = b; t < b + c; ++t)
+        if (P->owner[t] == h.rank) {
+          if (first < 0) first = t;
+          else if (t != first + cnt) return false;
+          cnt++;
+        }
+      *ob = first < 0 ? b : first;
+      *oc = cnt;
+      return true;
+    };
+    if (!range(T.lb[l], T.lc[l], &h.own_lb[l], &h.own_lc[l]) || !range(T.ib[l], T.ic[l], &h.own_ib[l], &h.own_ic[l])) {
+      set_error("partition ownership is not contiguous per level");
+      return OCTMG_E_INVALID;
+    }
+  }
+  h.own_cells = Ranges{};
+  for (int l = T.L; l >= 0; --l) {
+    if (!h.own_lc[l]) continue;
+    h.own_cells.begin[h.own_cells.n] = (int64_t)h.own_lb[l] * TB3 / 4;
+    h.own_cells.len[h.own_cells.n] = (int64_t)h.own_lc[l] * TB3 / 4;
+    h.own_cells.n++;
+    for (int t = h.own_lb[l]; t < h.own_lb[l] + h.own_lc[l]; ++t) tiles.push_back(t);
+  }
+  h.n_apply_tiles = (int)tiles.size();
+  OCTMG_TRY(halloc(h.allocs, &h.apply_tiles, tiles.size()));
+  OCTMG_CUDA(cudaMemcpy(h.apply_tiles, tiles.data(), sizeof(int) * tiles.size(), cudaMemcpyHostToDevice));
+  return OCTMG_OK;
+}
+
+bool valid_params(const octmg_mg_params& prm) {
+  return prm.alpha > 0.0f && prm.mu >= 1 && prm.mu <= 4 && prm.nu_pre >= 1 && prm.nu_post >= 1 &&
+         prm.nu_coarsest >= 1;
+}
+
+// a Group of `nparts` parts (1 = single GPU / one NCCL rank; >1 = loopback partition)
+octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void* nccl_comm, const uint8_t* kind,
+                        const float* fbeta, const float* ffrac, const octmg_mg_params* params, cudaStream_t s,
+                        octmg_hier** out) {
+  octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10};
+  if (params) prm = *params;
+  if (!valid_params(prm)) {
+    set_error("invalid multigrid parameters (need alpha > 0, 1 <= mu <= 4, nu_* >= 1)");
+    return OCTMG_E_INVALID;
+  }
+  auto* hh = new (std::nothrow) octmg_hier();
+  if (!hh) { set_error("host allocation failed"); return OCTMG_E_OOM; }
+  Group& g = hh->g;
+  auto fail = [&](octmg_status e) { delete hh; return e; };
+  for (int p = 0; p < nparts; ++p) {
+    Hier* h = new (std::nothrow) Hier();
+    if (!h) return fail(OCTMG_E_OOM);
+    g.parts.push_back(h);
+    h->rank = nparts > 1 ? p : rank;
+    h->nranks = nranks;
+    octmg_status st = setup_part(*h, &tree->t, kind, fbeta, ffrac, prm, s);
+    if (st) return fail(st);
+  }
+  const PartPlan* P = nullptr;
+  if (nranks > 1) {
+    g.plan = new PartPlanHolder();
+    PartInput in;
+    octmg_status st = plan_input(tree->t, in);
+    if (st) return fail(st);
+    const int lg = choose_partition_level(in, nranks);
+    build_partition(in, nranks, lg, g.plan->plan);
+    P = &g.plan->plan;
+    for (Hier* h : g.parts) h->lg = lg;
+    g.comm = nparts > 1 ? make_loopback_comm() : make_nccl_comm(nccl_comm, rank, nranks);
+  }
+  for (Hier* h : g.parts) {
+    octmg_status st = set_ownership(*h, P);
+    if (st) return fail(st);
+  }
+  if (P) {
+    octmg_status st = build_links(g, *P, s);
+    if (st) return fail(st);
+  }
+  octmg_status st = build_schedule(g);
+  if (st) return fail(st);
+  *out = hh;
+  return OCTMG_OK;
+}
+
+ApplyArgs apply_args(const Hier& h) {
+  const Tree& T = *h.tree;
+  ApplyArgs a;
+  a.tiles = h.apply_tiles; a.ntiles = h.n_apply_tiles;
+  a.tile = T.tile; a.nbr = T.nbr; a.child = T.child; a.coef = h.coef; a.glayer_val = h.glayer_val;
+  a.glayer = T.glayer; a.z = nullptr; a.pold = nullptr; a.pnew = nullptr; a.q = nullptr;
+  a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL; a.use_beta = 0;
+  return a;
+}
+
+}  // namespace
+}  // namespace octmg
+
+extern "C" {
+
 octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const float* face_beta,
                                    const float* face_frac, const octmg_mg_params* params, octmg_stream stream,
                                    octmg_hier** out) {
   if (!tree || !kind || !out) { set_error("null argument"); return OCTMG_E_INVALID; }
   *out = nullptr;
-  octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10};
-  if (params) prm = *params;
-  if (!(prm.alpha > 0.0f) || prm.mu < 1 || prm.mu > 4 || prm.nu_pre < 1 || prm.nu_post < 1 || prm.nu_coarsest < 1) {
-    set_error("invalid multigrid parameters (need alpha > 0, 1 <= mu <= 4, nu_* >= 1)");
-    return OCTMG_E_INVALID;
-  }
-  cudaStream_t s = (cudaStream_t)stream;
-  auto* hh = new (std::nothrow) octmg_hier();
-  if (!hh) { set_error("host allocation failed"); return OCTMG_E_OOM; }
-  Hier& h = hh->h;
-  h.tree = &tree->t;
-  h.prm = prm;
   const Tree& T = tree->t;
-  size_t NLc = (size_t)T.NL * TB3, NIc = (size_t)T.NI * TB3;
-  octmg_status st = OCTMG_OK;
-  auto fail = [&](octmg_status e) { delete hh; return e; };
-  if ((st = halloc(h.allocs, &h.coef, (size_t)T.T * TB3))) return fail(st);
-  if ((st = halloc(h.allocs, &h.glayer_val, (size_t)T.n_glayers * 64))) return fail(st);
-  if ((st = halloc(h.allocs, &h.act, NLc / 32))) return fail(st);
-  if ((st = halloc(h.allocs, &h.z, NLc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.uinA, NIc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.zB, NLc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.uinB, NIc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.binner, NIc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.ustar, NIc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.r, NLc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.p0, NLc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.p1, NLc))) return fail(st);
-  if ((st = halloc(h.allocs, &h.q, NLc))) return fail(st);
-  h.n_partial = std::max<size_t>((size_t)T.NL, 2 * (size_t)vec_grid()) + 16;
-  if ((st = halloc(h.allocs, &h.partial, h.n_partial))) return fail(st);
-  if ((st = halloc(h.allocs, &h.counter, 16))) return fail(st);
-  if ((st = halloc(h.allocs, &h.sc, 1))) return fail(st);
-  if (cudaMallocHost(&h.sc_host, sizeof(Scalars)) != cudaSuccess) {
-    cudaGetLastError();
-    set_error("pinned allocation failed");
-    return fail(OCTMG_E_OOM);
+  return make_group(tree, 1, T.rank, T.nranks, T.nccl_comm, kind, face_beta, face_frac, params, (cudaStream_t)stream,
+                    out);
+}
+
+octmg_status octmg_setup_hierarchy_loopback(octmg_tree* tree, int32_t nparts, const uint8_t* kind,
+                                            const float* face_beta, const float* face_frac,
+                                            const octmg_mg_params* params, octmg_stream stream, octmg_hier** out) {
+  if (!tree || !kind || !out || nparts < 1 || nparts > 64) { set_error("bad argument"); return OCTMG_E_INVALID; }
+  *out = nullptr;
+  return make_group(tree, nparts, 0, nparts, nullptr, kind, face_beta, face_frac, params, (cudaStream_t)stream, out);
+}
+
+octmg_status octmg_partition_info(const octmg_hier* hh, int32_t part, int32_t* lg, int32_t* rank, int32_t* nranks,
+                                  int32_t* own_leaf_begin, int32_t* own_leaf_count) {
+  if (!hh || part < 0 || part >= (int)hh->g.parts.size()) { set_error("bad argument"); return OCTMG_E_INVALID; }
+  const Hier& h = *hh->g.parts[part];
+  if (lg) *lg = h.lg;
+  if (rank) *rank = h.rank;
+  if (nranks) *nranks = h.nranks;
+  for (int l = 0; l <= h.tree->L; ++l) {
+    if (own_leaf_begin) own_leaf_begin[l] = h.own_lb[l];
+    if (own_leaf_count) own_leaf_count[l] = h.own_lc[l];
   }
-  cudaError_t e = cudaMemsetAsync(h.counter, 0, 16 * sizeof(unsigned), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h.uinA, 0, NIc * sizeof(float) + 0, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h.z, 0, NLc * sizeof(float), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(h.sc, 0, sizeof(Scalars), s);
-  if (e != cudaSuccess) return fail(cuda_status(e, "memset"));
-  if ((st = assemble_leaf_coefs(h, kind, face_beta, face_frac, s))) return fail(st);
-  if ((st = coarsen_all(h, s))) return fail(st);
-  launch_build_mask(h.coef, (int64_t)NLc, h.act, s);
-  e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(cuda_status(e, "setup"));
-  if ((st = build_schedule(h))) return fail(st);
-  if (e != cudaSuccess) return fail(cuda_status(e, "setup"));
-  *out = hh;
   return OCTMG_OK;
 }
 
+octmg_status octmg_nccl_unique_id(void* out128) {
+  if (!out128) { set_error("null argument"); return OCTMG_E_INVALID; }
+  return nccl_unique_id(out128);
+}
+
+octmg_status octmg_nccl_comm_init(int32_t rank, int32_t nranks, const void* id128, void** comm) {
+  if (!id128 || !comm) { set_error("null argument"); return OCTMG_E_INVALID; }
+  return nccl_comm_init(rank, nranks, id128, comm);
+}
+
+void octmg_nccl_comm_destroy(void* comm) { nccl_comm_destroy(comm); }
+
 octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size_t bytes) {
   if (!hh || !host_dst) { set_error("null argument"); return OCTMG_E_INVALID; }
-  const Hier& h = hh->h;
+  const Hier& h = *hh->g.parts[0];
   size_t need = (size_t)h.tree->T * TB3 * sizeof(float4);
   if (bytes != need) { set_error("export buffer size mismatch"); return OCTMG_E_INVALID; }
   OCTMG_CUDA(cudaDeviceSynchronize());
@@ -410,41 +632,33 @@ octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size
   return OCTMG_OK;
 }
 
-static ApplyArgs apply_args(const Hier& h) {
-  const Tree& T = *h.tree;
-  ApplyArgs a;
-  a.tile = T.tile; a.nbr = T.nbr; a.child = T.child; a.coef = h.coef; a.glayer_val = h.glayer_val;
-  a.glayer = T.glayer; a.z = nullptr; a.pold = nullptr; a.pnew = nullptr; a.q = nullptr;
-  a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL; a.use_beta = 0;
-  return a;
-}
-
 octmg_status octmg_apply(octmg_hier* hh, const float* x, float* y, octmg_stream stream) {
   if (!hh || !x || !y) { set_error("null argument"); return OCTMG_E_INVALID; }
-  Hier& h = hh->h;
+  Group& g = hh->g;
   cudaStream_t s = (cudaStream_t)stream;
-  // mask the caller's x to the active cells (the operator kernel relies on zeros there)
-  launch_mask_copy(x, h.act, h.p1, (int64_t)h.tree->NL * TB3, s);
-  ApplyArgs a = apply_args(h);
-  a.z = h.p1;
-  a.q = y;
-  {
-    ProfScope ps(h, KC_APPLY, s, (double)h.tree->NL * TB3 * 24.0);  // read x, record; write y
+  for (Hier* hp : g.parts) {
+    Hier& h = *hp;
+    // mask the caller's (replicated) x to the active cells: the operator relies on zeros
+    launch_mask_copy(x, h.act, h.p1, (int64_t)h.tree->NL * TB3, s);
+    ApplyArgs a = apply_args(h);
+    a.z = h.p1;
+    a.q = y;  // each part writes its owned leaf tiles
+    ProfScope ps(h, KC_APPLY, s, (double)h.n_apply_tiles * TB3 * 24.0);  // read x, record; write y
     launch_apply(a, s);
   }
-  h.launches += 1;
+  g.launches += 2 * (int64_t)g.parts.size();
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
 }
 
 octmg_status octmg_vcycle(octmg_hier* hh, const float* b, float* u, octmg_stream stream) {
   if (!hh || !b || !u) { set_error("null argument"); return OCTMG_E_INVALID; }
-  Hier& h = hh->h;
+  Group& g = hh->g;
   cudaStream_t s = (cudaStream_t)stream;
-  size_t N = (size_t)h.tree->NL * TB3;
-  launch_mask_copy(b, h.act, h.r, (int64_t)N, s);
-  OCTMG_TRY(run_M(h, s));
-  OCTMG_CUDA(cudaMemcpyAsync(u, h.z, N * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  for (Hier* h : g.parts) launch_mask_copy(b, h->act, h->r, (int64_t)h->tree->NL * TB3, s);
+  OCTMG_TRY(run_M(g, s));
+  for (Hier* h : g.parts) launch_copy_ranges(h->z, u, h->own_cells, s);  // owned cells of each part
+  g.launches += 2 * (int64_t)g.parts.size();
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
 }
@@ -452,17 +666,17 @@ octmg_status octmg_vcycle(octmg_hier* hh, const float* b, float* u, octmg_stream
 octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const octmg_solve_params* params,
                              octmg_solve_report* report, octmg_stream stream) {
   if (!hh || !b || !x) { set_error("null argument"); return OCTMG_E_INVALID; }
-  Hier& h = hh->h;
-  const Tree& T = *h.tree;
+  Group& g = hh->g;
+  Hier& h0 = *g.parts[0];
   cudaStream_t s = (cudaStream_t)stream;
   octmg_solve_params prm{1e-6, 200, -1};
   if (params) prm = *params;
   if (!(prm.rtol > 0.0) || prm.max_iters < 1) { set_error("invalid solve parameters"); return OCTMG_E_INVALID; }
-  const bool ns = prm.nullspace < 0 ? !h.any_dirichlet : prm.nullspace == 1;
-  const int64_t N = (int64_t)T.NL * TB3;
+  const bool ns = prm.nullspace < 0 ? !h0.any_dirichlet : prm.nullspace == 1;
   const int G = vec_grid();
-  const int64_t launches0 = h.launches;
-  Scalars* hs = h.sc_host;
+  const int64_t launches0 = g.launches;
+  const int np = (int)g.parts.size();
+  Scalars* hs = h0.sc_host;
   auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
     if (report) {
       report->iters = iters;
@@ -470,102 +684,111 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       report->rel_residual = rel;
       report->bnorm = bn;
       report->status = st;
-      report->kernel_launches = h.launches - launches0;
+      report->kernel_launches = g.launches - launches0;
     }
     return st;
   };
   auto fetch = [&]() -> octmg_status {
-    OCTMG_CUDA(cudaMemcpyAsync(hs, h.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    OCTMG_CUDA(cudaMemcpyAsync(hs, h0.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
     OCTMG_CUDA(cudaStreamSynchronize(s));
     return OCTMG_OK;
   };
-  // n_active for the projection mean
-  hs->n_active = h.n_active;
-  OCTMG_CUDA(cudaMemcpyAsync(&h.sc->n_active, &hs->n_active, sizeof(double), cudaMemcpyHostToDevice, s));
-  {
-    ProfScope ps(h, KC_INIT, s, (double)N * 12.125);  // read b, mask; write r, x
-    launch_init(b, h.act, h.r, x, N, h.partial, h.counter, h.sc, s, G);
+  auto project = [&]() -> octmg_status {  // r -= mean(r) over all parts, then ||r||^2
+    for (Hier* h : g.parts) {
+      ProfScope ps(*h, KC_PROJECT, s, (double)h->n_apply_tiles * TB3 * 8.125);  // read r, mask; write r
+      launch_project(h->r, h->act, h->own_cells, h->partial, h->counter + 1, h->sc, s, G);
+    }
+    g.launches += np;
+    return allreduce(g, SF_RR, 1, s);
+  };
+  auto dot_rz = [&]() -> octmg_status {
+    for (Hier* h : g.parts) {
+      ProfScope ps(*h, KC_DOT, s, (double)h->n_apply_tiles * TB3 * 8.0);
+      launch_dot_rz(h->r, h->z, h->own_cells, h->partial, h->counter + 2, h->sc, s, G);
+    }
+    g.launches += np;
+    return allreduce(g, SF_RZ, 1, s);
+  };
+  for (Hier* h : g.parts) {
+    ProfScope ps(*h, KC_INIT, s, (double)h->n_apply_tiles * TB3 * 12.125);  // read b, mask; write r, x
+    launch_init(b, h->act, h->r, x, h->own_cells, h->partial, h->counter, h->sc, s, G);
   }
-  h.launches++;
-  if (ns) {
-    ProfScope ps(h, KC_PROJECT, s, (double)N * 8.125);  // read r, mask; write r
-    launch_project(h.r, h.act, N, h.partial, h.counter + 1, h.sc, s, G);
-    h.launches++;
-  }
+  g.launches += np;
+  OCTMG_TRY(allreduce(g, SF_RR, 2, s));
+  if (ns) OCTMG_TRY(project());
   OCTMG_TRY(fetch());
-  if (hs->flags & 2) { set_error("non-finite right-hand side"); return fill(OCTMG_E_NONFINITE, 0, false, 0, 0); }
-  const double bn = std::sqrt(hs->rr);
+  if (!std::isfinite(hs->sum_rr)) { set_error("non-finite right-hand side"); return fill(OCTMG_E_NONFINITE, 0, false, 0, 0); }
+  const double bn = std::sqrt(hs->sum_rr);
   if (bn == 0.0) return fill(OCTMG_OK, 0, true, 0.0, 0.0);
-  OCTMG_TRY(run_M(h, s));
-  {
-    ProfScope ps(h, KC_DOT, s, (double)N * 8.0);
-    launch_dot_rz(h.r, h.z, N, h.partial, h.counter + 2, h.sc, 1, s, G);
-  }
-  h.launches++;
-  float* pcur = h.p0;
-  float* pprev = h.p1;
+  OCTMG_TRY(run_M(g, s));
+  OCTMG_TRY(dot_rz());
   int k = 0;
   double rel = 1.0;
+  int cur = 0;  // p0/p1 ping-pong: p_new in (cur ? p1 : p0)
   while (true) {
-    ApplyArgs a = apply_args(h);
-    a.z = h.z;
-    a.pold = k == 0 ? nullptr : pprev;
-    a.pnew = pcur;
-    a.q = h.q;
-    a.partial = h.partial;
-    a.counter = h.counter + 3;
-    a.use_beta = k > 0;
-    {
-      // read z, p_old, record (24 B/leaf); write p, q (8 B/leaf)
-      ProfScope ps(h, KC_APPLY, s, (double)N * 32.0);
-      launch_apply(a, s);
+    std::vector<Fld> pf;
+    for (Hier* h : g.parts) {
+      float* pcur = cur ? h->p1 : h->p0;
+      float* pprev = cur ? h->p0 : h->p1;
+      ApplyArgs a = apply_args(*h);
+      a.z = h->z;
+      a.pold = k == 0 ? nullptr : pprev;
+      a.pnew = pcur;
+      a.q = h->q;
+      a.partial = h->partial;
+      a.counter = h->counter + 3;
+      a.use_beta = k > 0;
+      {
+        // read z, p_old, record (24 B/leaf); write p, q (8 B/leaf)
+        ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 32.0);
+        launch_apply(a, s);
+      }
+      pf.push_back(Fld{pcur, nullptr});
     }
-    {
-      ProfScope ps(h, KC_UPDATE, s, (double)N * 24.0);  // read x, r, p, q; write x, r
-      launch_update(x, h.r, pcur, h.q, N, h.partial, h.counter + 4, h.sc, s, G);
+    g.launches += 2 * np;
+    OCTMG_TRY(allreduce(g, SF_PQ, 1, s));
+    if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
+    for (Hier* h : g.parts) {
+      ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r
+      launch_update(x, h->r, cur ? h->p1 : h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G);
     }
-    h.launches += 3;  // apply, finish_sigma, update
-    if (ns) {
-      ProfScope ps(h, KC_PROJECT, s, (double)N * 8.125);
-      launch_project(h.r, h.act, N, h.partial, h.counter + 1, h.sc, s, G);
-      h.launches++;
-    }
+    g.launches += np;
+    OCTMG_TRY(allreduce(g, SF_RR, 2, s));
+    if (ns) OCTMG_TRY(project());
     OCTMG_CUDA(cudaGetLastError());
     OCTMG_TRY(fetch());
     if (hs->flags & 1) {
       set_error("PCG breakdown: p.Ap <= 0");
       return fill(OCTMG_E_BREAKDOWN, k, false, rel, bn);
     }
-    if (hs->flags & 2) { set_error("non-finite PCG scalar"); return fill(OCTMG_E_NONFINITE, k, false, rel, bn); }
+    if (!std::isfinite(hs->sum_rr)) { set_error("non-finite PCG scalar"); return fill(OCTMG_E_NONFINITE, k, false, rel, bn); }
     k++;
-    rel = std::sqrt(hs->rr) / bn;
+    rel = std::sqrt(hs->sum_rr) / bn;
     if (report && report->history && k - 1 < report->history_cap) report->history[k - 1] = rel;
     if (rel <= prm.rtol) return fill(OCTMG_OK, k, true, rel, bn);
     if (k >= prm.max_iters) { set_error("PCG did not converge within max_iters"); return fill(OCTMG_E_MAXITER, k, false, rel, bn); }
-    OCTMG_TRY(run_M(h, s));
-    {
-      ProfScope ps(h, KC_DOT, s, (double)N * 8.0);
-      launch_dot_rz(h.r, h.z, N, h.partial, h.counter + 2, h.sc, 0, s, G);
-    }
-    h.launches++;
-    std::swap(pcur, pprev);
+    OCTMG_TRY(run_M(g, s));
+    OCTMG_TRY(dot_rz());
+    cur ^= 1;
   }
 }
 
 octmg_status octmg_profile_enable(octmg_hier* hh, int32_t on) {
   if (!hh) { set_error("null argument"); return OCTMG_E_INVALID; }
-  Hier& h = hh->h;
-  h.profiling = on != 0;
-  h.events.clear();
-  h.event_next = 0;
-  for (int c = 0; c < KC_COUNT; ++c) { h.prof_ms[c] = 0.0; h.prof_cnt[c] = 0; h.prof_bytes[c] = 0.0; }
+  for (Hier* hp : hh->g.parts) {
+    Hier& h = *hp;
+    h.profiling = on != 0;
+    h.events.clear();
+    h.event_next = 0;
+    for (int c = 0; c < KC_COUNT; ++c) { h.prof_ms[c] = 0.0; h.prof_cnt[c] = 0; h.prof_bytes[c] = 0.0; }
+  }
   return OCTMG_OK;
 }
 
 octmg_status octmg_profile_read(octmg_hier* hh, const char** names, double* ms, int64_t* counts, double* bytes,
                                 int32_t cap, int32_t* n) {
   if (!hh || !n) { set_error("null argument"); return OCTMG_E_INVALID; }
-  Hier& h = hh->h;
+  Hier& h = *hh->g.parts[0];
   OCTMG_CUDA(cudaDeviceSynchronize());
   for (auto& ev : h.events) {
     float t = 0.0f;

@@ -63,7 +63,6 @@ __device__ __forceinline__ float pval(const ApplyArgs& a, float beta, size_t i) 
 __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta, int t, int x, int y, int z,
                                                  const float4& q, float pi, float mP, float s0, const float* sp,
                                                  const float (*scm)[TB3]) {
-  const size_t base = (size_t)t * TB3;
   const int c[3] = {x, y, z};
   float s = s0;
 #pragma unroll
@@ -120,13 +119,14 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
 template <bool DOT>
 __global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
   __shared__ double sred[NT / 32];
-  const int t = blockIdx.x;
+  const int t = a.tiles[blockIdx.x];
   const int j = threadIdx.x;
   const int x2 = j & 3;
   const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
   const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
   const int x0 = 2 * x2;
-  const float beta = (a.use_beta && a.pold) ? (float)a.sc->beta : 0.0f;
+  // beta = (r_k, z_k) / (r_{k-1}, z_{k-1}) (Alg. 1 line 12)
+  const float beta = (a.use_beta && a.pold) ? (float)(a.sc->sum_rz / a.sc->rho) : 0.0f;
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
   const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
@@ -168,7 +168,7 @@ __global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
   }
 }
 
-// sigma = p.q from the per-tile partials (fixed order => deterministic), alpha = rho / sigma
+// sigma = p.q from the per-tile partials (fixed order => deterministic)
 __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, int n, Scalars* sc) {
   __shared__ double sred[32];
   double s = 0.0;
@@ -179,23 +179,45 @@ __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, in
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sred[w];
-    sc->sigma = tot;
-    if (!(tot > 0.0) || !isfinite(tot)) { sc->flags |= 1; sc->alpha = 0.0; }
-    else sc->alpha = sc->rho / tot;
+    sc->sum_pq = tot;
   }
 }
 
 // ------------------------------------------------------------------------------------
-// PCG vector kernels (grid-stride over float4, fixed grid => deterministic partials)
+// PCG vector kernels over this part's owned leaf cells (float4 index ranges); fixed grid and
+// fixed-order last-block reductions => deterministic.  They write raw local sums into the
+// Scalars; multi-part jobs sum those across parts before any consumer reads them.
 // ------------------------------------------------------------------------------------
 // activity nibble of the 4 cells of float4 index i (bit k = cell 4i+k active; mask bit per cell)
 __device__ __forceinline__ unsigned act4(const uint32_t* act, int64_t i) { return (act[i >> 3] >> ((i & 7) * 4)) & 0xFu; }
 
-__global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n4,
+#define FOR_RANGES(R, i)                                                                          \
+  for (int rr_ = 0; rr_ < (R).n; ++rr_)                                                           \
+    for (int64_t i = (R).begin[rr_] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;             \
+         i < (R).begin[rr_] + (R).len[rr_]; i += (int64_t)gridDim.x * blockDim.x)
+
+// two ordered sums (s2, s1) over the grid; the last block stores them at sc fields f2, f1
+__device__ __forceinline__ void reduce2(double s2, double s1, double* partial, unsigned* counter, Scalars* sc,
+                                        int f2, int f1, double* sred) {
+  double b2 = block_reduce_d(s2, sred);
+  __syncthreads();
+  double b1 = block_reduce_d(s1, sred);
+  double tot;
+  if (threadIdx.x == 0) partial[gridDim.x + blockIdx.x] = b1;
+  if (last_block_sum(b2, partial, counter, gridDim.x, &tot, sred)) {
+    double t1 = 0.0;
+    for (int k = 0; k < (int)gridDim.x; ++k) t1 += ((volatile double*)partial)[gridDim.x + k];
+    reinterpret_cast<double*>(sc)[f2] = tot;
+    if (f1 >= 0) reinterpret_cast<double*>(sc)[f1] = t1;
+  }
+}
+
+// r = b on active cells (0 elsewhere), x = 0; sums ||r||^2, sum r (Alg. 1 lines 3-4)
+__global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* act, float* r, float* x, Ranges R,
                                               double* partial, unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   double s2 = 0.0, s1 = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  FOR_RANGES(R, i) {
     float4 v = reinterpret_cast<const float4*>(b)[i];
     float m[4] = {v.x, v.y, v.z, v.w};
     const unsigned am = act4(act, i);
@@ -207,27 +229,20 @@ __global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* ac
     reinterpret_cast<float4*>(r)[i] = make_float4(m[0], m[1], m[2], m[3]);
     reinterpret_cast<float4*>(x)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  double b2 = block_reduce_d(s2, sred);
-  __syncthreads();
-  double b1 = block_reduce_d(s1, sred);
-  double tot;
-  // two sums: partial layout [0, grid) = s2, [grid, 2 grid) = s1
-  if (threadIdx.x == 0) partial[gridDim.x + blockIdx.x] = b1;
-  if (last_block_sum(b2, partial, counter, gridDim.x, &tot, sred)) {
-    double t1 = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) t1 += ((volatile double*)partial)[gridDim.x + k];
-    sc->rr = tot;
-    sc->rsum = t1;
-    sc->flags = isfinite(tot) ? 0 : 2;
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->flags = 0;
+  reduce2(s2, s1, partial, counter, sc, SF_RR, SF_R, sred);
 }
 
-__global__ __launch_bounds__(256) void k_update(float* x, float* r, const float* p, const float* q, int64_t n4,
+// x += alpha p, r -= alpha q with alpha = (r,z)/(p,Ap) (Alg. 1 lines 9-11); sums ||r||^2,
+// sum r.  The last block flags a breakdown and records rho = (r, z) for the next beta.
+__global__ __launch_bounds__(256) void k_update(float* x, float* r, const float* p, const float* q, Ranges R,
                                                 double* partial, unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
-  const float alpha = (sc->flags & 1) ? 0.0f : (float)sc->alpha;
+  const double pq = sc->sum_pq, rz = sc->sum_rz;
+  const bool ok = pq > 0.0 && isfinite(pq) && isfinite(rz);
+  const float alpha = ok ? (float)(rz / pq) : 0.0f;
   double s2 = 0.0, s1 = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  FOR_RANGES(R, i) {
     float4 xv = reinterpret_cast<float4*>(x)[i];
     float4 rv = reinterpret_cast<float4*>(r)[i];
     float4 pv = reinterpret_cast<const float4*>(p)[i];
@@ -249,19 +264,20 @@ __global__ __launch_bounds__(256) void k_update(float* x, float* r, const float*
   if (last_block_sum(b2, partial, counter, gridDim.x, &tot, sred)) {
     double t1 = 0.0;
     for (int k = 0; k < (int)gridDim.x; ++k) t1 += ((volatile double*)partial)[gridDim.x + k];
-    sc->rr = tot;
-    sc->rsum = t1;
-    if (!isfinite(tot)) sc->flags |= 2;
+    sc->sum_rr = tot;
+    sc->sum_r = t1;
+    sc->rho = rz;
+    if (!ok) sc->flags |= 1;
   }
 }
 
-// null-space projection r -= mean_active(r), recomputes ||r||^2
-__global__ __launch_bounds__(256) void k_project(float* r, const uint32_t* act, int64_t n4, double* partial,
+// null-space projection r -= mean_active(r), mean over all parts; ||r||^2
+__global__ __launch_bounds__(256) void k_project(float* r, const uint32_t* act, Ranges R, double* partial,
                                                  unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
-  const float m = (float)(sc->rsum / sc->n_active);
+  const float m = (float)(sc->sum_r / sc->n_active);
   double s2 = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  FOR_RANGES(R, i) {
     float4 v = reinterpret_cast<float4*>(r)[i];
     float e[4] = {v.x, v.y, v.z, v.w};
     const unsigned am = act4(act, i);
@@ -273,29 +289,26 @@ __global__ __launch_bounds__(256) void k_project(float* r, const uint32_t* act, 
   }
   double b2 = block_reduce_d(s2, sred);
   double tot;
-  if (last_block_sum(b2, partial, counter, gridDim.x, &tot, sred)) {
-    sc->rr = tot;
-    sc->mean = m;
-  }
+  if (last_block_sum(b2, partial, counter, gridDim.x, &tot, sred)) sc->sum_rr = tot;
 }
 
-__global__ __launch_bounds__(256) void k_dot_rz(const float* r, const float* z, int64_t n4, double* partial,
-                                                unsigned* counter, Scalars* sc, int first) {
+// (r, z) (Alg. 1 line 12)
+__global__ __launch_bounds__(256) void k_dot_rz(const float* r, const float* z, Ranges R, double* partial,
+                                                unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  FOR_RANGES(R, i) {
     float4 a = reinterpret_cast<const float4*>(r)[i];
     float4 b = reinterpret_cast<const float4*>(z)[i];
     s += (double)a.x * b.x + (double)a.y * b.y + (double)a.z * b.z + (double)a.w * b.w;
   }
   double bs = block_reduce_d(s, sred);
   double tot;
-  if (last_block_sum(bs, partial, counter, gridDim.x, &tot, sred)) {
-    if (first) { sc->beta = 0.0; }
-    else sc->beta = tot / sc->rho;
-    sc->rho = tot;
-    if (!isfinite(tot)) sc->flags |= 2;
-  }
+  if (last_block_sum(bs, partial, counter, gridDim.x, &tot, sred)) sc->sum_rz = tot;
+}
+
+__global__ void k_copy_ranges(const float* src, float* dst, Ranges R) {
+  FOR_RANGES(R, i) reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
 }
 
 __global__ void k_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n) {
@@ -315,30 +328,36 @@ __global__ void k_build_mask(const float4* coef, int64_t nwords, uint32_t* act) 
 }  // namespace
 
 void launch_apply(const ApplyArgs& a, cudaStream_t s) {
-  if (a.NL == 0) return;
+  if (a.ntiles == 0) {
+    if (a.partial) cudaMemsetAsync(&a.sc->sum_pq, 0, sizeof(double), s);
+    return;
+  }
   if (a.partial) {
-    k_apply<true><<<a.NL, NT, 0, s>>>(a);
-    k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.NL, a.sc);
+    k_apply<true><<<a.ntiles, NT, 0, s>>>(a);
+    k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.ntiles, a.sc);
   } else {
-    k_apply<false><<<a.NL, NT, 0, s>>>(a);
+    k_apply<false><<<a.ntiles, NT, 0, s>>>(a);
   }
 }
 
-void launch_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n, double* partial,
+void launch_init(const float* b, const uint32_t* act, float* r, float* x, const Ranges& R, double* partial,
                  unsigned* counter, Scalars* sc, cudaStream_t s, int grid) {
-  k_init<<<grid, 256, 0, s>>>(b, act, r, x, n / 4, partial, counter, sc);
+  k_init<<<grid, 256, 0, s>>>(b, act, r, x, R, partial, counter, sc);
 }
-void launch_update(float* x, float* r, const float* p, const float* q, int64_t n, double* partial,
+void launch_update(float* x, float* r, const float* p, const float* q, const Ranges& R, double* partial,
                    unsigned* counter, Scalars* sc, cudaStream_t s, int grid) {
-  k_update<<<grid, 256, 0, s>>>(x, r, p, q, n / 4, partial, counter, sc);
+  k_update<<<grid, 256, 0, s>>>(x, r, p, q, R, partial, counter, sc);
 }
-void launch_project(float* r, const uint32_t* act, int64_t n, double* partial, unsigned* counter, Scalars* sc,
+void launch_project(float* r, const uint32_t* act, const Ranges& R, double* partial, unsigned* counter, Scalars* sc,
                     cudaStream_t s, int grid) {
-  k_project<<<grid, 256, 0, s>>>(r, act, n / 4, partial, counter, sc);
+  k_project<<<grid, 256, 0, s>>>(r, act, R, partial, counter, sc);
 }
-void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, unsigned* counter, Scalars* sc,
-                   int first, cudaStream_t s, int grid) {
-  k_dot_rz<<<grid, 256, 0, s>>>(r, z, n / 4, partial, counter, sc, first);
+void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* partial, unsigned* counter, Scalars* sc,
+                   cudaStream_t s, int grid) {
+  k_dot_rz<<<grid, 256, 0, s>>>(r, z, R, partial, counter, sc);
+}
+void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s) {
+  k_copy_ranges<<<592, 256, 0, s>>>(src, dst, R);
 }
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s) {
   k_mask_copy<<<592, 256, 0, s>>>(src, act, dst, n);

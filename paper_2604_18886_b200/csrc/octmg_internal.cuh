@@ -44,6 +44,8 @@ struct Tree {
   int NL = 0, NI = 0, T = 0;
   int lb[MAXL + 1] = {}, lc[MAXL + 1] = {}, ib[MAXL + 1] = {}, ic[MAXL + 1] = {};
   int n_glayers = 0;
+  int rank = 0, nranks = 1;        // multi-GPU job (octmg_tree_desc)
+  void* nccl_comm = nullptr;
   // device
   uint64_t* leaf_keys = nullptr;   // [NL] sorted
   uint64_t* inner_keys = nullptr;  // [NI] sorted
@@ -68,18 +70,27 @@ __device__ __forceinline__ float* tptr(const Fld& f, int t, int NL) {
   return t < NL ? f.leaf + (size_t)t * TB3 : f.inner + (size_t)(t - NL) * TB3;
 }
 
-// PCG scalars, device resident (fp64)
+// PCG scalars, device resident (fp64).  The sum_* fields are the reductions of
+// the last kernel that produced them: local to this part first, then (multi-part) summed
+// over all parts in place before any consumer reads them.
 struct Scalars {
-  double rho;      // (r, z)
-  double sigma;    // (p, Ap)
-  double alpha;
-  double beta;
-  double rr;       // ||r||^2 (after projection if enabled)
-  double rsum;     // sum of r over active cells (null-space projection)
-  double mean;     // projection mean
-  double n_active; // number of active leaf cells
-  int flags;       // bit0: breakdown (sigma <= 0 or non-finite); bit1: non-finite rho/alpha
+  double sum_rr;   // ||r||^2
+  double sum_r;    // sum of r over active cells (null-space projection)
+  double sum_rz;   // (r, z) of the current iteration
+  double sum_pq;   // (p, A p)
+  double rho;      // (r, z) of the previous iteration (beta = sum_rz / rho)
+  double n_active; // number of active leaf cells (all parts)
+  int flags;       // bit0: breakdown (sigma <= 0 or non-finite)
   int pad;
+};
+// offsets (in doubles) of the reduced fields, for the cross-part sums
+enum { SF_RR = 0, SF_R = 1, SF_RZ = 2, SF_PQ = 3 };
+
+// owned leaf cells as float4 index ranges (one per level at most)
+struct Ranges {
+  int n = 0;
+  int64_t begin[OCTMG_MAX_LEVELS + 1] = {};
+  int64_t len[OCTMG_MAX_LEVELS + 1] = {};
 };
 
 // Kernel classes for profiling
@@ -93,6 +104,8 @@ struct Hier;
 
 // launch helpers implemented in kernels.cu
 struct ApplyArgs {
+  const int* tiles;     // leaf tiles to compute (owned by this part)
+  int ntiles;
   const int4* tile;
   const int* nbr;
   const int* child;
@@ -105,21 +118,22 @@ struct ApplyArgs {
   float* q;             // A p
   double* partial;      // per-tile fp64 partial of p.q (nullptr: no dot)
   unsigned* counter;
-  Scalars* sc;          // beta read from here; sigma/alpha written by the last block
+  Scalars* sc;          // beta = sum_rz / rho read from here; sum_pq written by the finish kernel
   int NL;
   int use_beta;
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
 // vector kernels (PCG)
-void launch_init(const float* b, const uint32_t* act, float* r, float* x, int64_t n, double* partial,
+void launch_init(const float* b, const uint32_t* act, float* r, float* x, const Ranges& R, double* partial,
                  unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
-void launch_update(float* x, float* r, const float* p, const float* q, int64_t n, double* partial,
+void launch_update(float* x, float* r, const float* p, const float* q, const Ranges& R, double* partial,
                    unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
-void launch_project(float* r, const uint32_t* act, int64_t n, double* partial, unsigned* counter,
+void launch_project(float* r, const uint32_t* act, const Ranges& R, double* partial, unsigned* counter,
                     Scalars* sc, cudaStream_t s, int grid);
-void launch_dot_rz(const float* r, const float* z, int64_t n, double* partial, unsigned* counter,
-                   Scalars* sc, int first, cudaStream_t s, int grid);
+void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* partial, unsigned* counter,
+                   Scalars* sc, cudaStream_t s, int grid);
+void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s);
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);
 void launch_build_mask(const float4* coef, int64_t n, uint32_t* act, cudaStream_t s);
 
@@ -171,7 +185,8 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
 // ------------------------------------------------------------------------------------
 struct Op {
   int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle,
-               // 5 fused RB iteration, 6 copy level buffer in -> out
+               // 5 fused RB iteration, 6 copy level buffer in -> out, 7 halo exchange of level
+               // `level` of u, 8 broadcast of the restricted partition-parent level
   int level;
   int stage;   // bit0 colour, bits1.. mode (SM_*); kind 5: bit0 first colour, bit1 zero
   int in_buf = 0, out_buf = 0;
@@ -202,17 +217,13 @@ struct Hier {
   Scalars* sc_host = nullptr;    // pinned mirror
   double n_active = 0;
   int any_dirichlet = 0;
-  // schedule of one preconditioner application
-  std::vector<Op> ops;
+  // per-level tile orders (this part's tiles at partitioned levels)
   int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
   int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes
-  cudaGraphExec_t graph = nullptr;
-  cudaStream_t graph_stream = nullptr;
-  int64_t launches = 0;
   // profiling
   bool profiling = false;
   struct Ev { int cls; double bytes; cudaEvent_t a, b; };
@@ -222,8 +233,33 @@ struct Hier {
   double prof_ms[KC_COUNT] = {};
   int64_t prof_cnt[KC_COUNT] = {};
   double prof_bytes[KC_COUNT] = {};
+  // partition (multi-part): this part's rank, owned ranges
+  int rank = 0, nranks = 1;
+  int lg = 0;                          // partition level (levels < lg replicated)
+  int own_lb[MAXL + 1] = {}, own_lc[MAXL + 1] = {};  // owned leaf tiles per level
+  int own_ib[MAXL + 1] = {}, own_ic[MAXL + 1] = {};  // owned inner tiles per level
+  Ranges own_cells;                    // owned leaf cells (float4 units)
+  int* apply_tiles = nullptr;          // owned leaf tiles
+  int n_apply_tiles = 0;
+  double n_active_local = 0;
   std::vector<void*> allocs;
   ~Hier();
+};
+
+struct PartPlanHolder;
+struct Comm;
+
+// A solver instance: one part (single GPU, or one rank of an NCCL job) or several parts
+// in one process (loopback partition on one GPU, for testing the distributed path).
+struct Group {
+  std::vector<Hier*> parts;
+  Comm* comm = nullptr;
+  PartPlanHolder* plan = nullptr;
+  std::vector<Op> ops;                 // identical for every part
+  cudaGraphExec_t graph = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int64_t launches = 0;
+  ~Group();
 };
 
 }  // namespace octmg
@@ -232,5 +268,5 @@ struct octmg_tree {
   octmg::Tree t;
 };
 struct octmg_hier {
-  octmg::Hier h;
+  octmg::Group g;
 };

@@ -198,7 +198,14 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
     T->wall[f] = desc->wall_bc[f];
   }
   if (desc->grade_repair != 0) { set_error("grade_repair is not supported; pass a graded tree"); return OCTMG_E_INVALID; }
-  if (desc->nranks > 1 || desc->nccl_comm) { set_error("multi-GPU trees are not supported in this release"); return OCTMG_E_INVALID; }
+  if (desc->nranks < 1 || desc->nranks > 64 || desc->rank < 0 || desc->rank >= desc->nranks ||
+      (desc->nranks > 1 && !desc->nccl_comm)) {
+    set_error("bad rank / nranks / nccl_comm");
+    return OCTMG_E_INVALID;
+  }
+  T->rank = desc->rank;
+  T->nranks = desc->nranks;
+  T->nccl_comm = desc->nccl_comm;
   std::vector<void*> tmp;  // freed at exit
   struct Guard { std::vector<void*>& v; ~Guard() { for (void* p : v) cudaFree(p); } } guard{tmp};
   Ext ext{{T->ext[0], T->ext[1], T->ext[2]}};

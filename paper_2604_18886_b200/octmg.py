@@ -58,6 +58,8 @@ EXPORT_TILES, EXPORT_NBR, EXPORT_PARENT, EXPORT_CHILD = 0, 1, 2, 3
 ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_tree_info_get",
                "octmg_tree_export", "octmg_setup_hierarchy", "octmg_hier_export_coefs", "octmg_apply",
                "octmg_vcycle", "octmg_pcg_solve", "octmg_profile_enable", "octmg_profile_read",
+               "octmg_setup_hierarchy_loopback", "octmg_partition_info", "octmg_nccl_unique_id",
+               "octmg_nccl_comm_init", "octmg_nccl_comm_destroy",
                "octmg_hier_destroy", "octmg_tree_destroy"]
 
 _lib = None
@@ -83,9 +85,15 @@ def lib():
         L.octmg_pcg_solve.argtypes = [P, P, P, C.POINTER(SolveParams), C.POINTER(SolveReport), P]
         L.octmg_profile_enable.argtypes = [P, I32]
         L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
+        L.octmg_setup_hierarchy_loopback.argtypes = [P, I32, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
+        L.octmg_partition_info.argtypes = [P, I32, P, P, P, P, P]
+        L.octmg_nccl_unique_id.argtypes = [P]
+        L.octmg_nccl_comm_init.argtypes = [I32, I32, P, C.POINTER(P)]
+        L.octmg_nccl_comm_destroy.argtypes = [P]
+        L.octmg_nccl_comm_destroy.restype = None
         L.octmg_hier_destroy.argtypes = [P]
         L.octmg_tree_destroy.argtypes = [P]
-        for name in ABI_SYMBOLS[2:12]:
+        for name in ABI_SYMBOLS[2:16]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -113,17 +121,48 @@ def version() -> str:
     return lib().octmg_version().decode()
 
 
+class NcclComm:
+    """NCCL communicator for an nranks-GPU job, bootstrapped through torch.distributed
+    (rank 0's unique id is broadcast over the default process group)."""
+
+    def __init__(self, rank: int, nranks: int):
+        import torch.distributed as dist
+        buf = (C.c_char * 128)()
+        if rank == 0:
+            _check(lib().octmg_nccl_unique_id(C.cast(buf, C.c_void_p)))
+        obj = [bytes(buf)] if rank == 0 else [None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _check(lib().octmg_nccl_comm_init(rank, nranks, C.cast(uid, C.c_void_p), C.byref(h)))
+        self.handle = h
+        self.rank, self.nranks = rank, nranks
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().octmg_nccl_comm_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 class Tree:
     """octmg_build_tree: graded leaf tiles (host int array (n,4): level,i,j,k)."""
 
-    def __init__(self, tiles, ext=(1, 1, 1), wall_bc=(1, 1, 1, 1, 1, 1), stream=None):
+    def __init__(self, tiles, ext=(1, 1, 1), wall_bc=(1, 1, 1, 1, 1, 1), stream=None, comm: "NcclComm" = None):
         t = np.ascontiguousarray(np.asarray(tiles, dtype=np.int32).reshape(-1, 4))
         d = TreeDesc()
         for a in range(3):
             d.ext[a] = int(ext[a])
         for f in range(6):
             d.wall_bc[f] = int(wall_bc[f])
-        d.grade_repair, d.rank, d.nranks, d.nccl_comm = 0, 0, 1, None
+        d.grade_repair = 0
+        if comm is None:
+            d.rank, d.nranks, d.nccl_comm = 0, 1, None
+        else:
+            d.rank, d.nranks, d.nccl_comm = comm.rank, comm.nranks, comm.handle
+        self.comm = comm
         h = C.c_void_p()
         _check(lib().octmg_build_tree(C.byref(d), t.ctypes.data_as(C.c_void_p), len(t), _stream(stream),
                                       C.byref(h)))
@@ -166,14 +205,29 @@ class Hierarchy:
     """octmg_setup_hierarchy + the solver calls.  Device tensors (torch, cuda) in and out."""
 
     def __init__(self, tree: Tree, kind, face_beta=None, face_frac=None, alpha=2.0, beta=2.0, mu=1,
-                 nu_pre=2, nu_post=2, nu_coarsest=10, stream=None):
+                 nu_pre=2, nu_post=2, nu_coarsest=10, stream=None, loopback_parts: int = 0):
         self.tree = tree
         p = MGParams(alpha, beta, mu, nu_pre, nu_post, nu_coarsest)
         h = C.c_void_p()
-        _check(lib().octmg_setup_hierarchy(tree._h, _ptr(kind), _ptr(face_beta), _ptr(face_frac), C.byref(p),
-                                           _stream(stream), C.byref(h)))
+        if loopback_parts:
+            _check(lib().octmg_setup_hierarchy_loopback(tree._h, loopback_parts, _ptr(kind), _ptr(face_beta),
+                                                        _ptr(face_frac), C.byref(p), _stream(stream), C.byref(h)))
+        else:
+            _check(lib().octmg_setup_hierarchy(tree._h, _ptr(kind), _ptr(face_beta), _ptr(face_frac), C.byref(p),
+                                               _stream(stream), C.byref(h)))
         self._h = h
         self.N = tree.N
+        self.parts = max(1, loopback_parts)
+
+    def partition(self, part: int = 0):
+        """(lg, rank, nranks, owned leaf tiles per level as (begin, count) arrays)"""
+        lg, rk, nr = C.c_int32(), C.c_int32(), C.c_int32()
+        b = (C.c_int32 * MAX_LEVELS)()
+        c = (C.c_int32 * MAX_LEVELS)()
+        _check(lib().octmg_partition_info(self._h, part, C.byref(lg), C.byref(rk), C.byref(nr),
+                                          C.cast(b, C.c_void_p), C.cast(c, C.c_void_p)))
+        L = self.tree.levels
+        return lg.value, rk.value, nr.value, np.array(b[:L]), np.array(c[:L])
 
     def apply(self, x, y, stream=None):
         _check(lib().octmg_apply(self._h, _ptr(x), _ptr(y), _stream(stream)))

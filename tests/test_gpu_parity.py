@@ -263,3 +263,44 @@ def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     x = torch.zeros_like(b)
     rep = h.pcg_solve(b, x, rtol=1e-6)
     assert abs(rep["iters"] - o.pcg(cfg["b"].astype(np.float64), rtol=1e-6, mu=cfg["mu"])["iters"]) <= 1
+
+
+# ---------------------------------------------------------------------------------------
+# partitioned solve through the loopback transport: P parts of a Morton-range
+# partition in one process; halo exchanges / parent broadcasts / scalar sums are device
+# copies.  Same kernels and schedule as an NCCL job.
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("parts", [2, 3, 4])
+@pytest.mark.parametrize("name", ["uniform64", "sphere_small", "tank_small", "sphere_small_dir"])
+def test_loopback_partition_matches_single(om, name, parts):
+    cfg = make_config(name)
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    kind = torch.from_numpy(cfg["kind"]).to(DEV)
+    frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(DEV)
+    h1 = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
+    hp = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"], loopback_parts=parts)
+    # ownership: every leaf tile owned by exactly one part
+    owned = np.zeros(tree.NL, dtype=np.int64)
+    for p in range(parts):
+        lg, rk, nr, b, c = hp.partition(p)
+        assert (rk, nr) == (p, parts)
+        for l in range(tree.levels):
+            owned[b[l]:b[l] + c[l]] += 1
+    assert np.all(owned == 1)
+    rng = np.random.default_rng(5)
+    r = torch.from_numpy(rng.standard_normal(tree.N).astype(np.float32)).to(DEV)
+    u1, up = torch.zeros_like(r), torch.zeros_like(r)
+    h1.vcycle(r, u1)
+    hp.vcycle(r, up)
+    assert torch.equal(u1, up)  # same per-cell arithmetic: bit-identical
+    y1, yp = torch.zeros_like(r), torch.zeros_like(r)
+    h1.apply(r, y1)
+    hp.apply(r, yp)
+    assert torch.equal(y1, yp)
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    x1, xp = torch.zeros_like(b), torch.zeros_like(b)
+    r1 = h1.pcg_solve(b, x1, rtol=1e-6)
+    rp = hp.pcg_solve(b, xp, rtol=1e-6)
+    assert rp["converged"] and abs(r1["iters"] - rp["iters"]) <= 1
+    a1, ap = x1.cpu().numpy().astype(np.float64), xp.cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(a1 - ap) <= 1e-5 * np.linalg.norm(a1)
