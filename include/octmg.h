@@ -159,6 +159,18 @@ octmg_status octmg_nccl_unique_id(void* out128);
 octmg_status octmg_nccl_comm_init(int32_t rank, int32_t nranks, const void* id128, void** comm);
 void octmg_nccl_comm_destroy(void* comm);
 
+/* Host-only partition planner (no device needed): from the canonical tree tables (as
+ * exported by octmg_tree_export; level_counts = 4 int32 per level l = 0..L: leaf_begin,
+ * leaf_count, inner_begin, inner_count), the partition level lg, the owner rank of every
+ * tile (-1 = replicated, level < lg) and the halo item lists: n_items_out[(l*nranks +
+ * from)*nranks + to] items of (tile, kind) pairs concatenated in that order into items_out
+ * (kind 0..5 = face layer of that face, 6 = whole tile).  items_cap = max item count. */
+octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr, const int32_t* parent,
+                                       const int32_t* child, int32_t NL, int32_t NI, int32_t L,
+                                       const int32_t* level_counts, int32_t nranks, int32_t* lg_out,
+                                       int32_t* owner_out, int32_t* n_items_out, int32_t* items_out,
+                                       int64_t items_cap);
+
 /* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
  * in tile order.  Synchronises `stream` of the last call. */
 octmg_status octmg_hier_export_coefs(const octmg_hier* h, float* host_dst, size_t bytes);

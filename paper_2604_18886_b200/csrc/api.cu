@@ -448,6 +448,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   return OCTMG_OK;
 }
 
+}  // namespace
 uint64_t morton3h(uint32_t i, uint32_t j, uint32_t k) {
   uint64_t m = 0;
   for (int b = 0; b < 21; ++b)
@@ -455,6 +456,7 @@ uint64_t morton3h(uint32_t i, uint32_t j, uint32_t k) {
          ((uint64_t)((k >> b) & 1) << (3 * b + 2));
   return m;
 }
+namespace {
 
 octmg_status plan_input(const Tree& T, PartInput& in) {
   in.L = T.L; in.NL = T.NL; in.NI = T.NI;
@@ -621,6 +623,49 @@ octmg_status octmg_nccl_comm_init(int32_t rank, int32_t nranks, const void* id12
 }
 
 void octmg_nccl_comm_destroy(void* comm) { nccl_comm_destroy(comm); }
+
+octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr, const int32_t* parent,
+                                       const int32_t* child, int32_t NL, int32_t NI, int32_t L,
+                                       const int32_t* level_counts, int32_t nranks, int32_t* lg_out,
+                                       int32_t* owner_out, int32_t* n_items_out, int32_t* items_out,
+                                       int64_t items_cap) {
+  if (!tiles4 || !nbr || !parent || !level_counts || !lg_out || !owner_out || !n_items_out || nranks < 1 ||
+      L < 0 || L > MAXL) {
+    set_error("bad argument");
+    return OCTMG_E_INVALID;
+  }
+  static thread_local int lb[MAXL + 1], lc[MAXL + 1], ib[MAXL + 1], ic[MAXL + 1];
+  int accl = 0, acci = NL;
+  for (int l = L; l >= 0; --l) {
+    lb[l] = accl; lc[l] = level_counts[4 * l + 1]; accl += lc[l];
+    ib[l] = acci; ic[l] = level_counts[4 * l + 3]; acci += ic[l];
+  }
+  PartInput in;
+  in.L = L; in.NL = NL; in.NI = NI;
+  in.lb = lb; in.lc = lc; in.ib = ib; in.ic = ic;
+  const int T = NL + NI;
+  in.tiles4.assign(tiles4, tiles4 + (size_t)T * 4);
+  in.nbr.assign(nbr, nbr + (size_t)T * 6);
+  in.parent.assign(parent, parent + T);
+  if (NI) in.child.assign(child, child + (size_t)NI * 8);
+  in.morton.resize(T);
+  for (int t = 0; t < T; ++t) in.morton[t] = morton3h(in.tiles4[4 * t + 1], in.tiles4[4 * t + 2], in.tiles4[4 * t + 3]);
+  PartPlan P;
+  const int lg = choose_partition_level(in, nranks);
+  build_partition(in, nranks, lg, P);
+  *lg_out = lg;
+  std::memcpy(owner_out, P.owner.data(), sizeof(int32_t) * T);
+  int64_t k = 0;
+  for (size_t q = 0; q < P.items.size(); ++q) {
+    n_items_out[q] = (int32_t)P.items[q].size();
+    for (const HaloItem& it : P.items[q]) {
+      if (items_out && k + 2 <= 2 * items_cap) { items_out[k] = it.tile; items_out[k + 1] = it.kind; }
+      k += 2;
+    }
+  }
+  if (k > 2 * items_cap) { set_error("items buffer too small"); return OCTMG_E_INVALID; }
+  return OCTMG_OK;
+}
 
 octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size_t bytes) {
   if (!hh || !host_dst) { set_error("null argument"); return OCTMG_E_INVALID; }

@@ -59,7 +59,7 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_tree_export", "octmg_setup_hierarchy", "octmg_hier_export_coefs", "octmg_apply",
                "octmg_vcycle", "octmg_pcg_solve", "octmg_profile_enable", "octmg_profile_read",
                "octmg_setup_hierarchy_loopback", "octmg_partition_info", "octmg_nccl_unique_id",
-               "octmg_nccl_comm_init", "octmg_nccl_comm_destroy",
+               "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
                "octmg_hier_destroy", "octmg_tree_destroy"]
 
 _lib = None
@@ -93,7 +93,8 @@ def lib():
         L.octmg_nccl_comm_destroy.restype = None
         L.octmg_hier_destroy.argtypes = [P]
         L.octmg_tree_destroy.argtypes = [P]
-        for name in ABI_SYMBOLS[2:16]:
+        L.octmg_partition_plan_host.argtypes = [P, P, P, P, I32, I32, I32, P, I32, P, P, P, P, I64]
+        for name in ABI_SYMBOLS[2:16] + ["octmg_partition_plan_host"]:
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -276,6 +277,35 @@ class Hierarchy:
                 self._h = None
         except Exception:
             pass
+
+
+def partition_plan_host(tables, L, NL, NI, level_counts, nranks):
+    """octmg_partition_plan_host on host tables (no GPU): (lg, owner[T], items) where items is
+    a dict (level, from, to) -> int32 array (n, 2) of (tile, kind)."""
+    T = NL + NI
+    t4 = np.ascontiguousarray(tables["tiles"], dtype=np.int32)
+    nb = np.ascontiguousarray(tables["nbr"], dtype=np.int32)
+    par = np.ascontiguousarray(tables["parent"], dtype=np.int32)
+    ch = np.ascontiguousarray(tables["child"], dtype=np.int32).reshape(-1)
+    if ch.size == 0:
+        ch = np.zeros(8, dtype=np.int32)
+    lcnt = np.ascontiguousarray(level_counts, dtype=np.int32)
+    lg = C.c_int32()
+    owner = np.zeros(T, dtype=np.int32)
+    nitems = np.zeros((L + 1) * nranks * nranks, dtype=np.int32)
+    cap = 64 * T + 1024
+    items = np.zeros(2 * cap, dtype=np.int32)
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    _check(lib().octmg_partition_plan_host(vp(t4), vp(nb), vp(par), vp(ch), NL, NI, L, vp(lcnt), nranks,
+                                           C.byref(lg), vp(owner), vp(nitems), vp(items), cap))
+    out, k = {}, 0
+    for l in range(L + 1):
+        for a in range(nranks):
+            for b in range(nranks):
+                n = int(nitems[(l * nranks + a) * nranks + b])
+                out[(l, a, b)] = items[2 * k:2 * (k + n)].reshape(n, 2).copy()
+                k += n
+    return lg.value, owner, out
 
 
 # C-ABI names as module-level functions (same names as include/octmg.h)
