@@ -10,8 +10,11 @@ Table 1 (reading #14).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
 
-N > 1 (torchrun): every rank solves its own instance (replicas),
-value = total cells / max-over-ranks time, "scaling": "weak".
+N > 1 (torchrun): the same workload is partitioned across the ranks by contiguous Morton
+ranges: NCCL halo exchange after every kernel that
+changes a partitioned level, fp64 allreduce for every PCG scalar.  value = total cells /
+max-over-ranks time, "scaling": "strong".  --replicas instead solves one independent
+instance per rank ("scaling": "weak", no data-path collective).
 """
 from __future__ import annotations
 
@@ -51,6 +54,7 @@ def parse():
     ap.add_argument("--rtol", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent instance per rank")
     return ap.parse_args()
 
 
@@ -189,7 +193,9 @@ def main():
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
 
     cfg = make_config(args.config)
-    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    partitioned = world > 1 and not args.replicas
+    comm = om.NcclComm(rank, world) if partitioned else None
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"], comm=comm)
     kind = torch.from_numpy(cfg["kind"]).to(dev)
     frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(dev)
     h = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
@@ -231,7 +237,8 @@ def main():
     barrier()
     clocks = sampler.stop()
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    value = world * N / (ms * 1e-3)
+    units = N if partitioned else world * N  # cells solved by the whole job per step
+    value = units / (ms * 1e-3)
 
     # ---- end to end through the public API with host buffers --------------------------
     for _ in range(max(1, args.warmup)):
@@ -272,11 +279,13 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS.get(args.config, args.config), "name": args.config,
                        "leaf_cells": N, "levels": tree.levels, "mu": cfg["mu"], "rtol": args.rtol,
-                       "pcg_iters": iters[-1], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "pcg_iters": iters[-1], "parallelism": (f"Morton-range partition x{world} (NCCL halo + allreduce)" if partitioned
+                                       else f"replicas x{world}" if world > 1 else "1 GPU"),
                        "l2": "working set > 126 MB L2 (coefficient store alone %.0f MB); no flush"
                              % (tree.T * 512 * 16 / 1e6)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -287,8 +296,8 @@ def main():
             "kernels": {k: {"ms_per_solve": v["ms"] / 2, "launches_per_solve": v["launches"] // 2,
                             "gbs": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] else None}
                         for k, v in prof.items() if v["launches"]},
-            "e2e": {"value": world * N / (ms_e2e * 1e-3), "unit": "cells/s", "h2d_bytes_per_step": 4 * N,
-                    "d2h_bytes_per_step": 4 * N, "ms_per_step": ms_e2e},
+            "e2e": {"value": units / (ms_e2e * 1e-3), "unit": "cells/s", "h2d_bytes_per_step": 4 * N * world,
+                    "d2h_bytes_per_step": 4 * N * world, "ms_per_step": ms_e2e},
             "gpu_launches": launches,
             "clocks": clocks,
             "paper_context": "RTX 4090: uniform (5-5) 256^3 = 2.41e8 cells/s (Table 1, P:L1797, M = 2^20)",
@@ -297,6 +306,8 @@ def main():
             line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
         print(json.dumps(line), flush=True)
     if world > 1:
+        del h, tree
+        comm = None
         torch.distributed.destroy_process_group()
     return 0
 

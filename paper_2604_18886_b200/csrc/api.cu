@@ -163,6 +163,10 @@ void read_env(Hier& h) {
   if (h.nranks > 1) h.rb_fused = 0;  // the partitioned schedule exchanges after every pass
   const char* pc = getenv("OCTMG_PASS_CPT");
   h.pass_cpt = pc ? std::max(1, std::min(2, atoi(pc))) : 2;
+  const char* pv = getenv("OCTMG_PASS_V");
+  h.pass_v2 = !(pv && std::string(pv) == "1");
+  const char* rv = getenv("OCTMG_RESTRICT_V");
+  h.restrict_v2 = rv && std::string(rv) == "2";
   const Tree& T = *h.tree;
   const char* sc = getenv("OCTMG_SUBCYCLE");
   h.sub_K = -1;
@@ -286,9 +290,9 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
   ProfScope ps(h, cls, s, bytes);
   if (mode == SM_RESTRICT) {
-    launch_restrict_direct(a, s);
+    launch_restrict_direct(a, s, h.restrict_v2);
   } else {
-    launch_pass_direct(a, s, a.n >= 1024 ? h.pass_cpt : 1);
+    launch_pass_direct(a, s, (a.n >= 1024 ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0));
   }
 }
 
@@ -572,6 +576,7 @@ ApplyArgs apply_args(const Hier& h) {
   a.tile = T.tile; a.nbr = T.nbr; a.child = T.child; a.coef = h.coef; a.glayer_val = h.glayer_val;
   a.glayer = T.glayer; a.z = nullptr; a.pold = nullptr; a.pnew = nullptr; a.q = nullptr;
   a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL; a.use_beta = 0;
+  a.v2 = h.pass_v2 ? 1 : 0;
   return a;
 }
 

@@ -57,6 +57,91 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_direct(SmoothArgs a)
     if (act[k] || MODE == SM_ZERO1 || MODE == SM_ZERO2) ut[offs[k]] = unew[k];
 }
 
+// Face sum of a cell of a tile with no ghost face, the tile's neighbour entries prefetched
+// in registers (nb).  Every load is issued unconditionally (walls read the tile itself and
+// are zeroed), so all loads of a cell are in flight at once and none waits on the cell's
+// activity test.
+__device__ __forceinline__ float face_sum_regular(const SmoothArgs& a, int t, const int (&nb)[6], int x, int y,
+                                                  int z, const float4& q) {
+  const float* ut = tptr(a.u, t, a.NL);
+  const float4* ct = a.coef + (size_t)t * TB3;
+  const int c[3] = {x, y, z};
+  float s = 0.0f;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
+    int nc[3] = {c[0], c[1], c[2]};
+    nc[ax] += sg;
+    const bool inside = nc[ax] >= 0 && nc[ax] < 8;
+    const int n = nb[f];
+    const bool wall = !inside && n < 0;
+    nc[ax] &= 7;
+    const int no = loff(nc[0], nc[1], nc[2]);
+    const float* up = inside || wall ? ut : tptr(a.u, n, a.NL);
+    float v = __ldg(up + no);
+    float cf;
+    if (f & 1) {
+      const float4* cp = inside || wall ? ct : a.coef + (size_t)n * TB3;
+      cf = comp(__ldg(cp + no), ax);
+    } else {
+      cf = comp(q, ax);
+    }
+    if (wall) v = 0.0f;
+    s = fmaf(cf, v, s);
+  }
+  return s;
+}
+
+// The colour pass with the neighbour entries prefetched and, on tiles without a ghost face
+// (every tile of a uniform level), the branch-free face sum above.
+template <int MODE, int CPT>
+__global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  int nb[6];
+  {
+    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
+    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
+    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
+  }
+  const int colour = a.stage[0] & 1;
+  const int j = threadIdx.x;
+  const int y = (j >> 2) & 7, z0 = j >> 5;
+  float* ut = tptr(a.u, t, a.NL);
+  const float* bt = tptr(a.b, t, a.NL);
+  bool ghost = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
+  ghost = ghost && MODE != SM_ZERO1;
+  float unew[CPT];
+  bool act[CPT];
+  int offs[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int z = z0 + k * (8 / CPT);
+    const int x = 2 * (j & 3) + ((colour + y + z) & 1);
+    const int off = loff(x, y, z);
+    offs[k] = off;
+    const float4 q = __ldg(a.coef + (size_t)t * TB3 + off);
+    const float b = __ldg(bt + off);
+    act[k] = q.x != 0.0f;
+    float v;
+    if (MODE == SM_ZERO1) {
+      v = b / q.x;
+    } else if (!ghost) {
+      v = (b - face_sum_regular(a, t, nb, x, y, z, q)) / q.x;
+    } else {
+      const float ui = MODE == SM_ZERO2 ? 0.0f : __ldg(ut + off);
+      const float mP = block_mean<MODE == SM_ZERO2>(a, t, x, y, z, colour);
+      v = act[k] ? (b - face_sum<MODE == SM_ZERO2>(a, t, x, y, z, q, ui, mP, colour, 0.0f)) / q.x : 0.0f;
+    }
+    unew[k] = act[k] ? v : 0.0f;
+  }
+  __syncthreads();  // every pass-start read of this tile precedes the in-place writes
+#pragma unroll
+  for (int k = 0; k < CPT; ++k)
+    if (act[k] || MODE == SM_ZERO1 || MODE == SM_ZERO2) ut[offs[k]] = unew[k];
+}
+
 // Residual r = b - A^l u and, per parent (inner, level l-1): u* = mean of the active
 // children (Avg, Alg. 4 line 9), u^{l-1} := u*, b^{l-1} := beta * (R r), R = P^T / alpha
 // (Alg. 4 lines 8-10; "residual computation and restriction step are fused").
@@ -92,6 +177,63 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
   float r0 = 0.0f, r1 = 0.0f;
   if (q0.x != 0.0f) r0 = bb.x - face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, q0.x * uu.x, su_t, scm);
   if (q1.x != 0.0f) r1 = bb.y - face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, q1.x * uu.y, su_t, scm);
+  float rs = r0 + r1;
+  rs += __shfl_xor_sync(0xffffffffu, rs, 4);
+  rs += __shfl_xor_sync(0xffffffffu, rs, 8);
+  if (((j >> 2) & 3) == 0) {
+    const int4 tv = __ldg(a.tile + t);
+    const int P = __ldg(a.parent + t);
+    const int pc = pcell_of(tv, x0, y, z);
+    const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
+    a.u.inner[pi] = mP;
+    a.ustar_w[pi] = mP;
+    a.b.inner[pi] = a.beta * (rs / a.alpha);
+  }
+}
+
+// Residual + restriction + Avg with the neighbour entries prefetched and, on tiles without a
+// ghost face, the branch-free face sum (every load in flight at once, in-tile neighbours
+// from L1).  Same thread layout and outputs as k_restrict_direct.
+__global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  int nb[6];
+  {
+    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
+    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
+    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
+  }
+  const int j = threadIdx.x;
+  const int x2 = j & 3;
+  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
+  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
+  const int x0 = 2 * x2;
+  const size_t base = (size_t)t * TB3;
+  const int off0 = loff(x0, y, z);
+  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float2 uu = __ldg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
+  const float2 bb = __ldg(reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0));
+  bool ghost = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
+  float f0, f1;
+  if (!ghost) {
+    f0 = face_sum_regular(a, t, nb, x0, y, z, q0);
+    f1 = face_sum_regular(a, t, nb, x0 + 1, y, z, q1);
+  }
+  // active u sum / count of the block (also the ghost m_P of its cells)
+  float su = (q0.x != 0.0f ? uu.x : 0.0f) + (q1.x != 0.0f ? uu.y : 0.0f);
+  int na = (q0.x != 0.0f) + (q1.x != 0.0f);
+  su += __shfl_xor_sync(0xffffffffu, su, 4);
+  na += __shfl_xor_sync(0xffffffffu, na, 4);
+  su += __shfl_xor_sync(0xffffffffu, su, 8);
+  na += __shfl_xor_sync(0xffffffffu, na, 8);
+  const float mP = na ? su / (float)na : 0.0f;
+  if (ghost) {
+    f0 = q0.x != 0.0f ? face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, 0.0f) : 0.0f;
+    f1 = q1.x != 0.0f ? face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, 0.0f) : 0.0f;
+  }
+  const float r0 = q0.x != 0.0f ? bb.x - fmaf(q0.x, uu.x, f0) : 0.0f;
+  const float r1 = q1.x != 0.0f ? bb.y - fmaf(q1.x, uu.y, f1) : 0.0f;
   float rs = r0 + r1;
   rs += __shfl_xor_sync(0xffffffffu, rs, 4);
   rs += __shfl_xor_sync(0xffffffffu, rs, 8);
@@ -156,8 +298,16 @@ void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s) {
 }
 
 template <int CPT>
-static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s) {
+static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool v2) {
   const int grid = a.n;
+  if (v2) {
+    switch (mode) {
+      case SM_ZERO1: k_pass_v2<SM_ZERO1, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+      case SM_ZERO2: k_pass_v2<SM_ZERO2, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+      default: k_pass_v2<SM_PLAIN, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+    }
+    return;
+  }
   switch (mode) {
     case SM_ZERO1: k_pass_direct<SM_ZERO1, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
     case SM_ZERO2: k_pass_direct<SM_ZERO2, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
@@ -168,12 +318,15 @@ static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s) {
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt) {
   if (a.n == 0) return;
   const int mode = a.stage[0] >> 1;
-  if (cpt == 2) launch_pass_cpt<2>(a, mode, s);
-  else launch_pass_cpt<1>(a, mode, s);
+  const bool v2 = cpt & 16;
+  if ((cpt & 15) == 2) launch_pass_cpt<2>(a, mode, s, v2);
+  else launch_pass_cpt<1>(a, mode, s, v2);
 }
 
-void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s) {
-  if (a.n) k_restrict_direct<<<a.n, NT, 0, s>>>(a);
+void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, bool v2) {
+  if (!a.n) return;
+  if (v2) k_restrict_v2<<<a.n, NT, 0, s>>>(a);
+  else k_restrict_direct<<<a.n, NT, 0, s>>>(a);
 }
 
 void launch_prolong(const SmoothArgs& a, cudaStream_t s) {

@@ -117,9 +117,7 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
 // (Alg. 1 lines 9-10; fp64 dots P:L1233).  Thread layout as the restriction: the
 // four lanes of a 2x2x2 block are xor 4 / xor 8 apart (ghost m_P by shuffles).
 template <bool DOT>
-__global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
-  __shared__ double sred[NT / 32];
-  const int t = a.tiles[blockIdx.x];
+__device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double* sred) {
   const int j = threadIdx.x;
   const int x2 = j & 3;
   const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
@@ -166,6 +164,86 @@ __global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
     double bs = block_reduce_d(d, sred);
     if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
   }
+}
+
+// q = A p as k_apply, on tiles whose six neighbours are all same-level leaves or walls (every
+// tile of a uniform tree): no shared-memory staging and no branches on the stencil path —
+// the neighbour entries are prefetched, every p of the stencil is formed from z and p_old
+// loads issued at once (in-tile neighbours hit L1), walls read the tile itself and are
+// zeroed.  Other tiles take the general composite path of k_apply.
+__device__ __forceinline__ float composite_regular(const ApplyArgs& a, float beta, int t, const int (&nb)[6], int x,
+                                                   int y, int z, const float4& q) {
+  const int c[3] = {x, y, z};
+  float s = 0.0f;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
+    int nc[3] = {c[0], c[1], c[2]};
+    nc[ax] += sg;
+    const bool inside = nc[ax] >= 0 && nc[ax] < 8;
+    const int n = nb[f];
+    const bool wall = !inside && n < 0;
+    nc[ax] &= 7;
+    const size_t ci = (size_t)(inside || wall ? t : n) * TB3 + loff(nc[0], nc[1], nc[2]);
+    float v = __ldg(a.z + ci);
+    if (a.pold) v = fmaf(beta, __ldg(a.pold + ci), v);
+    const float cf = (f & 1) ? comp(__ldg(a.coef + ci), ax) : comp(q, ax);
+    if (wall) v = 0.0f;
+    s = fmaf(cf, v, s);
+  }
+  return s;
+}
+
+template <bool DOT>
+__global__ __launch_bounds__(NT, 5) void k_apply_v2(ApplyArgs a) {
+  __shared__ double sred[NT / 32];
+  const int t = a.tiles[blockIdx.x];
+  int nb[6];
+  {
+    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
+    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
+    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
+  }
+  bool regular = true;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) regular &= nb[f] >= -1 && nb[f] < a.NL;
+  if (!regular) {
+    apply_general<DOT>(a, t, sred);
+    return;
+  }
+  const int j = threadIdx.x;
+  const int x2 = j & 3;
+  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
+  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
+  const int x0 = 2 * x2;
+  const float beta = (a.use_beta && a.pold) ? (float)(a.sc->sum_rz / a.sc->rho) : 0.0f;
+  const size_t base = (size_t)t * TB3;
+  const int off0 = loff(x0, y, z);
+  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  float2 pp = __ldg(reinterpret_cast<const float2*>(a.z + base + off0));
+  if (a.pold) {
+    const float2 po = __ldg(reinterpret_cast<const float2*>(a.pold + base + off0));
+    pp.x = fmaf(beta, po.x, pp.x);
+    pp.y = fmaf(beta, po.y, pp.y);
+  }
+  const float f0 = composite_regular(a, beta, t, nb, x0, y, z, q0);
+  const float f1 = composite_regular(a, beta, t, nb, x0 + 1, y, z, q1);
+  const float p0 = q0.x != 0.0f ? pp.x : 0.0f, p1 = q1.x != 0.0f ? pp.y : 0.0f;
+  const float r0 = q0.x != 0.0f ? fmaf(q0.x, p0, f0) : 0.0f;
+  const float r1 = q1.x != 0.0f ? fmaf(q1.x, p1, f1) : 0.0f;
+  if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0, p1);
+  *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
+  if (DOT) {
+    double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
+    double bs = block_reduce_d(d, sred);
+    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
+  }
+}
+
+template <bool DOT>
+__global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
+  __shared__ double sred[NT / 32];
+  apply_general<DOT>(a, a.tiles[blockIdx.x], sred);
 }
 
 // sigma = p.q from the per-tile partials (fixed order => deterministic)
@@ -333,10 +411,12 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
     return;
   }
   if (a.partial) {
-    k_apply<true><<<a.ntiles, NT, 0, s>>>(a);
+    if (a.v2) k_apply_v2<true><<<a.ntiles, NT, 0, s>>>(a);
+    else k_apply<true><<<a.ntiles, NT, 0, s>>>(a);
     k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.ntiles, a.sc);
   } else {
-    k_apply<false><<<a.ntiles, NT, 0, s>>>(a);
+    if (a.v2) k_apply_v2<false><<<a.ntiles, NT, 0, s>>>(a);
+    else k_apply<false><<<a.ntiles, NT, 0, s>>>(a);
   }
 }
 

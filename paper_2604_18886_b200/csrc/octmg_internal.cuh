@@ -121,6 +121,7 @@ struct ApplyArgs {
   Scalars* sc;          // beta = sum_rz / rho read from here; sum_pq written by the finish kernel
   int NL;
   int use_beta;
+  int v2;               // k_apply_v2 (regular tiles branch-free; OCTMG_PASS_V=1 selects k_apply)
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
@@ -160,7 +161,7 @@ struct SmoothArgs {
 };
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
-void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s);
+void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, bool v2);
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
 void launch_rb_fused(const SmoothArgs& a, bool zero, cudaStream_t s, bool shell = true);
 void launch_copy_level(const SmoothArgs& a, cudaStream_t s);
@@ -222,6 +223,8 @@ struct Hier {
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
   int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
+  bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
+  bool restrict_v2 = false;      // k_restrict_v2 (OCTMG_RESTRICT_V=2; measured slower than the staged one)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes
   // profiling

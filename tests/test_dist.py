@@ -22,7 +22,7 @@ def _plan(o, nranks):
     counts = np.zeros(4 * (o.L + 1), dtype=np.int32)
     for l in range(o.L + 1):
         counts[4 * l:4 * l + 4] = [o.leaf_begin[l], o.leaf_count[l], o.inner_begin[l], o.inner_count[l]]
-    return om.octmg.partition_plan_host(tb, o.L, o.NL, o.NI, counts, nranks)
+    return om.partition_plan_host(tb, o.L, o.NL, o.NI, counts, nranks)
 
 
 def _cells(kind):
