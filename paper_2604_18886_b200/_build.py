@@ -5,6 +5,7 @@ an in-tree shared object (liboctmg.so) that the ctypes binding loads.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -29,9 +30,24 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if force or _stale():
         nvcc = os.environ.get("NVCC", "nvcc")
         tmp = LIB + ".tmp%d" % os.getpid()
-        cmd = [nvcc] + NVCC_FLAGS + ["-o", tmp] + SOURCES + ["-ldl"]
+        objdir = os.path.join(HERE, "build")
+        os.makedirs(objdir, exist_ok=True)
+        cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+        objs, cmds = [], []
+        for src in SOURCES:
+            obj = os.path.join(objdir, os.path.basename(src) + ".o")
+            objs.append(obj)
+            cmds.append([nvcc] + cflags + ["-c", "-o", obj, src])
         if verbose:
-            print(" ".join(cmd))
-        subprocess.check_call(cmd)
+            for c in cmds:
+                print(" ".join(c))
+        # one nvcc per translation unit, in parallel, then one link
+        with concurrent.futures.ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+            for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+                f.result()
+        link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs + ["-ldl"]
+        if verbose:
+            print(" ".join(link))
+        subprocess.check_call(link)
         os.replace(tmp, LIB)
     return LIB

@@ -24,7 +24,7 @@ octmg_status cuda_status(cudaError_t e, const char* what) {
 const char* kclass_name[KC_COUNT] = {"rbgs_pass", "prolong", "residual_restrict", "coarsest",
                                      "fas_rhs", "coarse_levels", "apply", "pcg_update", "dot_rz", "project",
                                      "init", "setup", "memset", "coarse_subcycle", "rbgs_fused_iteration",
-                                     "copy_level"};
+                                     "copy_level", "coarse_grid"};
 
 template <class T>
 static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
@@ -132,6 +132,10 @@ struct Builder {
   // Alg. 4 at level l; fas_first: first of the mu calls from level l+1 (forms the FAS rhs)
   void fas(int l, bool fas_first) {
     const Tree& T = *h.tree;
+    if (l <= h.grid_K) {  // the rest of the cycle in one cooperative grid launch
+      push(Op{9, l, fas_first ? 1 : 0});
+      return;
+    }
     if (l <= h.sub_K) {  // the rest of the cycle runs on chip in one CTA
       push(Op{4, l, fas_first ? 1 : 0});
       return;
@@ -166,7 +170,7 @@ void read_env(Hier& h) {
   const char* pv = getenv("OCTMG_PASS_V");
   h.pass_v2 = !(pv && std::string(pv) == "1");
   const char* rv = getenv("OCTMG_RESTRICT_V");
-  h.restrict_v2 = rv && std::string(rv) == "2";
+  h.restrict_v2 = !(rv && std::string(rv) == "1");  // k_restrict_v2 (vectorised regular tiles) by default
   const Tree& T = *h.tree;
   const char* sc = getenv("OCTMG_SUBCYCLE");
   h.sub_K = -1;
@@ -176,6 +180,22 @@ void read_env(Hier& h) {
       if (h.nranks > 1 && l >= h.lg) break;  // only replicated levels run on chip
       h.sub_K = l;
     }
+  // cooperative coarse-cycle kernel (opt-in, OCTMG_GRID=1; measured slower than the
+  // per-level launches on config 2): every level below the finest from grid_K down fits it
+  // (OCTMG_GRID_TILES caps the tiles per level)
+  h.grid_K = -1;
+  const char* gv = getenv("OCTMG_GRID");
+  const int nb = (gv && std::string(gv) == "1") ? coarse_grid_blocks() : 0;
+  if (nb > 0) {
+    const char* gt = getenv("OCTMG_GRID_TILES");
+    const int cap = std::min(coarse_grid_max_tiles(nb), gt ? atoi(gt) : 1 << 30);
+    for (int l = 0; l < T.L && l <= coarse_grid_max_level(); ++l) {
+      if (h.lvl_n[l] > cap) break;
+      if (h.nranks > 1 && l >= h.lg) break;  // only replicated levels
+      h.grid_K = l;
+    }
+    if (h.grid_K <= h.sub_K) h.grid_K = -1;  // nothing above the one-CTA sub-cycle
+  }
 }
 
 octmg_status build_schedule(Group& g) {
@@ -259,6 +279,13 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     a.u2 = ubuf(h, op.out_buf);
     ProfScope ps(h, KC_COPY, s, 8.0 * a.n * TB3);
     launch_copy_level(a, s);
+    return;
+  }
+  if (op.kind == 9) {
+    ProfScope ps(h, KC_COARSE_GRID, s, 0.0);
+    cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
+                                       T.ic, h.bar, s);
+    if (e != cudaSuccess) set_error(std::string("k_coarse_grid launch: ") + cudaGetErrorString(e));
     return;
   }
   if (op.kind == 4) {
@@ -414,7 +441,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   h.prm = prm;
   const Tree& T = *tree;
   size_t NLc = (size_t)T.NL * TB3, NIc = (size_t)T.NI * TB3;
-  OCTMG_TRY(halloc(h.allocs, &h.coef, (size_t)T.T * TB3));
+  OCTMG_TRY(halloc(h.allocs, &h.coef, (size_t)T.T * TB3 * 4));
   OCTMG_TRY(halloc(h.allocs, &h.glayer_val, (size_t)T.n_glayers * 64));
   OCTMG_TRY(halloc(h.allocs, &h.act, NLc / 32));
   OCTMG_TRY(halloc(h.allocs, &h.z, NLc));
@@ -430,6 +457,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   h.n_partial = std::max<size_t>((size_t)T.NL, 2 * (size_t)vec_grid()) + 16;
   OCTMG_TRY(halloc(h.allocs, &h.partial, h.n_partial));
   OCTMG_TRY(halloc(h.allocs, &h.counter, 16));
+  OCTMG_TRY(halloc(h.allocs, &h.bar, 1));
   OCTMG_TRY(halloc(h.allocs, &h.sc, 1));
   if (cudaMallocHost(&h.sc_host, sizeof(Scalars)) != cudaSuccess) {
     cudaGetLastError();
@@ -678,7 +706,11 @@ octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size
   size_t need = (size_t)h.tree->T * TB3 * sizeof(float4);
   if (bytes != need) { set_error("export buffer size mismatch"); return OCTMG_E_INVALID; }
   OCTMG_CUDA(cudaDeviceSynchronize());
-  OCTMG_CUDA(cudaMemcpy(host_dst, h.coef, need, cudaMemcpyDeviceToHost));
+  std::vector<float> soa((size_t)h.tree->T * TB3 * 4);
+  OCTMG_CUDA(cudaMemcpy(soa.data(), h.coef, need, cudaMemcpyDeviceToHost));
+  // SoA planes per tile -> the ABI's record order (c, c_x-, c_y-, c_z-) per cell
+  for (size_t i = 0; i < (size_t)h.tree->T * TB3; ++i)
+    for (int k = 0; k < 4; ++k) host_dst[4 * i + k] = soa[cidx(i, k)];
   return OCTMG_OK;
 }
 

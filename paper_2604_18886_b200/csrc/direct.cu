@@ -6,6 +6,7 @@
 // in flight at once.  Ghost values are reconstructed per access (Eq. 12, P:L661-665,
 // P:L880-882) from the pass-start snapshot.
 #include "stencil.cuh"
+#include "rowstencil.cuh"
 
 namespace octmg {
 
@@ -34,7 +35,7 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_direct(SmoothArgs a)
     const int x = 2 * (j & 3) + ((colour + y + z) & 1);
     const int off = loff(x, y, z);
     offs[k] = off;
-    const float4 q = __ldg(a.coef + (size_t)t * TB3 + off);
+    const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
     const float b = __ldg(bt + off);
     act[k] = q.x != 0.0f;
     unew[k] = 0.0f;
@@ -64,7 +65,6 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_direct(SmoothArgs a)
 __device__ __forceinline__ float face_sum_regular(const SmoothArgs& a, int t, const int (&nb)[6], int x, int y,
                                                   int z, const float4& q) {
   const float* ut = tptr(a.u, t, a.NL);
-  const float4* ct = a.coef + (size_t)t * TB3;
   const int c[3] = {x, y, z};
   float s = 0.0f;
 #pragma unroll
@@ -81,8 +81,7 @@ __device__ __forceinline__ float face_sum_regular(const SmoothArgs& a, int t, co
     float v = __ldg(up + no);
     float cf;
     if (f & 1) {
-      const float4* cp = inside || wall ? ct : a.coef + (size_t)n * TB3;
-      cf = comp(__ldg(cp + no), ax);
+      cf = __ldg(a.coef + cidx((size_t)(inside || wall ? t : n) * TB3 + no, 1 + ax));
     } else {
       cf = comp(q, ax);
     }
@@ -121,7 +120,7 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
     const int x = 2 * (j & 3) + ((colour + y + z) & 1);
     const int off = loff(x, y, z);
     offs[k] = off;
-    const float4 q = __ldg(a.coef + (size_t)t * TB3 + off);
+    const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
     const float b = __ldg(bt + off);
     act[k] = q.x != 0.0f;
     float v;
@@ -156,7 +155,7 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
   const int x0 = 2 * x2;
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
-  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
   const float2 uu = *reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0);
   const float2 bb = *reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0);
   __shared__ float su_t[TB3];
@@ -207,9 +206,11 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
   const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
   const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
   const int x0 = 2 * x2;
-  const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
-  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float* cb = a.coef + ((size_t)t << 11);
+  const float2 qc = ldg2(cb + off0), qx = ldg2(cb + 512 + off0), qy = ldg2(cb + 1024 + off0),
+               qz = ldg2(cb + 1536 + off0);
+  const float4 q0 = make_float4(qc.x, qx.x, qy.x, qz.x), q1 = make_float4(qc.y, qx.y, qy.y, qz.y);
   const float2 uu = __ldg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
   const float2 bb = __ldg(reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0));
   bool ghost = false;
@@ -217,8 +218,14 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
   for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
   float f0, f1;
   if (!ghost) {
-    f0 = face_sum_regular(a, t, nb, x0, y, z, q0);
-    f1 = face_sum_regular(a, t, nb, x0 + 1, y, z, q1);
+    const Fld uf = a.u;
+    const int NL = a.NL;
+    auto val2 = [uf, NL](int tt, int o) { return ldg2(tptr(uf, tt, NL) + o); };
+    auto val1 = [uf, NL](int tt, int o) { return __ldg(tptr(uf, tt, NL) + o); };
+    const float2 f = row2_faces(a.coef, t, nb, x2, y, z, uu, make_float2(q0.y, q1.y), make_float2(q0.z, q1.z),
+                                make_float2(q0.w, q1.w), make_float2(q0.x * uu.x, q1.x * uu.y), val2, val1);
+    f0 = f.x;
+    f1 = f.y;
   }
   // active u sum / count of the block (also the ghost m_P of its cells)
   float su = (q0.x != 0.0f ? uu.x : 0.0f) + (q1.x != 0.0f ? uu.y : 0.0f);
@@ -229,11 +236,12 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
   na += __shfl_xor_sync(0xffffffffu, na, 8);
   const float mP = na ? su / (float)na : 0.0f;
   if (ghost) {
-    f0 = q0.x != 0.0f ? face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, 0.0f) : 0.0f;
-    f1 = q1.x != 0.0f ? face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, 0.0f) : 0.0f;
+    f0 = q0.x != 0.0f ? face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, q0.x * uu.x) : 0.0f;
+    f1 = q1.x != 0.0f ? face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, q1.x * uu.y) : 0.0f;
   }
-  const float r0 = q0.x != 0.0f ? bb.x - fmaf(q0.x, uu.x, f0) : 0.0f;
-  const float r1 = q1.x != 0.0f ? bb.y - fmaf(q1.x, uu.y, f1) : 0.0f;
+  // (A u) summed as c*u, then faces x-, x+, y-, y+, z-, z+ (the staged / sub-cycle order)
+  const float r0 = q0.x != 0.0f ? bb.x - f0 : 0.0f;
+  const float r1 = q1.x != 0.0f ? bb.y - f1 : 0.0f;
   float rs = r0 + r1;
   rs += __shfl_xor_sync(0xffffffffu, rs, 4);
   rs += __shfl_xor_sync(0xffffffffu, rs, 8);
@@ -256,19 +264,17 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
   const int x0 = 4 * (j & 1), y = (j >> 1) & 7, z = j >> 4;
   const int4 tv = __ldg(a.tile + t);
   const int P = __ldg(a.parent + t);
-  const size_t base = (size_t)t * TB3;
   float4* up = reinterpret_cast<float4*>(tptr(a.u, t, a.NL) + loff(x0, y, z));
   float4 u = *up;
   const float* uc = tptr(a.uc, P, a.NL);
   const float* us = a.ustar + (size_t)(P - a.NL) * TB3;
   const int pc0 = pcell_of(tv, x0, y, z), pc1 = pcell_of(tv, x0 + 2, y, z);
   const float c0 = __ldg(uc + pc0) - __ldg(us + pc0), c1 = __ldg(uc + pc1) - __ldg(us + pc1);
-  const float4 q0 = __ldg(a.coef + base + loff(x0, y, z)), q1 = __ldg(a.coef + base + loff(x0 + 1, y, z));
-  const float4 q2 = __ldg(a.coef + base + loff(x0 + 2, y, z)), q3 = __ldg(a.coef + base + loff(x0 + 3, y, z));
-  if (q0.x != 0.0f) u.x += c0;
-  if (q1.x != 0.0f) u.y += c0;
-  if (q2.x != 0.0f) u.z += c1;
-  if (q3.x != 0.0f) u.w += c1;
+  const float4 cc = __ldg(reinterpret_cast<const float4*>(a.coef + ((size_t)t << 11) + loff(x0, y, z)));
+  if (cc.x != 0.0f) u.x += c0;
+  if (cc.y != 0.0f) u.y += c0;
+  if (cc.z != 0.0f) u.z += c1;
+  if (cc.w != 0.0f) u.w += c1;
   *up = u;
 }
 
@@ -281,7 +287,7 @@ __global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
   const int y = (j >> 2) & 7, z = j >> 5, x0 = 2 * (j & 3);
   const int off0 = loff(x0, y, z);
   const size_t base = (size_t)t * TB3;
-  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
   const float2 uu = __ldg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
   float2* bp = reinterpret_cast<float2*>(a.b.inner + (size_t)(t - a.NL) * TB3 + off0);
   const float2 bb = *bp;

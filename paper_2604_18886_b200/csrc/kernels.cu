@@ -4,6 +4,7 @@
 // float4 (c, c_x-, c_y-, c_z-) and the +face coefficient comes from the neighbour record or
 // the ghost layer.
 #include "octmg_internal.cuh"
+#include "rowstencil.cuh"
 
 namespace octmg {
 
@@ -80,7 +81,7 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
       nc[ax] &= 7;
       const int no = loff(nc[0], nc[1], nc[2]);
       if (n >= 0) {
-        if (f & 1) cf = comp(__ldg(a.coef + (size_t)n * TB3 + no), ax);
+        if (f & 1) cf = comp(ldcoef(a.coef, (size_t)n * TB3 + no), ax);
         if (n < a.NL) {
           v = pval(a, beta, (size_t)n * TB3 + no);
         } else {
@@ -91,7 +92,7 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
             for (int dy = 0; dy < 2; ++dy)
               for (int dx = 0; dx < 2; ++dx) {
                 const size_t ci = (size_t)ct * TB3 + loff((2 * nc[0] + dx) & 7, (2 * nc[1] + dy) & 7, (2 * nc[2] + dz) & 7);
-                if (__ldg(a.coef + ci).x != 0.0f) { sm += pval(a, beta, ci); k++; }
+                if (ldcoef(a.coef, ci).x != 0.0f) { sm += pval(a, beta, ci); k++; }
               }
           v = k ? sm / (float)k : 0.0f;
         }
@@ -104,7 +105,7 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
         int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
         g[ax] += sg;
         const size_t ci = (size_t)C * TB3 + loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
-        if (__ldg(a.coef + ci).x != 0.0f) v = pi + 0.5f * (pval(a, beta, ci) - mP);
+        if (ldcoef(a.coef, ci).x != 0.0f) v = pi + 0.5f * (pval(a, beta, ci) - mP);
       }
     }
     s = fmaf(cf, v, s);
@@ -127,7 +128,7 @@ __device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double*
   const float beta = (a.use_beta && a.pold) ? (float)(a.sc->sum_rz / a.sc->rho) : 0.0f;
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
-  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
   float p0 = 0.0f, p1 = 0.0f;
   {
     float2 zz = __ldg(reinterpret_cast<const float2*>(a.z + base + off0));
@@ -168,34 +169,10 @@ __device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double*
 
 // q = A p as k_apply, on tiles whose six neighbours are all same-level leaves or walls (every
 // tile of a uniform tree): no shared-memory staging and no branches on the stencil path —
-// the neighbour entries are prefetched, every p of the stencil is formed from z and p_old
-// loads issued at once (in-tile neighbours hit L1), walls read the tile itself and are
-// zeroed.  Other tiles take the general composite path of k_apply.
-__device__ __forceinline__ float composite_regular(const ApplyArgs& a, float beta, int t, const int (&nb)[6], int x,
-                                                   int y, int z, const float4& q) {
-  const int c[3] = {x, y, z};
-  float s = 0.0f;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
-    int nc[3] = {c[0], c[1], c[2]};
-    nc[ax] += sg;
-    const bool inside = nc[ax] >= 0 && nc[ax] < 8;
-    const int n = nb[f];
-    const bool wall = !inside && n < 0;
-    nc[ax] &= 7;
-    const size_t ci = (size_t)(inside || wall ? t : n) * TB3 + loff(nc[0], nc[1], nc[2]);
-    float v = __ldg(a.z + ci);
-    if (a.pold) v = fmaf(beta, __ldg(a.pold + ci), v);
-    const float cf = (f & 1) ? comp(__ldg(a.coef + ci), ax) : comp(q, ax);
-    if (wall) v = 0.0f;
-    s = fmaf(cf, v, s);
-  }
-  return s;
-}
-
+// the neighbour entries are prefetched and the pair face sums are vectorised (row2_faces).
+// Other tiles take the general composite path of k_apply.
 template <bool DOT>
-__global__ __launch_bounds__(NT, 5) void k_apply_v2(ApplyArgs a) {
+__global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
   __shared__ double sred[NT / 32];
   const int t = a.tiles[blockIdx.x];
   int nb[6];
@@ -219,18 +196,35 @@ __global__ __launch_bounds__(NT, 5) void k_apply_v2(ApplyArgs a) {
   const float beta = (a.use_beta && a.pold) ? (float)(a.sc->sum_rz / a.sc->rho) : 0.0f;
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
-  const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
-  float2 pp = __ldg(reinterpret_cast<const float2*>(a.z + base + off0));
-  if (a.pold) {
-    const float2 po = __ldg(reinterpret_cast<const float2*>(a.pold + base + off0));
-    pp.x = fmaf(beta, po.x, pp.x);
-    pp.y = fmaf(beta, po.y, pp.y);
-  }
-  const float f0 = composite_regular(a, beta, t, nb, x0, y, z, q0);
-  const float f1 = composite_regular(a, beta, t, nb, x0 + 1, y, z, q1);
-  const float p0 = q0.x != 0.0f ? pp.x : 0.0f, p1 = q1.x != 0.0f ? pp.y : 0.0f;
-  const float r0 = q0.x != 0.0f ? fmaf(q0.x, p0, f0) : 0.0f;
-  const float r1 = q1.x != 0.0f ? fmaf(q1.x, p1, f1) : 0.0f;
+  const float* cb = a.coef + ((size_t)t << 11);
+  const float2 c0 = ldg2(cb + off0), cxm = ldg2(cb + 512 + off0), cym = ldg2(cb + 1024 + off0),
+               czm = ldg2(cb + 1536 + off0);
+  // p = z + beta p_old of any leaf cell (zero on inactive cells, see pval)
+  const float* zp = a.z;
+  const float* po = a.pold;
+  auto val2 = [zp, po, beta](int tt, int o) {
+    const size_t i = ((size_t)tt << 9) + o;
+    float2 v = ldg2(zp + i);
+    if (po) {
+      const float2 w = ldg2(po + i);
+      v.x = fmaf(beta, w.x, v.x);
+      v.y = fmaf(beta, w.y, v.y);
+    }
+    return v;
+  };
+  auto val1 = [zp, po, beta](int tt, int o) {
+    const size_t i = ((size_t)tt << 9) + o;
+    float v = __ldg(zp + i);
+    if (po) v = fmaf(beta, __ldg(po + i), v);
+    return v;
+  };
+  const float2 pp = val2(t, off0);
+  const float p0 = c0.x != 0.0f ? pp.x : 0.0f, p1 = c0.y != 0.0f ? pp.y : 0.0f;
+  // same summation order as the general path: c*p, then the faces x-, x+, y-, y+, z-, z+
+  const float2 f = row2_faces(a.coef, t, nb, x2, y, z, pp, cxm, cym, czm, make_float2(c0.x * p0, c0.y * p1),
+                              val2, val1);
+  const float r0 = c0.x != 0.0f ? f.x : 0.0f;
+  const float r1 = c0.y != 0.0f ? f.y : 0.0f;
   if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0, p1);
   *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
   if (DOT) {
@@ -395,10 +389,10 @@ __global__ void k_mask_copy(const float* src, const uint32_t* act, float* dst, i
 }
 
 // activity bitmask of the leaf cells (bit i%32 of word i/32: c_i != 0)
-__global__ void k_build_mask(const float4* coef, int64_t nwords, uint32_t* act) {
+__global__ void k_build_mask(const float* coef, int64_t nwords, uint32_t* act) {
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
     uint32_t m = 0;
-    for (int k = 0; k < 32; ++k) m |= (coef[32 * w + k].x != 0.0f ? 1u : 0u) << k;
+    for (int k = 0; k < 32; ++k) m |= (coef[cidx(32 * w + k, 0)] != 0.0f ? 1u : 0u) << k;
     act[w] = m;
   }
 }
@@ -442,7 +436,7 @@ void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStrea
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s) {
   k_mask_copy<<<592, 256, 0, s>>>(src, act, dst, n);
 }
-void launch_build_mask(const float4* coef, int64_t n, uint32_t* act, cudaStream_t s) {
+void launch_build_mask(const float* coef, int64_t n, uint32_t* act, cudaStream_t s) {
   k_build_mask<<<592, 256, 0, s>>>(coef, n / 32, act);
 }
 

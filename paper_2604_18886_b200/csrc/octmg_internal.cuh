@@ -70,6 +70,25 @@ __device__ __forceinline__ float* tptr(const Fld& f, int t, int NL) {
   return t < NL ? f.leaf + (size_t)t * TB3 : f.inner + (size_t)(t - NL) * TB3;
 }
 
+// Coefficient store (Eq. 3 compact record (c, c_x-, c_y-, c_z-)), SoA per tile:
+// tile t holds 4 planes of 512 floats (c, c_x-, c_y-, c_z-) at coef + t*2048, so a row of
+// cells loads each component as a 128-bit vector.  Cell index i = t*512 + cell.
+__host__ __device__ __forceinline__ size_t cidx(size_t i, int k) {
+  return ((i >> 9) << 11) + ((size_t)k << 9) + (i & 511);
+}
+__device__ __forceinline__ float4 ldcoef(const float* c, size_t i) {
+  const float* p = c + ((i >> 9) << 11) + (i & 511);
+  return make_float4(__ldg(p), __ldg(p + 512), __ldg(p + 1024), __ldg(p + 1536));
+}
+__device__ __forceinline__ float4 rdcoef(const float* c, size_t i) {  // coherent (setup kernels)
+  const float* p = c + ((i >> 9) << 11) + (i & 511);
+  return make_float4(p[0], p[512], p[1024], p[1536]);
+}
+__device__ __forceinline__ void stcoef(float* c, size_t i, const float4& v) {
+  float* p = c + ((i >> 9) << 11) + (i & 511);
+  p[0] = v.x; p[512] = v.y; p[1024] = v.z; p[1536] = v.w;
+}
+
 // PCG scalars, device resident (fp64).  The sum_* fields are the reductions of
 // the last kernel that produced them: local to this part first, then (multi-part) summed
 // over all parts in place before any consumer reads them.
@@ -96,7 +115,7 @@ struct Ranges {
 // Kernel classes for profiling
 enum KClass {
   KC_PASS = 0, KC_PROLONG, KC_RESTRICT, KC_COARSEST, KC_FASRHS, KC_SMOOTH_COARSE,
-  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_RBFUSED, KC_COPY, KC_COUNT
+  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_RBFUSED, KC_COPY, KC_COARSE_GRID, KC_COUNT
 };
 extern const char* kclass_name[KC_COUNT];
 
@@ -109,7 +128,7 @@ struct ApplyArgs {
   const int4* tile;
   const int* nbr;
   const int* child;
-  const float4* coef;
+  const float* coef;    // SoA per tile: planes c, c_x-, c_y-, c_z- (cidx)
   const float* glayer_val;
   const int* glayer;
   const float* z;       // direction source (user x for octmg_apply)
@@ -136,14 +155,14 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
                    Scalars* sc, cudaStream_t s, int grid);
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s);
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);
-void launch_build_mask(const float4* coef, int64_t n, uint32_t* act, cudaStream_t s);
+void launch_build_mask(const float* coef, int64_t n, uint32_t* act, cudaStream_t s);
 
 // smoother kernels (direct.cu, rbfused.cu, subcycle.cu)
 struct SmoothArgs {
   const int4* tile;
   const int* nbr;
   const int* parent;
-  const float4* coef;
+  const float* coef;    // SoA per tile: planes c, c_x-, c_y-, c_z- (cidx)
   const float* glayer_val;
   const int* glayer;
   Fld u;                // level values read (in place: also written)
@@ -167,6 +186,12 @@ void launch_rb_fused(const SmoothArgs& a, bool zero, cudaStream_t s, bool shell 
 void launch_copy_level(const SmoothArgs& a, cudaStream_t s);
 int subcycle_max_tiles();
 int subcycle_max_level();
+int coarse_grid_max_level();
+int coarse_grid_max_tiles(int nblocks);
+int coarse_grid_blocks();  // co-resident CTAs of k_coarse_grid (one per SM), 0 if it cannot run
+cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int fas_first,
+                               const octmg_mg_params& prm, const int* order_all, const int* lvl_off,
+                               const int* lvl_n, const int* ib, const int* ic, unsigned* bar, cudaStream_t s);
 void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
                      const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
                      cudaStream_t s);
@@ -187,7 +212,8 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
 struct Op {
   int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle,
                // 5 fused RB iteration, 6 copy level buffer in -> out, 7 halo exchange of level
-               // `level` of u, 8 broadcast of the restricted partition-parent level
+               // `level` of u, 8 broadcast of the restricted partition-parent level,
+               // 9 cooperative coarse cycle from `level` down (k_coarse_grid)
   int level;
   int stage;   // bit0 colour, bits1.. mode (SM_*); kind 5: bit0 first colour, bit1 zero
   int in_buf = 0, out_buf = 0;
@@ -196,7 +222,7 @@ struct Op {
 struct Hier {
   Tree* tree = nullptr;
   octmg_mg_params prm{};
-  float4* coef = nullptr;        // [T*512] (c, cxm, cym, czm)
+  float* coef = nullptr;         // [T*2048] SoA per tile: c, cxm, cym, czm planes (cidx)
   uint32_t* act = nullptr;       // [NL*512/32] activity bitmask of the leaf cells
   float* glayer_val = nullptr;   // [n_glayers*64]
   // multigrid buffers
@@ -224,8 +250,10 @@ struct Hier {
   int lvl_n[MAXL + 1] = {};
   int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
-  bool restrict_v2 = false;      // k_restrict_v2 (OCTMG_RESTRICT_V=2; measured slower than the staged one)
+  bool restrict_v2 = true;       // k_restrict_v2: vectorised regular tiles (OCTMG_RESTRICT_V=1: staged k_restrict_direct)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
+  int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
+  unsigned* bar = nullptr;       // its grid barrier counter
   int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes
   // profiling
   bool profiling = false;

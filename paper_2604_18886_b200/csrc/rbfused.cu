@@ -58,14 +58,14 @@ __device__ __forceinline__ float fsum_tile(const SmoothArgs& a, const RBSmem& S,
         const int no = loff(nc[0], nc[1], nc[2]);
         if (use_shell) v = S.shell[f][face_idx(ax, nc[0], nc[1], nc[2])];
         else v = ZERO ? 0.0f : __ldg(tptr(a.u, n, a.NL) + no);
-        if (f & 1) cf = comp(__ldg(a.coef + (size_t)n * TB3 + no), ax);
+        if (f & 1) cf = comp(ldcoef(a.coef, (size_t)n * TB3 + no), ax);
       } else if (n <= -2) {
         if (f & 1) cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 + face_idx(ax, x, y, z));
         const int C = -2 - n;
         int g[3] = {S.tv.y * 8 + c[0], S.tv.z * 8 + c[1], S.tv.w * 8 + c[2]};
         g[ax] += sg;
         const int co = loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
-        if (__ldg(a.coef + (size_t)C * TB3 + co).x != 0.0f) {
+        if (ldcoef(a.coef, (size_t)C * TB3 + co).x != 0.0f) {
           const float uc = ZERO ? 0.0f : __ldg(tptr(a.uc, C, a.NL) + co);
           v = ui + 0.5f * (uc - mP);
         }
@@ -105,8 +105,8 @@ __global__ __launch_bounds__(NT, 6) void k_rb_fused(SmoothArgs a) {
     const float2 bb = __ldg(reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0));
     S.u[off0] = uu.x; S.u[off0 + 1] = uu.y;
     S.b[off0] = bb.x; S.b[off0 + 1] = bb.y;
-    S.c4[off0] = __ldg(a.coef + base + off0);
-    S.c4[off0 + 1] = __ldg(a.coef + base + off0 + 1);
+    S.c4[off0] = ldcoef(a.coef, base + off0);
+    S.c4[off0 + 1] = ldcoef(a.coef, base + off0 + 1);
   }
   __syncthreads();
   // 2. first-colour values of the neighbours' face layers (32 of the 64 cells per face)
@@ -131,7 +131,7 @@ __global__ __launch_bounds__(NT, 6) void k_rb_fused(SmoothArgs a) {
         cc[0] = tmp[0]; cc[1] = tmp[1]; cc[2] = tmp[2];
       }
       const int no = loff(cc[0], cc[1], cc[2]);
-      const float4 qn = __ldg(a.coef + (size_t)n * TB3 + no);
+      const float4 qn = ldcoef(a.coef, (size_t)n * TB3 + no);
       float v = 0.0f;
       if (qn.x != 0.0f) {
         const float bn = __ldg(tptr(a.b, n, a.NL) + no);

@@ -70,7 +70,7 @@ struct AsmArgs {
   const int* glayer;
   const uint8_t* kind;
   WIn w;
-  float4* coef;
+  float* coef;  // SoA per tile (cidx)
   float* glayer_val;
   int NL;
   uint8_t wall[6];
@@ -104,7 +104,7 @@ __global__ __launch_bounds__(256) void k_assemble_diag(AsmArgs a) {
         }
       }
     }
-    a.coef[i] = make_float4(c, 0.f, 0.f, 0.f);
+    stcoef(a.coef, i, make_float4(c, 0.f, 0.f, 0.f));
   }
 }
 
@@ -129,7 +129,7 @@ __global__ __launch_bounds__(256) void k_assemble_offdiag(AsmArgs a) {
         fine_subs(a.child, a.NL, nb, f, sub);
         float acc = 0.0f;
         for (int k = 0; k < 4; ++k)
-          if (a.coef[sub[k]].x != 0.0f) acc += a.w.w(f ^ 1, sub[k]) * (0.5f * h);
+          if (a.coef[cidx(sub[k], 0)] != 0.0f) acc += a.w.w(f ^ 1, sub[k]) * (0.5f * h);
         v = -0.5f * acc;
       } else if (nb.what == NB_GHOST) {
         if (a.kind[(size_t)nb.tile * TB3 + nb.off] != KN) v = -a.w.w(f, i) * h;
@@ -147,9 +147,9 @@ __global__ __launch_bounds__(256) void k_assemble_offdiag(AsmArgs a) {
         }
       }
     }
-    float4 r = a.coef[i];
-    r.y = cm[0]; r.z = cm[1]; r.w = cm[2];
-    a.coef[i] = r;
+    a.coef[cidx(i, 1)] = cm[0];
+    a.coef[cidx(i, 2)] = cm[1];
+    a.coef[cidx(i, 3)] = cm[2];
   }
 }
 
@@ -157,7 +157,7 @@ struct CoarsenArgs {
   const int4* tile;
   const int* nbr;
   const int* child;
-  float4* coef;
+  float* coef;  // SoA per tile (cidx)
   int NL;
   int toff;  // first inner tile of level l-1
   float alpha;
@@ -180,30 +180,30 @@ __global__ __launch_bounds__(256) void k_coarsen(CoarsenArgs a) {
         for (int dx = 0; dx < 2; ++dx) {
           int d[3] = {dx, dy, dz};
           int cx[3] = {(2 * x + dx) & 7, (2 * y + dy) & 7, (2 * z + dz) & 7};
-          float4 ci = a.coef[(size_t)ct * TB3 + loff(cx[0], cx[1], cx[2])];
+          float4 ci = rdcoef(a.coef, (size_t)ct * TB3 + loff(cx[0], cx[1], cx[2]));
           bool act = ci.x != 0.0f;
           if (act) { cnt++; cI += ci.x / a.alpha; }
           for (int ax = 0; ax < 3; ++ax) {
             if (d[ax] == 1) {
               int sx[3] = {cx[0], cx[1], cx[2]};
               sx[ax] -= 1;
-              bool sact = a.coef[(size_t)ct * TB3 + loff(sx[0], sx[1], sx[2])].x != 0.0f;
+              bool sact = a.coef[cidx((size_t)ct * TB3 + loff(sx[0], sx[1], sx[2]), 0)] != 0.0f;
               if (act && sact) cI += (2.0f / a.alpha) * comp(ci, ax);
             } else {
               NbRef nb = nb_ref(a.nbr, ctv, ct, a.NL, cx[0], cx[1], cx[2], 2 * ax);
-              bool nact = nb.what != NB_WALL && a.coef[(size_t)nb.tile * TB3 + nb.off].x != 0.0f;
+              bool nact = nb.what != NB_WALL && a.coef[cidx((size_t)nb.tile * TB3 + nb.off, 0)] != 0.0f;
               if (act && nact) cIm[ax] += comp(ci, ax) / a.alpha;
             }
           }
         }
-    a.coef[(size_t)P * TB3 + off] = make_float4(cnt ? cI : 0.0f, cIm[0], cIm[1], cIm[2]);
+    stcoef(a.coef, (size_t)P * TB3 + off, make_float4(cnt ? cI : 0.0f, cIm[0], cIm[1], cIm[2]));
   }
 }
 
-__global__ void k_count_active(const float4* coef, int64_t n, unsigned long long* cnt) {
+__global__ void k_count_active(const float* coef, int64_t n, unsigned long long* cnt) {
   unsigned long long c = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    c += coef[i].x != 0.0f;
+    c += coef[cidx(i, 0)] != 0.0f;
   for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
 }

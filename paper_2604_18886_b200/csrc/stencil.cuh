@@ -1,9 +1,9 @@
 // Per-cell stencil helpers shared by the tile kernels (direct.cu) and the on-chip coarse
 // sub-cycle (subcycle.cu).  Cell (x,y,z) of tile t at the tile's level; coefficient record
 // float4 (c, c_x-, c_y-, c_z-); face order x-, x+, y-, y+, z-, z+ (the oracle's).
-// NC: values may be read through the non-coherent path (true when no thread of the kernel
-// writes them before they are read); false inside the sub-cycle kernel, which reads values
-// its own threads wrote earlier in the launch.
+// NC: load path of the values (see ldv): 1 in the tile kernels (nothing they read is written
+// before it is read), 0 / 2 inside the coarse-cycle kernels, which read what they wrote in
+// earlier phases (0: one CTA, 2: several CTAs across grid barriers).
 #pragma once
 #include "octmg_internal.cuh"
 
@@ -11,9 +11,12 @@ namespace octmg {
 
 enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
 
-template <bool NC>
+// NC: 1 = read-only path (__ldg), 2 = L2 only (__ldcg; data written by other CTAs earlier
+// in the same launch, across a grid barrier), 0 = plain load (same-CTA data)
+template <int NC>
 __device__ __forceinline__ float ldv(const float* p) {
-  if (NC) return __ldg(p);
+  if (NC == 1) return __ldg(p);
+  if (NC == 2) return __ldcg(p);
   return *p;
 }
 
@@ -27,7 +30,7 @@ __device__ __forceinline__ int pcell_of(int4 tv, int x, int y, int z) {
 // its level, values from u; ghosts use ui (the cell's snapshot value) and mP (mean of the
 // active cells of its parent block) — only evaluated if the tile has a ghost face.
 // ZERO_OWN: cells of `colour` read as 0 (first black pass of a cycle).
-template <bool ZERO_OWN, bool NC = true>
+template <bool ZERO_OWN, int NC = 1>
 __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int y, int z, const float4& q,
                                           float ui, float mP, int colour, float s0, const float* su = nullptr,
                                           const float (*scm)[TB3] = nullptr) {
@@ -45,7 +48,7 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
       const int no = loff(nc[0], nc[1], nc[2]);
       v = su ? su[no] : ldv<NC>(ut + no);  // su: this tile's values staged in shared memory
       if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
-      if (f & 1) cf = scm ? scm[ax][no] : comp(__ldg(a.coef + base + no), ax);  // scm: staged SoA
+      if (f & 1) cf = scm ? scm[ax][no] : comp(ldcoef(a.coef, base + no), ax);  // scm: staged SoA
     } else {
       const int n = __ldg(a.nbr + 6 * t + f);
       nc[ax] &= 7;
@@ -53,7 +56,7 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
       if (n >= 0) {
         v = ldv<NC>(tptr(a.u, n, a.NL) + no);
         if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
-        if (f & 1) cf = comp(__ldg(a.coef + (size_t)n * TB3 + no), ax);
+        if (f & 1) cf = comp(ldcoef(a.coef, (size_t)n * TB3 + no), ax);
       } else if (n <= -2) {
         if (f & 1)
           cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 +
@@ -63,7 +66,7 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
         int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
         g[ax] += sg;
         const int co = loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
-        if (__ldg(a.coef + (size_t)C * TB3 + co).x != 0.0f) {
+        if (ldcoef(a.coef, (size_t)C * TB3 + co).x != 0.0f) {
           const float uc = ZERO_OWN ? 0.0f : ldv<NC>(tptr(a.uc, C, a.NL) + co);
           v = ui + 0.5f * (uc - mP);
         }
@@ -82,7 +85,7 @@ __device__ __forceinline__ bool has_ghost(const SmoothArgs& a, int t) {
 }
 
 // mean of the active cells of the 2x2x2 block holding (x,y,z) (pass-start values)
-template <bool ZERO_OWN, bool NC = true>
+template <bool ZERO_OWN, int NC = 1>
 __device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, int y, int z, int colour) {
   const size_t base = (size_t)t * TB3;
   const float* ut = tptr(a.u, t, a.NL);
@@ -93,7 +96,7 @@ __device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, i
       for (int dx = 0; dx < 2; ++dx) {
         const int bx = (x & ~1) + dx, by = (y & ~1) + dy, bz = (z & ~1) + dz;
         const int bo = loff(bx, by, bz);
-        if (__ldg(a.coef + base + bo).x != 0.0f) {
+        if (ldcoef(a.coef, base + bo).x != 0.0f) {
           float bv = ldv<NC>(ut + bo);
           if (ZERO_OWN && ((bx + by + bz) & 1) == colour) bv = 0.0f;
           sm += bv;

@@ -1,9 +1,20 @@
-// On-chip coarse sub-cycle (sm_100a): the whole FAS-style mu-cycle below a small level K
-// (Alg. 4) runs inside ONE CTA of 1024 threads, phase by phase with
-// __syncthreads between phases, instead of ~30 tiny kernel launches per visit.  The levels
-// it covers hold <= 16 tiles each (8K cells), so every phase is a few L1/L2 round trips;
-// their data stays in L1/L2.  Same per-cell arithmetic as the tile kernels (stencil.cuh),
-// with coherent loads (NC = false) because the CTA reads what it wrote in earlier phases.
+// Coarse-cycle kernels (sm_100a): the whole FAS-style mu-cycle below a level (Alg. 4,
+// P:L723-756) in ONE launch instead of ~11 launches per level visit.
+//
+//  * k_subcycle: one CTA of 1024 threads, phases separated by __syncthreads; for the
+//    smallest levels (<= 16 tiles each, 8K cells), whose data stays in L1/L2.
+//  * k_coarse_grid: a persistent cooperative grid (one 1024-thread CTA per SM, co-resident
+//    by cooperative launch) for the levels below the finest ones (up to a few thousand
+//    tiles each, L2-resident): every phase is spread over all CTAs and ends with a grid
+//    barrier; when the recursion reaches the sub-cycle level, CTA 0 runs the rest of the
+//    cycle alone (the k_subcycle phases) while the other CTAs wait at the next barrier.
+//
+// Every phase has the same per-cell arithmetic as the tile kernels (stencil.cuh).  Mapping:
+// a tile's cells are handled by 256 consecutive threads of one CTA (colour passes: one
+// colour cell per thread and tile), so the in-place colour pass needs only a CTA barrier
+// between its reads and writes (it reads other tiles' cells of the other colour only).
+// Loads of mutable data: plain in the one-CTA kernel (M = 0), L2-only (__ldcg, M = 2) in
+// the grid kernel, where other CTAs wrote them before a grid barrier.
 #include "stencil.cuh"
 
 namespace octmg {
@@ -12,35 +23,68 @@ namespace {
 
 constexpr int SUB_THREADS = 1024;
 constexpr int SUB_MAXL = 4;
-constexpr int SUB_MAX_PER_THREAD = 4;  // colour cells per thread (16 tiles * 256 / 1024)
+constexpr int SUB_MAX_PER_THREAD = 4;   // colour cells per thread of the one-CTA kernel
+constexpr int GRID_MAX_PER_THREAD = 8;  // colour cells per thread of the grid kernel
+constexpr int GRID_MAXL = 10;
 
 struct SubArgs {
   SmoothArgs a;
   int L;                 // finest level of the tree
-  int K;                 // top level of this sub-cycle
+  int K;                 // top level of this (sub-)cycle
+  int sK;                // grid kernel: levels <= sK run in CTA 0 alone (-1: none)
   int fas_first;         // form the FAS rhs of level K's inner rows first
   int mu, nu_pre, nu_post, nu_coarsest;
   const int* order_all;  // tiles of each level in rank order
-  int lvl_off[SUB_MAXL + 1], lvl_n[SUB_MAXL + 1];
-  int ib[SUB_MAXL + 1], ic[SUB_MAXL + 1];
+  int lvl_off[GRID_MAXL + 1], lvl_n[GRID_MAXL + 1];
+  int ib[GRID_MAXL + 1], ic[GRID_MAXL + 1];
+  unsigned* bar;         // grid barrier counter (zeroed before the launch)
 };
 
-__device__ void sc_pass(const SubArgs& A, int l, int colour, int mode) {
+// phase extent: all threads of the grid (GRID) or of this CTA
+template <bool GRID>
+__device__ __forceinline__ int ph_tid() { return GRID ? blockIdx.x * SUB_THREADS + threadIdx.x : threadIdx.x; }
+template <bool GRID>
+__device__ __forceinline__ int ph_nthreads() { return GRID ? gridDim.x * SUB_THREADS : SUB_THREADS; }
+
+// grid barrier: monotonic arrival counter, barrier k waits for k * gridDim arrivals
+__device__ __forceinline__ void grid_barrier(const SubArgs& A, unsigned& epoch) {
+  __syncthreads();
+  epoch += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(A.bar, 1u);
+    const volatile unsigned* vb = A.bar;
+    while (*vb < epoch) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <bool GRID>
+__device__ __forceinline__ void phase_end(const SubArgs& A, unsigned& epoch) {
+  if (GRID) grid_barrier(A, epoch);
+  else __syncthreads();
+}
+
+template <bool GRID, int M>
+__device__ __noinline__ void sc_pass(const SubArgs& A, int l, int colour, int mode, unsigned& epoch) {
+  constexpr int MAXK = GRID ? GRID_MAX_PER_THREAD : SUB_MAX_PER_THREAD;
   const SmoothArgs& a = A.a;
   const int* ord = A.order_all + A.lvl_off[l];
   const int ncell = A.lvl_n[l] * 256;
-  float unew[SUB_MAX_PER_THREAD];
-  float* dst[SUB_MAX_PER_THREAD];
+  float unew[MAXK];
+  float* dst[MAXK];
   int k = 0;
-  for (int s = threadIdx.x; s < ncell; s += SUB_THREADS, ++k) {
-    const int t = ord[s >> 8];
+  for (int s = ph_tid<GRID>(); s < ncell && k < MAXK; s += ph_nthreads<GRID>(), ++k) {
+    const int t = __ldg(ord + (s >> 8));
     const int j = s & 255;
     const int y = (j >> 2) & 7, z = j >> 5;
     const int x = 2 * (j & 3) + ((colour + y + z) & 1);
     const int off = loff(x, y, z);
     float* ut = tptr(a.u, t, a.NL);
-    const float4 q = __ldg(a.coef + (size_t)t * TB3 + off);
-    const float b = ldv<false>(tptr(a.b, t, a.NL) + off);
+    const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
+    const float b = ldv<M>(tptr(a.b, t, a.NL) + off);
     dst[k] = nullptr;
     unew[k] = 0.0f;
     if (q.x != 0.0f) {
@@ -50,11 +94,11 @@ __device__ void sc_pass(const SubArgs& A, int l, int colour, int mode) {
         const bool z2 = mode == SM_ZERO2;
         float ui = 0.0f, mP = 0.0f;
         if (has_ghost(a, t)) {
-          ui = z2 ? 0.0f : ldv<false>(ut + off);
-          mP = z2 ? block_mean<true, false>(a, t, x, y, z, colour) : block_mean<false, false>(a, t, x, y, z, colour);
+          ui = z2 ? 0.0f : ldv<M>(ut + off);
+          mP = z2 ? block_mean<true, M>(a, t, x, y, z, colour) : block_mean<false, M>(a, t, x, y, z, colour);
         }
-        const float fs = z2 ? face_sum<true, false>(a, t, x, y, z, q, ui, mP, colour, 0.0f)
-                            : face_sum<false, false>(a, t, x, y, z, q, ui, mP, colour, 0.0f);
+        const float fs = z2 ? face_sum<true, M>(a, t, x, y, z, q, ui, mP, colour, 0.0f)
+                            : face_sum<false, M>(a, t, x, y, z, q, ui, mP, colour, 0.0f);
         unew[k] = (b - fs) / q.x;
       }
       dst[k] = ut + off;
@@ -62,28 +106,32 @@ __device__ void sc_pass(const SubArgs& A, int l, int colour, int mode) {
       dst[k] = ut + off;
     }
   }
-  __syncthreads();  // all pass-start reads before the in-place writes
+  __syncthreads();  // all pass-start reads of each tile (one CTA per tile) before the writes
   for (int i = 0; i < k; ++i)
     if (dst[i]) *dst[i] = unew[i];
-  __syncthreads();
+  phase_end<GRID>(A, epoch);
 }
 
-__device__ void sc_passes(const SubArgs& A, int l, int iters, bool red_first, int m1, int m2) {
+template <bool GRID, int M>
+__device__ void sc_passes(const SubArgs& A, int l, int iters, bool red_first, int m1, int m2, unsigned& epoch) {
   for (int k = 0; k < iters; ++k) {
-    sc_pass(A, l, red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN);
-    sc_pass(A, l, red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN);
+    sc_pass<GRID, M>(A, l, red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN, epoch);
+    sc_pass<GRID, M>(A, l, red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN, epoch);
   }
 }
 
-// residual + restriction + Avg of level l into level l-1 (k_restrict_direct's arithmetic)
-__device__ void sc_restrict(const SubArgs& A, int l) {
+// residual + restriction + Avg of level l into level l-1 (k_restrict_direct's arithmetic);
+// groups of 256 threads own one tile at a time
+template <bool GRID, int M>
+__device__ __noinline__ void sc_restrict(const SubArgs& A, int l, unsigned& epoch) {
   const SmoothArgs& a = A.a;
   const int* ord = A.order_all + A.lvl_off[l];
   const int n = A.lvl_n[l];
-  for (int t0 = 0; t0 < n; t0 += SUB_THREADS / 256) {
-    const int ti = t0 + (threadIdx.x >> 8);
+  const int ngrp = ph_nthreads<GRID>() / 256;
+  for (int t0 = 0; t0 < n; t0 += ngrp) {
+    const int ti = t0 + ph_tid<GRID>() / 256;
     if (ti < n) {  // uniform per 256-thread group, so the shuffles below are converged
-      const int t = ord[ti];
+      const int t = __ldg(ord + ti);
       const int j = threadIdx.x & 255;
       const int x2 = j & 3;
       const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
@@ -91,11 +139,11 @@ __device__ void sc_restrict(const SubArgs& A, int l) {
       const int x0 = 2 * x2;
       const size_t base = (size_t)t * TB3;
       const int off0 = loff(x0, y, z);
-      const float4 q0 = __ldg(a.coef + base + off0), q1 = __ldg(a.coef + base + off0 + 1);
+      const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
       const float* ut = tptr(a.u, t, a.NL);
       const float* bt = tptr(a.b, t, a.NL);
-      const float u0 = ut[off0], u1 = ut[off0 + 1];
-      const float b0 = bt[off0], b1 = bt[off0 + 1];
+      const float u0 = ldv<M>(ut + off0), u1 = ldv<M>(ut + off0 + 1);
+      const float b0 = ldv<M>(bt + off0), b1 = ldv<M>(bt + off0 + 1);
       float su = (q0.x != 0.0f ? u0 : 0.0f) + (q1.x != 0.0f ? u1 : 0.0f);
       int na = (q0.x != 0.0f) + (q1.x != 0.0f);
       su += __shfl_xor_sync(0xffffffffu, su, 4);
@@ -104,8 +152,8 @@ __device__ void sc_restrict(const SubArgs& A, int l) {
       na += __shfl_xor_sync(0xffffffffu, na, 8);
       const float mP = na ? su / (float)na : 0.0f;
       float r0 = 0.0f, r1 = 0.0f;
-      if (q0.x != 0.0f) r0 = b0 - face_sum<false, false>(a, t, x0, y, z, q0, u0, mP, 0, q0.x * u0);
-      if (q1.x != 0.0f) r1 = b1 - face_sum<false, false>(a, t, x0 + 1, y, z, q1, u1, mP, 0, q1.x * u1);
+      if (q0.x != 0.0f) r0 = b0 - face_sum<false, M>(a, t, x0, y, z, q0, u0, mP, 0, q0.x * u0);
+      if (q1.x != 0.0f) r1 = b1 - face_sum<false, M>(a, t, x0 + 1, y, z, q1, u1, mP, 0, q1.x * u1);
       float rs = r0 + r1;
       rs += __shfl_xor_sync(0xffffffffu, rs, 4);
       rs += __shfl_xor_sync(0xffffffffu, rs, 8);
@@ -119,109 +167,191 @@ __device__ void sc_restrict(const SubArgs& A, int l) {
       }
     }
   }
-  __syncthreads();
+  phase_end<GRID>(A, epoch);
 }
 
 // b_I = beta R r (in b) + (A^l u*)_I on the inner rows of level l (Alg. 4 line 10)
-__device__ void sc_fasrhs(const SubArgs& A, int l) {
+template <bool GRID, int M>
+__device__ __noinline__ void sc_fasrhs(const SubArgs& A, int l, unsigned& epoch) {
   const SmoothArgs& a = A.a;
   const int ncell = A.ic[l] * TB3;
-  for (int s = threadIdx.x; s < ncell; s += SUB_THREADS) {
+  for (int s = ph_tid<GRID>(); s < ncell; s += ph_nthreads<GRID>()) {
     const int t = A.ib[l] + (s >> 9);
     const int off = s & 511;
     const int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
-    const float4 q = __ldg(a.coef + (size_t)t * TB3 + off);
+    const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
     float* bi = a.b.inner + (size_t)(t - a.NL) * TB3 + off;
     if (q.x != 0.0f) {
-      const float u = tptr(a.u, t, a.NL)[off];
-      *bi = *bi + face_sum<false, false>(a, t, x, y, z, q, 0.0f, 0.0f, 0, q.x * u);  // no ghosts
+      const float u = ldv<M>(tptr(a.u, t, a.NL) + off);
+      *bi = ldv<M>(bi) + face_sum<false, M>(a, t, x, y, z, q, 0.0f, 0.0f, 0, q.x * u);  // no ghosts
     } else {
       *bi = 0.0f;
     }
   }
-  __syncthreads();
+  phase_end<GRID>(A, epoch);
 }
 
 // u += P (u^{l-1} - u*) on the active cells of level l (Alg. 4 line 15)
-__device__ void sc_prolong(const SubArgs& A, int l) {
+template <bool GRID, int M>
+__device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch) {
   const SmoothArgs& a = A.a;
   const int* ord = A.order_all + A.lvl_off[l];
   const int ncell = A.lvl_n[l] * TB3;
-  for (int s = threadIdx.x; s < ncell; s += SUB_THREADS) {
-    const int t = ord[s >> 9];
+  for (int s = ph_tid<GRID>(); s < ncell; s += ph_nthreads<GRID>()) {
+    const int t = __ldg(ord + (s >> 9));
     const int off = s & 511;
-    if (__ldg(a.coef + (size_t)t * TB3 + off).x == 0.0f) continue;
+    if (ldcoef(a.coef, (size_t)t * TB3 + off).x == 0.0f) continue;
     const int4 tv = __ldg(a.tile + t);
     const int P = __ldg(a.parent + t);
     const int pc = pcell_of(tv, off & 7, (off >> 3) & 7, off >> 6);
-    tptr(a.u, t, a.NL)[off] += tptr(a.uc, P, a.NL)[pc] - a.ustar[(size_t)(P - a.NL) * TB3 + pc];
+    float* up = tptr(a.u, t, a.NL) + off;
+    *up = ldv<M>(up) + (ldv<M>(tptr(a.uc, P, a.NL) + pc) - ldv<M>(a.ustar + (size_t)(P - a.NL) * TB3 + pc));
   }
-  __syncthreads();
+  phase_end<GRID>(A, epoch);
 }
 
-// compile-time level recursion (no device call stack): sc_fas<l> calls sc_fas<l-1>
-template <int l>
-__device__ void sc_fas(const SubArgs& A, bool fas_first);
-
-template <int l>
-__device__ __forceinline__ void sc_fas_level(const SubArgs& A, bool fas_first) {
-  if (l < A.L && fas_first && A.ic[l] > 0) sc_fasrhs(A, l);
-  const bool finest = l == A.L;
-  if constexpr (l == 0) {
-    const int h1 = A.nu_coarsest / 2;
-    sc_passes(A, 0, h1, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN);
-    const bool zz = finest && h1 == 0;
-    sc_passes(A, 0, A.nu_coarsest - h1, false, zz ? SM_ZERO1 : SM_PLAIN, zz ? SM_ZERO2 : SM_PLAIN);
-  } else {
-    sc_passes(A, l, A.nu_pre, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN);
-    sc_restrict(A, l);
-    for (int k = 0; k < A.mu; ++k) sc_fas<l - 1>(A, k == 0);
-    sc_prolong(A, l);
-    sc_passes(A, l, A.nu_post, false, SM_PLAIN, SM_PLAIN);
-  }
+// smoothing at the coarsest level: nu_b/2 x (R,B) then nu_b/2 x (B,R)
+template <bool GRID, int M>
+__device__ void sc_coarsest(const SubArgs& A, bool finest, unsigned& epoch) {
+  const int h1 = A.nu_coarsest / 2;
+  sc_passes<GRID, M>(A, 0, h1, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN, epoch);
+  const bool zz = finest && h1 == 0;
+  sc_passes<GRID, M>(A, 0, A.nu_coarsest - h1, false, zz ? SM_ZERO1 : SM_PLAIN, zz ? SM_ZERO2 : SM_PLAIN, epoch);
 }
 
-template <int l>
-__device__ void sc_fas(const SubArgs& A, bool fas_first) {
-  sc_fas_level<l>(A, fas_first);
+// Alg. 4 from level `top` down, iteratively (explicit per-level count of the mu coarse
+// calls made; every thread runs the same control flow).  GRID: levels <= A.sK run in CTA 0
+// alone (the one-CTA version of this function) while the other CTAs wait at a barrier.
+template <bool GRID, int M>
+__device__ void sc_cycle(const SubArgs& A, int top, bool fas_first, unsigned& epoch) {
+  int done[GRID_MAXL + 1];
+  int l = top;
+  bool ff = fas_first;
+  bool entering = true;
+  while (true) {
+    if (entering) {
+      bool leaf_work = true;
+      if constexpr (GRID) {
+        if (l <= A.sK) {
+          if (blockIdx.x == 0) {
+            unsigned dummy = 0;
+            sc_cycle<false, M>(A, l, ff, dummy);
+          }
+          grid_barrier(A, epoch);
+          leaf_work = false;
+        }
+      }
+      if (leaf_work) {
+        if (l < A.L && ff && A.ic[l] > 0) sc_fasrhs<GRID, M>(A, l, epoch);
+        const bool finest = l == A.L;
+        if (l == 0) {
+          sc_coarsest<GRID, M>(A, finest, epoch);
+        } else {
+          sc_passes<GRID, M>(A, l, A.nu_pre, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN,
+                             epoch);
+          sc_restrict<GRID, M>(A, l, epoch);
+          done[l] = 0;
+          l -= 1;
+          ff = true;
+          continue;  // enter the first coarse call
+        }
+      }
+      entering = false;  // level l finished
+    }
+    if (l == top) break;
+    const int p = l + 1;
+    if (++done[p] < A.mu) {  // next coarse call starts from the previous one's u^{l}
+      l = p - 1;
+      ff = false;
+      entering = true;
+      continue;
+    }
+    sc_prolong<GRID, M>(A, p, epoch);
+    sc_passes<GRID, M>(A, p, A.nu_post, false, SM_PLAIN, SM_PLAIN, epoch);
+    l = p;  // level p finished
+  }
 }
 
 __global__ __launch_bounds__(SUB_THREADS, 1) void k_subcycle(SubArgs A) {
-  const bool ff = A.fas_first != 0;
-  switch (A.K) {
-    case 0: sc_fas<0>(A, ff); break;
-    case 1: sc_fas<1>(A, ff); break;
-    case 2: sc_fas<2>(A, ff); break;
-    case 3: sc_fas<3>(A, ff); break;
-    default: sc_fas<4>(A, ff); break;
-  }
+  unsigned e = 0;
+  sc_cycle<false, 0>(A, A.K, A.fas_first != 0, e);
 }
 
-}  // namespace
+__global__ __launch_bounds__(SUB_THREADS, 1) void k_coarse_grid(SubArgs A) {
+  unsigned e = 0;
+  sc_cycle<true, 2>(A, A.K, A.fas_first != 0, e);
+}
 
-int subcycle_max_tiles() { return SUB_THREADS * SUB_MAX_PER_THREAD / 256; }
-int subcycle_max_level() { return SUB_MAXL; }
-
-void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
-                     const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
-                     cudaStream_t s) {
+SubArgs make_args(const SmoothArgs& base, int L, int K, int sK, int fas_first, const octmg_mg_params& prm,
+                  const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic) {
   SubArgs A;
   A.a = base;
   A.L = L;
   A.K = K;
+  A.sK = sK;
   A.fas_first = fas_first;
   A.mu = prm.mu;
   A.nu_pre = prm.nu_pre;
   A.nu_post = prm.nu_post;
   A.nu_coarsest = prm.nu_coarsest;
   A.order_all = order_all;
-  for (int l = 0; l <= SUB_MAXL; ++l) {
+  for (int l = 0; l <= GRID_MAXL; ++l) {
     A.lvl_off[l] = l <= K ? lvl_off[l] : 0;
     A.lvl_n[l] = l <= K ? lvl_n[l] : 0;
     A.ib[l] = l <= K ? ib[l] : 0;
     A.ic[l] = l <= K ? ic[l] : 0;
   }
+  A.bar = nullptr;
+  return A;
+}
+
+}  // namespace
+
+int subcycle_max_tiles() { return SUB_THREADS * SUB_MAX_PER_THREAD / 256; }
+int subcycle_max_level() { return SUB_MAXL; }
+int coarse_grid_max_level() { return GRID_MAXL; }
+
+// tiles per level the grid kernel takes: GRID_MAX_PER_THREAD colour cells per thread
+int coarse_grid_max_tiles(int nblocks) { return nblocks * SUB_THREADS * GRID_MAX_PER_THREAD / 256; }
+
+int coarse_grid_blocks() {
+  static int nb = -1;
+  if (nb < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_coarse_grid, SUB_THREADS, 0);
+    nb = per >= 1 ? sms : 0;
+  }
+  return nb;
+}
+
+void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
+                     const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
+                     cudaStream_t s) {
+  SubArgs A = make_args(base, L, K, -1, fas_first, prm, order_all, lvl_off, lvl_n, ib, ic);
   k_subcycle<<<1, SUB_THREADS, 0, s>>>(A);
+}
+
+cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int fas_first,
+                               const octmg_mg_params& prm, const int* order_all, const int* lvl_off,
+                               const int* lvl_n, const int* ib, const int* ic, unsigned* bar, cudaStream_t s) {
+  SubArgs A = make_args(base, L, K, sK, fas_first, prm, order_all, lvl_off, lvl_n, ib, ic);
+  A.bar = bar;
+  cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  // cooperative launch: every CTA co-resident (the grid barrier relies on it)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(coarse_grid_blocks());
+  cfg.blockDim = dim3(SUB_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_coarse_grid, A);
 }
 
 }  // namespace octmg
