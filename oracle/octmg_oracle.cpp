@@ -6,8 +6,8 @@
 // compact matrix-free Poisson coefficients (Eq. 3), the T-junction
 // stencil (Eqs. 9-12), Galerkin coarsening (Alg. 3), RBGS
 // (L407-409), the FAS-style mu-cycle (Alg. 4), the standard mu-cycle
-// (Alg. 2, used only as an equivalence check on uniform trees) and PCG
-// (Alg. 1).  Readings of silent/ambiguous passages follow SURVEY.md
+// (Alg. 2, used only as an equivalence check on uniform trees), PCG
+// (Alg. 1) and multigrid as a standalone solver (L145, L411).  Readings of silent/ambiguous passages follow SURVEY.md
 // 8(c) and are listed in DESIGN.md "Readings".
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
@@ -396,8 +396,10 @@ int assemble(Oracle& o) {
 }
 
 // Alg. 3 with the activity test on the off-diagonal branch (SURVEY c-3 / c-8
-// #3): c^{l-1}_I from the 8 children i = 2I + d at level l.
-void coarsen_level(Oracle& o, int l) {
+// #3): c^{l-1}_I from the 8 children i = 2I + d at level l.  literal = 1: Alg. 3 exactly as
+// printed (the non-diagonal branch adds c^l_{i,e-}/alpha
+// with no activity test).
+void coarsen_level(Oracle& o, int l, bool literal) {
   const double al = o.alpha;
   int lc = l - 1;
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t) {
@@ -423,7 +425,7 @@ void coarsen_level(Oracle& o, int l) {
               if (d[a] == 1) {
                 if (act && nact) cI += (2.0 / al) * o.cm[a][i];  // 2 cross terms in the diagonal
               } else {
-                if (act && nact) cIm[a] += o.cm[a][i] / al;     // non-diagonal
+                if (literal || (act && nact)) cIm[a] += o.cm[a][i] / al;  // non-diagonal
               }
             }
           }
@@ -434,7 +436,7 @@ void coarsen_level(Oracle& o, int l) {
   }
 }
 
-int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha) {
+int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha, bool literal) {
   size_t N = (size_t)o.NL * o.B3;
   o.kind.assign(kind, kind + N);
   for (int f = 0; f < 6; ++f) {
@@ -446,7 +448,7 @@ int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha) {
   o.alpha = alpha;
   int st = assemble(o);
   if (st) return st;
-  for (int l = o.L; l >= 1; --l) coarsen_level(o, l);
+  for (int l = o.L; l >= 1; --l) coarsen_level(o, l, literal);
   o.setup = true;
   size_t NC = (size_t)o.T * o.B3;
   o.u.assign(NC, 0.0); o.b.assign(NC, 0.0); o.ustar.assign(NC, 0.0);
@@ -795,6 +797,42 @@ int pcg(Oracle& o, const MG& p, int precond_kind, const double* bin, double* x, 
   }
 }
 
+// Multigrid as a standalone solver ("can be used as standalone solvers"; P:L411
+// "if multigrid is used as a standalone solver, beta should be set to 1"): the stationary
+// iteration x_{k+1} = x_k + M(b - A x_k) from x_0 = 0, with the residual updated as
+// r_{k+1} = r_k - A z_k and tested like Alg. 1 line 8 (||r_k|| <= rtol ||r_0||).
+int mg_solve(Oracle& o, const MG& p, bool fas_form, const double* bin, double* x, double rtol, int max_iters,
+             int nullspace, int* iters_out, double* relres_out, double* bnorm_out, double* hist, int hcap) {
+  size_t N = (size_t)o.NL * o.B3;
+  bool ns = nullspace < 0 ? pure_neumann(o) : nullspace == 1;
+  std::vector<double> r(N), z(N), q(N);
+  for (size_t i = 0; i < N; ++i) { x[i] = 0.0; r[i] = o.c[i] != 0.0 ? bin[i] : 0.0; }
+  if (ns) project_mean(o, r.data());
+  double bn = std::sqrt(dot(o, r.data(), r.data()));
+  *bnorm_out = bn;
+  *iters_out = 0;
+  *relres_out = 0.0;
+  if (bn == 0.0) return S_OK;
+  int k = 0;
+  while (true) {
+    precond(o, p, r.data(), z.data(), fas_form);   // z = M(r)
+    apply_composite(o, z.data(), q.data());        // q = A z
+    for (size_t i = 0; i < N; ++i) {
+      if (o.c[i] == 0.0) continue;
+      x[i] += z[i];
+      r[i] -= q[i];
+    }
+    if (ns) project_mean(o, r.data());
+    k++;
+    double rn = std::sqrt(dot(o, r.data(), r.data()));
+    if (k - 1 < hcap) hist[k - 1] = rn / bn;
+    *iters_out = k;
+    *relres_out = rn / bn;
+    if (rn <= rtol * bn) return S_OK;
+    if (k >= max_iters) return S_MAXITER;
+  }
+}
+
 MG mg_from(const double* prm) {
   MG p;
   if (prm) {
@@ -848,8 +886,8 @@ void orc_tables(void* h, int32_t* tiles, int32_t* nbr, int32_t* parent, int32_t*
   if (o->NI) std::memcpy(child, o->child.data(), sizeof(int32_t) * o->child.size());
 }
 
-int32_t orc_setup(void* h, const uint8_t* kind, const float* w, double alpha) {
-  return setup(*(Oracle*)h, kind, w, alpha);
+int32_t orc_setup(void* h, const uint8_t* kind, const float* w, double alpha, int32_t literal) {
+  return setup(*(Oracle*)h, kind, w, alpha, literal != 0);
 }
 
 // out: T*B3*4 doubles (c, cxm, cym, czm) per cell in all-tile order
@@ -893,6 +931,17 @@ int32_t orc_pcg(void* h, const double* prm, int32_t precond_kind, const double* 
   int it = 0;
   int st = pcg(*(Oracle*)h, mg_from(prm), precond_kind, b, x, rtol, max_iters, nullspace, &it,
                relres, bnorm, hist, hcap);
+  *iters = it;
+  return st;
+}
+
+// form: 1 = Alg. 4 (FAS), 0 = Alg. 2
+int32_t orc_mg_solve(void* h, const double* prm, int32_t form, const double* b, double* x, double rtol,
+                     int32_t max_iters, int32_t nullspace, int32_t* iters, double* relres, double* bnorm,
+                     double* hist, int32_t hcap) {
+  int it = 0;
+  int st = mg_solve(*(Oracle*)h, mg_from(prm), form == 1, b, x, rtol, max_iters, nullspace, &it, relres, bnorm,
+                    hist, hcap);
   *iters = it;
   return st;
 }

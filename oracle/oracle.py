@@ -43,7 +43,7 @@ def lib():
         _lib.orc_info.argtypes = [P, P]
         _lib.orc_tables.argtypes = [P, P, P, P, P]
         _lib.orc_setup.restype = I32
-        _lib.orc_setup.argtypes = [P, P, P, D]
+        _lib.orc_setup.argtypes = [P, P, P, D, I32]
         _lib.orc_coefs.argtypes = [P, P]
         _lib.orc_ghost_coef.restype = I32
         _lib.orc_ghost_coef.argtypes = [P, I32, I64, I64, I64, P]
@@ -53,6 +53,8 @@ def lib():
         _lib.orc_vcycle.argtypes = [P, P, P, P, I32]
         _lib.orc_pcg.restype = I32
         _lib.orc_pcg.argtypes = [P, P, I32, P, P, D, I32, I32, P, P, P, P, I32]
+        _lib.orc_mg_solve.restype = I32
+        _lib.orc_mg_solve.argtypes = [P, P, I32, P, P, D, I32, I32, P, P, P, P, I32]
     return _lib
 
 
@@ -115,15 +117,15 @@ class Oracle:
         return dict(tiles=tiles, nbr=nbr, parent=parent, child=child[:NI])
 
     # ---- setup ---------------------------------------------------------------------
-    def setup(self, kind=None, w=None, alpha: float = 2.0):
+    def setup(self, kind=None, w=None, alpha: float = 2.0, coarsen_literal: bool = False):
         N = self.N
         k = np.zeros(N, dtype=np.uint8) if kind is None else np.ascontiguousarray(kind, dtype=np.uint8)
         assert k.size == N
         if w is not None:
             wv = np.ascontiguousarray(np.asarray(w, dtype=np.float32).reshape(6, N))
-            st = lib().orc_setup(self._h, _p(k), _p(wv), alpha)
+            st = lib().orc_setup(self._h, _p(k), _p(wv), alpha, int(coarsen_literal))
         else:
-            st = lib().orc_setup(self._h, _p(k), None, alpha)
+            st = lib().orc_setup(self._h, _p(k), None, alpha, int(coarsen_literal))
         if st:
             raise OracleError(st, lib().orc_last_error().decode())
         self.alpha = alpha
@@ -176,6 +178,21 @@ class Oracle:
         pk = {"identity": 0, "fas": 1, "alg2": 2}[precond]
         st = lib().orc_pcg(self._h, _p(prm), pk, _p(b), _p(x), rtol, max_iters, nullspace,
                            _p(it), _p(rr), _p(bn), _p(hist), hcap)
+        n = int(it[0])
+        return dict(x=x, iters=n, rel_residual=float(rr[0]), bnorm=float(bn[0]),
+                    status=STATUS.get(st, st), history=hist[:min(n, hcap)].copy())
+
+    def mg_solve(self, b, rtol=1e-6, max_iters=200, nullspace=-1, form="fas", hcap=512, **mg):
+        """Standalone multigrid x += M(b - A x) (use beta = 1)."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(self.N)
+        prm = mg_params(**mg)
+        it = np.zeros(1, dtype=np.int32)
+        rr = np.zeros(1)
+        bn = np.zeros(1)
+        hist = np.zeros(hcap)
+        st = lib().orc_mg_solve(self._h, _p(prm), 1 if form == "fas" else 0, _p(b), _p(x), rtol, max_iters,
+                                nullspace, _p(it), _p(rr), _p(bn), _p(hist), hcap)
         n = int(it[0])
         return dict(x=x, iters=n, rel_residual=float(rr[0]), bnorm=float(bn[0]),
                     status=STATUS.get(st, st), history=hist[:min(n, hcap)].copy())
