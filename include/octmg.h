@@ -115,6 +115,14 @@ typedef struct {
   int32_t nu_pre;       /* RBGS iterations (red+black) before coarsening: 2        */
   int32_t nu_post;      /* RBGS iterations after (opposite colour order): 2                 */
   int32_t nu_coarsest;  /* RBGS iterations at level 0, two opposite-order halves: 10        */
+  int32_t form;         /* 0: FAS-style mu-cycle, Alg. 4, beta at restriction;
+                           1: standard mu-cycle, Alg. 2, beta at prolongation,
+                           zero coarse initial guess — uniform trees only (every leaf at the
+                           finest level), else OCTMG_E_INVALID                                */
+  int32_t coarsen_literal; /* 1: Alg. 3 exactly as printed (the non-diagonal
+                           branch without the activity test); 0 (default): with the test,
+                           so that Alg. 3 equals R A P over the fluid unknowns (DESIGN.md
+                           reading 3)                                                        */
 } octmg_mg_params;
 
 /*
@@ -210,6 +218,17 @@ typedef struct {
  */
 octmg_status octmg_pcg_solve(octmg_hier* h, const float* b, float* x, const octmg_solve_params* params,
                              octmg_solve_report* report, octmg_stream stream);
+
+/*
+ * Multigrid as a standalone solver (use beta = 1, "to prevent
+ * oscillations"): x_0 = 0, r_0 = b (masked, projected if nullspace), then
+ *   z_k = M r_k;  x_{k+1} = x_k + z_k;  r_{k+1} = r_k - A z_k
+ * until ||r_k|| <= rtol ||r_0|| (tested like Alg. 1 line 8).  M is the hierarchy's cycle
+ * (its mg params, including beta).  Same buffers, report and synchronisation as
+ * octmg_pcg_solve; report.iters = cycles applied.
+ */
+octmg_status octmg_mg_solve(octmg_hier* h, const float* b, float* x, const octmg_solve_params* params,
+                            octmg_solve_report* report, octmg_stream stream);
 
 /* Per-kernel-class device time of the work issued since the last reset while profiling
  * is on (CUDA events bracketing each launch on the launch stream; CUDA-graph replay is

@@ -140,7 +140,7 @@ struct Builder {
       push(Op{4, l, fas_first ? 1 : 0});
       return;
     }
-    if (l < T.L && fas_first && T.ic[l] > 0) push(Op{1, l, 0});
+    if (l < T.L && fas_first && T.ic[l] > 0 && h.prm.form == 0) push(Op{1, l, 0});
     const bool finest = l == T.L;
     if (l == 0) {
       int nb = h.prm.nu_coarsest;
@@ -260,7 +260,12 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
   a.glayer = T.glayer; a.u = ubuf(h); a.u2 = ubuf(h, 1); a.uc = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar;
   a.b = Fld{h.r, h.binner};
-  a.beta = h.prm.beta; a.alpha = h.prm.alpha; a.NL = T.NL;
+  a.alpha = h.prm.alpha; a.NL = T.NL;
+  // FAS form (Alg. 4): beta at restriction, prolongation of u^{l-1} - u*; standard form
+  // (Alg. 2): R r as the coarse rhs, zero coarse guess (u* = 0), beta at prolongation
+  a.std_form = h.prm.form == 1;
+  a.beta = a.std_form ? 1.0f : h.prm.beta;
+  a.pro_scale = a.std_form ? h.prm.beta : 1.0f;
   a.order = h.order + h.lvl_order_off[l];
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
@@ -545,17 +550,21 @@ octmg_status set_ownership(Hier& h, const PartPlan* P) {
 
 bool valid_params(const octmg_mg_params& prm) {
   return prm.alpha > 0.0f && prm.mu >= 1 && prm.mu <= 4 && prm.nu_pre >= 1 && prm.nu_post >= 1 &&
-         prm.nu_coarsest >= 1;
+         prm.nu_coarsest >= 1 && (prm.form == 0 || prm.form == 1) && (prm.coarsen_literal == 0 || prm.coarsen_literal == 1);
 }
 
 // a Group of `nparts` parts (1 = single GPU / one NCCL rank; >1 = loopback partition)
 octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void* nccl_comm, const uint8_t* kind,
                         const float* fbeta, const float* ffrac, const octmg_mg_params* params, cudaStream_t s,
                         octmg_hier** out) {
-  octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10};
+  octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10, 0, 0};
   if (params) prm = *params;
   if (!valid_params(prm)) {
-    set_error("invalid multigrid parameters (need alpha > 0, 1 <= mu <= 4, nu_* >= 1)");
+    set_error("invalid multigrid parameters (need alpha > 0, 1 <= mu <= 4, nu_* >= 1, form and coarsen_literal 0/1)");
+    return OCTMG_E_INVALID;
+  }
+  if (prm.form == 1 && tree->t.NL != tree->t.lc[tree->t.L]) {
+    set_error("the standard mu-cycle (Alg. 2, form = 1) needs a uniform tree (every leaf at the finest level)");
     return OCTMG_E_INVALID;
   }
   auto* hh = new (std::nothrow) octmg_hier();
@@ -852,6 +861,90 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     OCTMG_TRY(run_M(g, s));
     OCTMG_TRY(dot_rz());
     cur ^= 1;
+  }
+}
+
+// Multigrid as a standalone solver: x += M r, r -= A (M r).
+octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octmg_solve_params* params,
+                            octmg_solve_report* report, octmg_stream stream) {
+  if (!hh || !b || !x) { set_error("null argument"); return OCTMG_E_INVALID; }
+  Group& g = hh->g;
+  Hier& h0 = *g.parts[0];
+  cudaStream_t s = (cudaStream_t)stream;
+  octmg_solve_params prm{1e-6, 200, -1};
+  if (params) prm = *params;
+  if (!(prm.rtol > 0.0) || prm.max_iters < 1) { set_error("invalid solve parameters"); return OCTMG_E_INVALID; }
+  const bool ns = prm.nullspace < 0 ? !h0.any_dirichlet : prm.nullspace == 1;
+  const int G = vec_grid();
+  const int64_t launches0 = g.launches;
+  const int np = (int)g.parts.size();
+  Scalars* hs = h0.sc_host;
+  auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
+    if (report) {
+      report->iters = iters;
+      report->converged = conv ? 1 : 0;
+      report->rel_residual = rel;
+      report->bnorm = bn;
+      report->status = st;
+      report->kernel_launches = g.launches - launches0;
+    }
+    return st;
+  };
+  auto fetch = [&]() -> octmg_status {
+    OCTMG_CUDA(cudaMemcpyAsync(hs, h0.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    OCTMG_CUDA(cudaStreamSynchronize(s));
+    return OCTMG_OK;
+  };
+  auto project = [&]() -> octmg_status {
+    for (Hier* h : g.parts) {
+      ProfScope ps(*h, KC_PROJECT, s, (double)h->n_apply_tiles * TB3 * 8.125);
+      launch_project(h->r, h->act, h->own_cells, h->partial, h->counter + 1, h->sc, s, G);
+    }
+    g.launches += np;
+    return allreduce(g, SF_RR, 1, s);
+  };
+  for (Hier* h : g.parts) {
+    ProfScope ps(*h, KC_INIT, s, (double)h->n_apply_tiles * TB3 * 12.125);
+    launch_init(b, h->act, h->r, x, h->own_cells, h->partial, h->counter, h->sc, s, G);
+  }
+  g.launches += np;
+  OCTMG_TRY(allreduce(g, SF_RR, 2, s));
+  if (ns) OCTMG_TRY(project());
+  OCTMG_TRY(fetch());
+  if (!std::isfinite(hs->sum_rr)) { set_error("non-finite right-hand side"); return fill(OCTMG_E_NONFINITE, 0, false, 0, 0); }
+  const double bn = std::sqrt(hs->sum_rr);
+  if (bn == 0.0) return fill(OCTMG_OK, 0, true, 0.0, 0.0);
+  int k = 0;
+  double rel = 1.0;
+  while (true) {
+    OCTMG_TRY(run_M(g, s));  // z = M r (z = leaf part of the cycle's u)
+    for (Hier* h : g.parts) {
+      ApplyArgs a = apply_args(*h);
+      a.z = h->z;
+      a.pold = nullptr;
+      a.pnew = h->p0;  // z masked to the active cells
+      a.q = h->q;      // A z
+      a.partial = nullptr;
+      a.use_beta = 0;
+      ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 28.0);  // read z, record; write p, q
+      launch_apply(a, s);
+    }
+    g.launches += np;
+    for (Hier* h : g.parts) {
+      ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);
+      launch_update(x, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G, 1.0f);
+    }
+    g.launches += np;
+    OCTMG_TRY(allreduce(g, SF_RR, 2, s));
+    if (ns) OCTMG_TRY(project());
+    OCTMG_CUDA(cudaGetLastError());
+    OCTMG_TRY(fetch());
+    if (!std::isfinite(hs->sum_rr)) { set_error("non-finite residual"); return fill(OCTMG_E_NONFINITE, k, false, rel, bn); }
+    k++;
+    rel = std::sqrt(hs->sum_rr) / bn;
+    if (report && report->history && k - 1 < report->history_cap) report->history[k - 1] = rel;
+    if (rel <= prm.rtol) return fill(OCTMG_OK, k, true, rel, bn);
+    if (k >= prm.max_iters) { set_error("multigrid did not converge within max_iters"); return fill(OCTMG_E_MAXITER, k, false, rel, bn); }
   }
 }
 

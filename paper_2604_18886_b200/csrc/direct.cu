@@ -184,8 +184,8 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
     const int P = __ldg(a.parent + t);
     const int pc = pcell_of(tv, x0, y, z);
     const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
-    a.u.inner[pi] = mP;
-    a.ustar_w[pi] = mP;
+    a.u.inner[pi] = a.std_form ? 0.0f : mP;  // Alg. 2: zero coarse guess, u* = 0
+    a.ustar_w[pi] = a.std_form ? 0.0f : mP;
     a.b.inner[pi] = a.beta * (rs / a.alpha);
   }
 }
@@ -250,8 +250,8 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
     const int P = __ldg(a.parent + t);
     const int pc = pcell_of(tv, x0, y, z);
     const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
-    a.u.inner[pi] = mP;
-    a.ustar_w[pi] = mP;
+    a.u.inner[pi] = a.std_form ? 0.0f : mP;  // Alg. 2: zero coarse guess, u* = 0
+    a.ustar_w[pi] = a.std_form ? 0.0f : mP;
     a.b.inner[pi] = a.beta * (rs / a.alpha);
   }
 }
@@ -269,7 +269,8 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
   const float* uc = tptr(a.uc, P, a.NL);
   const float* us = a.ustar + (size_t)(P - a.NL) * TB3;
   const int pc0 = pcell_of(tv, x0, y, z), pc1 = pcell_of(tv, x0 + 2, y, z);
-  const float c0 = __ldg(uc + pc0) - __ldg(us + pc0), c1 = __ldg(uc + pc1) - __ldg(us + pc1);
+  const float c0 = a.pro_scale * (__ldg(uc + pc0) - __ldg(us + pc0));
+  const float c1 = a.pro_scale * (__ldg(uc + pc1) - __ldg(us + pc1));
   const float4 cc = __ldg(reinterpret_cast<const float4*>(a.coef + ((size_t)t << 11) + loff(x0, y, z)));
   if (cc.x != 0.0f) u.x += c0;
   if (cc.y != 0.0f) u.y += c0;

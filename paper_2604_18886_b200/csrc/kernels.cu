@@ -307,12 +307,13 @@ __global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* ac
 
 // x += alpha p, r -= alpha q with alpha = (r,z)/(p,Ap) (Alg. 1 lines 9-11); sums ||r||^2,
 // sum r.  The last block flags a breakdown and records rho = (r, z) for the next beta.
+// alpha_fixed != 0: that step length instead (standalone multigrid: x += z, r -= A z)
 __global__ __launch_bounds__(256) void k_update(float* x, float* r, const float* p, const float* q, Ranges R,
-                                                double* partial, unsigned* counter, Scalars* sc) {
+                                                double* partial, unsigned* counter, Scalars* sc, float alpha_fixed) {
   __shared__ double sred[8];
   const double pq = sc->sum_pq, rz = sc->sum_rz;
-  const bool ok = pq > 0.0 && isfinite(pq) && isfinite(rz);
-  const float alpha = ok ? (float)(rz / pq) : 0.0f;
+  const bool ok = alpha_fixed != 0.0f || (pq > 0.0 && isfinite(pq) && isfinite(rz));
+  const float alpha = alpha_fixed != 0.0f ? alpha_fixed : (ok ? (float)(rz / pq) : 0.0f);
   double s2 = 0.0, s1 = 0.0;
   FOR_RANGES(R, i) {
     float4 xv = reinterpret_cast<float4*>(x)[i];
@@ -419,8 +420,8 @@ void launch_init(const float* b, const uint32_t* act, float* r, float* x, const 
   k_init<<<grid, 256, 0, s>>>(b, act, r, x, R, partial, counter, sc);
 }
 void launch_update(float* x, float* r, const float* p, const float* q, const Ranges& R, double* partial,
-                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid) {
-  k_update<<<grid, 256, 0, s>>>(x, r, p, q, R, partial, counter, sc);
+                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid, float alpha_fixed) {
+  k_update<<<grid, 256, 0, s>>>(x, r, p, q, R, partial, counter, sc, alpha_fixed);
 }
 void launch_project(float* r, const uint32_t* act, const Ranges& R, double* partial, unsigned* counter, Scalars* sc,
                     cudaStream_t s, int grid) {

@@ -148,7 +148,7 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s);
 void launch_init(const float* b, const uint32_t* act, float* r, float* x, const Ranges& R, double* partial,
                  unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
 void launch_update(float* x, float* r, const float* p, const float* q, const Ranges& R, double* partial,
-                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
+                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid, float alpha_fixed = 0.0f);
 void launch_project(float* r, const uint32_t* act, const Ranges& R, double* partial, unsigned* counter,
                     Scalars* sc, cudaStream_t s, int grid);
 void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* partial, unsigned* counter,
@@ -171,7 +171,9 @@ struct SmoothArgs {
   const float* ustar;   // inner-indexed u* (prolongation)
   float* ustar_w;       // inner-indexed u* output (restrict stage)
   Fld b;                // leaf = PCG residual r, inner = FAS rhs
-  float beta, alpha;
+  float beta, alpha;    // restriction: b^{l-1} = beta R r, R = P^T / alpha
+  int std_form;         // Alg. 2: u^{l-1} := 0 and u* := 0 at restriction (no Avg, no FAS rhs)
+  float pro_scale;      // prolongation: u += pro_scale (u^{l-1} - u*) (Alg. 2: beta; Alg. 4: 1)
   int NL;
   const int* order;     // tiles of the level in rank order (slab-major)
   int n;                // tiles in the level
@@ -200,7 +202,7 @@ void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const 
 struct SetupArgs;
 octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
                                  cudaStream_t s);
-octmg_status coarsen_all(Hier& h, cudaStream_t s);
+octmg_status coarsen_all(Hier& h, cudaStream_t s);  // literal Alg. 3 if h.prm.coarsen_literal
 
 // tree build (tree.cu)
 octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, int64_t n, cudaStream_t s,

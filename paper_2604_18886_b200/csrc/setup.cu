@@ -161,6 +161,7 @@ struct CoarsenArgs {
   int NL;
   int toff;  // first inner tile of level l-1
   float alpha;
+  int literal;  // Alg. 3 as printed: no activity test on the non-diagonal branch
 };
 
 __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
@@ -192,7 +193,7 @@ __global__ __launch_bounds__(256) void k_coarsen(CoarsenArgs a) {
             } else {
               NbRef nb = nb_ref(a.nbr, ctv, ct, a.NL, cx[0], cx[1], cx[2], 2 * ax);
               bool nact = nb.what != NB_WALL && a.coef[cidx((size_t)nb.tile * TB3 + nb.off, 0)] != 0.0f;
-              if (act && nact) cIm[ax] += comp(ci, ax) / a.alpha;
+              if (a.literal || (act && nact)) cIm[ax] += comp(ci, ax) / a.alpha;
             }
           }
         }
@@ -260,7 +261,7 @@ octmg_status coarsen_all(Hier& h, cudaStream_t s) {
   for (int l = T.L; l >= 1; --l) {
     int lc = l - 1;
     if (T.ic[lc] == 0) continue;
-    CoarsenArgs a{T.tile, T.nbr, T.child, h.coef, T.NL, T.ib[lc], h.prm.alpha};
+    CoarsenArgs a{T.tile, T.nbr, T.child, h.coef, T.NL, T.ib[lc], h.prm.alpha, h.prm.coarsen_literal};
     k_coarsen<<<T.ic[lc], 256, 0, s>>>(a);
   }
   OCTMG_CUDA(cudaGetLastError());

@@ -161,8 +161,8 @@ __device__ __noinline__ void sc_restrict(const SubArgs& A, int l, unsigned& epoc
         const int4 tv = __ldg(a.tile + t);
         const int P = __ldg(a.parent + t);
         const size_t pi = (size_t)(P - a.NL) * TB3 + pcell_of(tv, x0, y, z);
-        a.u.inner[pi] = mP;
-        a.ustar_w[pi] = mP;
+        a.u.inner[pi] = a.std_form ? 0.0f : mP;  // Alg. 2: zero coarse guess, u* = 0
+        a.ustar_w[pi] = a.std_form ? 0.0f : mP;
         a.b.inner[pi] = a.beta * (rs / a.alpha);
       }
     }
@@ -205,7 +205,7 @@ __device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch
     const int P = __ldg(a.parent + t);
     const int pc = pcell_of(tv, off & 7, (off >> 3) & 7, off >> 6);
     float* up = tptr(a.u, t, a.NL) + off;
-    *up = ldv<M>(up) + (ldv<M>(tptr(a.uc, P, a.NL) + pc) - ldv<M>(a.ustar + (size_t)(P - a.NL) * TB3 + pc));
+    *up = ldv<M>(up) + a.pro_scale * (ldv<M>(tptr(a.uc, P, a.NL) + pc) - ldv<M>(a.ustar + (size_t)(P - a.NL) * TB3 + pc));
   }
   phase_end<GRID>(A, epoch);
 }
@@ -242,7 +242,7 @@ __device__ void sc_cycle(const SubArgs& A, int top, bool fas_first, unsigned& ep
         }
       }
       if (leaf_work) {
-        if (l < A.L && ff && A.ic[l] > 0) sc_fasrhs<GRID, M>(A, l, epoch);
+        if (l < A.L && ff && A.ic[l] > 0 && !A.a.std_form) sc_fasrhs<GRID, M>(A, l, epoch);
         const bool finest = l == A.L;
         if (l == 0) {
           sc_coarsest<GRID, M>(A, finest, epoch);

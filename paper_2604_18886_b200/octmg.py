@@ -39,7 +39,8 @@ class TreeInfo(C.Structure):
 
 class MGParams(C.Structure):
     _fields_ = [("alpha", C.c_float), ("beta", C.c_float), ("mu", C.c_int32), ("nu_pre", C.c_int32),
-                ("nu_post", C.c_int32), ("nu_coarsest", C.c_int32)]
+                ("nu_post", C.c_int32), ("nu_coarsest", C.c_int32), ("form", C.c_int32),
+                ("coarsen_literal", C.c_int32)]
 
 
 class SolveParams(C.Structure):
@@ -60,7 +61,7 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_vcycle", "octmg_pcg_solve", "octmg_profile_enable", "octmg_profile_read",
                "octmg_setup_hierarchy_loopback", "octmg_partition_info", "octmg_nccl_unique_id",
                "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
-               "octmg_hier_destroy", "octmg_tree_destroy"]
+               "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve"]
 
 _lib = None
 
@@ -83,6 +84,8 @@ def lib():
         L.octmg_apply.argtypes = [P, P, P, P]
         L.octmg_vcycle.argtypes = [P, P, P, P]
         L.octmg_pcg_solve.argtypes = [P, P, P, C.POINTER(SolveParams), C.POINTER(SolveReport), P]
+        L.octmg_mg_solve.argtypes = [P, P, P, C.POINTER(SolveParams), C.POINTER(SolveReport), P]
+        L.octmg_mg_solve.restype = C.c_int
         L.octmg_profile_enable.argtypes = [P, I32]
         L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
         L.octmg_setup_hierarchy_loopback.argtypes = [P, I32, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
@@ -206,9 +209,11 @@ class Hierarchy:
     """octmg_setup_hierarchy + the solver calls.  Device tensors (torch, cuda) in and out."""
 
     def __init__(self, tree: Tree, kind, face_beta=None, face_frac=None, alpha=2.0, beta=2.0, mu=1,
-                 nu_pre=2, nu_post=2, nu_coarsest=10, stream=None, loopback_parts: int = 0):
+                 nu_pre=2, nu_post=2, nu_coarsest=10, stream=None, loopback_parts: int = 0, form="fas",
+                 coarsen_literal=False):
         self.tree = tree
-        p = MGParams(alpha, beta, mu, nu_pre, nu_post, nu_coarsest)
+        p = MGParams(alpha, beta, mu, nu_pre, nu_post, nu_coarsest, {"fas": 0, "alg2": 1}[form],
+                     int(coarsen_literal))
         h = C.c_void_p()
         if loopback_parts:
             _check(lib().octmg_setup_hierarchy_loopback(tree._h, loopback_parts, _ptr(kind), _ptr(face_beta),
@@ -238,12 +243,22 @@ class Hierarchy:
 
     def pcg_solve(self, b, x, rtol=1e-6, max_iters=200, nullspace=-1, history_cap=256, stream=None,
                   raise_on_error=True):
+        return self._solve(lib().octmg_pcg_solve, b, x, rtol, max_iters, nullspace, history_cap, stream,
+                           raise_on_error)
+
+    def mg_solve(self, b, x, rtol=1e-6, max_iters=200, nullspace=-1, history_cap=256, stream=None,
+                 raise_on_error=True):
+        """octmg_mg_solve: multigrid as a standalone solver (set up the hierarchy with beta=1)."""
+        return self._solve(lib().octmg_mg_solve, b, x, rtol, max_iters, nullspace, history_cap, stream,
+                           raise_on_error)
+
+    def _solve(self, fn, b, x, rtol, max_iters, nullspace, history_cap, stream, raise_on_error):
         prm = SolveParams(rtol, max_iters, nullspace)
         hist = (C.c_double * max(history_cap, 1))()
         rep = SolveReport()
         rep.history = C.cast(hist, C.POINTER(C.c_double))
         rep.history_cap = history_cap
-        st = lib().octmg_pcg_solve(self._h, _ptr(b), _ptr(x), C.byref(prm), C.byref(rep), _stream(stream))
+        st = fn(self._h, _ptr(b), _ptr(x), C.byref(prm), C.byref(rep), _stream(stream))
         out = dict(iters=rep.iters, converged=bool(rep.converged), rel_residual=rep.rel_residual,
                    bnorm=rep.bnorm, status=STATUS.get(st, st), kernel_launches=int(rep.kernel_launches),
                    history=np.array(hist[:min(rep.iters, history_cap)]))
@@ -327,3 +342,7 @@ def octmg_vcycle(h: Hierarchy, b, u, stream=None):
 
 def octmg_pcg_solve(h: Hierarchy, b, x, **kw):
     return h.pcg_solve(b, x, **kw)
+
+
+def octmg_mg_solve(h: Hierarchy, b, x, **kw):
+    return h.mg_solve(b, x, **kw)

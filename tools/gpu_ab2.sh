@@ -1,1 +1,4 @@
-for V in fused fused_noshell split; do OCTMG_RB=$V python tools/time_vcycle.py 2>&1 | grep -E "rbgs|total|coarse"; done
+timeout 1200 python -m pytest tests -x -q -m "gpu and not slow" 2>&1 | tail -4
+timeout 900 python tools/ab_inproc.py cfg2_uniform256 '' 'OCTMG_SUBCYCLE_GLOBAL=1' 'OCTMG_RB=fused_coarse' 'OCTMG_GRID=1,OCTMG_GRID_TILES=600'
+timeout 900 python tools/ab_inproc.py cfg1_octant '' 'OCTMG_SUBCYCLE_GLOBAL=1'
+timeout 1500 python tools/ab_inproc.py cfg4_tank '' 'OCTMG_SUBCYCLE_GLOBAL=1' 'OCTMG_RB=fused_coarse' 'OCTMG_GRID=1' 'OCTMG_GRID=1,OCTMG_GRID_TILES=600'
