@@ -7,7 +7,8 @@
 // stencil (Eqs. 9-12), Galerkin coarsening (Alg. 3), RBGS
 // (L407-409), the FAS-style mu-cycle (Alg. 4), the standard mu-cycle
 // (Alg. 2, used only as an equivalence check on uniform trees), PCG
-// (Alg. 1) and multigrid as a standalone solver (L145, L411).  Readings of silent/ambiguous passages follow SURVEY.md
+// (Alg. 1), multigrid as a standalone solver (L145, L411) and the cut-cell
+// geometry of the tank scene (L1605-1616, L1924).  Readings of silent/ambiguous passages follow SURVEY.md
 // 8(c) and are listed in DESIGN.md "Readings".
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
@@ -833,6 +834,108 @@ int mg_solve(Oracle& o, const MG& p, bool fas_form, const double* bin, double* x
   }
 }
 
+// -------------------------------------------------------------------------------------
+// Cut-cell geometry of the static tank scene ("signed distance
+// values are evaluated at cell corners"; fluid face fractions by marching
+// squares, ghost-fluid classification from the cell-centre SDF).  phi < 0 is solid.
+// -------------------------------------------------------------------------------------
+double sphere_phi(const double p[3], const double c[3], double r) {
+  double dx = p[0] - c[0], dy = p[1] - c[1], dz = p[2] - c[2];
+  return std::sqrt(dx * dx + dy * dy + dz * dz) - r;
+}
+
+// fluid (phi >= 0) area fraction of a unit square from its corner samples in cyclic order
+// (0,0),(1,0),(1,1),(0,1): the polygon of fluid corners and linear edge crossings, area by
+// the shoelace formula; the saddle (diagonal corners alike, neighbours opposite) with a
+// solid face centre is two separate fluid corner triangles.
+double face_fraction(const double phi[4], double phi_centre) {
+  static const double P[4][2] = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+  bool fl[4];
+  for (int k = 0; k < 4; ++k) fl[k] = phi[k] >= 0.0;
+  const bool saddle = fl[0] == fl[2] && fl[1] == fl[3] && fl[0] != fl[1];
+  if (saddle && phi_centre < 0.0) {
+    double area = 0.0;
+    for (int k = 0; k < 4; ++k) {
+      if (!fl[k]) continue;
+      int nx = (k + 1) % 4, pv = (k + 3) % 4;
+      double a = phi[k] / (phi[k] - phi[nx]);
+      double b = phi[k] / (phi[k] - phi[pv]);
+      area += 0.5 * a * b;
+    }
+    return std::min(1.0, std::max(0.0, area));
+  }
+  double pts[8][2];
+  int n = 0;
+  for (int e = 0; e < 4; ++e) {
+    int a = e, b = (e + 1) % 4;
+    if (fl[a]) { pts[n][0] = P[a][0]; pts[n][1] = P[a][1]; ++n; }
+    if (fl[a] != fl[b]) {
+      double t = phi[a] / (phi[a] - phi[b]);
+      pts[n][0] = P[a][0] + t * (P[b][0] - P[a][0]);
+      pts[n][1] = P[a][1] + t * (P[b][1] - P[a][1]);
+      ++n;
+    }
+  }
+  double area = 0.0;
+  for (int k = 0; k < n; ++k) {
+    int k1 = (k + 1) % n;
+    area += pts[k][0] * pts[k1][1] - pts[k1][0] * pts[k][1];
+  }
+  return std::min(1.0, std::max(0.0, 0.5 * std::fabs(area)));
+}
+
+// kind, face weights and right-hand side of every leaf cell of the tank scene: solid
+// sphere obstacle (centre c, radius r; r <= 0: none) -> Neumann cells where phi(centre) <
+// 0; face weight = fluid fraction of the face from its 4 corner samples; tank walls solid
+// (w = 0) except the open top y = ext_y (w = 1); b = h^2 (w_y+ - w_y-) on fluid cells
+// (unit downward velocity, volume-integrated divergence).  tiles: canonical leaf order.
+void tank_fields(const int32_t* tiles, int64_t n, int B, const double* ext, const double* c, double r,
+                 uint8_t* kind, float* w, float* bout) {
+  const int64_t B3 = (int64_t)B * B * B, N = n * B3;
+  for (int64_t t = 0; t < n; ++t) {
+    const int l = tiles[4 * t];
+    const double h = std::ldexp(1.0, -l) / B;
+    for (int64_t off = 0; off < B3; ++off) {
+      const int64_t i = t * B3 + off;
+      const int64_t X = (int64_t)tiles[4 * t + 1] * B + off % B;
+      const int64_t Y = (int64_t)tiles[4 * t + 2] * B + (off / B) % B;
+      const int64_t Z = (int64_t)tiles[4 * t + 3] * B + off / (B * B);
+      const double cen[3] = {(X + 0.5) * h, (Y + 0.5) * h, (Z + 0.5) * h};
+      const bool solid = r > 0.0 && sphere_phi(cen, c, r) < 0.0;
+      kind[i] = solid ? K_NEUMANN : K_FLUID;
+      double wf[6];
+      for (int f = 0; f < 6; ++f) {
+        const int a = f / 2, side = f % 2;
+        const int o1 = a == 0 ? 1 : 0, o2 = a == 2 ? 1 : 2;
+        double pc[3] = {cen[0], cen[1], cen[2]};
+        pc[a] += (side - 0.5) * h;
+        double frac = 1.0;
+        if (r > 0.0) {
+          static const int U[4] = {-1, 1, 1, -1}, V[4] = {-1, -1, 1, 1};
+          double phi[4];
+          for (int k = 0; k < 4; ++k) {
+            double q[3] = {pc[0], pc[1], pc[2]};
+            q[o1] += 0.5 * U[k] * h;
+            q[o2] += 0.5 * V[k] * h;
+            phi[k] = sphere_phi(q, c, r);
+          }
+          frac = face_fraction(phi, sphere_phi(pc, c, r));
+        }
+        const bool lo = pc[a] <= 0.0, hi = pc[a] >= ext[a];
+        if (a == 1) {
+          if (lo) frac = 0.0;
+          if (hi) frac = 1.0;
+        } else if (lo || hi) {
+          frac = 0.0;
+        }
+        wf[f] = (double)(float)frac;
+        w[(size_t)f * N + i] = (float)frac;
+      }
+      bout[i] = solid ? 0.0f : (float)(h * h * (wf[3] - wf[2]));
+    }
+  }
+}
+
 MG mg_from(const double* prm) {
   MG p;
   if (prm) {
@@ -944,6 +1047,13 @@ int32_t orc_mg_solve(void* h, const double* prm, int32_t form, const double* b, 
                     hist, hcap);
   *iters = it;
   return st;
+}
+
+double orc_face_fraction(const double* phi4, double phi_centre) { return face_fraction(phi4, phi_centre); }
+
+void orc_tank_fields(const int32_t* tiles, int64_t n, int32_t B, const double* ext, const double* centre,
+                     double radius, uint8_t* kind, float* w, float* b) {
+  tank_fields(tiles, n, B, ext, centre, radius, kind, w, b);
 }
 
 }  // extern "C"

@@ -53,6 +53,9 @@ def lib():
         _lib.orc_vcycle.argtypes = [P, P, P, P, I32]
         _lib.orc_pcg.restype = I32
         _lib.orc_pcg.argtypes = [P, P, I32, P, P, D, I32, I32, P, P, P, P, I32]
+        _lib.orc_face_fraction.restype = D
+        _lib.orc_face_fraction.argtypes = [P, D]
+        _lib.orc_tank_fields.argtypes = [P, I64, I32, P, P, D, P, P, P]
         _lib.orc_mg_solve.restype = I32
         _lib.orc_mg_solve.argtypes = [P, P, I32, P, P, D, I32, I32, P, P, P, P, I32]
     return _lib
@@ -60,6 +63,25 @@ def lib():
 
 def _p(a):
     return a.ctypes.data_as(C.c_void_p)
+
+
+def face_fraction(phi4, phi_centre):
+    """Fluid (phi >= 0) area fraction of a unit face from corner samples (cyclic order)."""
+    a = np.ascontiguousarray(phi4, dtype=np.float64)
+    return lib().orc_face_fraction(_p(a), float(phi_centre))
+
+
+def tank_fields(tiles_sorted, ext=(1, 1, 1), centre=(0.5, 0.5, 0.5), radius=0.3, B: int = 8):
+    """Oracle cut-cell fields of the tank scene: kind u8[N], w f32[6][N], b f32[N]."""
+    t = np.ascontiguousarray(np.asarray(tiles_sorted, dtype=np.int32).reshape(-1, 4))
+    N = len(t) * B ** 3
+    kind = np.zeros(N, dtype=np.uint8)
+    w = np.zeros((6, N), dtype=np.float32)
+    b = np.zeros(N, dtype=np.float32)
+    e = np.asarray(ext, dtype=np.float64)
+    c = np.asarray(centre, dtype=np.float64)
+    lib().orc_tank_fields(_p(t), len(t), B, _p(e), _p(c), float(radius), _p(kind), _p(w), _p(b))
+    return kind, w, b
 
 
 class OracleError(RuntimeError):
