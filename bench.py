@@ -40,6 +40,8 @@ WORKLOADS = {
     "cfg3_sphere": "BASELINE config 3: sphere band l0=4..7 (60.1M leaves), paper Sec. 5.3 setup",
     "uniform128": "uniform 128^3 (paper Table 1 uniform (4-4)), Sec. 5.3 setup",
     "tank_mid": "cut-cell tank, sphere obstacle r=0.3, levels 3..5, W-cycle mu=2",
+    "cfg4_tank": "BASELINE config 4: cut-cell tank, sphere obstacle r=0.30, l0=4..8 (155.2M leaves), W-cycle mu=2",
+    "cfg5_tank": "BASELINE config 5: cut-cell tank, sphere obstacle r=0.35, l0=4..9 (838.8M leaves), W-cycle mu=2",
 }
 CPU_SAMPLE = "uniform64"  # same recipe as cfg2 at 64^3: the bounded oracle sample
 
@@ -192,14 +194,24 @@ def main():
     from octgen import make_config
     assert args.warmup >= 3 or os.environ.get("BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
 
-    cfg = make_config(args.config)
+    # cut-cell tank configs: the fields come from the device geometry pipeline
+    # (octmg_tank_fields, parity-tested against the oracle); the others from octgen
+    cfg = make_config(args.config, with_fields=False)
+    tank = cfg["bc"] == "tank"
+    if not tank:
+        cfg = make_config(args.config)
     partitioned = world > 1 and not args.replicas
     comm = om.NcclComm(rank, world) if partitioned else None
     tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"], comm=comm)
-    kind = torch.from_numpy(cfg["kind"]).to(dev)
-    frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(dev)
+    if tank:
+        kind, frac, b = om.tank_fields(tree, (0.5, 0.5, 0.5), cfg["radius"])
+        b_host = b.cpu().pin_memory()
+    else:
+        kind = torch.from_numpy(cfg["kind"]).to(dev)
+        frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(dev)
+        b_host = torch.from_numpy(cfg["b"]).pin_memory()
     h = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
-    b_host = torch.from_numpy(cfg["b"]).pin_memory()
+    del frac
     b = b_host.to(dev)
     x = torch.zeros_like(b)
     x_host = torch.empty_like(b_host).pin_memory()

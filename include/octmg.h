@@ -179,6 +179,21 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
                                        int32_t* owner_out, int32_t* n_items_out, int32_t* items_out,
                                        int64_t items_cap);
 
+/*
+ * Cut-cell fields of the static tank scene: a solid sphere
+ * obstacle (centre, radius in level-0 tile units; radius <= 0: none) in a tank with solid
+ * bottom and side walls and an open top y = ext_y.  For every leaf cell (leaf-slot order),
+ * on the device: kind (2 Neumann/solid where the SDF phi = |x - centre| - radius < 0 at the
+ * cell centre, else 0 fluid; ghost-fluid classification P:L318-320), face_frac[6][N] the
+ * fluid area fraction of each face from the SDF sampled at its 4 corners by
+ * marching squares, a saddle split when the face-centre sample is solid;
+ * tank walls 0, the open top 1; and b = h^2 (w_y+ - w_y-) on fluid cells (0 on solid),
+ * the volume-integrated divergence of a unit downward velocity.  fp64 arithmetic, fp32
+ * outputs.  kind, face_frac, b: device buffers of N, 6N, N elements (caller-owned).
+ */
+octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind,
+                               float* face_frac, float* b, octmg_stream stream);
+
 /* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
  * in tile order.  Synchronises `stream` of the last call. */
 octmg_status octmg_hier_export_coefs(const octmg_hier* h, float* host_dst, size_t bytes);

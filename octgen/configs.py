@@ -48,7 +48,7 @@ def make_config(name: str, rhs: str = "default", seed: int = 0, with_fields: boo
     tiles = gen()
     tiles = tiles[canonical_order(tiles)]
     walls = {"dirichlet": DIRICHLET_WALLS, "neumann_layer": NEUMANN_WALLS, "tank": TANK_WALLS}[bc]
-    cfg = dict(name=name, tiles=tiles, ext=(1, 1, 1), wall_bc=walls, mu=mu, bc=bc,
+    cfg = dict(name=name, tiles=tiles, ext=(1, 1, 1), wall_bc=walls, mu=mu, bc=bc, radius=radius,
                n_cells=len(tiles) * 512, kind=None, w=None, b=None)
     if not with_fields:
         return cfg

@@ -37,7 +37,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         for src in SOURCES:
             obj = os.path.join(objdir, os.path.basename(src) + ".o")
             objs.append(obj)
-            cmds.append([nvcc] + cflags + ["-c", "-o", obj, src])
+            extra = ["-fmad=false"] if os.path.basename(src) == "geometry.cu" else []  # fp64 SDF = oracle's IEEE ops
+            cmds.append([nvcc] + cflags + extra + ["-c", "-o", obj, src])
         if verbose:
             for c in cmds:
                 print(" ".join(c))

@@ -172,11 +172,16 @@ void read_env(Hier& h) {
   const char* rv = getenv("OCTMG_RESTRICT_V");
   h.restrict_v2 = !(rv && std::string(rv) == "1");  // k_restrict_v2 (vectorised regular tiles) by default
   const Tree& T = *h.tree;
+  const char* gv = getenv("OCTMG_GRID");
+  const bool grid = gv && std::string(gv) == "1";
   const char* sc = getenv("OCTMG_SUBCYCLE");
+  // the grid kernel's CTA-0 tail is the one-CTA sub-cycle, so then its levels must fit one CTA
+  h.sub_ctas = grid ? 1 : subcycle_ctas();
+  const int sub_cap = subcycle_max_tiles(h.sub_ctas);
   h.sub_K = -1;
   if (!(sc && std::string(sc) == "0"))
     for (int l = 0; l <= std::min(T.L, subcycle_max_level()); ++l) {
-      if (h.lvl_n[l] > subcycle_max_tiles()) break;
+      if (h.lvl_n[l] > sub_cap) break;
       if (h.nranks > 1 && l >= h.lg) break;  // only replicated levels run on chip
       h.sub_K = l;
     }
@@ -184,8 +189,7 @@ void read_env(Hier& h) {
   // per-level launches on config 2): every level below the finest from grid_K down fits it
   // (OCTMG_GRID_TILES caps the tiles per level)
   h.grid_K = -1;
-  const char* gv = getenv("OCTMG_GRID");
-  const int nb = (gv && std::string(gv) == "1") ? coarse_grid_blocks() : 0;
+  const int nb = grid ? coarse_grid_blocks() : 0;
   if (nb > 0) {
     const char* gt = getenv("OCTMG_GRID_TILES");
     const int cap = std::min(coarse_grid_max_tiles(nb), gt ? atoi(gt) : 1 << 30);
@@ -295,7 +299,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   }
   if (op.kind == 4) {
     ProfScope ps(h, KC_SUBCYCLE, s, 0.0);
-    launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, s);
+    launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, h.sub_ctas, s);
     return;
   }
   if (op.kind == 3) {
@@ -707,6 +711,12 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
   }
   if (k > 2 * items_cap) { set_error("items buffer too small"); return OCTMG_E_INVALID; }
   return OCTMG_OK;
+}
+
+octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind,
+                               float* face_frac, float* b, octmg_stream stream) {
+  if (!tree || !centre3 || !kind || !face_frac || !b) { set_error("null argument"); return OCTMG_E_INVALID; }
+  return tank_fields(tree->t, centre3, radius, kind, face_frac, b, (cudaStream_t)stream);
 }
 
 octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size_t bytes) {

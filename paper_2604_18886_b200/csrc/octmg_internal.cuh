@@ -186,7 +186,8 @@ void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, bool v2);
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
 void launch_rb_fused(const SmoothArgs& a, bool zero, cudaStream_t s, bool shell = true);
 void launch_copy_level(const SmoothArgs& a, cudaStream_t s);
-int subcycle_max_tiles();
+int subcycle_ctas();
+int subcycle_max_tiles(int ctas);
 int subcycle_max_level();
 int coarse_grid_max_level();
 int coarse_grid_max_tiles(int nblocks);
@@ -196,13 +197,17 @@ cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int
                                const int* lvl_n, const int* ib, const int* ic, unsigned* bar, cudaStream_t s);
 void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
                      const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
-                     cudaStream_t s);
+                     int ctas, cudaStream_t s);
 
 // setup kernels (setup.cu)
 struct SetupArgs;
 octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
                                  cudaStream_t s);
 octmg_status coarsen_all(Hier& h, cudaStream_t s);  // literal Alg. 3 if h.prm.coarsen_literal
+
+// cut-cell geometry of the tank scene (geometry.cu)
+octmg_status tank_fields(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac, float* b,
+                         cudaStream_t s);
 
 // tree build (tree.cu)
 octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, int64_t n, cudaStream_t s,
@@ -254,6 +259,7 @@ struct Hier {
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
   bool restrict_v2 = true;       // k_restrict_v2: vectorised regular tiles (OCTMG_RESTRICT_V=1: staged k_restrict_direct)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
+  int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
   unsigned* bar = nullptr;       // its grid barrier counter
   int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes

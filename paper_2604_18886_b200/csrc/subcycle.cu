@@ -3,6 +3,8 @@
 //
 //  * k_subcycle: one CTA of 1024 threads, phases separated by __syncthreads; for the
 //    smallest levels (<= 16 tiles each, 8K cells), whose data stays in L1/L2.
+//    k_subcycle_cluster (OCTMG_SUBCYCLE_CTAS=8): the same spread over one thread-block
+//    cluster of 8 CTAs with the hardware cluster barrier (<= 128 tiles per level).
 //  * k_coarse_grid: a persistent cooperative grid (one 1024-thread CTA per SM, co-resident
 //    by cooperative launch) for the levels below the finest ones (up to a few thousand
 //    tiles each, L2-resident): every phase is spread over all CTAs and ends with a grid
@@ -15,6 +17,8 @@
 // between its reads and writes (it reads other tiles' cells of the other colour only).
 // Loads of mutable data: plain in the one-CTA kernel (M = 0), L2-only (__ldcg, M = 2) in
 // the grid kernel, where other CTAs wrote them before a grid barrier.
+#include <cstdlib>
+
 #include "stencil.cuh"
 
 namespace octmg {
@@ -26,6 +30,7 @@ constexpr int SUB_MAXL = 4;
 constexpr int SUB_MAX_PER_THREAD = 4;   // colour cells per thread of the one-CTA kernel
 constexpr int GRID_MAX_PER_THREAD = 8;  // colour cells per thread of the grid kernel
 constexpr int GRID_MAXL = 10;
+constexpr int SUB_CLUSTER = 8;          // CTAs of the sub-cycle cluster (portable maximum)
 
 struct SubArgs {
   SmoothArgs a;
@@ -40,11 +45,19 @@ struct SubArgs {
   unsigned* bar;         // grid barrier counter (zeroed before the launch)
 };
 
-// phase extent: all threads of the grid (GRID) or of this CTA
-template <bool GRID>
-__device__ __forceinline__ int ph_tid() { return GRID ? blockIdx.x * SUB_THREADS + threadIdx.x : threadIdx.x; }
-template <bool GRID>
-__device__ __forceinline__ int ph_nthreads() { return GRID ? gridDim.x * SUB_THREADS : SUB_THREADS; }
+// Phase modes: PM 0 = one CTA (__syncthreads), 1 = cooperative grid (global barrier),
+// 2 = one thread-block cluster (hardware cluster barrier).  Phase extent: all threads of the
+// launch (PM 1, 2: the grid is one cluster / the co-resident grid) or of this CTA.
+template <int PM>
+__device__ __forceinline__ int ph_tid() { return PM ? blockIdx.x * SUB_THREADS + threadIdx.x : threadIdx.x; }
+template <int PM>
+__device__ __forceinline__ int ph_nthreads() { return PM ? gridDim.x * SUB_THREADS : SUB_THREADS; }
+
+// cluster barrier with release/acquire semantics at cluster scope: writes of every CTA of
+// the cluster before it are visible to every CTA after it
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 
 // grid barrier: monotonic arrival counter, barrier k waits for k * gridDim arrivals
 __device__ __forceinline__ void grid_barrier(const SubArgs& A, unsigned& epoch) {
@@ -61,22 +74,23 @@ __device__ __forceinline__ void grid_barrier(const SubArgs& A, unsigned& epoch) 
   __syncthreads();
 }
 
-template <bool GRID>
+template <int PM>
 __device__ __forceinline__ void phase_end(const SubArgs& A, unsigned& epoch) {
-  if (GRID) grid_barrier(A, epoch);
+  if (PM == 1) grid_barrier(A, epoch);
+  else if (PM == 2) cluster_barrier();
   else __syncthreads();
 }
 
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ __noinline__ void sc_pass(const SubArgs& A, int l, int colour, int mode, unsigned& epoch) {
-  constexpr int MAXK = GRID ? GRID_MAX_PER_THREAD : SUB_MAX_PER_THREAD;
+  constexpr int MAXK = PM == 1 ? GRID_MAX_PER_THREAD : SUB_MAX_PER_THREAD;
   const SmoothArgs& a = A.a;
   const int* ord = A.order_all + A.lvl_off[l];
   const int ncell = A.lvl_n[l] * 256;
   float unew[MAXK];
   float* dst[MAXK];
   int k = 0;
-  for (int s = ph_tid<GRID>(); s < ncell && k < MAXK; s += ph_nthreads<GRID>(), ++k) {
+  for (int s = ph_tid<PM>(); s < ncell && k < MAXK; s += ph_nthreads<PM>(), ++k) {
     const int t = __ldg(ord + (s >> 8));
     const int j = s & 255;
     const int y = (j >> 2) & 7, z = j >> 5;
@@ -109,27 +123,27 @@ __device__ __noinline__ void sc_pass(const SubArgs& A, int l, int colour, int mo
   __syncthreads();  // all pass-start reads of each tile (one CTA per tile) before the writes
   for (int i = 0; i < k; ++i)
     if (dst[i]) *dst[i] = unew[i];
-  phase_end<GRID>(A, epoch);
+  phase_end<PM>(A, epoch);
 }
 
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ void sc_passes(const SubArgs& A, int l, int iters, bool red_first, int m1, int m2, unsigned& epoch) {
   for (int k = 0; k < iters; ++k) {
-    sc_pass<GRID, M>(A, l, red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN, epoch);
-    sc_pass<GRID, M>(A, l, red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN, epoch);
+    sc_pass<PM, M>(A, l, red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN, epoch);
+    sc_pass<PM, M>(A, l, red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN, epoch);
   }
 }
 
 // residual + restriction + Avg of level l into level l-1 (k_restrict_direct's arithmetic);
 // groups of 256 threads own one tile at a time
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ __noinline__ void sc_restrict(const SubArgs& A, int l, unsigned& epoch) {
   const SmoothArgs& a = A.a;
   const int* ord = A.order_all + A.lvl_off[l];
   const int n = A.lvl_n[l];
-  const int ngrp = ph_nthreads<GRID>() / 256;
+  const int ngrp = ph_nthreads<PM>() / 256;
   for (int t0 = 0; t0 < n; t0 += ngrp) {
-    const int ti = t0 + ph_tid<GRID>() / 256;
+    const int ti = t0 + ph_tid<PM>() / 256;
     if (ti < n) {  // uniform per 256-thread group, so the shuffles below are converged
       const int t = __ldg(ord + ti);
       const int j = threadIdx.x & 255;
@@ -167,15 +181,15 @@ __device__ __noinline__ void sc_restrict(const SubArgs& A, int l, unsigned& epoc
       }
     }
   }
-  phase_end<GRID>(A, epoch);
+  phase_end<PM>(A, epoch);
 }
 
 // b_I = beta R r (in b) + (A^l u*)_I on the inner rows of level l (Alg. 4 line 10)
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ __noinline__ void sc_fasrhs(const SubArgs& A, int l, unsigned& epoch) {
   const SmoothArgs& a = A.a;
   const int ncell = A.ic[l] * TB3;
-  for (int s = ph_tid<GRID>(); s < ncell; s += ph_nthreads<GRID>()) {
+  for (int s = ph_tid<PM>(); s < ncell; s += ph_nthreads<PM>()) {
     const int t = A.ib[l] + (s >> 9);
     const int off = s & 511;
     const int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
@@ -188,16 +202,16 @@ __device__ __noinline__ void sc_fasrhs(const SubArgs& A, int l, unsigned& epoch)
       *bi = 0.0f;
     }
   }
-  phase_end<GRID>(A, epoch);
+  phase_end<PM>(A, epoch);
 }
 
 // u += P (u^{l-1} - u*) on the active cells of level l (Alg. 4 line 15)
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch) {
   const SmoothArgs& a = A.a;
   const int* ord = A.order_all + A.lvl_off[l];
   const int ncell = A.lvl_n[l] * TB3;
-  for (int s = ph_tid<GRID>(); s < ncell; s += ph_nthreads<GRID>()) {
+  for (int s = ph_tid<PM>(); s < ncell; s += ph_nthreads<PM>()) {
     const int t = __ldg(ord + (s >> 9));
     const int off = s & 511;
     if (ldcoef(a.coef, (size_t)t * TB3 + off).x == 0.0f) continue;
@@ -207,22 +221,22 @@ __device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch
     float* up = tptr(a.u, t, a.NL) + off;
     *up = ldv<M>(up) + a.pro_scale * (ldv<M>(tptr(a.uc, P, a.NL) + pc) - ldv<M>(a.ustar + (size_t)(P - a.NL) * TB3 + pc));
   }
-  phase_end<GRID>(A, epoch);
+  phase_end<PM>(A, epoch);
 }
 
 // smoothing at the coarsest level: nu_b/2 x (R,B) then nu_b/2 x (B,R)
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ void sc_coarsest(const SubArgs& A, bool finest, unsigned& epoch) {
   const int h1 = A.nu_coarsest / 2;
-  sc_passes<GRID, M>(A, 0, h1, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN, epoch);
+  sc_passes<PM, M>(A, 0, h1, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN, epoch);
   const bool zz = finest && h1 == 0;
-  sc_passes<GRID, M>(A, 0, A.nu_coarsest - h1, false, zz ? SM_ZERO1 : SM_PLAIN, zz ? SM_ZERO2 : SM_PLAIN, epoch);
+  sc_passes<PM, M>(A, 0, A.nu_coarsest - h1, false, zz ? SM_ZERO1 : SM_PLAIN, zz ? SM_ZERO2 : SM_PLAIN, epoch);
 }
 
 // Alg. 4 from level `top` down, iteratively (explicit per-level count of the mu coarse
-// calls made; every thread runs the same control flow).  GRID: levels <= A.sK run in CTA 0
+// calls made; every thread runs the same control flow).  PM 1: levels <= A.sK run in CTA 0
 // alone (the one-CTA version of this function) while the other CTAs wait at a barrier.
-template <bool GRID, int M>
+template <int PM, int M>
 __device__ void sc_cycle(const SubArgs& A, int top, bool fas_first, unsigned& epoch) {
   int done[GRID_MAXL + 1];
   int l = top;
@@ -231,25 +245,25 @@ __device__ void sc_cycle(const SubArgs& A, int top, bool fas_first, unsigned& ep
   while (true) {
     if (entering) {
       bool leaf_work = true;
-      if constexpr (GRID) {
+      if constexpr (PM == 1) {
         if (l <= A.sK) {
           if (blockIdx.x == 0) {
             unsigned dummy = 0;
-            sc_cycle<false, M>(A, l, ff, dummy);
+            sc_cycle<0, M>(A, l, ff, dummy);
           }
           grid_barrier(A, epoch);
           leaf_work = false;
         }
       }
       if (leaf_work) {
-        if (l < A.L && ff && A.ic[l] > 0 && !A.a.std_form) sc_fasrhs<GRID, M>(A, l, epoch);
+        if (l < A.L && ff && A.ic[l] > 0 && !A.a.std_form) sc_fasrhs<PM, M>(A, l, epoch);
         const bool finest = l == A.L;
         if (l == 0) {
-          sc_coarsest<GRID, M>(A, finest, epoch);
+          sc_coarsest<PM, M>(A, finest, epoch);
         } else {
-          sc_passes<GRID, M>(A, l, A.nu_pre, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN,
+          sc_passes<PM, M>(A, l, A.nu_pre, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN,
                              epoch);
-          sc_restrict<GRID, M>(A, l, epoch);
+          sc_restrict<PM, M>(A, l, epoch);
           done[l] = 0;
           l -= 1;
           ff = true;
@@ -266,20 +280,27 @@ __device__ void sc_cycle(const SubArgs& A, int top, bool fas_first, unsigned& ep
       entering = true;
       continue;
     }
-    sc_prolong<GRID, M>(A, p, epoch);
-    sc_passes<GRID, M>(A, p, A.nu_post, false, SM_PLAIN, SM_PLAIN, epoch);
+    sc_prolong<PM, M>(A, p, epoch);
+    sc_passes<PM, M>(A, p, A.nu_post, false, SM_PLAIN, SM_PLAIN, epoch);
     l = p;  // level p finished
   }
 }
 
 __global__ __launch_bounds__(SUB_THREADS, 1) void k_subcycle(SubArgs A) {
   unsigned e = 0;
-  sc_cycle<false, 0>(A, A.K, A.fas_first != 0, e);
+  sc_cycle<0, 0>(A, A.K, A.fas_first != 0, e);
+}
+
+// the sub-cycle spread over one cluster of SUB_CLUSTER CTAs (one per SM); mutable data are
+// read through L2 (M = 2) since the CTAs of the cluster run on different SMs
+__global__ __launch_bounds__(SUB_THREADS, 1) void k_subcycle_cluster(SubArgs A) {
+  unsigned e = 0;
+  sc_cycle<2, 2>(A, A.K, A.fas_first != 0, e);
 }
 
 __global__ __launch_bounds__(SUB_THREADS, 1) void k_coarse_grid(SubArgs A) {
   unsigned e = 0;
-  sc_cycle<true, 2>(A, A.K, A.fas_first != 0, e);
+  sc_cycle<1, 2>(A, A.K, A.fas_first != 0, e);
 }
 
 SubArgs make_args(const SmoothArgs& base, int L, int K, int sK, int fas_first, const octmg_mg_params& prm,
@@ -307,7 +328,13 @@ SubArgs make_args(const SmoothArgs& base, int L, int K, int sK, int fas_first, c
 
 }  // namespace
 
-int subcycle_max_tiles() { return SUB_THREADS * SUB_MAX_PER_THREAD / 256; }
+// CTAs of the sub-cycle: 1 (default) or a cluster of SUB_CLUSTER (OCTMG_SUBCYCLE_CTAS=8;
+// measured slower: every phase then reads through L2)
+int subcycle_ctas() {
+  const char* e = getenv("OCTMG_SUBCYCLE_CTAS");
+  return (e && atoi(e) > 1) ? SUB_CLUSTER : 1;
+}
+int subcycle_max_tiles(int ctas) { return ctas * SUB_THREADS * SUB_MAX_PER_THREAD / 256; }
 int subcycle_max_level() { return SUB_MAXL; }
 int coarse_grid_max_level() { return GRID_MAXL; }
 
@@ -328,9 +355,24 @@ int coarse_grid_blocks() {
 
 void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
                      const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
-                     cudaStream_t s) {
+                     int ctas, cudaStream_t s) {
   SubArgs A = make_args(base, L, K, -1, fas_first, prm, order_all, lvl_off, lvl_n, ib, ic);
-  k_subcycle<<<1, SUB_THREADS, 0, s>>>(A);
+  if (ctas <= 1) {
+    k_subcycle<<<1, SUB_THREADS, 0, s>>>(A);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(SUB_CLUSTER);
+  cfg.blockDim = dim3(SUB_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = SUB_CLUSTER;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_subcycle_cluster, A);
 }
 
 cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int fas_first,

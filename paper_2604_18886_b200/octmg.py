@@ -61,7 +61,7 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_vcycle", "octmg_pcg_solve", "octmg_profile_enable", "octmg_profile_read",
                "octmg_setup_hierarchy_loopback", "octmg_partition_info", "octmg_nccl_unique_id",
                "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
-               "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve"]
+               "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields"]
 
 _lib = None
 
@@ -86,6 +86,8 @@ def lib():
         L.octmg_pcg_solve.argtypes = [P, P, P, C.POINTER(SolveParams), C.POINTER(SolveReport), P]
         L.octmg_mg_solve.argtypes = [P, P, P, C.POINTER(SolveParams), C.POINTER(SolveReport), P]
         L.octmg_mg_solve.restype = C.c_int
+        L.octmg_tank_fields.argtypes = [P, P, C.c_double, P, P, P, P]
+        L.octmg_tank_fields.restype = C.c_int
         L.octmg_profile_enable.argtypes = [P, I32]
         L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
         L.octmg_setup_hierarchy_loopback.argtypes = [P, I32, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
@@ -203,6 +205,20 @@ class Tree:
                 self._h = None
         except Exception:
             pass
+
+
+def tank_fields(tree, centre=(0.5, 0.5, 0.5), radius=0.3, stream=None):
+    """octmg_tank_fields on the device: (kind u8[N], face_frac f32[6][N], b f32[N]) torch tensors."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    N = tree.N
+    kind = torch.empty(N, dtype=torch.uint8, device=dev)
+    frac = torch.empty((6, N), dtype=torch.float32, device=dev)
+    b = torch.empty(N, dtype=torch.float32, device=dev)
+    c = (C.c_double * 3)(*centre)
+    _check(lib().octmg_tank_fields(tree._h, C.cast(c, C.c_void_p), float(radius), _ptr(kind), _ptr(frac), _ptr(b),
+                                   _stream(stream)))
+    return kind, frac, b
 
 
 class Hierarchy:
@@ -342,6 +358,10 @@ def octmg_vcycle(h: Hierarchy, b, u, stream=None):
 
 def octmg_pcg_solve(h: Hierarchy, b, x, **kw):
     return h.pcg_solve(b, x, **kw)
+
+
+def octmg_tank_fields(tree, centre=(0.5, 0.5, 0.5), radius=0.3, stream=None):
+    return tank_fields(tree, centre, radius, stream)
 
 
 def octmg_mg_solve(h: Hierarchy, b, x, **kw):
