@@ -798,6 +798,103 @@ int pcg(Oracle& o, const MG& p, int precond_kind, const double* bin, double* x, 
   }
 }
 
+// -------------------------------------------------------------------------------------
+// Projection operators on the composite octree ("apply the pressure gradient
+// to project the velocity field and measure the divergence").  Face
+// velocities u6[f][i]: the velocity component along +axis(f) on face f of leaf cell i
+// (shared faces stored by both cells); fluid face area S = frac * h^2; the outward flux
+// of face f is s_f u S with s_f = -1 on - faces, +1 on + faces.
+// -------------------------------------------------------------------------------------
+// Per-face decomposition of the composite operator's row i (Eq. 2 P:L295-297 per face,
+// T-junction faces Eqs. 9-12): F_f = kd_f p_i + c_f v_f with kd_f the face's
+// share of the geometric diagonal (the assembly's per-face term), c_f the face's coupling
+// and v_f the composite neighbour value; sum_f F_f = (A p)_i.
+void face_fluxes(const Oracle& o, int t, int off, const double* p, double F[6]) {
+  const int l = o.tlev(t);
+  const double h = o.hcell(l);
+  const size_t i = o.idx(t, off);
+  int64_t X, Y, Z;
+  o.coords(t, off, &X, &Y, &Z);
+  std::vector<size_t> subs;
+  for (int f = 0; f < 6; ++f) {
+    int a = f / 2, sg = (f & 1) ? 1 : -1;
+    int64_t q[3] = {X, Y, Z};
+    q[a] += sg;
+    Loc n = o.locate(l, q[0], q[1], q[2]);
+    double kd = 0.0, coef = sg < 0 ? o.cm[a][i] : coef_plus(o, l, a, n, q[0], q[1], q[2]), v = 0.0;
+    if (n.what == L_WALL) {
+      if (o.wall[f] == 1) kd = o.wf(f, i) * h;
+    } else if (n.what == L_CELL && n.tile < o.NL) {
+      size_t j = o.idx(n.tile, n.off);
+      if (o.kind[j] != K_NEUMANN) kd = (sg < 0 ? o.wf(f, i) : o.wf(f ^ 1, j)) * h;
+      v = o.c[j] != 0.0 ? p[j] : 0.0;
+    } else if (n.what == L_CELL) {
+      fine_subcells(o, l, n, f, subs);
+      for (size_t sidx : subs)
+        if (o.kind[sidx] != K_NEUMANN) kd += 0.5 * o.wf(f ^ 1, sidx) * (0.5 * h);
+      v = child_mean(o, l, n, p);
+    } else if (n.what == L_GHOST) {
+      size_t C = o.idx(n.tile, n.off);
+      if (o.kind[C] != K_NEUMANN) kd = o.wf(f, i) * h;
+      if (o.c[C] != 0.0) v = p[i] + 0.5 * (p[C] - parent_mean(o, l, t, X, Y, Z, p));
+    }
+    F[f] = kd * p[i] + coef * v;
+  }
+}
+
+// b_i = -(net outflow of u) over the faces of active leaf cell i; a coarse leaf's face
+// toward finer cells takes the fine cells' entries (the finer side is authoritative).
+void divergence(const Oracle& o, const float* frac, const double* u6, double* b) {
+  const size_t N = (size_t)o.NL * o.B3;
+  std::vector<size_t> subs;
+  for (int t = 0; t < o.NL; ++t) {
+    const int l = o.tlev(t);
+    const double h = o.hcell(l);
+    for (int off = 0; off < o.B3; ++off) {
+      const size_t i = o.idx(t, off);
+      b[i] = 0.0;
+      if (o.c[i] == 0.0) continue;
+      int64_t X, Y, Z;
+      o.coords(t, off, &X, &Y, &Z);
+      double out = 0.0;
+      for (int f = 0; f < 6; ++f) {
+        int a = f / 2, sg = (f & 1) ? 1 : -1;
+        int64_t q[3] = {X, Y, Z};
+        q[a] += sg;
+        Loc n = o.locate(l, q[0], q[1], q[2]);
+        if (n.what == L_CELL && n.tile >= o.NL) {
+          fine_subcells(o, l, n, f, subs);
+          const double hs = 0.5 * h;
+          for (size_t sidx : subs)
+            out += sg * u6[(size_t)(f ^ 1) * N + sidx] * (double)frac[(size_t)(f ^ 1) * N + sidx] * hs * hs;
+        } else {
+          out += sg * u6[(size_t)f * N + i] * (double)frac[(size_t)f * N + i] * h * h;
+        }
+      }
+      b[i] = -out;
+    }
+  }
+}
+
+// u6 <- u6 - G p: on every face of an active leaf cell with fluid area S > 0, the normal
+// velocity changes by F_f / S (outward), so that divergence(u - G p) = divergence(u) - A p.
+void subtract_gradient(const Oracle& o, const float* frac, const double* p, double* u6) {
+  const size_t N = (size_t)o.NL * o.B3;
+  for (int t = 0; t < o.NL; ++t) {
+    const double h = o.hcell(o.tlev(t));
+    for (int off = 0; off < o.B3; ++off) {
+      const size_t i = o.idx(t, off);
+      if (o.c[i] == 0.0) continue;
+      double F[6];
+      face_fluxes(o, t, off, p, F);
+      for (int f = 0; f < 6; ++f) {
+        const double S = (double)frac[(size_t)f * N + i] * h * h;
+        if (S > 0.0) u6[(size_t)f * N + i] += ((f & 1) ? 1.0 : -1.0) * F[f] / S;
+      }
+    }
+  }
+}
+
 // Multigrid as a standalone solver ("can be used as standalone solvers"; P:L411
 // "if multigrid is used as a standalone solver, beta should be set to 1"): the stationary
 // iteration x_{k+1} = x_k + M(b - A x_k) from x_0 = 0, with the residual updated as
@@ -1047,6 +1144,18 @@ int32_t orc_mg_solve(void* h, const double* prm, int32_t form, const double* b, 
                     hist, hcap);
   *iters = it;
   return st;
+}
+
+void orc_divergence(void* h, const float* frac, const double* u6, double* b) {
+  divergence(*(Oracle*)h, frac, u6, b);
+}
+
+void orc_subtract_gradient(void* h, const float* frac, const double* p, double* u6) {
+  subtract_gradient(*(Oracle*)h, frac, p, u6);
+}
+
+void orc_face_fluxes(void* h, int32_t t, int32_t off, const double* p, double* F) {
+  face_fluxes(*(Oracle*)h, t, off, p, F);
 }
 
 double orc_face_fraction(const double* phi4, double phi_centre) { return face_fraction(phi4, phi_centre); }

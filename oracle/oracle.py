@@ -53,6 +53,9 @@ def lib():
         _lib.orc_vcycle.argtypes = [P, P, P, P, I32]
         _lib.orc_pcg.restype = I32
         _lib.orc_pcg.argtypes = [P, P, I32, P, P, D, I32, I32, P, P, P, P, I32]
+        _lib.orc_divergence.argtypes = [P, P, P, P]
+        _lib.orc_subtract_gradient.argtypes = [P, P, P, P]
+        _lib.orc_face_fluxes.argtypes = [P, I32, I32, P, P]
         _lib.orc_face_fraction.restype = D
         _lib.orc_face_fraction.argtypes = [P, D]
         _lib.orc_tank_fields.argtypes = [P, I64, I32, P, P, D, P, P, P]
@@ -218,6 +221,29 @@ class Oracle:
         n = int(it[0])
         return dict(x=x, iters=n, rel_residual=float(rr[0]), bnorm=float(bn[0]),
                     status=STATUS.get(st, st), history=hist[:min(n, hcap)].copy())
+
+    # ---- projection ---------------------------------------------------
+    def divergence(self, frac, u6):
+        """b = -(net outflow) of the face velocities u6 (6, N) with fluid fractions frac (6, N)."""
+        fr = np.ascontiguousarray(np.asarray(frac, dtype=np.float32).reshape(6, self.N))
+        uu = np.ascontiguousarray(np.asarray(u6, dtype=np.float64).reshape(6, self.N))
+        b = np.zeros(self.N)
+        lib().orc_divergence(self._h, _p(fr), _p(uu), _p(b))
+        return b
+
+    def subtract_gradient(self, frac, p, u6):
+        """u6 - G p (fp64 copy of u6), the projection step consistent with the operator."""
+        fr = np.ascontiguousarray(np.asarray(frac, dtype=np.float32).reshape(6, self.N))
+        pp = np.ascontiguousarray(p, dtype=np.float64)
+        uu = np.array(u6, dtype=np.float64, copy=True).reshape(6, self.N)
+        lib().orc_subtract_gradient(self._h, _p(fr), _p(pp), _p(uu))
+        return uu
+
+    def face_fluxes(self, t, off, p):
+        pp = np.ascontiguousarray(p, dtype=np.float64)
+        F = np.zeros(6)
+        lib().orc_face_fluxes(self._h, int(t), int(off), _p(pp), _p(F))
+        return F
 
     # ---- geometry helpers (plain index arithmetic on the exported tile list) -----------
     def cell_coords(self):
