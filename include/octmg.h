@@ -194,6 +194,34 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
 octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind,
                                float* face_frac, float* b, octmg_stream stream);
 
+/*
+ * Projection operators on the composite octree (after the pressure solve
+ * "apply the pressure gradient to project the velocity field and measure the divergence";
+ * SPEC S:L170-178).  Face velocities u6: device f32[6][N], u6[f][i] = the velocity
+ * component along the +axis of face f (x-,x+,y-,y+,z-,z+) on that face of leaf cell i
+ * (both cells of a shared face hold a copy); face_frac: device f32[6][N] fluid fractions
+ * (NULL = 1), S = frac h^2.  Single-part hierarchies only (OCTMG_E_INVALID otherwise).
+ *
+ * octmg_divergence: b_i = -(sum over the faces of i of the outward flux s_f u S), s_f = -1
+ * on - faces and +1 on + faces, on every active leaf cell (0 on inactive cells) — the
+ * right-hand side convention of the solver (for u = (0,-1,0) in the tank it is the
+ * h^2 (w_y+ - w_y-) of octmg_tank_fields).  A coarse leaf's face toward finer cells sums
+ * the fine cells' entries (the finer side is authoritative, as for the coefficients).
+ * b: device f32[N].
+ *
+ * octmg_subtract_gradient: u6 -= G p in place: on every face of every active leaf cell with
+ * S > 0, u += s_f F_f / S where F_f is the composite operator's flux through that face
+ * (the face's share of the diagonal times p_i plus the coupling times the neighbour value,
+ * T-junction ghosts by Eq. 12), so that divergence(u - G p) = divergence(u) -
+ * A p: after a converged solve of A p = divergence(u) the projected field's divergence is
+ * the solver's residual.  kind, face_beta, face_frac: the arrays given to
+ * octmg_setup_hierarchy (face_beta / face_frac NULL = 1).  p: device f32[N].
+ */
+octmg_status octmg_divergence(const octmg_hier* h, const float* face_frac, const float* u6, float* b,
+                              octmg_stream stream);
+octmg_status octmg_subtract_gradient(const octmg_hier* h, const uint8_t* kind, const float* face_beta,
+                                     const float* face_frac, const float* p, float* u6, octmg_stream stream);
+
 /* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
  * in tile order.  Synchronises `stream` of the last call. */
 octmg_status octmg_hier_export_coefs(const octmg_hier* h, float* host_dst, size_t bytes);

@@ -713,6 +713,26 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
   return OCTMG_OK;
 }
 
+octmg_status octmg_divergence(const octmg_hier* hh, const float* face_frac, const float* u6, float* b,
+                              octmg_stream stream) {
+  if (!hh || !u6 || !b) { set_error("null argument"); return OCTMG_E_INVALID; }
+  if (hh->g.parts.size() != 1 || hh->g.parts[0]->nranks != 1) {
+    set_error("octmg_divergence: single-part hierarchies only");
+    return OCTMG_E_INVALID;
+  }
+  return divergence(*hh->g.parts[0], face_frac, u6, b, (cudaStream_t)stream);
+}
+
+octmg_status octmg_subtract_gradient(const octmg_hier* hh, const uint8_t* kind, const float* face_beta,
+                                     const float* face_frac, const float* p, float* u6, octmg_stream stream) {
+  if (!hh || !kind || !p || !u6) { set_error("null argument"); return OCTMG_E_INVALID; }
+  if (hh->g.parts.size() != 1 || hh->g.parts[0]->nranks != 1) {
+    set_error("octmg_subtract_gradient: single-part hierarchies only");
+    return OCTMG_E_INVALID;
+  }
+  return subtract_gradient(*hh->g.parts[0], kind, face_beta, face_frac, p, u6, (cudaStream_t)stream);
+}
+
 octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind,
                                float* face_frac, float* b, octmg_stream stream) {
   if (!tree || !centre3 || !kind || !face_frac || !b) { set_error("null argument"); return OCTMG_E_INVALID; }

@@ -205,6 +205,11 @@ octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbet
                                  cudaStream_t s);
 octmg_status coarsen_all(Hier& h, cudaStream_t s);  // literal Alg. 3 if h.prm.coarsen_literal
 
+// projection operators (projection.cu)
+octmg_status divergence(const Hier& h, const float* frac, const float* u6, float* b, cudaStream_t s);
+octmg_status subtract_gradient(const Hier& h, const uint8_t* kind, const float* fbeta, const float* frac,
+                               const float* p, float* u6, cudaStream_t s);
+
 // cut-cell geometry of the tank scene (geometry.cu)
 octmg_status tank_fields(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac, float* b,
                          cudaStream_t s);

@@ -291,11 +291,13 @@ __global__ __launch_bounds__(SUB_THREADS, 1) void k_subcycle(SubArgs A) {
   sc_cycle<0, 0>(A, A.K, A.fas_first != 0, e);
 }
 
-// the sub-cycle spread over one cluster of SUB_CLUSTER CTAs (one per SM); mutable data are
-// read through L2 (M = 2) since the CTAs of the cluster run on different SMs
+// the sub-cycle spread over one cluster of SUB_CLUSTER CTAs (one per SM).  M = 2: mutable
+// data read through L2; M = 0: plain (L1-cached) loads, relying on the cluster barrier's
+// release/acquire semantics at cluster scope for visibility of the other CTAs' writes
+template <int M>
 __global__ __launch_bounds__(SUB_THREADS, 1) void k_subcycle_cluster(SubArgs A) {
   unsigned e = 0;
-  sc_cycle<2, 2>(A, A.K, A.fas_first != 0, e);
+  sc_cycle<2, M>(A, A.K, A.fas_first != 0, e);
 }
 
 __global__ __launch_bounds__(SUB_THREADS, 1) void k_coarse_grid(SubArgs A) {
@@ -372,7 +374,9 @@ void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_subcycle_cluster, A);
+  const char* ld = getenv("OCTMG_SUBCYCLE_LD");
+  if (ld && atoi(ld) == 2) cudaLaunchKernelEx(&cfg, k_subcycle_cluster<2>, A);
+  else cudaLaunchKernelEx(&cfg, k_subcycle_cluster<0>, A);
 }
 
 cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int fas_first,

@@ -61,7 +61,8 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_vcycle", "octmg_pcg_solve", "octmg_profile_enable", "octmg_profile_read",
                "octmg_setup_hierarchy_loopback", "octmg_partition_info", "octmg_nccl_unique_id",
                "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
-               "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields"]
+               "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields",
+               "octmg_divergence", "octmg_subtract_gradient"]
 
 _lib = None
 
@@ -88,6 +89,10 @@ def lib():
         L.octmg_mg_solve.restype = C.c_int
         L.octmg_tank_fields.argtypes = [P, P, C.c_double, P, P, P, P]
         L.octmg_tank_fields.restype = C.c_int
+        L.octmg_divergence.argtypes = [P, P, P, P, P]
+        L.octmg_divergence.restype = C.c_int
+        L.octmg_subtract_gradient.argtypes = [P, P, P, P, P, P, P]
+        L.octmg_subtract_gradient.restype = C.c_int
         L.octmg_profile_enable.argtypes = [P, I32]
         L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
         L.octmg_setup_hierarchy_loopback.argtypes = [P, I32, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
@@ -281,6 +286,15 @@ class Hierarchy:
         if raise_on_error and st not in (0, 10):
             _check(st)
         return out
+
+    def divergence(self, u6, b, face_frac=None, stream=None):
+        """octmg_divergence: b = -(net outflow of the face velocities u6 (6, N))."""
+        _check(lib().octmg_divergence(self._h, _ptr(face_frac), _ptr(u6), _ptr(b), _stream(stream)))
+
+    def subtract_gradient(self, p, u6, kind, face_beta=None, face_frac=None, stream=None):
+        """octmg_subtract_gradient: u6 -= G p in place (consistent with the operator)."""
+        _check(lib().octmg_subtract_gradient(self._h, _ptr(kind), _ptr(face_beta), _ptr(face_frac), _ptr(p),
+                                             _ptr(u6), _stream(stream)))
 
     def export_coefs(self):
         out = np.zeros((self.tree.T * 512, 4), dtype=np.float32)
