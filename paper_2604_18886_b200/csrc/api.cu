@@ -614,6 +614,7 @@ ApplyArgs apply_args(const Hier& h) {
   const Tree& T = *h.tree;
   ApplyArgs a;
   a.tiles = h.apply_tiles; a.ntiles = h.n_apply_tiles;
+  if (h.nranks == 1 && h.n_apply_tiles == h.tree->NL) a.tiles = nullptr;  // identity: skip the indirection
   a.tile = T.tile; a.nbr = T.nbr; a.child = T.child; a.coef = h.coef; a.glayer_val = h.glayer_val;
   a.glayer = T.glayer; a.z = nullptr; a.pold = nullptr; a.pnew = nullptr; a.q = nullptr;
   a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL; a.use_beta = 0;
@@ -828,7 +829,12 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       launch_dot_rz(h->r, h->z, h->own_cells, h->partial, h->counter + 2, h->sc, s, G);
     }
     g.launches += np;
-    return allreduce(g, SF_RZ, 1, s);
+    OCTMG_TRY(allreduce(g, SF_RZ, 1, s));
+    if (g.comm) {  // beta from the summed (r, z)
+      for (Hier* h : g.parts) launch_set_beta(h->sc, s);
+      g.launches += np;
+    }
+    return OCTMG_OK;
   };
   for (Hier* h : g.parts) {
     ProfScope ps(*h, KC_INIT, s, (double)h->n_apply_tiles * TB3 * 12.125);  // read b, mask; write r, x

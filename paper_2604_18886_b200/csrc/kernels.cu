@@ -125,7 +125,7 @@ __device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double*
   const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
   const int x0 = 2 * x2;
   // beta = (r_k, z_k) / (r_{k-1}, z_{k-1}) (Alg. 1 line 12)
-  const float beta = (a.use_beta && a.pold) ? (float)(a.sc->sum_rz / a.sc->rho) : 0.0f;
+  const float beta = (a.use_beta && a.pold) ? a.sc->beta_f : 0.0f;  // Alg. 1 line 12
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
   const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
@@ -174,7 +174,7 @@ __device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double*
 template <bool DOT>
 __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
   __shared__ double sred[NT / 32];
-  const int t = a.tiles[blockIdx.x];
+  const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
   int nb[6];
   {
     const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
@@ -193,7 +193,7 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
   const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
   const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
   const int x0 = 2 * x2;
-  const float beta = (a.use_beta && a.pold) ? (float)(a.sc->sum_rz / a.sc->rho) : 0.0f;
+  const float beta = (a.use_beta && a.pold) ? a.sc->beta_f : 0.0f;  // Alg. 1 line 12
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
   const float* cb = a.coef + ((size_t)t << 11);
@@ -237,14 +237,24 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
 template <bool DOT>
 __global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
   __shared__ double sred[NT / 32];
-  apply_general<DOT>(a, a.tiles[blockIdx.x], sred);
+  apply_general<DOT>(a, a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x, sred);
 }
 
 // sigma = p.q from the per-tile partials (fixed order => deterministic)
 __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, int n, Scalars* sc) {
   __shared__ double sred[32];
-  double s = 0.0;
-  for (int k = threadIdx.x; k < n; k += blockDim.x) s += partial[k];
+  // four independent accumulators per thread keep several loads in flight (fixed order)
+  const int bd = blockDim.x;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = threadIdx.x;
+  for (; k + 3 * bd < n; k += 4 * bd) {
+    s0 += partial[k];
+    s1 += partial[k + bd];
+    s2 += partial[k + 2 * bd];
+    s3 += partial[k + 3 * bd];
+  }
+  for (; k < n; k += bd) s0 += partial[k];
+  double s = (s0 + s1) + (s2 + s3);
   for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -377,8 +387,13 @@ __global__ __launch_bounds__(256) void k_dot_rz(const float* r, const float* z, 
   }
   double bs = block_reduce_d(s, sred);
   double tot;
-  if (last_block_sum(bs, partial, counter, gridDim.x, &tot, sred)) sc->sum_rz = tot;
+  if (last_block_sum(bs, partial, counter, gridDim.x, &tot, sred)) {
+    sc->sum_rz = tot;
+    sc->beta_f = (float)(tot / sc->rho);  // (multi-part jobs recompute it after the allreduce)
+  }
 }
+
+__global__ void k_set_beta(Scalars* sc) { sc->beta_f = (float)(sc->sum_rz / sc->rho); }
 
 __global__ void k_copy_ranges(const float* src, float* dst, Ranges R) {
   FOR_RANGES(R, i) reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
@@ -431,6 +446,8 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
                    cudaStream_t s, int grid) {
   k_dot_rz<<<grid, 256, 0, s>>>(r, z, R, partial, counter, sc);
 }
+void launch_set_beta(Scalars* sc, cudaStream_t s) { k_set_beta<<<1, 1, 0, s>>>(sc); }
+
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s) {
   k_copy_ranges<<<592, 256, 0, s>>>(src, dst, R);
 }

@@ -100,7 +100,7 @@ struct Scalars {
   double rho;      // (r, z) of the previous iteration (beta = sum_rz / rho)
   double n_active; // number of active leaf cells (all parts)
   int flags;       // bit0: breakdown (sigma <= 0 or non-finite)
-  int pad;
+  float beta_f;    // beta = sum_rz / rho of Alg. 1 line 12 in fp32, set once per iteration
 };
 // offsets (in doubles) of the reduced fields, for the cross-part sums
 enum { SF_RR = 0, SF_R = 1, SF_RZ = 2, SF_PQ = 3 };
@@ -123,7 +123,7 @@ struct Hier;
 
 // launch helpers implemented in kernels.cu
 struct ApplyArgs {
-  const int* tiles;     // leaf tiles to compute (owned by this part)
+  const int* tiles;     // leaf tiles to compute (owned by this part); nullptr: tiles 0..ntiles-1
   int ntiles;
   const int4* tile;
   const int* nbr;
@@ -154,6 +154,7 @@ void launch_project(float* r, const uint32_t* act, const Ranges& R, double* part
 void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* partial, unsigned* counter,
                    Scalars* sc, cudaStream_t s, int grid);
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s);
+void launch_set_beta(Scalars* sc, cudaStream_t s);  // beta_f from the (all-part) sums
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);
 void launch_build_mask(const float* coef, int64_t n, uint32_t* act, cudaStream_t s);
 
