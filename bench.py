@@ -201,8 +201,26 @@ def main():
     if not tank:
         cfg = make_config(args.config)
     partitioned = world > 1 and not args.replicas
-    comm = om.NcclComm(rank, world) if partitioned else None
-    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"], comm=comm)
+    setup_note = None
+    comm = None
+    if partitioned:
+        # every rank takes the same branch: a failed NCCL bootstrap / partitioned tree build on
+        # any rank switches all ranks to independent replicas, and the line says so
+        try:
+            comm = om.NcclComm(rank, world)
+            tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"], comm=comm)
+            ok = 1.0
+        except Exception as e:  # noqa: BLE001
+            setup_note = f"partitioned setup failed on rank {rank}: {e}"
+            ok = 0.0
+        flag = torch.tensor([ok], device=dev)
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if flag.item() < 1.0:
+            partitioned = False
+            comm = None
+            setup_note = setup_note or "partitioned setup failed on another rank"
+    if not partitioned:
+        tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
     if tank:
         kind, frac, b = om.tank_fields(tree, (0.5, 0.5, 0.5), cfg["radius"])
         b_host = b.cpu().pin_memory()
@@ -313,6 +331,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks,
             "paper_context": "RTX 4090: uniform (5-5) 256^3 = 2.41e8 cells/s (Table 1, P:L1797, M = 2^20)",
+            "setup_note": setup_note,
         }
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
