@@ -114,16 +114,6 @@ struct Builder {
     }
   }
   void passes(int l, int iters, bool red_first, int m1, int m2) {
-    if (h.rb_fused) {  // one launch per RB iteration, ping-pong A -> B -> A ...
-      int cur = 0;
-      for (int k = 0; k < iters; ++k) {
-        const int zero = (k == 0 && m1 == SM_ZERO1) ? 2 : 0;
-        push(Op{5, l, (red_first ? 0 : 1) | zero, cur, 1 - cur});
-        cur = 1 - cur;
-      }
-      if (cur == 1) push(Op{6, l, 0, 1, 0});  // odd count: back to the rest buffer
-      return;
-    }
     for (int k = 0; k < iters; ++k) {
       stage(l, stage_desc(red_first ? 0 : 1, k == 0 ? m1 : SM_PLAIN));
       stage(l, stage_desc(red_first ? 1 : 0, k == 0 ? m2 : SM_PLAIN));
@@ -160,11 +150,6 @@ struct Builder {
 };
 
 void read_env(Hier& h) {
-  const char* rbv = getenv("OCTMG_RB");
-  // default: one launch per colour pass; OCTMG_RB=fused selects the fused RB iteration
-  // (parity-tested, currently slower: see DESIGN.md "Fused red-black")
-  h.rb_fused = (rbv && std::string(rbv) == "fused") ? 1 : ((rbv && std::string(rbv) == "fused_noshell") ? 2 : 0);
-  if (h.nranks > 1) h.rb_fused = 0;  // the partitioned schedule exchanges after every pass
   const char* pc = getenv("OCTMG_PASS_CPT");
   h.pass_cpt = pc ? std::max(1, std::min(2, atoi(pc))) : 2;
   const char* pv = getenv("OCTMG_PASS_V");
@@ -274,22 +259,6 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
   a.stage[0] = op.stage;
-  if (op.kind == 5) {
-    a.u = ubuf(h, op.in_buf);
-    a.u2 = ubuf(h, op.out_buf);
-    a.stage[0] = op.stage & 1;
-    // one HBM pass per RB iteration: read u, b, 16-byte record, write u (28 B/cell)
-    ProfScope ps(h, l < T.L ? KC_SMOOTH_COARSE : KC_RBFUSED, s, 28.0 * a.n * TB3);
-    launch_rb_fused(a, (op.stage & 2) != 0, s, h.rb_fused != 2);
-    return;
-  }
-  if (op.kind == 6) {
-    a.u = ubuf(h, op.in_buf);
-    a.u2 = ubuf(h, op.out_buf);
-    ProfScope ps(h, KC_COPY, s, 8.0 * a.n * TB3);
-    launch_copy_level(a, s);
-    return;
-  }
   if (op.kind == 9) {
     ProfScope ps(h, KC_COARSE_GRID, s, 0.0);
     cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
@@ -460,6 +429,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_TRY(halloc(h.allocs, &h.binner, NIc));
   OCTMG_TRY(halloc(h.allocs, &h.ustar, NIc));
   OCTMG_TRY(halloc(h.allocs, &h.r, NLc));
+  OCTMG_TRY(halloc(h.allocs, &h.xs, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.p0, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.p1, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.q, NLc));
@@ -748,9 +718,13 @@ octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size
   OCTMG_CUDA(cudaDeviceSynchronize());
   std::vector<float> soa((size_t)h.tree->T * TB3 * 4);
   OCTMG_CUDA(cudaMemcpy(soa.data(), h.coef, need, cudaMemcpyDeviceToHost));
-  // SoA planes per tile -> the ABI's record order (c, c_x-, c_y-, c_z-) per cell
-  for (size_t i = 0; i < (size_t)h.tree->T * TB3; ++i)
-    for (int k = 0; k < 4; ++k) host_dst[4 * i + k] = soa[cidx(i, k)];
+  // SoA planes per tile in slot order -> the ABI's record order (c, c_x-, c_y-, c_z-) per
+  // cell in natural order
+  for (size_t t = 0; t < (size_t)h.tree->T; ++t)
+    for (int sl = 0; sl < TB3; ++sl) {
+      const size_t i = t * TB3 + sl, o = t * TB3 + slot_nat(sl);
+      for (int k = 0; k < 4; ++k) host_dst[4 * o + k] = soa[cidx(i, k)];
+    }
   return OCTMG_OK;
 }
 
@@ -761,14 +735,17 @@ octmg_status octmg_apply(octmg_hier* hh, const float* x, float* y, octmg_stream 
   for (Hier* hp : g.parts) {
     Hier& h = *hp;
     // mask the caller's (replicated) x to the active cells: the operator relies on zeros
-    launch_mask_copy(x, h.act, h.p1, (int64_t)h.tree->NL * TB3, s);
+    launch_mask_copy(x, h.act, h.p1, (int64_t)h.tree->NL * TB3, s);  // caller's order -> slots
     ApplyArgs a = apply_args(h);
     a.z = h.p1;
-    a.q = y;  // each part writes its owned leaf tiles
-    ProfScope ps(h, KC_APPLY, s, (double)h.n_apply_tiles * TB3 * 24.0);  // read x, record; write y
-    launch_apply(a, s);
+    a.q = h.q;
+    {
+      ProfScope ps(h, KC_APPLY, s, (double)h.n_apply_tiles * TB3 * 24.0);  // read x, record; write y
+      launch_apply(a, s);
+    }
+    launch_copy_to_nat(h.q, y, h.own_cells, s);  // each part writes its owned leaf tiles
   }
-  g.launches += 2 * (int64_t)g.parts.size();
+  g.launches += 3 * (int64_t)g.parts.size();
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
 }
@@ -779,7 +756,7 @@ octmg_status octmg_vcycle(octmg_hier* hh, const float* b, float* u, octmg_stream
   cudaStream_t s = (cudaStream_t)stream;
   for (Hier* h : g.parts) launch_mask_copy(b, h->act, h->r, (int64_t)h->tree->NL * TB3, s);
   OCTMG_TRY(run_M(g, s));
-  for (Hier* h : g.parts) launch_copy_ranges(h->z, u, h->own_cells, s);  // owned cells of each part
+  for (Hier* h : g.parts) launch_copy_to_nat(h->z, u, h->own_cells, s);  // owned cells of each part
   g.launches += 2 * (int64_t)g.parts.size();
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
@@ -800,6 +777,9 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   const int np = (int)g.parts.size();
   Scalars* hs = h0.sc_host;
   auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
+    // the iterate (slot order) -> the caller's x (natural order), owned cells of each part
+    for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
+    cudaStreamSynchronize(s);
     if (report) {
       report->iters = iters;
       report->converged = conv ? 1 : 0;
@@ -838,7 +818,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   };
   for (Hier* h : g.parts) {
     ProfScope ps(*h, KC_INIT, s, (double)h->n_apply_tiles * TB3 * 12.125);  // read b, mask; write r, x
-    launch_init(b, h->act, h->r, x, h->own_cells, h->partial, h->counter, h->sc, s, G);
+    launch_init(b, h->act, h->r, h->xs, h->own_cells, h->partial, h->counter, h->sc, s, G);
   }
   g.launches += np;
   OCTMG_TRY(allreduce(g, SF_RR, 2, s));
@@ -877,7 +857,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r
-      launch_update(x, h->r, cur ? h->p1 : h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G);
+      launch_update(h->xs, h->r, cur ? h->p1 : h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G);
     }
     g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RR, 2, s));
@@ -916,6 +896,9 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
   const int np = (int)g.parts.size();
   Scalars* hs = h0.sc_host;
   auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
+    // the iterate (slot order) -> the caller's x (natural order), owned cells of each part
+    for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
+    cudaStreamSynchronize(s);
     if (report) {
       report->iters = iters;
       report->converged = conv ? 1 : 0;
@@ -941,7 +924,7 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
   };
   for (Hier* h : g.parts) {
     ProfScope ps(*h, KC_INIT, s, (double)h->n_apply_tiles * TB3 * 12.125);
-    launch_init(b, h->act, h->r, x, h->own_cells, h->partial, h->counter, h->sc, s, G);
+    launch_init(b, h->act, h->r, h->xs, h->own_cells, h->partial, h->counter, h->sc, s, G);
   }
   g.launches += np;
   OCTMG_TRY(allreduce(g, SF_RR, 2, s));
@@ -968,7 +951,7 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
     g.launches += np;
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);
-      launch_update(x, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G, 1.0f);
+      launch_update(h->xs, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G, 1.0f);
     }
     g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RR, 2, s));

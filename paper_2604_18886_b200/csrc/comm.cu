@@ -24,7 +24,7 @@ __device__ __forceinline__ int item_cell(int kind, int c) {
   xyz[ax] = layer;
   xyz[o1] = c & 7;
   xyz[o2] = c >> 3;
-  return xyz[0] + 8 * xyz[1] + 64 * xyz[2];
+  return cslot(xyz[0], xyz[1], xyz[2]);
 }
 
 __global__ void k_pack(Fld f, int NL, const int2* items, const int* offs, float* buf) {

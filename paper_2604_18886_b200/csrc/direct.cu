@@ -58,41 +58,59 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_direct(SmoothArgs a)
     if (act[k] || MODE == SM_ZERO1 || MODE == SM_ZERO2) ut[offs[k]] = unew[k];
 }
 
-// Face sum of a cell of a tile with no ghost face, the tile's neighbour entries prefetched
-// in registers (nb).  Every load is issued unconditionally (walls read the tile itself and
-// are zeroed), so all loads of a cell are in flight at once and none waits on the cell's
-// activity test.
-__device__ __forceinline__ float face_sum_regular(const SmoothArgs& a, int t, const int (&nb)[6], int x, int y,
-                                                  int z, const float4& q) {
-  const float* ut = tptr(a.u, t, a.NL);
-  const int c[3] = {x, y, z};
+// Regular-tile stencil context: the tile's and its six neighbours' value pointers and the
+// +face coupling planes, set up once per thread and shared by its colour cells.  In the
+// colour-split slot order all six neighbours of a cell sit in the other colour's half at
+// fixed offsets from the cell's own index q (x: q-1+p / q+p with p = x&1; y: q-+4; z: q-+32;
+// wrapped into the neighbour tile: +3 / -3, +28 / -28, +224 / -224).
+struct RegCtx {
+  const float* un[6];   // u of the face-neighbour tile (own tile at walls)
+  const float* cn[3];   // c_x- / c_y- / c_z- planes of the +x / +y / +z neighbour tile
+  const float* cown[3]; // the same planes of this tile
+  bool wall[6];
+};
+
+__device__ __forceinline__ void reg_ctx(const SmoothArgs& a, int t, const int (&nb)[6], const float* ut, RegCtx& c) {
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int n = nb[f];
+    c.wall[f] = n < 0;
+    c.un[f] = n >= 0 ? tptr(a.u, n, a.NL) : ut;
+  }
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const int n = nb[2 * ax + 1];
+    c.cown[ax] = a.coef + ((size_t)t << 11) + ((1 + ax) << 9);
+    c.cn[ax] = n >= 0 ? a.coef + ((size_t)n << 11) + ((1 + ax) << 9) : c.cown[ax];
+  }
+}
+
+// Face sum of a cell (slot sl, coordinates x, y, z) of a tile with no ghost face.  Every
+// load is issued unconditionally (walls read the tile itself and are zeroed), so all loads
+// of a cell are in flight at once and none waits on the cell's activity test.
+__device__ __forceinline__ float face_sum_regular(const RegCtx& c, const float* ut, int sl, int x, int y, int z,
+                                                  const float4& q) {
+  const int base = sl ^ 256;
+  const int p = x & 1;
+  const bool in[6] = {x > 0, x < 7, y > 0, y < 7, z > 0, z < 7};
+  const int dlt[6] = {in[0] ? p - 1 : 3, in[1] ? p : -3, in[2] ? -4 : 28, in[3] ? 4 : -28, in[4] ? -32 : 224,
+                      in[5] ? 32 : -224};
   float s = 0.0f;
 #pragma unroll
   for (int f = 0; f < 6; ++f) {
-    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
-    int nc[3] = {c[0], c[1], c[2]};
-    nc[ax] += sg;
-    const bool inside = nc[ax] >= 0 && nc[ax] < 8;
-    const int n = nb[f];
-    const bool wall = !inside && n < 0;
-    nc[ax] &= 7;
-    const int no = loff(nc[0], nc[1], nc[2]);
-    const float* up = inside || wall ? ut : tptr(a.u, n, a.NL);
-    float v = __ldg(up + no);
-    float cf;
-    if (f & 1) {
-      cf = __ldg(a.coef + cidx((size_t)(inside || wall ? t : n) * TB3 + no, 1 + ax));
-    } else {
-      cf = comp(q, ax);
-    }
-    if (wall) v = 0.0f;
+    const int ax = f >> 1;
+    const int no = base + dlt[f];
+    float v = __ldg((in[f] ? ut : c.un[f]) + no);
+    const float cf = (f & 1) ? __ldg((in[f] ? c.cown[ax] : c.cn[ax]) + no) : comp(q, ax);
+    if (!in[f] && c.wall[f]) v = 0.0f;
     s = fmaf(cf, v, s);
   }
   return s;
 }
 
 // The colour pass with the neighbour entries prefetched and, on tiles without a ghost face
-// (every tile of a uniform level), the branch-free face sum above.
+// (every tile of a uniform level), the branch-free face sum above.  Thread j's colour cells
+// are the contiguous slots colour*256 + j + k*256/CPT.
 template <int MODE, int CPT>
 __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
   const int t = a.order[blockIdx.x];
@@ -107,10 +125,13 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
   const int y = (j >> 2) & 7, z0 = j >> 5;
   float* ut = tptr(a.u, t, a.NL);
   const float* bt = tptr(a.b, t, a.NL);
+  const float* ct = a.coef + ((size_t)t << 11);
   bool ghost = false;
 #pragma unroll
   for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
   ghost = ghost && MODE != SM_ZERO1;
+  RegCtx rc;
+  if (MODE != SM_ZERO1 && !ghost) reg_ctx(a, t, nb, ut, rc);
   float unew[CPT];
   bool act[CPT];
   int offs[CPT];
@@ -118,16 +139,17 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
   for (int k = 0; k < CPT; ++k) {
     const int z = z0 + k * (8 / CPT);
     const int x = 2 * (j & 3) + ((colour + y + z) & 1);
-    const int off = loff(x, y, z);
+    const int off = (colour << 8) + j + k * (256 / CPT);  // = loff(x, y, z): this colour's q
     offs[k] = off;
-    const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
+    const float4 q = make_float4(__ldg(ct + off), __ldg(ct + 512 + off), __ldg(ct + 1024 + off),
+                                 __ldg(ct + 1536 + off));
     const float b = __ldg(bt + off);
     act[k] = q.x != 0.0f;
     float v;
     if (MODE == SM_ZERO1) {
       v = b / q.x;
     } else if (!ghost) {
-      v = (b - face_sum_regular(a, t, nb, x, y, z, q)) / q.x;
+      v = (b - face_sum_regular(rc, ut, off, x, y, z, q)) / q.x;
     } else {
       const float ui = MODE == SM_ZERO2 ? 0.0f : __ldg(ut + off);
       const float mP = block_mean<MODE == SM_ZERO2>(a, t, x, y, z, colour);
@@ -154,16 +176,16 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
   const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
   const int x0 = 2 * x2;
   const size_t base = (size_t)t * TB3;
-  const int off0 = loff(x0, y, z);
-  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
-  const float2 uu = *reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0);
-  const float2 bb = *reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0);
+  const int off0 = loff(x0, y, z), off1 = off0 ^ 256;  // the x-pair: same q, opposite colours
+  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off1);
+  const float2 uu = ldpair(tptr(a.u, t, a.NL), off0);
+  const float2 bb = ldpair(tptr(a.b, t, a.NL), off0);
   __shared__ float su_t[TB3];
   __shared__ float scm[3][TB3];
   su_t[off0] = uu.x;
-  su_t[off0 + 1] = uu.y;
+  su_t[off1] = uu.y;
   scm[0][off0] = q0.y; scm[1][off0] = q0.z; scm[2][off0] = q0.w;
-  scm[0][off0 + 1] = q1.y; scm[1][off0 + 1] = q1.z; scm[2][off0 + 1] = q1.w;
+  scm[0][off1] = q1.y; scm[1][off1] = q1.z; scm[2][off1] = q1.w;
   // active u sum / count of the block (also the ghost m_P of its cells)
   float su = (q0.x != 0.0f ? uu.x : 0.0f) + (q1.x != 0.0f ? uu.y : 0.0f);
   int na = (q0.x != 0.0f) + (q1.x != 0.0f);
@@ -208,11 +230,11 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
   const int x0 = 2 * x2;
   const int off0 = loff(x0, y, z);
   const float* cb = a.coef + ((size_t)t << 11);
-  const float2 qc = ldg2(cb + off0), qx = ldg2(cb + 512 + off0), qy = ldg2(cb + 1024 + off0),
-               qz = ldg2(cb + 1536 + off0);
+  const float2 qc = ldpair(cb, off0), qx = ldpair(cb + 512, off0), qy = ldpair(cb + 1024, off0),
+               qz = ldpair(cb + 1536, off0);
   const float4 q0 = make_float4(qc.x, qx.x, qy.x, qz.x), q1 = make_float4(qc.y, qx.y, qy.y, qz.y);
-  const float2 uu = __ldg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
-  const float2 bb = __ldg(reinterpret_cast<const float2*>(tptr(a.b, t, a.NL) + off0));
+  const float2 uu = ldpair(tptr(a.u, t, a.NL), off0);
+  const float2 bb = ldpair(tptr(a.b, t, a.NL), off0);
   bool ghost = false;
 #pragma unroll
   for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
@@ -220,7 +242,7 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
   if (!ghost) {
     const Fld uf = a.u;
     const int NL = a.NL;
-    auto val2 = [uf, NL](int tt, int o) { return ldg2(tptr(uf, tt, NL) + o); };
+    auto val2 = [uf, NL](int tt, int o) { return ldpair(tptr(uf, tt, NL), o); };
     auto val1 = [uf, NL](int tt, int o) { return __ldg(tptr(uf, tt, NL) + o); };
     const float2 f = row2_faces(a.coef, t, nb, x2, y, z, uu, make_float2(q0.y, q1.y), make_float2(q0.z, q1.z),
                                 make_float2(q0.w, q1.w), make_float2(q0.x * uu.x, q1.x * uu.y), val2, val1);
@@ -260,23 +282,23 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
 // cell (Alg. 4 line 15; no beta).  4 cells per thread (float4).
 __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
   const int t = a.order[blockIdx.x];
-  const int j = threadIdx.x;  // cells 4j .. 4j+3: x0 = 4*(j&1), y = (j>>1)&7, z = j>>4
-  const int x0 = 4 * (j & 1), y = (j >> 1) & 7, z = j >> 4;
+  // thread j: the 4 same-q cells at slots j, j + 128 (red) and j + 256, j + 384 (black):
+  // every access is a coalesced scalar per warp
   const int4 tv = __ldg(a.tile + t);
   const int P = __ldg(a.parent + t);
-  float4* up = reinterpret_cast<float4*>(tptr(a.u, t, a.NL) + loff(x0, y, z));
-  float4 u = *up;
+  float* ut = tptr(a.u, t, a.NL);
+  const float* cc = a.coef + ((size_t)t << 11);
   const float* uc = tptr(a.uc, P, a.NL);
   const float* us = a.ustar + (size_t)(P - a.NL) * TB3;
-  const int pc0 = pcell_of(tv, x0, y, z), pc1 = pcell_of(tv, x0 + 2, y, z);
-  const float c0 = a.pro_scale * (__ldg(uc + pc0) - __ldg(us + pc0));
-  const float c1 = a.pro_scale * (__ldg(uc + pc1) - __ldg(us + pc1));
-  const float4 cc = __ldg(reinterpret_cast<const float4*>(a.coef + ((size_t)t << 11) + loff(x0, y, z)));
-  if (cc.x != 0.0f) u.x += c0;
-  if (cc.y != 0.0f) u.y += c0;
-  if (cc.z != 0.0f) u.z += c1;
-  if (cc.w != 0.0f) u.w += c1;
-  *up = u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int sl = threadIdx.x + 128 * k;
+    int x, y, z;
+    slot_xyz(sl, x, y, z);
+    const int pc = pcell_of(tv, x, y, z);
+    const float c = a.pro_scale * (__ldg(uc + pc) - __ldg(us + pc));
+    if (__ldg(cc + sl) != 0.0f) ut[sl] += c;
+  }
 }
 
 // FAS right-hand side of the inner rows of a coarse level (Alg. 4 line 10):
@@ -286,16 +308,14 @@ __global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
   const int t = a.first_tile + blockIdx.x;
   const int j = threadIdx.x;
   const int y = (j >> 2) & 7, z = j >> 5, x0 = 2 * (j & 3);
-  const int off0 = loff(x0, y, z);
+  const int off0 = loff(x0, y, z), off1 = off0 ^ 256;
   const size_t base = (size_t)t * TB3;
-  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
-  const float2 uu = __ldg(reinterpret_cast<const float2*>(tptr(a.u, t, a.NL) + off0));
-  float2* bp = reinterpret_cast<float2*>(a.b.inner + (size_t)(t - a.NL) * TB3 + off0);
-  const float2 bb = *bp;
-  float2 out;
-  out.x = q0.x != 0.0f ? bb.x + face_sum<false>(a, t, x0, y, z, q0, 0.0f, 0.0f, 0, q0.x * uu.x) : 0.0f;
-  out.y = q1.x != 0.0f ? bb.y + face_sum<false>(a, t, x0 + 1, y, z, q1, 0.0f, 0.0f, 0, q1.x * uu.y) : 0.0f;
-  *bp = out;
+  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off1);
+  const float2 uu = ldpair(tptr(a.u, t, a.NL), off0);
+  float* bt = a.b.inner + (size_t)(t - a.NL) * TB3;
+  const float b0 = bt[off0], b1 = bt[off1];
+  bt[off0] = q0.x != 0.0f ? b0 + face_sum<false>(a, t, x0, y, z, q0, 0.0f, 0.0f, 0, q0.x * uu.x) : 0.0f;
+  bt[off1] = q1.x != 0.0f ? b1 + face_sum<false>(a, t, x0 + 1, y, z, q1, 0.0f, 0.0f, 0, q1.x * uu.y) : 0.0f;
 }
 
 }  // namespace

@@ -12,7 +12,7 @@ namespace {
 
 constexpr int NT = 256;  // threads per tile CTA; thread -> cells (2*x2, y, z), (2*x2+1, y, z)
 
-__device__ __forceinline__ int loff(int x, int y, int z) { return x + 8 * y + 64 * z; }
+__device__ __forceinline__ int loff(int x, int y, int z) { return cslot(x, y, z); }  // slot order
 __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
 
 
@@ -127,27 +127,29 @@ __device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double*
   // beta = (r_k, z_k) / (r_{k-1}, z_{k-1}) (Alg. 1 line 12)
   const float beta = (a.use_beta && a.pold) ? a.sc->beta_f : 0.0f;  // Alg. 1 line 12
   const size_t base = (size_t)t * TB3;
-  const int off0 = loff(x0, y, z);
-  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
+  const int off0 = loff(x0, y, z), off1 = off0 ^ 256;  // the pair: same q, opposite colours
+  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off1);
   float p0 = 0.0f, p1 = 0.0f;
   {
-    float2 zz = __ldg(reinterpret_cast<const float2*>(a.z + base + off0));
-    p0 = zz.x; p1 = zz.y;
+    p0 = __ldg(a.z + base + off0);
+    p1 = __ldg(a.z + base + off1);
     if (a.pold) {
-      float2 pp = __ldg(reinterpret_cast<const float2*>(a.pold + base + off0));
-      p0 = fmaf(beta, pp.x, p0);
-      p1 = fmaf(beta, pp.y, p1);
+      p0 = fmaf(beta, __ldg(a.pold + base + off0), p0);
+      p1 = fmaf(beta, __ldg(a.pold + base + off1), p1);
     }
     if (q0.x == 0.0f) p0 = 0.0f;
     if (q1.x == 0.0f) p1 = 0.0f;
   }
-  if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0, p1);
+  if (a.pnew) {
+    a.pnew[base + off0] = p0;
+    a.pnew[base + off1] = p1;
+  }
   __shared__ float sp[TB3];
   __shared__ float scm[3][TB3];
   sp[off0] = p0;
-  sp[off0 + 1] = p1;
+  sp[off1] = p1;
   scm[0][off0] = q0.y; scm[1][off0] = q0.z; scm[2][off0] = q0.w;
-  scm[0][off0 + 1] = q1.y; scm[1][off0 + 1] = q1.z; scm[2][off0 + 1] = q1.w;
+  scm[0][off1] = q1.y; scm[1][off1] = q1.z; scm[2][off1] = q1.w;
   float su = p0 + p1;
   int na = (q0.x != 0.0f) + (q1.x != 0.0f);
   su += __shfl_xor_sync(0xffffffffu, su, 4);
@@ -158,7 +160,8 @@ __device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double*
   __syncthreads();
   const float r0 = q0.x != 0.0f ? composite_faces(a, beta, t, x0, y, z, q0, p0, mP, q0.x * p0, sp, scm) : 0.0f;
   const float r1 = q1.x != 0.0f ? composite_faces(a, beta, t, x0 + 1, y, z, q1, p1, mP, q1.x * p1, sp, scm) : 0.0f;
-  *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
+  a.q[base + off0] = r0;
+  a.q[base + off1] = r1;
   if (DOT) {
     // per-tile fp64 partial; k_finish_sigma sums them in tile order (no per-CTA fence)
     double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
@@ -197,16 +200,16 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
   const size_t base = (size_t)t * TB3;
   const int off0 = loff(x0, y, z);
   const float* cb = a.coef + ((size_t)t << 11);
-  const float2 c0 = ldg2(cb + off0), cxm = ldg2(cb + 512 + off0), cym = ldg2(cb + 1024 + off0),
-               czm = ldg2(cb + 1536 + off0);
+  const float2 c0 = ldpair(cb, off0), cxm = ldpair(cb + 512, off0), cym = ldpair(cb + 1024, off0),
+               czm = ldpair(cb + 1536, off0);
   // p = z + beta p_old of any leaf cell (zero on inactive cells, see pval)
   const float* zp = a.z;
   const float* po = a.pold;
   auto val2 = [zp, po, beta](int tt, int o) {
-    const size_t i = ((size_t)tt << 9) + o;
-    float2 v = ldg2(zp + i);
+    const size_t i = (size_t)tt << 9;
+    float2 v = ldpair(zp + i, o);
     if (po) {
-      const float2 w = ldg2(po + i);
+      const float2 w = ldpair(po + i, o);
       v.x = fmaf(beta, w.x, v.x);
       v.y = fmaf(beta, w.y, v.y);
     }
@@ -225,8 +228,12 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
                               val2, val1);
   const float r0 = c0.x != 0.0f ? f.x : 0.0f;
   const float r1 = c0.y != 0.0f ? f.y : 0.0f;
-  if (a.pnew) *reinterpret_cast<float2*>(a.pnew + base + off0) = make_float2(p0, p1);
-  *reinterpret_cast<float2*>(a.q + base + off0) = make_float2(r0, r1);
+  if (a.pnew) {
+    a.pnew[base + off0] = p0;
+    a.pnew[base + (off0 ^ 256)] = p1;
+  }
+  a.q[base + off0] = r0;
+  a.q[base + (off0 ^ 256)] = r1;
   if (DOT) {
     double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
     double bs = block_reduce_d(d, sred);
@@ -294,14 +301,18 @@ __device__ __forceinline__ void reduce2(double s2, double s1, double* partial, u
   }
 }
 
-// r = b on active cells (0 elsewhere), x = 0; sums ||r||^2, sum r (Alg. 1 lines 3-4)
+// r = b on active cells (0 elsewhere), x = 0; sums ||r||^2, sum r (Alg. 1 lines 3-4).
+// r and x are internal (slot order), b the caller's vector (natural order).
 __global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* act, float* r, float* x, Ranges R,
                                               double* partial, unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   double s2 = 0.0, s1 = 0.0;
   FOR_RANGES(R, i) {
-    float4 v = reinterpret_cast<const float4*>(b)[i];
-    float m[4] = {v.x, v.y, v.z, v.w};
+    // b is in the caller's natural cell order: gather the 4 slots' cells
+    const int64_t c0 = 4 * i, tb = c0 & ~(int64_t)511;
+    const int s0 = (int)(c0 & 511);
+    float m[4];
+    for (int k = 0; k < 4; ++k) m[k] = __ldg(b + tb + slot_nat(s0 + k));
     const unsigned am = act4(act, i);
     for (int k = 0; k < 4; ++k) {
       if (!((am >> k) & 1u)) m[k] = 0.0f;
@@ -399,9 +410,35 @@ __global__ void k_copy_ranges(const float* src, float* dst, Ranges R) {
   FOR_RANGES(R, i) reinterpret_cast<float4*>(dst)[i] = reinterpret_cast<const float4*>(src)[i];
 }
 
+// dst (slot order) = src (caller's natural order) on the active cells, 0 elsewhere
 __global__ void k_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = ((act[i >> 5] >> (i & 31)) & 1u) ? src[i] : 0.0f;
+    dst[i] = ((act[i >> 5] >> (i & 31)) & 1u) ? src[(i & ~(int64_t)511) + slot_nat((int)(i & 511))] : 0.0f;
+}
+
+// dst (caller's natural order) = src (slot order) on the cells of the ranges
+__global__ void k_copy_to_nat(const float* src, float* dst, Ranges R) {
+  FOR_RANGES(R, i) {
+    const float4 v = reinterpret_cast<const float4*>(src)[i];
+    const int64_t c0 = 4 * i, tb = c0 & ~(int64_t)511;
+    const int s0 = (int)(c0 & 511);
+    dst[tb + slot_nat(s0)] = v.x;
+    dst[tb + slot_nat(s0 + 1)] = v.y;
+    dst[tb + slot_nat(s0 + 2)] = v.z;
+    dst[tb + slot_nat(s0 + 3)] = v.w;
+  }
+}
+
+// per-cell arrays of nf fields (field stride n) between natural and slot order
+template <class T>
+__global__ void k_permute(const T* src, T* dst, int64_t n, int nf, int to_slots) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = (i & ~(int64_t)511) + slot_nat((int)(i & 511));
+    for (int f = 0; f < nf; ++f) {
+      if (to_slots) dst[(size_t)f * n + i] = src[(size_t)f * n + j];
+      else dst[(size_t)f * n + j] = src[(size_t)f * n + i];
+    }
+  }
 }
 
 // activity bitmask of the leaf cells (bit i%32 of word i/32: c_i != 0)
@@ -450,6 +487,15 @@ void launch_set_beta(Scalars* sc, cudaStream_t s) { k_set_beta<<<1, 1, 0, s>>>(s
 
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s) {
   k_copy_ranges<<<592, 256, 0, s>>>(src, dst, R);
+}
+void launch_copy_to_nat(const float* src, float* dst, const Ranges& R, cudaStream_t s) {
+  k_copy_to_nat<<<592, 256, 0, s>>>(src, dst, R);
+}
+void launch_permute_f32(const float* src, float* dst, int64_t n, int nf, bool to_slots, cudaStream_t s) {
+  k_permute<float><<<592, 256, 0, s>>>(src, dst, n, nf, to_slots ? 1 : 0);
+}
+void launch_permute_u8(const uint8_t* src, uint8_t* dst, int64_t n, bool to_slots, cudaStream_t s) {
+  k_permute<uint8_t><<<592, 256, 0, s>>>(src, dst, n, 1, to_slots ? 1 : 0);
 }
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s) {
   k_mask_copy<<<592, 256, 0, s>>>(src, act, dst, n);

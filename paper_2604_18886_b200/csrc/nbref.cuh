@@ -16,7 +16,7 @@ struct NbRef {
   int what, tile, off;
 };
 
-__device__ __forceinline__ int loff(int x, int y, int z) { return x + 8 * y + 64 * z; }
+__device__ __forceinline__ int loff(int x, int y, int z) { return cslot(x, y, z); }  // slot order
 
 // neighbour of cell (x,y,z) of tile t (tile coords tv) across face f
 __device__ __forceinline__ NbRef nb_ref(const int* nbr, int4 tv, int t, int NL, int x, int y, int z, int f) {
@@ -51,7 +51,8 @@ struct WIn {
 // the 4 fine sub-cells (leaf cells at level l+1) of the inner cell nb that touch the
 // fine-to-coarse face f of our cell; order dz, dy, dx as in the oracle
 __device__ __forceinline__ void fine_subs(const int* child, int NL, const NbRef& nb, int f, size_t out[4]) {
-  int xn = nb.off & 7, yn = (nb.off >> 3) & 7, zn = nb.off >> 6;
+  int xn, yn, zn;
+  slot_xyz(nb.off, xn, yn, zn);
   int ct = child[8 * (nb.tile - NL) + (xn >> 2) + 2 * (yn >> 2) + 4 * (zn >> 2)];
   int a = f >> 1;
   int facing = (f & 1) ? 0 : 1;

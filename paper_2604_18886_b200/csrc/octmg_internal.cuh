@@ -58,6 +58,27 @@ struct Tree {
   ~Tree();
 };
 
+// Cell order inside a tile ("slot"): colour-split, red (x+y+z even) cells first,
+//   slot = ((x+y+z) & 1) * 256 + (x >> 1) + 4 y + 32 z,
+// so a red-black colour pass reads and writes contiguous halves of every field (its own
+// colour's values and coefficients, the other colour's neighbour values).  User vectors
+// keep the natural order x + 8y + 64z (the ABI's leaf-slot order); the library permutes at
+// its boundary.
+__host__ __device__ __forceinline__ int cslot(int x, int y, int z) {
+  return (((x + y + z) & 1) << 8) | ((x >> 1) + 4 * y + 32 * z);
+}
+__host__ __device__ __forceinline__ void slot_xyz(int s, int& x, int& y, int& z) {
+  const int q = s & 255;
+  y = (q >> 2) & 7;
+  z = q >> 5;
+  x = 2 * (q & 3) + (((s >> 8) + y + z) & 1);
+}
+__host__ __device__ __forceinline__ int slot_nat(int s) {  // natural offset x + 8y + 64z of a slot
+  int x, y, z;
+  slot_xyz(s, x, y, z);
+  return x + 8 * y + 64 * z;
+}
+
 // A field over all tiles, stored as a leaf part and an inner part (either may alias a
 // caller / PCG vector).  Tile t's 512 cells start at leaf + t*512 (t < NL) or
 // inner + (t-NL)*512.
@@ -155,7 +176,10 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
                    Scalars* sc, cudaStream_t s, int grid);
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s);
 void launch_set_beta(Scalars* sc, cudaStream_t s);  // beta_f from the (all-part) sums
-void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);
+void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);  // nat -> slots
+void launch_copy_to_nat(const float* src, float* dst, const Ranges& R, cudaStream_t s);  // slots -> nat, owned
+void launch_permute_f32(const float* src, float* dst, int64_t n, int nf, bool to_slots, cudaStream_t s);
+void launch_permute_u8(const uint8_t* src, uint8_t* dst, int64_t n, bool to_slots, cudaStream_t s);
 void launch_build_mask(const float* coef, int64_t n, uint32_t* act, cudaStream_t s);
 
 // smoother kernels (direct.cu, rbfused.cu, subcycle.cu)
@@ -185,8 +209,6 @@ void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, bool v2);
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
-void launch_rb_fused(const SmoothArgs& a, bool zero, cudaStream_t s, bool shell = true);
-void launch_copy_level(const SmoothArgs& a, cudaStream_t s);
 int subcycle_ctas();
 int subcycle_max_tiles(int ctas);
 int subcycle_max_level();
@@ -246,6 +268,7 @@ struct Hier {
   float* binner = nullptr;       // [NI*512]
   float* ustar = nullptr;        // [NI*512]
   float* r = nullptr;            // [NL*512] PCG residual = leaf part of the cycle rhs
+  float* xs = nullptr;           // [NL*512] PCG iterate (slot order; copied to the caller's x)
   // PCG
   float* p0 = nullptr;
   float* p1 = nullptr;
@@ -268,7 +291,6 @@ struct Hier {
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
   unsigned* bar = nullptr;       // its grid barrier counter
-  int rb_fused = 0;              // 1: fused RB iterations (OCTMG_RB=fused); 0: per-colour passes
   // profiling
   bool profiling = false;
   struct Ev { int cls; double bytes; cudaEvent_t a, b; };

@@ -11,6 +11,8 @@
 //    assembly does; c_f, v_f: the operator's coupling and neighbour value, Eq. 12 ghosts at
 //    T-junctions) and u += s_f F_f / S, so that div(u - G p) = div(u) - A p.
 // One thread per cell, one CTA per leaf tile.
+#include <algorithm>
+
 #include "nbref.cuh"
 
 namespace octmg {
@@ -44,7 +46,8 @@ __device__ __forceinline__ float fr(const ProjArgs& a, int f, size_t i) {
 __global__ __launch_bounds__(512) void k_divergence(ProjArgs a) {
   const int t = blockIdx.x;
   const int off = threadIdx.x;
-  const int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+  int x, y, z;
+    slot_xyz(off, x, y, z);
   const size_t i = (size_t)t * TB3 + off;
   const int4 tv = a.tile[t];
   const float h = ldexpf(1.0f, -tv.x) * 0.125f;
@@ -83,7 +86,8 @@ __device__ __forceinline__ float block_mean_p(const ProjArgs& a, int t, int x, i
 __global__ __launch_bounds__(512) void k_subtract_gradient(ProjArgs a) {
   const int t = blockIdx.x;
   const int off = threadIdx.x;
-  const int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+  int x, y, z;
+    slot_xyz(off, x, y, z);
   const size_t i = (size_t)t * TB3 + off;
   if (cplane(a.coef, i, 0) == 0.0f) return;  // inactive cell: its faces are left unchanged
   const int4 tv = a.tile[t];
@@ -110,7 +114,8 @@ __global__ __launch_bounds__(512) void k_subtract_gradient(ProjArgs a) {
       const size_t n = (size_t)nb.tile * TB3 + nb.off;
       if (f & 1) cf = cplane(a.coef, n, 1 + ax);
       // inner neighbour value: mean of its active children (all leaves)
-      const int xn = nb.off & 7, yn = (nb.off >> 3) & 7, zn = nb.off >> 6;
+      int xn, yn, zn;
+      slot_xyz(nb.off, xn, yn, zn);
       const int ct = a.child[8 * (nb.tile - a.NL) + (xn >> 2) + 2 * (yn >> 2) + 4 * (zn >> 2)];
       float s = 0.0f;
       int c = 0;
@@ -160,26 +165,70 @@ ProjArgs proj_args(const Hier& h) {
 
 }  // namespace
 
+// The caller's arrays are in natural cell order; the kernels work in slot order on
+// temporaries (the projection is not on the solver's hot path).
+template <class T>
+static octmg_status tmp(T** p, size_t n, cudaStream_t s) {
+  return cudaMallocAsync((void**)p, sizeof(T) * std::max<size_t>(n, 1), s) == cudaSuccess ? OCTMG_OK
+                                                                                     : cuda_status(cudaErrorMemoryAllocation, "projection temporaries");
+}
+
 octmg_status divergence(const Hier& h, const float* frac, const float* u6, float* b, cudaStream_t s) {
+  const int64_t N = (int64_t)h.tree->NL * TB3;
+  float *fr_s = nullptr, *u_s = nullptr, *b_s = nullptr;
+  if (frac) {
+    OCTMG_TRY(tmp(&fr_s, 6 * (size_t)N, s));
+    launch_permute_f32(frac, fr_s, N, 6, true, s);
+  }
+  OCTMG_TRY(tmp(&u_s, 6 * (size_t)N, s));
+  OCTMG_TRY(tmp(&b_s, (size_t)N, s));
+  launch_permute_f32(u6, u_s, N, 6, true, s);
   ProjArgs a = proj_args(h);
-  a.frac = frac;
-  a.u6 = u6;
-  a.b = b;
+  a.frac = fr_s;
+  a.u6 = u_s;
+  a.b = b_s;
   if (h.tree->NL) k_divergence<<<h.tree->NL, TB3, 0, s>>>(a);
+  launch_permute_f32(b_s, b, N, 1, false, s);
+  if (fr_s) cudaFreeAsync(fr_s, s);
+  cudaFreeAsync(u_s, s);
+  cudaFreeAsync(b_s, s);
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
 }
 
 octmg_status subtract_gradient(const Hier& h, const uint8_t* kind, const float* fbeta, const float* frac,
                                const float* p, float* u6, cudaStream_t s) {
+  const int64_t N = (int64_t)h.tree->NL * TB3;
+  uint8_t* k_s = nullptr;
+  float *be_s = nullptr, *fr_s = nullptr, *p_s = nullptr, *u_s = nullptr;
+  OCTMG_TRY(tmp(&k_s, (size_t)N, s));
+  launch_permute_u8(kind, k_s, N, true, s);
+  if (fbeta) {
+    OCTMG_TRY(tmp(&be_s, 6 * (size_t)N, s));
+    launch_permute_f32(fbeta, be_s, N, 6, true, s);
+  }
+  if (frac) {
+    OCTMG_TRY(tmp(&fr_s, 6 * (size_t)N, s));
+    launch_permute_f32(frac, fr_s, N, 6, true, s);
+  }
+  OCTMG_TRY(tmp(&p_s, (size_t)N, s));
+  OCTMG_TRY(tmp(&u_s, 6 * (size_t)N, s));
+  launch_permute_f32(p, p_s, N, 1, true, s);
+  launch_permute_f32(u6, u_s, N, 6, true, s);
   ProjArgs a = proj_args(h);
-  a.kind = kind;
-  a.w = WIn{fbeta, frac, (size_t)h.tree->NL * TB3};
-  a.frac = frac;
-  a.p = p;
-  a.u6 = u6;
-  a.u6w = u6;  // in place: each thread reads and writes only its own cell's six entries
+  a.kind = k_s;
+  a.w = WIn{be_s, fr_s, (size_t)N};
+  a.frac = fr_s;
+  a.p = p_s;
+  a.u6 = u_s;
+  a.u6w = u_s;  // in place: each thread reads and writes only its own cell's six entries
   if (h.tree->NL) k_subtract_gradient<<<h.tree->NL, TB3, 0, s>>>(a);
+  launch_permute_f32(u_s, u6, N, 6, false, s);
+  cudaFreeAsync(k_s, s);
+  if (be_s) cudaFreeAsync(be_s, s);
+  if (fr_s) cudaFreeAsync(fr_s, s);
+  cudaFreeAsync(p_s, s);
+  cudaFreeAsync(u_s, s);
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
 }

@@ -1,6 +1,8 @@
 // Coefficient setup: leaf assembly (Eq. 3; ghost-fluid kinds P:L318-337;
 // T-junction faces Eqs. 9-10) and Galerkin coarsening (Alg. 3)
 // of the compact record (c, c_x-, c_y-, c_z-) held as one float4 per cell.
+#include <algorithm>
+
 #include "nbref.cuh"
 
 namespace octmg {
@@ -26,7 +28,8 @@ __global__ __launch_bounds__(256) void k_assemble_diag(AsmArgs a) {
   int4 tv = a.tile[t];
   float h = ldexpf(1.0f, -tv.x) * 0.125f;
   for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
-    int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    int x, y, z;
+    slot_xyz(off, x, y, z);
     size_t i = (size_t)t * TB3 + off;
     float c = 0.0f;
     if (a.kind[i] == KF) {
@@ -58,7 +61,8 @@ __global__ __launch_bounds__(256) void k_assemble_offdiag(AsmArgs a) {
   int4 tv = a.tile[t];
   float h = ldexpf(1.0f, -tv.x) * 0.125f;
   for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
-    int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    int x, y, z;
+    slot_xyz(off, x, y, z);
     size_t i = (size_t)t * TB3 + off;
     if (a.kind[i] == KN) continue;  // Neumann: all-zero record (already zero)
     float cm[3];
@@ -115,7 +119,8 @@ __global__ __launch_bounds__(256) void k_coarsen(CoarsenArgs a) {
   int P = a.toff + blockIdx.x;
   const int* ch8 = a.child + 8 * (P - a.NL);
   for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
-    int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    int x, y, z;
+    slot_xyz(off, x, y, z);
     int ct = ch8[(x >> 2) + 2 * (y >> 2) + 4 * (z >> 2)];
     int4 ctv = a.tile[ct];
     float cI = 0.0f, cIm[3] = {0.f, 0.f, 0.f};
@@ -163,13 +168,29 @@ __global__ void k_any_dirichlet(const uint8_t* kind, int64_t n, int* flag) {
 octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
                                  cudaStream_t s) {
   Tree& T = *h.tree;
+  const int64_t Nc = (int64_t)T.NL * TB3;
+  // the caller's per-cell inputs (natural cell order) -> slot order, in temporaries
+  uint8_t* kind_s = nullptr;
+  float* beta_s = nullptr;
+  float* frac_s = nullptr;
+  OCTMG_CUDA(cudaMallocAsync(&kind_s, std::max<int64_t>(Nc, 1), s));
+  launch_permute_u8(kind, kind_s, Nc, true, s);
+  if (fbeta) {
+    OCTMG_CUDA(cudaMallocAsync(&beta_s, sizeof(float) * 6 * std::max<int64_t>(Nc, 1), s));
+    launch_permute_f32(fbeta, beta_s, Nc, 6, true, s);
+  }
+  if (ffrac) {
+    OCTMG_CUDA(cudaMallocAsync(&frac_s, sizeof(float) * 6 * std::max<int64_t>(Nc, 1), s));
+    launch_permute_f32(ffrac, frac_s, Nc, 6, true, s);
+  }
+  kind = kind_s;
   AsmArgs a;
   a.tile = T.tile;
   a.nbr = T.nbr;
   a.child = T.child;
   a.glayer = T.glayer;
   a.kind = kind;
-  a.w = WIn{fbeta, ffrac, (size_t)T.NL * TB3};
+  a.w = WIn{beta_s, frac_s, (size_t)T.NL * TB3};
   a.coef = h.coef;
   a.glayer_val = h.glayer_val;
   a.NL = T.NL;
@@ -192,6 +213,9 @@ octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbet
   OCTMG_CUDA(cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, s));
   OCTMG_CUDA(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   OCTMG_CUDA(cudaFreeAsync(d_cnt, s));
+  OCTMG_CUDA(cudaFreeAsync(kind_s, s));
+  if (beta_s) OCTMG_CUDA(cudaFreeAsync(beta_s, s));
+  if (frac_s) OCTMG_CUDA(cudaFreeAsync(frac_s, s));
   OCTMG_CUDA(cudaStreamSynchronize(s));
   h.n_active = (double)cnt;
   int wall_d = 0;

@@ -20,7 +20,7 @@ __device__ __forceinline__ float ldv(const float* p) {
   return *p;
 }
 
-__device__ __forceinline__ int loff(int x, int y, int z) { return x + 8 * y + 64 * z; }
+__device__ __forceinline__ int loff(int x, int y, int z) { return cslot(x, y, z); }  // slot order
 __device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
 __device__ __forceinline__ int pcell_of(int4 tv, int x, int y, int z) {
   return loff(((tv.y & 1) << 2) + (x >> 1), ((tv.z & 1) << 2) + (y >> 1), ((tv.w & 1) << 2) + (z >> 1));

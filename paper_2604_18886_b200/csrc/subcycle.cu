@@ -153,11 +153,12 @@ __device__ __noinline__ void sc_restrict(const SubArgs& A, int l, unsigned& epoc
       const int x0 = 2 * x2;
       const size_t base = (size_t)t * TB3;
       const int off0 = loff(x0, y, z);
-      const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off0 + 1);
+      const int off1 = loff(x0 + 1, y, z);
+      const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off1);
       const float* ut = tptr(a.u, t, a.NL);
       const float* bt = tptr(a.b, t, a.NL);
-      const float u0 = ldv<M>(ut + off0), u1 = ldv<M>(ut + off0 + 1);
-      const float b0 = ldv<M>(bt + off0), b1 = ldv<M>(bt + off0 + 1);
+      const float u0 = ldv<M>(ut + off0), u1 = ldv<M>(ut + off1);
+      const float b0 = ldv<M>(bt + off0), b1 = ldv<M>(bt + off1);
       float su = (q0.x != 0.0f ? u0 : 0.0f) + (q1.x != 0.0f ? u1 : 0.0f);
       int na = (q0.x != 0.0f) + (q1.x != 0.0f);
       su += __shfl_xor_sync(0xffffffffu, su, 4);
@@ -192,7 +193,8 @@ __device__ __noinline__ void sc_fasrhs(const SubArgs& A, int l, unsigned& epoch)
   for (int s = ph_tid<PM>(); s < ncell; s += ph_nthreads<PM>()) {
     const int t = A.ib[l] + (s >> 9);
     const int off = s & 511;
-    const int x = off & 7, y = (off >> 3) & 7, z = off >> 6;
+    int x, y, z;
+    slot_xyz(off, x, y, z);
     const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
     float* bi = a.b.inner + (size_t)(t - a.NL) * TB3 + off;
     if (q.x != 0.0f) {
@@ -217,7 +219,9 @@ __device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch
     if (ldcoef(a.coef, (size_t)t * TB3 + off).x == 0.0f) continue;
     const int4 tv = __ldg(a.tile + t);
     const int P = __ldg(a.parent + t);
-    const int pc = pcell_of(tv, off & 7, (off >> 3) & 7, off >> 6);
+    int ox, oy, oz;
+    slot_xyz(off, ox, oy, oz);
+    const int pc = pcell_of(tv, ox, oy, oz);
     float* up = tptr(a.u, t, a.NL) + off;
     *up = ldv<M>(up) + a.pro_scale * (ldv<M>(tptr(a.uc, P, a.NL) + pc) - ldv<M>(a.ustar + (size_t)(P - a.NL) * TB3 + pc));
   }

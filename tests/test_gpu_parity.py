@@ -246,7 +246,7 @@ def test_full_size_cfg2_parity(om):
 # ---------------------------------------------------------------------------------------
 # alternative schedules selected at setup (same semantics, must match the oracle too)
 # ---------------------------------------------------------------------------------------
-@pytest.mark.parametrize("env", [{"OCTMG_RB": "fused"}, {"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
+@pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
                                  {"OCTMG_GRID": "1"}, {"OCTMG_GRID": "1", "OCTMG_SUBCYCLE": "0"},
                                  {"OCTMG_SUBCYCLE_CTAS": "8"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
