@@ -151,7 +151,7 @@ struct Builder {
 
 void read_env(Hier& h) {
   const char* pc = getenv("OCTMG_PASS_CPT");
-  h.pass_cpt = pc ? std::max(1, std::min(2, atoi(pc))) : 2;
+  h.pass_cpt = pc ? (atoi(pc) >= 4 ? 4 : std::max(1, std::min(2, atoi(pc)))) : 4;
   const char* pv = getenv("OCTMG_PASS_V");
   h.pass_v2 = !(pv && std::string(pv) == "1");
   const char* rv = getenv("OCTMG_RESTRICT_V");

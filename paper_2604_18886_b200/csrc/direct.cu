@@ -215,7 +215,7 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
 // Residual + restriction + Avg with the neighbour entries prefetched and, on tiles without a
 // ghost face, the branch-free face sum (every load in flight at once, in-tile neighbours
 // from L1).  Same thread layout and outputs as k_restrict_direct.
-__global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
+__global__ __launch_bounds__(NT, 6) void k_restrict_v2(SmoothArgs a) {
   const int t = a.order[blockIdx.x];
   int nb[6];
   {
@@ -240,12 +240,14 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_v2(SmoothArgs a) {
   for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
   float f0, f1;
   if (!ghost) {
-    const Fld uf = a.u;
-    const int NL = a.NL;
-    auto val2 = [uf, NL](int tt, int o) { return ldpair(tptr(uf, tt, NL), o); };
-    auto val1 = [uf, NL](int tt, int o) { return __ldg(tptr(uf, tt, NL) + o); };
-    const float2 f = row2_faces(a.coef, t, nb, x2, y, z, uu, make_float2(q0.y, q1.y), make_float2(q0.z, q1.z),
-                                make_float2(q0.w, q1.w), make_float2(q0.x * uu.x, q1.x * uu.y), val2, val1);
+    const RowTiles rt = row_tiles(t, nb, y, z);
+    FldVals vals;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) vals.p[f] = tptr(a.u, rt.tf[f], a.NL);
+    const float2 f = row2_faces(vals, rt, x2, y, z, uu, make_float2(q0.y, q1.y), make_float2(q0.z, q1.z),
+                                make_float2(q0.w, q1.w), make_float2(q0.x * uu.x, q1.x * uu.y),
+                                a.coef + ((size_t)rt.tf[1] << 11) + 512, a.coef + ((size_t)rt.tf[3] << 11) + 1024,
+                                a.coef + ((size_t)rt.tf[5] << 11) + 1536);
     f0 = f.x;
     f1 = f.y;
   }
@@ -346,7 +348,8 @@ void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt) {
   if (a.n == 0) return;
   const int mode = a.stage[0] >> 1;
   const bool v2 = cpt & 16;
-  if ((cpt & 15) == 2) launch_pass_cpt<2>(a, mode, s, v2);
+  if ((cpt & 15) == 4) launch_pass_cpt<4>(a, mode, s, v2);
+  else if ((cpt & 15) == 2) launch_pass_cpt<2>(a, mode, s, v2);
   else launch_pass_cpt<1>(a, mode, s, v2);
 }
 

@@ -203,29 +203,24 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
   const float2 c0 = ldpair(cb, off0), cxm = ldpair(cb + 512, off0), cym = ldpair(cb + 1024, off0),
                czm = ldpair(cb + 1536, off0);
   // p = z + beta p_old of any leaf cell (zero on inactive cells, see pval)
-  const float* zp = a.z;
-  const float* po = a.pold;
-  auto val2 = [zp, po, beta](int tt, int o) {
-    const size_t i = (size_t)tt << 9;
-    float2 v = ldpair(zp + i, o);
-    if (po) {
-      const float2 w = ldpair(po + i, o);
-      v.x = fmaf(beta, w.x, v.x);
-      v.y = fmaf(beta, w.y, v.y);
-    }
-    return v;
-  };
-  auto val1 = [zp, po, beta](int tt, int o) {
-    const size_t i = ((size_t)tt << 9) + o;
-    float v = __ldg(zp + i);
-    if (po) v = fmaf(beta, __ldg(po + i), v);
-    return v;
-  };
-  const float2 pp = val2(t, off0);
+  const RowTiles rt = row_tiles(t, nb, y, z);
+  DirVals vals;
+  vals.beta = beta;
+  vals.z = a.z;
+  vals.po = a.pold;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) vals.tf[f] = rt.tf[f];
+  float2 pp = ldpair(a.z + base, off0);
+  if (a.pold) {
+    const float2 w = ldpair(a.pold + base, off0);
+    pp.x = fmaf(beta, w.x, pp.x);
+    pp.y = fmaf(beta, w.y, pp.y);
+  }
   const float p0 = c0.x != 0.0f ? pp.x : 0.0f, p1 = c0.y != 0.0f ? pp.y : 0.0f;
   // same summation order as the general path: c*p, then the faces x-, x+, y-, y+, z-, z+
-  const float2 f = row2_faces(a.coef, t, nb, x2, y, z, pp, cxm, cym, czm, make_float2(c0.x * p0, c0.y * p1),
-                              val2, val1);
+  const float2 f = row2_faces(vals, rt, x2, y, z, pp, cxm, cym, czm, make_float2(c0.x * p0, c0.y * p1),
+                              a.coef + ((size_t)rt.tf[1] << 11) + 512, a.coef + ((size_t)rt.tf[3] << 11) + 1024,
+                              a.coef + ((size_t)rt.tf[5] << 11) + 1536);
   const float r0 = c0.x != 0.0f ? f.x : 0.0f;
   const float r1 = c0.y != 0.0f ? f.y : 0.0f;
   if (a.pnew) {

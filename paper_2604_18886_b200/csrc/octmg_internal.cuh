@@ -284,7 +284,7 @@ struct Hier {
   int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
-  int pass_cpt = 2;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
+  int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
   bool restrict_v2 = true;       // k_restrict_v2: vectorised regular tiles (OCTMG_RESTRICT_V=1: staged k_restrict_direct)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)

@@ -17,47 +17,62 @@ namespace octmg {
 // the two cells of the pair starting at slot sA of a tile-contiguous array
 __device__ __forceinline__ float2 ldpair(const float* p, int sA) { return make_float2(__ldg(p + sA), __ldg(p + (sA ^ 256))); }
 
-// val2(tile, sA) -> float2 of the values of the pair at slots sA, sA ^ 256 of `tile`;
-// val1(tile, s) -> one value.  cxm/cym/czm: the pair's own -face coefficients; s0: the
-// starting sums (the diagonal terms c*u, as the general paths start).  Returns the sums.
-template <class V2, class V1>
-__device__ __forceinline__ float2 row2_faces(const float* coef, int t, const int (&nb)[6], int x2, int y, int z,
-                                             const float2 v, const float2 cxm, const float2 cym, const float2 czm,
-                                             const float2 s0, const V2& val2, const V1& val1) {
+// The tile read across each face of a thread's pair (the own tile inside the tile and at
+// walls; x faces: the row-end tiles, read by every lane) and whether the face is a wall.
+struct RowTiles {
+  int tf[6];
+  bool wall[6];
+};
+__device__ __forceinline__ RowTiles row_tiles(int t, const int (&nb)[6], int y, int z) {
+  RowTiles r;
+  const bool in[6] = {false, false, y > 0, y < 7, z > 0, z < 7};
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    r.wall[f] = !in[f] && nb[f] < 0;
+    r.tf[f] = in[f] || nb[f] < 0 ? t : nb[f];
+  }
+  return r;
+}
+
+// Face sums of the pair.  vals.pair(f, s) / vals.one(f, s): values at slot s of the tile
+// across face f (row_tiles); v: the pair's own values; cxm/cym/czm: its -face
+// coefficients; cxr/cyp/czp planes: the c_x- / c_y- / c_z- planes of the tiles across the
+// x+ (row end) / y+ / z+ faces; s0: the starting sums (the diagonal terms c*u, as the
+// general paths start).
+template <class V>
+__device__ __forceinline__ float2 row2_faces(const V& vals, const RowTiles& rt, int x2, int y, int z, const float2 v,
+                                             const float2 cxm, const float2 cym, const float2 czm, const float2 s0,
+                                             const float* cx_plane, const float* cy_plane, const float* cz_plane) {
   const unsigned FULL = 0xffffffffu;
   const int x0 = 2 * x2;
   // x-neighbours inside the row (lanes j-1, j+1 of the same row)
   float left = __shfl_up_sync(FULL, v.y, 1);
   float right = __shfl_down_sync(FULL, v.x, 1);
   float cxr = __shfl_down_sync(FULL, cxm.x, 1);  // c_x- of cell x0+2 = +x coupling of x0+1
-  // row ends: every lane issues both edge loads (the four lanes of a row hit the same
-  // sectors), so no load waits behind a divergent branch
-  const int nl = nb[0], nr = nb[1];
+  // row ends (every lane issues both loads; the four lanes of a row hit the same sectors)
   const int sl = cslot(7, y, z), sr = cslot(0, y, z);
-  const float wl = val1(nl >= 0 ? nl : t, sl);
-  const float wr = val1(nr >= 0 ? nr : t, sr);
-  const float cr = __ldg(coef + ((size_t)(nr >= 0 ? nr : t) << 11) + 512 + sr);
-  if (x2 == 0) left = nl >= 0 ? wl : 0.0f;
+  const float wl = vals.one(0, sl);
+  const float wr = vals.one(1, sr);
+  const float cr = __ldg(cx_plane + sr);
+  if (x2 == 0) left = rt.wall[0] ? 0.0f : wl;
   if (x2 == 3) {
-    right = nr >= 0 ? wr : 0.0f;
-    cxr = nr >= 0 ? cr : 0.0f;
+    right = rt.wall[1] ? 0.0f : wr;
+    cxr = rt.wall[1] ? 0.0f : cr;
   }
   // the pairs of the y- / y+ / z- / z+ rows: other colour half, q -+ 4 / -+ 32 (wrapped into
   // the neighbour tile: +28 / -28 / +224 / -224)
   const int ob = cslot(x0, y, z) ^ 256;
   const int oym = ob + (y > 0 ? -4 : 28), oyp = ob + (y < 7 ? 4 : -28);
   const int ozm = ob + (z > 0 ? -32 : 224), ozp = ob + (z < 7 ? 32 : -224);
-  const int nym = y > 0 ? t : nb[2], nyp = y < 7 ? t : nb[3];
-  const int nzm = z > 0 ? t : nb[4], nzp = z < 7 ? t : nb[5];
-  float2 vym = val2(nym >= 0 ? nym : t, oym), vyp = val2(nyp >= 0 ? nyp : t, oyp);
-  float2 vzm = val2(nzm >= 0 ? nzm : t, ozm), vzp = val2(nzp >= 0 ? nzp : t, ozp);
-  const float2 cyp = ldpair(coef + ((size_t)(nyp >= 0 ? nyp : t) << 11) + 1024, oyp);
-  const float2 czp = ldpair(coef + ((size_t)(nzp >= 0 ? nzp : t) << 11) + 1536, ozp);
+  float2 vym = vals.pair(2, oym), vyp = vals.pair(3, oyp);
+  float2 vzm = vals.pair(4, ozm), vzp = vals.pair(5, ozp);
+  const float2 cyp = ldpair(cy_plane, oyp);
+  const float2 czp = ldpair(cz_plane, ozp);
   const float2 Z2 = make_float2(0.0f, 0.0f);
-  if (nym < 0) vym = Z2;
-  if (nyp < 0) vyp = Z2;
-  if (nzm < 0) vzm = Z2;
-  if (nzp < 0) vzp = Z2;
+  if (rt.wall[2]) vym = Z2;
+  if (rt.wall[3]) vyp = Z2;
+  if (rt.wall[4]) vzm = Z2;
+  if (rt.wall[5]) vzp = Z2;
   float a0 = fmaf(cxm.x, left, s0.x);
   a0 = fmaf(cxm.y, v.y, a0);
   a0 = fmaf(cym.x, vym.x, a0);
@@ -72,5 +87,36 @@ __device__ __forceinline__ float2 row2_faces(const float* coef, int t, const int
   a1 = fmaf(czp.y, vzp.y, a1);
   return make_float2(a0, a1);
 }
+
+// values of one field (a tile-contiguous leaf/inner pair) across the faces
+struct FldVals {
+  const float* p[6];
+  __device__ __forceinline__ float2 pair(int f, int s) const { return ldpair(p[f], s); }
+  __device__ __forceinline__ float one(int f, int s) const { return __ldg(p[f] + s); }
+};
+// z + beta p_old across the faces (leaf vectors; tiles addressed by index to keep the
+// register footprint small)
+struct DirVals {
+  const float* z;
+  const float* po;  // null: beta = 0
+  int tf[6];
+  float beta;
+  __device__ __forceinline__ float2 pair(int f, int s) const {
+    const size_t b = (size_t)tf[f] << 9;
+    float2 v = ldpair(z + b, s);
+    if (po) {
+      const float2 w = ldpair(po + b, s);
+      v.x = fmaf(beta, w.x, v.x);
+      v.y = fmaf(beta, w.y, v.y);
+    }
+    return v;
+  }
+  __device__ __forceinline__ float one(int f, int s) const {
+    const size_t b = (size_t)tf[f] << 9;
+    float v = __ldg(z + b + s);
+    if (po) v = fmaf(beta, __ldg(po + b + s), v);
+    return v;
+  }
+};
 
 }  // namespace octmg

@@ -37,26 +37,30 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
   const size_t base = (size_t)t * TB3;
   const float* ut = tptr(a.u, t, a.NL);
   const int c[3] = {x, y, z};
+  // every face neighbour is in the other colour half at a fixed slot offset (in the tile or
+  // wrapped into the neighbour tile), see face_sum_regular in direct.cu
+  const int nbase = loff(x, y, z) ^ 256;
+  const int nown = ((x + y + z) & 1) ^ 1;  // colour of every face neighbour
+  const int p = x & 1;
   float s = s0;
 #pragma unroll
   for (int f = 0; f < 6; ++f) {
     const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
-    int nc[3] = {c[0], c[1], c[2]};
-    nc[ax] += sg;
+    const bool inside = c[ax] + sg >= 0 && c[ax] + sg < 8;
+    const int dlt = f == 0 ? (inside ? p - 1 : 3) : f == 1 ? (inside ? p : -3) : f == 2 ? (inside ? -4 : 28)
+                  : f == 3 ? (inside ? 4 : -28) : f == 4 ? (inside ? -32 : 224) : (inside ? 32 : -224);
+    const int no = nbase + dlt;
     float v = 0.0f, cf = (f & 1) ? 0.0f : comp(q, ax);
-    if (nc[ax] >= 0 && nc[ax] < 8) {
-      const int no = loff(nc[0], nc[1], nc[2]);
+    if (inside) {
       v = su ? su[no] : ldv<NC>(ut + no);  // su: this tile's values staged in shared memory
-      if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
-      if (f & 1) cf = scm ? scm[ax][no] : comp(ldcoef(a.coef, base + no), ax);  // scm: staged SoA
+      if (ZERO_OWN && nown == colour) v = 0.0f;
+      if (f & 1) cf = scm ? scm[ax][no] : __ldg(a.coef + cidx(base + no, 1 + ax));  // scm: staged SoA
     } else {
       const int n = __ldg(a.nbr + 6 * t + f);
-      nc[ax] &= 7;
-      const int no = loff(nc[0], nc[1], nc[2]);
       if (n >= 0) {
         v = ldv<NC>(tptr(a.u, n, a.NL) + no);
-        if (ZERO_OWN && (((nc[0] + nc[1] + nc[2]) & 1) == colour)) v = 0.0f;
-        if (f & 1) cf = comp(ldcoef(a.coef, (size_t)n * TB3 + no), ax);
+        if (ZERO_OWN && nown == colour) v = 0.0f;
+        if (f & 1) cf = __ldg(a.coef + cidx((size_t)n * TB3 + no, 1 + ax));
       } else if (n <= -2) {
         if (f & 1)
           cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 +
@@ -91,14 +95,17 @@ __device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, i
   const float* ut = tptr(a.u, t, a.NL);
   float sm = 0.0f;
   int nn = 0;
+  // the block's cells: q0 + 4 dy + 32 dz in the half of colour (dx + dy + dz) & 1 (the
+  // block corner (x&~1, y&~1, z&~1) has even coordinates, hence colour 0)
+  const int q0 = (x >> 1) + 4 * (y & ~1) + 32 * (z & ~1);
   for (int dz = 0; dz < 2; ++dz)
     for (int dy = 0; dy < 2; ++dy)
       for (int dx = 0; dx < 2; ++dx) {
-        const int bx = (x & ~1) + dx, by = (y & ~1) + dy, bz = (z & ~1) + dz;
-        const int bo = loff(bx, by, bz);
-        if (ldcoef(a.coef, base + bo).x != 0.0f) {
+        const int cb = (dx + dy + dz) & 1;
+        const int bo = (cb << 8) + q0 + 4 * dy + 32 * dz;
+        if (__ldg(a.coef + cidx(base + bo, 0)) != 0.0f) {
           float bv = ldv<NC>(ut + bo);
-          if (ZERO_OWN && ((bx + by + bz) & 1) == colour) bv = 0.0f;
+          if (ZERO_OWN && cb == colour) bv = 0.0f;
           sm += bv;
           nn++;
         }
