@@ -276,8 +276,9 @@ octmg_status octmg_mg_solve(octmg_hier* h, const float* b, float* x, const octmg
 /* Per-kernel-class device time of the work issued since the last reset while profiling
  * is on (CUDA events bracketing each launch on the launch stream; CUDA-graph replay is
  * disabled while profiling), with the launch count and the ALGORITHMIC bytes those
- * launches must move at minimum (e.g. 28 B per cell for an RBGS
- * pass: read u, b, the 16-byte coefficient record, write u).  names/ms/counts/bytes:
+ * launches must move at minimum (e.g. 20 B per cell for an RBGS
+ * colour pass in the colour-split cell order: the other colour's u and coupling planes,
+ * its own colour's b and coefficient record, its own u written).  names/ms/counts/bytes:
  * arrays of cap entries (any may be NULL); *n = number of classes.  Synchronises. */
 octmg_status octmg_profile_enable(octmg_hier* h, int32_t on);
 octmg_status octmg_profile_read(octmg_hier* h, const char** names, double* ms, int64_t* counts,

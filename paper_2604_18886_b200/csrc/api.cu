@@ -272,8 +272,8 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     return;
   }
   if (op.kind == 3) {
-    // read u, record; write u (8 + 16 B/cell) + the parents' u, u* (1 B/cell)
-    ProfScope ps(h, KC_PROLONG, s, 25.0 * a.n * TB3);
+    // read u and the c plane, write u (12 B/cell) + the parents' u, u* (1 B/cell)
+    ProfScope ps(h, KC_PROLONG, s, 13.0 * a.n * TB3);
     launch_prolong(a, s);
     return;
   }
@@ -285,11 +285,13 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     return;
   }
   const int mode = op.stage >> 1;
-  // algorithmic bytes per cell of the level: colour pass = read u, b, 16-byte record, write
-  // u (28 B; 24 B when u is known zero); restrict = read u, b, record (24 B) + the parents'
-  // u, u*, b (1.5 B); prolongation-fused passes read the parents' u, u* (+1 B)
+  // algorithmic bytes per cell of the level (colour-split slot order): a colour pass reads
+  // the other colour's u (2 B), its own colour's b (2 B) and 4 coefficient planes (8 B), the
+  // other colour's 3 coupling planes (6 B) and writes its own u (2 B): 20 B; the first pass
+  // of a cycle (u known 0: u = b / c) 6 B; restrict = read u, b, record (24 B) + the
+  // parents' u, u*, b (1.5 B); prolongation-fused passes read the parents' u, u* (+1 B)
   const double cells = (double)a.n * TB3;
-  double bytes = cells * (mode == SM_RESTRICT ? 25.5 : (mode == SM_ZERO1 ? 24.0 : 28.0));
+  double bytes = cells * (mode == SM_RESTRICT ? 25.5 : (mode == SM_ZERO1 ? 6.0 : 20.0));
   if (mode == SM_PRO1 || mode == SM_PRO2) bytes += cells;
   int cls = mode == SM_RESTRICT ? KC_RESTRICT
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
