@@ -81,6 +81,32 @@ __device__ __forceinline__ void phase_end(const SubArgs& A, unsigned& epoch) {
   else __syncthreads();
 }
 
+// Face sum of a cell of a tile with no ghost face (as face_sum_regular in direct.cu, with
+// the sub-cycle's load path M for the values): every neighbour is in the other colour half
+// at a fixed slot offset, in this tile or wrapped into the face-neighbour tile.
+template <int M>
+__device__ __forceinline__ float face_sum_reg(const SmoothArgs& a, int t, const int (&nb)[6], int sl, int x, int y,
+                                              int z, const float4& q, float s0 = 0.0f) {
+  const int base = sl ^ 256;
+  const int p = x & 1;
+  const bool in[6] = {x > 0, x < 7, y > 0, y < 7, z > 0, z < 7};
+  const int dlt[6] = {in[0] ? p - 1 : 3, in[1] ? p : -3, in[2] ? -4 : 28, in[3] ? 4 : -28, in[4] ? -32 : 224,
+                      in[5] ? 32 : -224};
+  float s = s0;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1;
+    const bool wall = !in[f] && nb[f] < 0;
+    const int tn = in[f] || wall ? t : nb[f];
+    const int no = base + dlt[f];
+    float v = ldv<M>(tptr(a.u, tn, a.NL) + no);
+    const float cf = (f & 1) ? __ldg(a.coef + ((size_t)tn << 11) + ((1 + ax) << 9) + no) : comp(q, ax);
+    if (wall) v = 0.0f;
+    s = fmaf(cf, v, s);
+  }
+  return s;
+}
+
 template <int PM, int M>
 __device__ __noinline__ void sc_pass(const SubArgs& A, int l, int colour, int mode, unsigned& epoch) {
   constexpr int MAXK = PM == 1 ? GRID_MAX_PER_THREAD : SUB_MAX_PER_THREAD;
@@ -106,13 +132,24 @@ __device__ __noinline__ void sc_pass(const SubArgs& A, int l, int colour, int mo
         unew[k] = b / q.x;
       } else {
         const bool z2 = mode == SM_ZERO2;
-        float ui = 0.0f, mP = 0.0f;
-        if (has_ghost(a, t)) {
-          ui = z2 ? 0.0f : ldv<M>(ut + off);
-          mP = z2 ? block_mean<true, M>(a, t, x, y, z, colour) : block_mean<false, M>(a, t, x, y, z, colour);
+        int nb[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) nb[f] = __ldg(a.nbr + 6 * t + f);
+        bool ghost = false;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
+        float fs;
+        if (!ghost) {  // (face neighbours have the other colour: ZERO2 reads them as PLAIN does)
+          fs = face_sum_reg<M>(a, t, nb, off, x, y, z, q);  // slot-offset stencil, no ghosts
+        } else {
+          float ui = 0.0f, mP = 0.0f;
+          if (ghost) {
+            ui = z2 ? 0.0f : ldv<M>(ut + off);
+            mP = z2 ? block_mean<true, M>(a, t, x, y, z, colour) : block_mean<false, M>(a, t, x, y, z, colour);
+          }
+          fs = z2 ? face_sum<true, M>(a, t, x, y, z, q, ui, mP, colour, 0.0f)
+                  : face_sum<false, M>(a, t, x, y, z, q, ui, mP, colour, 0.0f);
         }
-        const float fs = z2 ? face_sum<true, M>(a, t, x, y, z, q, ui, mP, colour, 0.0f)
-                            : face_sum<false, M>(a, t, x, y, z, q, ui, mP, colour, 0.0f);
         unew[k] = (b - fs) / q.x;
       }
       dst[k] = ut + off;
@@ -167,8 +204,19 @@ __device__ __noinline__ void sc_restrict(const SubArgs& A, int l, unsigned& epoc
       na += __shfl_xor_sync(0xffffffffu, na, 8);
       const float mP = na ? su / (float)na : 0.0f;
       float r0 = 0.0f, r1 = 0.0f;
-      if (q0.x != 0.0f) r0 = b0 - face_sum<false, M>(a, t, x0, y, z, q0, u0, mP, 0, q0.x * u0);
-      if (q1.x != 0.0f) r1 = b1 - face_sum<false, M>(a, t, x0 + 1, y, z, q1, u1, mP, 0, q1.x * u1);
+      int nb[6];
+#pragma unroll
+      for (int f = 0; f < 6; ++f) nb[f] = __ldg(a.nbr + 6 * t + f);
+      bool ghost = false;
+#pragma unroll
+      for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
+      if (!ghost) {
+        if (q0.x != 0.0f) r0 = b0 - face_sum_reg<M>(a, t, nb, off0, x0, y, z, q0, q0.x * u0);
+        if (q1.x != 0.0f) r1 = b1 - face_sum_reg<M>(a, t, nb, off1, x0 + 1, y, z, q1, q1.x * u1);
+      } else {
+        if (q0.x != 0.0f) r0 = b0 - face_sum<false, M>(a, t, x0, y, z, q0, u0, mP, 0, q0.x * u0);
+        if (q1.x != 0.0f) r1 = b1 - face_sum<false, M>(a, t, x0 + 1, y, z, q1, u1, mP, 0, q1.x * u1);
+      }
       float rs = r0 + r1;
       rs += __shfl_xor_sync(0xffffffffu, rs, 4);
       rs += __shfl_xor_sync(0xffffffffu, rs, 8);
