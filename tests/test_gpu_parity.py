@@ -306,3 +306,53 @@ def test_loopback_partition_matches_single(om, name, parts):
     assert rp["converged"] and abs(r1["iters"] - rp["iters"]) <= 1
     a1, ap = x1.cpu().numpy().astype(np.float64), xp.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(a1 - ap) <= 1e-5 * np.linalg.norm(a1)
+
+
+def _full_size_apply_and_residual(om, cfg, kind, w, b, mu):
+    """Full-size check in the bench's launch configuration: the device apply of a random
+    vector against the oracle's (every row), and the device solve's normwise backward error
+    eta = ||b - A x||_inf / (||A||_inf ||x||_inf + ||b||_inf) with the fp64 oracle operator
+    (a property that holds at any size: the fp32 iterate is the exact solution of a system
+    within eta of the oracle's; an fp32 solution cannot do better than ~1e-7, and its 2-norm
+    relative residual is floored near 1e-3 here by the rounding of x on 1e-3-size cells)."""
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    kd = torch.from_numpy(kind).to(DEV)
+    wd = None if w is None else torch.from_numpy(np.ascontiguousarray(w)).to(DEV)
+    h = om.Hierarchy(tree, kd, face_frac=wd, mu=mu)
+    del wd
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    o.setup(kind, w)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(o.N).astype(np.float32)
+    y = torch.zeros(o.N, device=DEV)
+    h.apply(torch.from_numpy(x).to(DEV), y)
+    assert _rel(y.cpu().numpy().astype(np.float64), o.apply(x.astype(np.float64))) <= 1e-5
+    bd = torch.from_numpy(b).to(DEV)
+    xg = torch.zeros_like(bd)
+    rep = h.pcg_solve(bd, xg, rtol=1e-6)
+    assert rep["converged"] and rep["iters"] <= 9, rep["iters"]
+    act = o.coefs()[:o.N, 0] != 0
+    bb = np.where(act, b.astype(np.float64), 0.0)
+    if not any(cfg["wall_bc"]) and not np.any(kind == 1):  # pure Neumann: the projected rhs
+        bb = bb - bb[act].mean() * act
+    xs = xg.cpu().numpy().astype(np.float64)
+    res = bb - o.apply(xs)
+    cf = o.coefs()
+    anorm = 2.0 * np.abs(cf[:o.N, 0]).max()  # ||A||_inf <= 2 max c_i (diagonal dominance)
+    eta = np.abs(res[act]).max() / (anorm * np.abs(xs[act]).max() + np.abs(bb[act]).max())
+    assert eta <= 5e-6, eta
+    return rep
+
+
+@pytest.mark.slow
+def test_full_size_cfg3_apply_and_true_residual(om):
+    cfg = make_config("cfg3_sphere")  # 60.1M leaves, V-cycle
+    _full_size_apply_and_residual(om, cfg, cfg["kind"], cfg["w"], cfg["b"], cfg["mu"])
+
+
+@pytest.mark.slow
+def test_full_size_cfg4_apply_and_true_residual(om):
+    from oracle.oracle import tank_fields
+    cfg = make_config("cfg4_tank", with_fields=False)  # 155.2M leaves, W-cycle, cut cells
+    kind, w, b = tank_fields(cfg["tiles"], radius=cfg["radius"])
+    _full_size_apply_and_residual(om, cfg, kind, w, b, cfg["mu"])
