@@ -71,7 +71,8 @@ typedef struct {
   uint8_t wall_bc[6];  /* per domain face x-,x+,y-,y+,z-,z+: 0 Neumann, 1 Dirichlet p=0
                           at the centre of a virtual wall cell of the boundary cell's
                           size (P:L328-330 ghost-fluid Dirichlet)                         */
-  int32_t grade_repair;/* must be 0: ungraded input is rejected with NOT_GRADED          */
+  int32_t grade_repair;/* 0: ungraded input is rejected with NOT_GRADED; 1: the list is first
+                          repaired on the host (octmg_grade_repair_host)                 */
   int32_t rank, nranks;/* this process's rank and the number of ranks (1 = single GPU)    */
   void* nccl_comm;     /* ncclComm_t over the nranks GPUs (octmg_nccl_comm_init), or NULL
                           when nranks == 1.  The leaf-tile list is replicated on all ranks;
@@ -221,6 +222,32 @@ octmg_status octmg_divergence(const octmg_hier* h, const float* face_frac, const
                               octmg_stream stream);
 octmg_status octmg_subtract_gradient(const octmg_hier* h, const uint8_t* kind, const float* face_beta,
                                      const float* face_frac, const float* p, float* u6, octmg_stream stream);
+
+/*
+ * 2:1 face-grading repair on the host (no device needed, SPEC S:L82;
+ * grading P:L548-550): every leaf tile that covers an in-domain face-neighbour position of
+ * a leaf two or more levels finer is replaced by its 8 children, to fixpoint (the least
+ * graded refinement of the input; the order of the input does not matter).  tiles: n leaf
+ * tiles (host); ext3: the domain in level-0 tiles; out: host array of cap tiles (any
+ * order).  *n_out = the repaired count; if cap is too small nothing is written and the
+ * call fails with OCTMG_E_INVALID (call again with *n_out).
+ */
+octmg_status octmg_grade_repair_host(const octmg_tile* tiles, int64_t n, const int32_t* ext3, octmg_tile* out,
+                                     int64_t cap, int64_t* n_out);
+
+/*
+ * Allocator hook: every persistent device buffer of the handles created afterwards (tree
+ * tables, coefficient store, multigrid and PCG buffers, halo buffers) is obtained with
+ * alloc(bytes, stream, ctx) and returned with release(ptr, stream, ctx) (stream = NULL:
+ * the legacy default stream), e.g. to draw from PyTorch's caching allocator.  Each
+ * pointer is released through the allocator that made it, so the hook may change between
+ * handles.  Short-lived setup temporaries still use cudaMalloc(Async).  NULL, NULL restores
+ * cudaMalloc / cudaFree.  alloc returns NULL on failure (the call then fails with
+ * OCTMG_E_OOM).  Process-wide; thread-safe.
+ */
+typedef void* (*octmg_alloc_fn)(size_t bytes, octmg_stream stream, void* ctx);
+typedef void (*octmg_free_fn)(void* ptr, octmg_stream stream, void* ctx);
+octmg_status octmg_set_allocator(octmg_alloc_fn alloc, octmg_free_fn release, void* ctx);
 
 /* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
  * in tile order.  Synchronises `stream` of the last call. */

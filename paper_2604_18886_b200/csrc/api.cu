@@ -1,5 +1,7 @@
 // C-ABI entry points (include/octmg.h), hierarchy management, the unrolled mu-cycle
 // schedule (captured once into a CUDA graph) and the PCG driver (Alg. 1).
+#include <mutex>
+#include <unordered_map>
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -26,13 +28,48 @@ const char* kclass_name[KC_COUNT] = {"rbgs_pass", "prolong", "residual_restrict"
                                      "init", "setup", "memset", "coarse_subcycle", "rbgs_fused_iteration",
                                      "copy_level", "coarse_grid"};
 
+// ------------------------------------------------------------------------------------
+// allocator hook (octmg_set_allocator)
+// ------------------------------------------------------------------------------------
+namespace {
+struct Allocator {
+  octmg_alloc_fn alloc = nullptr;
+  octmg_free_fn release = nullptr;
+  void* ctx = nullptr;
+};
+std::mutex g_alloc_mu;
+Allocator g_alloc;                                  // current (nullptr: cudaMalloc)
+std::unordered_map<void*, Allocator> g_alloc_owner;  // who made each live pointer
+}  // namespace
+
+void* dev_malloc(size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  void* q = nullptr;
+  if (g_alloc.alloc) {
+    q = g_alloc.alloc(bytes, nullptr, g_alloc.ctx);
+  } else if (cudaMalloc(&q, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    q = nullptr;
+  }
+  if (q) g_alloc_owner[q] = g_alloc;
+  return q;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  auto it = g_alloc_owner.find(p);
+  Allocator a = it == g_alloc_owner.end() ? Allocator{} : it->second;
+  if (it != g_alloc_owner.end()) g_alloc_owner.erase(it);
+  if (a.release) a.release(p, nullptr, a.ctx);
+  else cudaFree(p);
+}
+
 template <class T>
 static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
-  void* q = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
-  if (e != cudaSuccess) {
-    cudaGetLastError();
+  void* q = dev_malloc(count * sizeof(T));
+  if (!q) {
     set_error("device allocation failed (" + std::to_string(count * sizeof(T)) + " bytes)");
     return OCTMG_E_OOM;
   }
@@ -43,7 +80,7 @@ static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
 
 Hier::~Hier() {
   for (auto e : event_pool) cudaEventDestroy(e);
-  for (void* p : allocs) cudaFree(p);
+  for (void* p : allocs) dev_free(p);
   if (sc_host) cudaFreeHost(sc_host);
 }
 
@@ -364,13 +401,36 @@ const char* octmg_last_error(void) { return g_err.c_str(); }
 
 const char* octmg_version(void) { return "octmg 0.1.0 (sm_100a, fp32 fields / fp64 dots)"; }
 
+octmg_status octmg_set_allocator(octmg_alloc_fn alloc, octmg_free_fn release, void* ctx) {
+  if ((alloc == nullptr) != (release == nullptr)) {
+    set_error("alloc and release must both be set or both be NULL");
+    return OCTMG_E_INVALID;
+  }
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  g_alloc.alloc = alloc;
+  g_alloc.release = release;
+  g_alloc.ctx = ctx;
+  return OCTMG_OK;
+}
+
 octmg_status octmg_build_tree(const octmg_tree_desc* desc, const octmg_tile* leaf_tiles_host, int64_t n,
                               octmg_stream stream, octmg_tree** out) {
   if (!desc || !leaf_tiles_host || !out) { set_error("null argument"); return OCTMG_E_INVALID; }
   *out = nullptr;
   auto* t = new (std::nothrow) octmg_tree();
   if (!t) { set_error("host allocation failed"); return OCTMG_E_OOM; }
-  octmg_status st = build_tree(desc, leaf_tiles_host, n, (cudaStream_t)stream, &t->t);
+  octmg_status st;
+  if (desc->grade_repair == 1) {  // refine the coarser side to fixpoint first (host)
+    std::vector<octmg_tile> rep;
+    st = n < 0 ? OCTMG_E_INVALID : grade_repair(leaf_tiles_host, n, desc->ext, rep);
+    if (st == OCTMG_OK) {
+      octmg_tree_desc d2 = *desc;
+      d2.grade_repair = 0;
+      st = build_tree(&d2, rep.data(), (int64_t)rep.size(), (cudaStream_t)stream, &t->t);
+    }
+  } else {
+    st = build_tree(desc, leaf_tiles_host, n, (cudaStream_t)stream, &t->t);
+  }
   if (st != OCTMG_OK) { delete t; return st; }
   *out = t;
   return OCTMG_OK;

@@ -56,9 +56,8 @@ __global__ void k_sum_scalars(Scalars* const* scs, int nparts, int first, int co
 
 template <class T>
 octmg_status dalloc(std::vector<void*>& list, T** p, size_t count) {
-  void* q = nullptr;
-  if (cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) {
-    cudaGetLastError();
+  void* q = dev_malloc(std::max<size_t>(count, 1) * sizeof(T));
+  if (!q) {
     set_error("device allocation failed (halo buffers)");
     return OCTMG_E_OOM;
   }
@@ -262,7 +261,7 @@ struct NcclComm : Comm {
 }  // namespace
 
 PartLinks::~PartLinks() {
-  for (void* p : allocs) cudaFree(p);
+  for (void* p : allocs) dev_free(p);
 }
 
 Comm* make_loopback_comm() { return new LoopbackComm(); }

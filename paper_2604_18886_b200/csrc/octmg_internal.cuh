@@ -34,6 +34,11 @@ octmg_status cuda_status(cudaError_t e, const char* what);
     if (s_ != OCTMG_OK) return s_;                                         \
   } while (0)
 
+// Device memory of the handles (octmg_set_allocator): allocations go through the allocator
+// current at allocation time, and each pointer is released through the one that made it.
+void* dev_malloc(size_t bytes);  // nullptr on failure
+void dev_free(void* p);
+
 // ------------------------------------------------------------------------------------
 // Tree (device tables + host metadata)
 // ------------------------------------------------------------------------------------
@@ -236,6 +241,9 @@ octmg_status subtract_gradient(const Hier& h, const uint8_t* kind, const float* 
 // cut-cell geometry of the tank scene (geometry.cu)
 octmg_status tank_fields(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac, float* b,
                          cudaStream_t s);
+
+// 2:1 grading repair of a leaf-tile list (grade.cpp, host)
+octmg_status grade_repair(const octmg_tile* in, int64_t n, const int32_t* ext, std::vector<octmg_tile>& out);
 
 // tree build (tree.cu)
 octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, int64_t n, cudaStream_t s,

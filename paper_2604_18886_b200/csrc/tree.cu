@@ -169,11 +169,9 @@ inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 template <class T>
 static octmg_status dalloc(std::vector<void*>& list, T** p, size_t count) {
-  void* q = nullptr;
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
-  if (e != cudaSuccess) {
-    cudaGetLastError();
+  void* q = dev_malloc(count * sizeof(T));
+  if (!q) {
     set_error("device allocation failed");
     return OCTMG_E_OOM;
   }
@@ -183,7 +181,7 @@ static octmg_status dalloc(std::vector<void*>& list, T** p, size_t count) {
 }
 
 Tree::~Tree() {
-  for (void* p : allocs) cudaFree(p);
+  for (void* p : allocs) dev_free(p);
 }
 
 octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, int64_t n, cudaStream_t s,
@@ -197,7 +195,7 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
     if (desc->wall_bc[f] > 1) { set_error("wall_bc must be 0 or 1"); return OCTMG_E_INVALID; }
     T->wall[f] = desc->wall_bc[f];
   }
-  if (desc->grade_repair != 0) { set_error("grade_repair is not supported; pass a graded tree"); return OCTMG_E_INVALID; }
+  if (desc->grade_repair != 0) { set_error("grade_repair must be 0 or 1"); return OCTMG_E_INVALID; }  // 1: api.cu repairs first
   if (desc->nranks < 1 || desc->nranks > 64 || desc->rank < 0 || desc->rank >= desc->nranks ||
       (desc->nranks > 1 && !desc->nccl_comm)) {
     set_error("bad rank / nranks / nccl_comm");

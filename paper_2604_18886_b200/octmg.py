@@ -62,7 +62,8 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_setup_hierarchy_loopback", "octmg_partition_info", "octmg_nccl_unique_id",
                "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
                "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields",
-               "octmg_divergence", "octmg_subtract_gradient"]
+               "octmg_divergence", "octmg_subtract_gradient",
+               "octmg_grade_repair_host", "octmg_set_allocator"]
 
 _lib = None
 
@@ -89,6 +90,10 @@ def lib():
         L.octmg_mg_solve.restype = C.c_int
         L.octmg_tank_fields.argtypes = [P, P, C.c_double, P, P, P, P]
         L.octmg_tank_fields.restype = C.c_int
+        L.octmg_set_allocator.argtypes = [P, P, P]
+        L.octmg_set_allocator.restype = C.c_int
+        L.octmg_grade_repair_host.argtypes = [P, I64, P, P, I64, P]
+        L.octmg_grade_repair_host.restype = C.c_int
         L.octmg_divergence.argtypes = [P, P, P, P, P]
         L.octmg_divergence.restype = C.c_int
         L.octmg_subtract_gradient.argtypes = [P, P, P, P, P, P, P]
@@ -161,14 +166,15 @@ class NcclComm:
 class Tree:
     """octmg_build_tree: graded leaf tiles (host int array (n,4): level,i,j,k)."""
 
-    def __init__(self, tiles, ext=(1, 1, 1), wall_bc=(1, 1, 1, 1, 1, 1), stream=None, comm: "NcclComm" = None):
+    def __init__(self, tiles, ext=(1, 1, 1), wall_bc=(1, 1, 1, 1, 1, 1), stream=None, comm: "NcclComm" = None,
+                 grade_repair: bool = False):
         t = np.ascontiguousarray(np.asarray(tiles, dtype=np.int32).reshape(-1, 4))
         d = TreeDesc()
         for a in range(3):
             d.ext[a] = int(ext[a])
         for f in range(6):
             d.wall_bc[f] = int(wall_bc[f])
-        d.grade_repair = 0
+        d.grade_repair = 1 if grade_repair else 0
         if comm is None:
             d.rank, d.nranks, d.nccl_comm = 0, 1, None
         else:
@@ -322,6 +328,54 @@ class Hierarchy:
                 self._h = None
         except Exception:
             pass
+
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+_allocator_refs = []  # keep the ctypes callbacks alive
+
+
+def set_allocator(alloc=None, release=None):
+    """octmg_set_allocator with Python callables alloc(nbytes) -> int and release(ptr);
+    None, None restores cudaMalloc."""
+    if alloc is None:
+        _check(lib().octmg_set_allocator(None, None, None))
+        return
+    fa = _ALLOC_FN(lambda n, stream, ctx: alloc(int(n)) or None)
+    ff = _FREE_FN(lambda p, stream, ctx: release(int(p)))
+    _allocator_refs.append((fa, ff))
+    _check(lib().octmg_set_allocator(C.cast(fa, C.c_void_p), C.cast(ff, C.c_void_p), None))
+
+
+def use_torch_allocator():
+    """Draw the library's device buffers from PyTorch's caching allocator."""
+    import torch
+
+    def alloc(n):
+        try:
+            return torch.cuda.caching_allocator_alloc(n)
+        except RuntimeError:
+            return 0
+
+    set_allocator(alloc, torch.cuda.caching_allocator_delete)
+
+
+def grade_repair_host(tiles, ext=(1, 1, 1)):
+    """octmg_grade_repair_host: the least 2:1-graded refinement of a leaf-tile list (host, no GPU)."""
+    t = np.ascontiguousarray(np.asarray(tiles, dtype=np.int32).reshape(-1, 4))
+    e = np.asarray(ext, dtype=np.int32)
+    n_out = C.c_int64()
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    cap = 8 * len(t) + 64
+    while True:
+        out = np.zeros((cap, 4), dtype=np.int32)
+        st = lib().octmg_grade_repair_host(vp(t), len(t), vp(e), vp(out), cap, C.byref(n_out))
+        if st == 0:
+            return out[:n_out.value].copy()
+        if n_out.value > cap:
+            cap = n_out.value
+            continue
+        _check(st)
 
 
 def partition_plan_host(tables, L, NL, NI, level_counts, nranks):

@@ -356,3 +356,31 @@ def test_full_size_cfg4_apply_and_true_residual(om):
     cfg = make_config("cfg4_tank", with_fields=False)  # 155.2M leaves, W-cycle, cut cells
     kind, w, b = tank_fields(cfg["tiles"], radius=cfg["radius"])
     _full_size_apply_and_residual(om, cfg, kind, w, b, cfg["mu"])
+
+
+def test_grade_repair_on_build_and_torch_allocator(om):
+    """octmg_build_tree with grade_repair = 1 on an unrepaired sphere band equals the build of
+    the repaired list (bit-exact tables); a hierarchy built through the allocator hook
+    (PyTorch's caching allocator) solves identically to one on cudaMalloc."""
+    raw = sphere_band_tiles(2, 2, r=0.25, repair=False)
+    t1 = om.Tree(raw, grade_repair=True)
+    rep = om.grade_repair_host(raw)
+    t2 = om.Tree(rep)
+    for k, v in t1.tables().items():
+        assert np.array_equal(v, t2.tables()[k]), k
+    cfg = make_config("sphere_small_dir")
+    tree, h, o = _setup(om, cfg)
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    x1 = torch.zeros_like(b)
+    h.pcg_solve(b, x1)
+    before = torch.cuda.memory_allocated()
+    om.use_torch_allocator()
+    try:
+        tree2, h2, _ = _setup(om, cfg)
+        assert torch.cuda.memory_allocated() > before  # the library's buffers come from torch
+        x2 = torch.zeros_like(b)
+        h2.pcg_solve(b, x2)
+        assert torch.equal(x1, x2)
+        del h2, tree2
+    finally:
+        om.set_allocator(None, None)
