@@ -205,7 +205,7 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
   T->nranks = desc->nranks;
   T->nccl_comm = desc->nccl_comm;
   std::vector<void*> tmp;  // freed at exit
-  struct Guard { std::vector<void*>& v; ~Guard() { for (void* p : v) cudaFree(p); } } guard{tmp};
+  struct Guard { std::vector<void*>& v; ~Guard() { for (void* p : v) dev_free(p); } } guard{tmp};
   Ext ext{{T->ext[0], T->ext[1], T->ext[2]}};
   int nl = (int)n;
 
