@@ -33,7 +33,8 @@ __device__ __forceinline__ int pcell_of(int4 tv, int x, int y, int z) {
 template <bool ZERO_OWN, int NC = 1>
 __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int y, int z, const float4& q,
                                           float ui, float mP, int colour, float s0, const float* su = nullptr,
-                                          const float (*scm)[TB3] = nullptr) {
+                                          const float (*scm)[TB3] = nullptr, const int* nbp = nullptr,
+                                          const int4* tvp = nullptr) {
   const size_t base = (size_t)t * TB3;
   const float* ut = tptr(a.u, t, a.NL);
   const int c[3] = {x, y, z};
@@ -56,7 +57,7 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
       if (ZERO_OWN && nown == colour) v = 0.0f;
       if (f & 1) cf = scm ? scm[ax][no] : __ldg(a.coef + cidx(base + no, 1 + ax));  // scm: staged SoA
     } else {
-      const int n = __ldg(a.nbr + 6 * t + f);
+      const int n = nbp ? nbp[f] : __ldg(a.nbr + 6 * t + f);  // nbp: the caller's prefetched entries
       if (n >= 0) {
         v = ldv<NC>(tptr(a.u, n, a.NL) + no);
         if (ZERO_OWN && nown == colour) v = 0.0f;
@@ -66,14 +67,14 @@ __device__ __forceinline__ float face_sum(const SmoothArgs& a, int t, int x, int
           cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 +
                      (ax == 0 ? y + 8 * z : (ax == 1 ? x + 8 * z : x + 8 * y)));
         const int C = -2 - n;
-        const int4 tv = __ldg(a.tile + t);
+        const int4 tv = tvp ? *tvp : __ldg(a.tile + t);
         int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
         g[ax] += sg;
         const int co = loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
-        if (ldcoef(a.coef, (size_t)C * TB3 + co).x != 0.0f) {
-          const float uc = ZERO_OWN ? 0.0f : ldv<NC>(tptr(a.uc, C, a.NL) + co);
-          v = ui + 0.5f * (uc - mP);
-        }
+        // the coarse leaf's activity and value are loaded together (no dependent load)
+        const float cC = __ldg(a.coef + cidx((size_t)C * TB3 + co, 0));
+        const float uc = ZERO_OWN ? 0.0f : ldv<NC>(tptr(a.uc, C, a.NL) + co);
+        if (cC != 0.0f) v = ui + 0.5f * (uc - mP);
       }
     }
     s = fmaf(cf, v, s);
