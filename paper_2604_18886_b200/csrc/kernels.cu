@@ -86,14 +86,17 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
           v = pval(a, beta, (size_t)n * TB3 + no);
         } else {
           const int ct = __ldg(a.child + 8 * (n - a.NL) + (nc[0] >> 2) + 2 * (nc[1] >> 2) + 4 * (nc[2] >> 2));
+          // the 8 children: activity and value loaded together (no load behind a branch)
           float sm = 0.0f;
           int k = 0;
-          for (int dz = 0; dz < 2; ++dz)
-            for (int dy = 0; dy < 2; ++dy)
-              for (int dx = 0; dx < 2; ++dx) {
-                const size_t ci = (size_t)ct * TB3 + loff((2 * nc[0] + dx) & 7, (2 * nc[1] + dy) & 7, (2 * nc[2] + dz) & 7);
-                if (ldcoef(a.coef, ci).x != 0.0f) { sm += pval(a, beta, ci); k++; }
-              }
+#pragma unroll
+          for (int d = 0; d < 8; ++d) {
+            const size_t ci = (size_t)ct * TB3 + loff((2 * nc[0] + (d & 1)) & 7, (2 * nc[1] + ((d >> 1) & 1)) & 7,
+                                                      (2 * nc[2] + (d >> 2)) & 7);
+            const float cc = __ldg(a.coef + cidx(ci, 0));
+            const float pv = pval(a, beta, ci);
+            if (cc != 0.0f) { sm += pv; k++; }
+          }
           v = k ? sm / (float)k : 0.0f;
         }
       } else if (n <= -2) {
@@ -105,7 +108,9 @@ __device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta,
         int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
         g[ax] += sg;
         const size_t ci = (size_t)C * TB3 + loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
-        if (ldcoef(a.coef, ci).x != 0.0f) v = pi + 0.5f * (pval(a, beta, ci) - mP);
+        const float cC = __ldg(a.coef + cidx(ci, 0));
+        const float pC = pval(a, beta, ci);
+        if (cC != 0.0f) v = pi + 0.5f * (pC - mP);
       }
     }
     s = fmaf(cf, v, s);

@@ -104,8 +104,9 @@ __device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, i
       for (int dx = 0; dx < 2; ++dx) {
         const int cb = (dx + dy + dz) & 1;
         const int bo = (cb << 8) + q0 + 4 * dy + 32 * dz;
-        if (__ldg(a.coef + cidx(base + bo, 0)) != 0.0f) {
-          float bv = ldv<NC>(ut + bo);
+        const float cc = __ldg(a.coef + cidx(base + bo, 0));
+        float bv = ldv<NC>(ut + bo);  // loaded with the activity (no load behind a branch)
+        if (cc != 0.0f) {
           if (ZERO_OWN && cb == colour) bv = 0.0f;
           sm += bv;
           nn++;
