@@ -280,8 +280,10 @@ __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, in
 // activity nibble of the 4 cells of float4 index i (bit k = cell 4i+k active; mask bit per cell)
 __device__ __forceinline__ unsigned act4(const uint32_t* act, int64_t i) { return (act[i >> 3] >> ((i & 7) * 4)) & 0xFu; }
 
+// (the inner loop is unrolled 4x so that several iterations' loads are in flight at once)
 #define FOR_RANGES(R, i)                                                                          \
   for (int rr_ = 0; rr_ < (R).n; ++rr_)                                                           \
+    _Pragma("unroll 4")                                                                           \
     for (int64_t i = (R).begin[rr_] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;             \
          i < (R).begin[rr_] + (R).len[rr_]; i += (int64_t)gridDim.x * blockDim.x)
 
@@ -329,7 +331,8 @@ __global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* ac
 // x += alpha p, r -= alpha q with alpha = (r,z)/(p,Ap) (Alg. 1 lines 9-11); sums ||r||^2,
 // sum r.  The last block flags a breakdown and records rho = (r, z) for the next beta.
 // alpha_fixed != 0: that step length instead (standalone multigrid: x += z, r -= A z)
-__global__ __launch_bounds__(256) void k_update(float* x, float* r, const float* p, const float* q, Ranges R,
+__global__ __launch_bounds__(256) void k_update(float* __restrict__ x, float* __restrict__ r,
+                                                const float* __restrict__ p, const float* __restrict__ q, Ranges R,
                                                 double* partial, unsigned* counter, Scalars* sc, float alpha_fixed) {
   __shared__ double sred[8];
   const double pq = sc->sum_pq, rz = sc->sum_rz;
@@ -339,8 +342,8 @@ __global__ __launch_bounds__(256) void k_update(float* x, float* r, const float*
   FOR_RANGES(R, i) {
     float4 xv = reinterpret_cast<float4*>(x)[i];
     float4 rv = reinterpret_cast<float4*>(r)[i];
-    float4 pv = reinterpret_cast<const float4*>(p)[i];
-    float4 qv = reinterpret_cast<const float4*>(q)[i];
+    float4 pv = __ldg(reinterpret_cast<const float4*>(p) + i);
+    float4 qv = __ldg(reinterpret_cast<const float4*>(q) + i);
     xv.x = fmaf(alpha, pv.x, xv.x); xv.y = fmaf(alpha, pv.y, xv.y);
     xv.z = fmaf(alpha, pv.z, xv.z); xv.w = fmaf(alpha, pv.w, xv.w);
     rv.x = fmaf(-alpha, qv.x, rv.x); rv.y = fmaf(-alpha, qv.y, rv.y);
@@ -366,7 +369,8 @@ __global__ __launch_bounds__(256) void k_update(float* x, float* r, const float*
 }
 
 // null-space projection r -= mean_active(r), mean over all parts; ||r||^2
-__global__ __launch_bounds__(256) void k_project(float* r, const uint32_t* act, Ranges R, double* partial,
+__global__ __launch_bounds__(256) void k_project(float* __restrict__ r, const uint32_t* __restrict__ act, Ranges R,
+                                                 double* partial,
                                                  unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   const float m = (float)(sc->sum_r / sc->n_active);
@@ -387,13 +391,14 @@ __global__ __launch_bounds__(256) void k_project(float* r, const uint32_t* act, 
 }
 
 // (r, z) (Alg. 1 line 12)
-__global__ __launch_bounds__(256) void k_dot_rz(const float* r, const float* z, Ranges R, double* partial,
+__global__ __launch_bounds__(256) void k_dot_rz(const float* __restrict__ r, const float* __restrict__ z, Ranges R,
+                                                double* partial,
                                                 unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   double s = 0.0;
   FOR_RANGES(R, i) {
-    float4 a = reinterpret_cast<const float4*>(r)[i];
-    float4 b = reinterpret_cast<const float4*>(z)[i];
+    float4 a = __ldg(reinterpret_cast<const float4*>(r) + i);
+    float4 b = __ldg(reinterpret_cast<const float4*>(z) + i);
     s += (double)a.x * b.x + (double)a.y * b.y + (double)a.z * b.z + (double)a.w * b.w;
   }
   double bs = block_reduce_d(s, sred);
