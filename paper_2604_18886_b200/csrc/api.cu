@@ -244,7 +244,7 @@ int64_t schedule_kernels(const Group& g) {
   return n * (int64_t)g.parts.size();
 }
 
-Fld ubuf(const Hier& h, int which = 0) { return which == 0 ? Fld{h.z, h.uinA} : Fld{h.zB, h.uinB}; }
+Fld ubuf(const Hier& h) { return Fld{h.z, h.uinA}; }
 
 cudaEvent_t next_event(Hier& h) {
   if (h.event_next == h.event_pool.size()) {
@@ -284,7 +284,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   const int l = op.level;
   SmoothArgs a;
   a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
-  a.glayer = T.glayer; a.u = ubuf(h); a.u2 = ubuf(h, 1); a.uc = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar;
+  a.glayer = T.glayer; a.u = ubuf(h); a.uc = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar;
   a.b = Fld{h.r, h.binner};
   a.alpha = h.prm.alpha; a.NL = T.NL;
   // FAS form (Alg. 4): beta at restriction, prolongation of u^{l-1} - u*; standard form
@@ -486,8 +486,6 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_TRY(halloc(h.allocs, &h.act, NLc / 32));
   OCTMG_TRY(halloc(h.allocs, &h.z, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.uinA, NIc));
-  OCTMG_TRY(halloc(h.allocs, &h.zB, NLc));
-  OCTMG_TRY(halloc(h.allocs, &h.uinB, NIc));
   OCTMG_TRY(halloc(h.allocs, &h.binner, NIc));
   OCTMG_TRY(halloc(h.allocs, &h.ustar, NIc));
   OCTMG_TRY(halloc(h.allocs, &h.r, NLc));

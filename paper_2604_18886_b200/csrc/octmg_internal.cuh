@@ -196,7 +196,6 @@ struct SmoothArgs {
   const float* glayer_val;
   const int* glayer;
   Fld u;                // level values read (in place: also written)
-  Fld u2;               // fused RB iteration: output buffer of the ping-pong pair
   Fld uc;               // rest buffer of every level (ghost sources, prolongation parents)
   const float* ustar;   // inner-indexed u* (prolongation)
   float* ustar_w;       // inner-indexed u* output (restrict stage)
@@ -254,11 +253,11 @@ octmg_status build_tree(const octmg_tree_desc* desc, const octmg_tile* tiles, in
 // ------------------------------------------------------------------------------------
 struct Op {
   int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle,
-               // 5 fused RB iteration, 6 copy level buffer in -> out, 7 halo exchange of level
+               // (5, 6: retired fused-RB kinds), 7 halo exchange of level
                // `level` of u, 8 broadcast of the restricted partition-parent level,
                // 9 cooperative coarse cycle from `level` down (k_coarse_grid)
   int level;
-  int stage;   // bit0 colour, bits1.. mode (SM_*); kind 5: bit0 first colour, bit1 zero
+  int stage;   // bit0 colour, bits1.. mode (SM_*)
   int in_buf = 0, out_buf = 0;
 };
 
@@ -271,8 +270,6 @@ struct Hier {
   // multigrid buffers
   float* z = nullptr;            // [NL*512] leaf part of the cycle's u (buffer A) = M output
   float* uinA = nullptr;         // [NI*512] inner part of u (buffer A)
-  float* zB = nullptr;           // [NL*512] buffer B (fused RB ping-pong)
-  float* uinB = nullptr;         // [NI*512]
   float* binner = nullptr;       // [NI*512]
   float* ustar = nullptr;        // [NI*512]
   float* r = nullptr;            // [NL*512] PCG residual = leaf part of the cycle rhs
