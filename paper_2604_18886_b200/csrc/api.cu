@@ -26,7 +26,7 @@ octmg_status cuda_status(cudaError_t e, const char* what) {
 const char* kclass_name[KC_COUNT] = {"rbgs_pass", "prolong", "residual_restrict", "coarsest",
                                      "fas_rhs", "coarse_levels", "apply", "pcg_update", "dot_rz", "project",
                                      "init", "setup", "memset", "coarse_subcycle", "rbgs_fused_iteration",
-                                     "copy_level", "coarse_grid"};
+                                     "copy_level", "coarse_grid", "p_update"};
 
 // ------------------------------------------------------------------------------------
 // allocator hook (octmg_set_allocator)
@@ -891,33 +891,49 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   OCTMG_TRY(dot_rz());
   int k = 0;
   double rel = 1.0;
-  int cur = 0;  // p0/p1 ping-pong: p_new in (cur ? p1 : p0)
+  // direction update p = z + beta p (own cells, in place), halo of p, then q = A p with
+  // the fp64 p.q (OCTMG_PCG_FUSED=1: the older fused form, p formed inside the apply from
+  // z and the previous p of a ping-pong pair)
+  const char* fu = getenv("OCTMG_PCG_FUSED");
+  const bool fused = fu && atoi(fu) == 1;
+  int cur = 0;  // fused form: p0/p1 ping-pong, p_new in (cur ? p1 : p0)
   while (true) {
     std::vector<Fld> pf;
+    if (!fused) {
+      for (Hier* h : g.parts) {
+        ProfScope ps(*h, KC_PUPDATE, s, (double)h->n_apply_tiles * TB3 * (k > 0 ? 12.0 : 8.0));  // read z, p; write p
+        launch_pupdate(h->z, h->p0, h->own_cells, h->sc, k > 0, s, G);
+        pf.push_back(Fld{h->p0, nullptr});
+      }
+      g.launches += np;
+      if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
+    }
     for (Hier* h : g.parts) {
-      float* pcur = cur ? h->p1 : h->p0;
+      float* pcur = fused ? (cur ? h->p1 : h->p0) : h->p0;
       float* pprev = cur ? h->p0 : h->p1;
       ApplyArgs a = apply_args(*h);
-      a.z = h->z;
-      a.pold = k == 0 ? nullptr : pprev;
-      a.pnew = pcur;
+      a.z = fused ? h->z : h->p0;
+      a.pold = (fused && k > 0) ? pprev : nullptr;
+      a.pnew = fused ? pcur : nullptr;
       a.q = h->q;
       a.partial = h->partial;
       a.counter = h->counter + 3;
-      a.use_beta = k > 0;
+      a.use_beta = fused && k > 0;
+      if (!fused && a.v2) a.v2 = 4;  // p precomputed: the colour-layout apply (k_apply_v4)
       {
-        // read z, p_old, record (24 B/leaf); write p, q (8 B/leaf)
-        ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 32.0);
+        // fused: read z, p_old, record (24 B/leaf), write p, q (8); split: read p, record, write q
+        ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * (fused ? 32.0 : 24.0));
         launch_apply(a, s);
       }
-      pf.push_back(Fld{pcur, nullptr});
+      if (fused) pf.push_back(Fld{pcur, nullptr});
     }
     g.launches += 2 * np;
     OCTMG_TRY(allreduce(g, SF_PQ, 1, s));
-    if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
+    if (g.comm && fused) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r
-      launch_update(h->xs, h->r, cur ? h->p1 : h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G);
+      launch_update(h->xs, h->r, fused ? (cur ? h->p1 : h->p0) : h->p0, h->q, h->own_cells, h->partial,
+                    h->counter + 4, h->sc, s, G);
     }
     g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RR, 2, s));

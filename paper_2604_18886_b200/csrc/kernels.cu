@@ -241,6 +241,75 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
   }
 }
 
+// q = A p for a precomputed p (split PCG form: a.z = p, no p_old), tiles without a ghost face
+// or inner neighbour: thread j < 128 owns red cells j, j + 128 of the tile, thread j >= 128
+// the black ones — the colour-pass layout: every neighbour of a cell is in the other colour
+// half at a fixed slot offset (see face_sum_regular in direct.cu), one load per neighbour.
+// Other tiles take the general composite path (same 256-thread CTA).
+template <bool DOT>
+__global__ __launch_bounds__(NT, 6) void k_apply_v4(ApplyArgs a) {
+  __shared__ double sred[NT / 32];
+  const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
+  int nb[6];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) nb[f] = __ldg(a.nbr + 6 * (size_t)t + f);
+  bool regular = true;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) regular &= nb[f] >= -1 && nb[f] < a.NL;
+  if (!regular) {
+    apply_general<DOT>(a, t, sred);
+    return;
+  }
+  const int j = threadIdx.x;
+  const int colour = j >> 7, jj = j & 127;
+  const int y = (jj >> 2) & 7, z0 = jj >> 5;
+  const float* pt = a.z + ((size_t)t << 9);
+  const float* ct = a.coef + ((size_t)t << 11);
+  const float* pn[6];
+  const float* cn[3];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) pn[f] = nb[f] >= 0 ? a.z + ((size_t)nb[f] << 9) : pt;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const int n = nb[2 * ax + 1];
+    cn[ax] = (n >= 0 ? a.coef + ((size_t)n << 11) : ct) + ((1 + ax) << 9);
+  }
+  double d = 0.0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int z = z0 + 4 * k;
+    const int x = 2 * (jj & 3) + ((colour + y + z) & 1);
+    const int sl = (colour << 8) + jj + 128 * k;
+    const float c0 = __ldg(ct + sl), cxm = __ldg(ct + 512 + sl), cym = __ldg(ct + 1024 + sl),
+                czm = __ldg(ct + 1536 + sl);
+    const float pc = __ldg(pt + sl);
+    const int base = sl ^ 256;
+    const int p = x & 1;
+    const bool in[6] = {x > 0, x < 7, y > 0, y < 7, z > 0, z < 7};
+    const int dlt[6] = {in[0] ? p - 1 : 3, in[1] ? p : -3, in[2] ? -4 : 28, in[3] ? 4 : -28, in[4] ? -32 : 224,
+                        in[5] ? 32 : -224};
+    const float cm3[3] = {cxm, cym, czm};
+    const float pv = c0 != 0.0f ? pc : 0.0f;
+    float sm = c0 * pv;  // the general path's order: c*p, then x-, x+, y-, y+, z-, z+
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      const int ax = f >> 1;
+      const int no = base + dlt[f];
+      float v = __ldg((in[f] ? pt : pn[f]) + no);
+      const float cf = (f & 1) ? __ldg((in[f] ? ct + ((1 + ax) << 9) : cn[ax]) + no) : cm3[ax];
+      if (!in[f] && nb[f] < 0) v = 0.0f;
+      sm = fmaf(cf, v, sm);
+    }
+    const float r = c0 != 0.0f ? sm : 0.0f;
+    a.q[((size_t)t << 9) + sl] = r;
+    d += (double)pv * (double)r;
+  }
+  if (DOT) {
+    double bs = block_reduce_d(d, sred);
+    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
+  }
+}
+
 template <bool DOT>
 __global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
   __shared__ double sred[NT / 32];
@@ -409,6 +478,23 @@ __global__ __launch_bounds__(256) void k_dot_rz(const float* __restrict__ r, con
   }
 }
 
+// p = z + beta p_old in place (Alg. 1 line 13; beta = 0 on the first iteration), over the
+// owned leaf cells.  z and p_old are zero on inactive cells, so p is too.
+__global__ __launch_bounds__(256) void k_pupdate(const float* __restrict__ z, float* __restrict__ p, Ranges R,
+                                                 const Scalars* sc, int use_beta) {
+  const float beta = use_beta ? sc->beta_f : 0.0f;
+  FOR_RANGES(R, i) {
+    const float4 zv = __ldg(reinterpret_cast<const float4*>(z) + i);
+    float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (use_beta) pv = reinterpret_cast<const float4*>(p)[i];
+    pv.x = fmaf(beta, pv.x, zv.x);
+    pv.y = fmaf(beta, pv.y, zv.y);
+    pv.z = fmaf(beta, pv.z, zv.z);
+    pv.w = fmaf(beta, pv.w, zv.w);
+    reinterpret_cast<float4*>(p)[i] = pv;
+  }
+}
+
 __global__ void k_set_beta(Scalars* sc) { sc->beta_f = (float)(sc->sum_rz / sc->rho); }
 
 __global__ void k_copy_ranges(const float* src, float* dst, Ranges R) {
@@ -463,11 +549,13 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
     return;
   }
   if (a.partial) {
-    if (a.v2) k_apply_v2<true><<<a.ntiles, NT, 0, s>>>(a);
+    if (a.v2 == 4) k_apply_v4<true><<<a.ntiles, NT, 0, s>>>(a);
+    else if (a.v2) k_apply_v2<true><<<a.ntiles, NT, 0, s>>>(a);
     else k_apply<true><<<a.ntiles, NT, 0, s>>>(a);
     k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.ntiles, a.sc);
   } else {
-    if (a.v2) k_apply_v2<false><<<a.ntiles, NT, 0, s>>>(a);
+    if (a.v2 == 4) k_apply_v4<false><<<a.ntiles, NT, 0, s>>>(a);
+    else if (a.v2) k_apply_v2<false><<<a.ntiles, NT, 0, s>>>(a);
     else k_apply<false><<<a.ntiles, NT, 0, s>>>(a);
   }
 }
@@ -489,6 +577,10 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
   k_dot_rz<<<grid, 256, 0, s>>>(r, z, R, partial, counter, sc);
 }
 void launch_set_beta(Scalars* sc, cudaStream_t s) { k_set_beta<<<1, 1, 0, s>>>(sc); }
+void launch_pupdate(const float* z, float* p, const Ranges& R, const Scalars* sc, bool use_beta, cudaStream_t s,
+                    int grid) {
+  k_pupdate<<<grid, 256, 0, s>>>(z, p, R, sc, use_beta ? 1 : 0);
+}
 
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s) {
   k_copy_ranges<<<592, 256, 0, s>>>(src, dst, R);

@@ -141,7 +141,7 @@ struct Ranges {
 // Kernel classes for profiling
 enum KClass {
   KC_PASS = 0, KC_PROLONG, KC_RESTRICT, KC_COARSEST, KC_FASRHS, KC_SMOOTH_COARSE,
-  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_RBFUSED, KC_COPY, KC_COARSE_GRID, KC_COUNT
+  KC_APPLY, KC_UPDATE, KC_DOT, KC_PROJECT, KC_INIT, KC_SETUP, KC_MEMSET, KC_SUBCYCLE, KC_RBFUSED, KC_COPY, KC_COARSE_GRID, KC_PUPDATE, KC_COUNT
 };
 extern const char* kclass_name[KC_COUNT];
 
@@ -166,7 +166,7 @@ struct ApplyArgs {
   Scalars* sc;          // beta = sum_rz / rho read from here; sum_pq written by the finish kernel
   int NL;
   int use_beta;
-  int v2;               // k_apply_v2 (regular tiles branch-free; OCTMG_PASS_V=1 selects k_apply)
+  int v2;               // 4: k_apply_v4 (p precomputed), 1: k_apply_v2 (p formed inside), 0: k_apply
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
@@ -181,6 +181,8 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
                    Scalars* sc, cudaStream_t s, int grid);
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s);
 void launch_set_beta(Scalars* sc, cudaStream_t s);  // beta_f from the (all-part) sums
+void launch_pupdate(const float* z, float* p, const Ranges& R, const Scalars* sc, bool use_beta, cudaStream_t s,
+                    int grid);  // p = z + beta p in place
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);  // nat -> slots
 void launch_copy_to_nat(const float* src, float* dst, const Ranges& R, cudaStream_t s);  // slots -> nat, owned
 void launch_permute_f32(const float* src, float* dst, int64_t n, int nf, bool to_slots, cudaStream_t s);

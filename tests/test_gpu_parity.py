@@ -248,7 +248,7 @@ def test_full_size_cfg2_parity(om):
 # ---------------------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
                                  {"OCTMG_GRID": "1"}, {"OCTMG_GRID": "1", "OCTMG_SUBCYCLE": "0"},
-                                 {"OCTMG_SUBCYCLE_CTAS": "8"}])
+                                 {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_PCG_FUSED": "1"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     for k, v in env.items():
