@@ -411,3 +411,62 @@ def test_table1_grids_iteration_counts_on_device(om):
         hist = rep["history"]  # relative residual after each iteration; fit from iteration 1 on
         red = (hist[0] / hist[-1]) ** (1.0 / (len(hist) - 1))
         assert red >= 15.0, (len(tiles), red)
+
+
+@pytest.mark.parametrize("ext,walls", [((2, 1, 3), (1, 0, 0, 1, 1, 0)), ((1, 3, 1), (0, 0, 0, 0, 0, 0))])
+def test_non_cubic_domains_match_oracle(om, ext, walls):
+    """Ragged (non-cubic) domains of several level-0 tiles, adaptive, mixed walls (incl. pure
+    Neumann): tables bit-exact, apply and the PCG solution against the oracle."""
+    rng = np.random.default_rng(sum(ext))
+    tiles = random_graded_tree(rng, 1, 2, 0.25, ext=ext)
+    tree = om.Tree(tiles, ext, walls)
+    o = Oracle(tiles, ext, walls)
+    ref = o.tables()
+    for k, v in tree.tables().items():
+        assert np.array_equal(v, ref[k]), k
+    N = o.N
+    kind = np.where(rng.random(N) < 0.05, 2, 0).astype(np.uint8)
+    w = (0.3 + 0.7 * rng.random((6, N))).astype(np.float32)
+    h = om.Hierarchy(tree, torch.from_numpy(kind).to(DEV), face_frac=torch.from_numpy(w).to(DEV))
+    o.setup(kind, w)
+    x = rng.standard_normal(N).astype(np.float32)
+    y = torch.zeros(N, device=DEV)
+    h.apply(torch.from_numpy(x).to(DEV), y)
+    assert _rel(y.cpu().numpy().astype(np.float64), o.apply(x.astype(np.float64))) <= 1e-5
+    b = rng.standard_normal(N).astype(np.float32)
+    b[kind != 0] = 0.0
+    xg = torch.zeros(N, device=DEV)
+    rep = h.pcg_solve(torch.from_numpy(b).to(DEV), xg, rtol=1e-6)
+    r = o.pcg(b.astype(np.float64), rtol=1e-6)
+    assert rep["converged"] and abs(rep["iters"] - r["iters"]) <= 1
+    act = o.coefs()[:N, 0] != 0
+    a, c = xg.cpu().numpy().astype(np.float64), r["x"]
+    if not any(walls):
+        a, c = a - a[act].mean() * act, c - c[act].mean() * act
+    assert _rel(a, c) <= 1e-5
+
+
+def test_degenerate_activity(om):
+    """No active cell (every cell Dirichlet): the rhs is masked to zero, the solve returns
+    x = 0 after 0 iterations; a single active fluid cell surrounded by Dirichlet cells is
+    solved exactly (x = b / c) in one iteration."""
+    tiles = uniform_tiles(1)
+    tiles = tiles[canonical_order(tiles)]
+    tree = om.Tree(tiles)
+    N = tree.N
+    kind = np.ones(N, dtype=np.uint8)
+    h = om.Hierarchy(tree, torch.from_numpy(kind).to(DEV))
+    x = torch.zeros(N, device=DEV)
+    rep = h.pcg_solve(torch.ones(N, device=DEV), x)
+    assert rep["iters"] == 0 and rep["converged"] and torch.count_nonzero(x) == 0
+    kind[777] = 0
+    h1 = om.Hierarchy(tree, torch.from_numpy(kind).to(DEV))
+    b = torch.zeros(N, device=DEV)
+    b[777] = 3.0
+    rep = h1.pcg_solve(b, x)
+    o = Oracle(tiles)
+    o.setup(kind)
+    c = o.coefs()[777, 0]
+    assert rep["converged"] and rep["iters"] == 1
+    assert abs(float(x[777]) - 3.0 / c) <= 1e-6 * abs(3.0 / c)
+    assert torch.count_nonzero(x) == 1
