@@ -250,7 +250,8 @@ typedef void (*octmg_free_fn)(void* ptr, octmg_stream stream, void* ctx);
 octmg_status octmg_set_allocator(octmg_alloc_fn alloc, octmg_free_fn release, void* ctx);
 
 /* Host copy of the coefficient store: (NL+NI)*512 records of 4 floats (c, cxm, cym, czm)
- * in tile order.  Synchronises `stream` of the last call. */
+ * in tile order, cells x + 8y + 64z within a tile (the library's internal colour-split,
+ * structure-of-arrays layout is converted).  Synchronises `stream` of the last call. */
 octmg_status octmg_hier_export_coefs(const octmg_hier* h, float* host_dst, size_t bytes);
 
 /* y = A x, the composite operator over all leaf cells (T-junction ghosts, Eq. 12,
