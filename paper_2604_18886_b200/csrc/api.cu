@@ -1,6 +1,8 @@
 // C-ABI entry points (include/octmg.h), hierarchy management, the unrolled mu-cycle
 // schedule (captured once into a CUDA graph) and the PCG driver (Alg. 1).
 #include <mutex>
+#include <cstddef>
+#include <cmath>
 #include <unordered_map>
 #include <algorithm>
 #include <cstdlib>
@@ -86,6 +88,9 @@ Hier::~Hier() {
 
 Group::~Group() {
   if (graph) cudaGraphExecDestroy(graph);
+  if (loop_graph) cudaGraphExecDestroy(loop_graph);
+  if (loop) cudaFree(loop);
+  if (loop_host) cudaFreeHost(loop_host);
   if (graph_stream) cudaStreamDestroy(graph_stream);
   for (Hier* h : parts) delete h;
   delete comm;
@@ -822,6 +827,75 @@ octmg_status octmg_vcycle(octmg_hier* hh, const float* b, float* u, octmg_stream
   return OCTMG_OK;
 }
 
+}  // extern "C"
+
+namespace octmg {
+namespace {
+
+// The whole PCG loop (Alg. 1 lines 8-13) as ONE CUDA graph with a conditional while node
+// (SURVEY 8(a) S12): each body iteration is z = M r, (r, z) and beta, p = z + beta p,
+// q = A p and p.q, the x / r update, the null-space projection, and the stopping test,
+// which sets the while condition on the device — no host round trip per iteration.
+// Single-part hierarchies (the NCCL / loopback transports stay on the host-driven loop).
+octmg_status build_loop_graph(Group& g, bool ns) {
+  Hier& h = *g.parts[0];
+  if (!g.graph_stream) OCTMG_CUDA(cudaStreamCreateWithFlags(&g.graph_stream, cudaStreamNonBlocking));
+  if (!g.loop) {
+    OCTMG_CUDA(cudaMalloc(&g.loop, sizeof(LoopState)));
+    OCTMG_CUDA(cudaMallocHost(&g.loop_host, sizeof(LoopState)));
+  }
+  if (g.loop_graph) {
+    cudaGraphExecDestroy(g.loop_graph);
+    g.loop_graph = nullptr;
+  }
+  cudaGraph_t graph;
+  OCTMG_CUDA(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle hd;
+  OCTMG_CUDA(cudaGraphConditionalHandleCreate(&hd, graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hd;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  OCTMG_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs = g.graph_stream;
+  const int G = vec_grid();
+  OCTMG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  octmg_status st = launch_ops(g, cs);  // z = M r
+  if (st == OCTMG_OK) {
+    launch_dot_rz(h.r, h.z, h.own_cells, h.partial, h.counter + 2, h.sc, cs, G);  // (r, z), beta
+    launch_pupdate(h.z, h.p0, h.own_cells, h.sc, true, cs, G);                     // p = z + beta p
+    ApplyArgs a = apply_args(h);
+    a.z = h.p0;
+    a.pold = nullptr;
+    a.pnew = nullptr;
+    a.q = h.q;
+    a.partial = h.partial;
+    a.counter = h.counter + 3;
+    a.use_beta = 0;
+    if (a.v2) a.v2 = 4;
+    launch_apply(a, cs);                                                           // q = A p, p.q
+    launch_update(h.xs, h.r, h.p0, h.q, h.own_cells, h.partial, h.counter + 4, h.sc, cs, G);
+    if (ns) launch_project(h.r, h.act, h.own_cells, h.partial, h.counter + 1, h.sc, cs, G);
+    launch_pcg_check(h.sc, g.loop, (unsigned long long)hd, cs);
+  }
+  cudaError_t e = cudaStreamEndCapture(cs, &body);
+  if (st != OCTMG_OK) { cudaGraphDestroy(graph); return st; }
+  if (e != cudaSuccess) { cudaGraphDestroy(graph); return cuda_status(e, "cudaStreamEndCapture (PCG loop)"); }
+  e = cudaGraphInstantiate(&g.loop_graph, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate (PCG loop)");
+  g.loop_ns = ns ? 1 : 0;
+  return OCTMG_OK;
+}
+
+}  // namespace
+}  // namespace octmg
+
+extern "C" {
+
 octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const octmg_solve_params* params,
                              octmg_solve_report* report, octmg_stream stream) {
   if (!hh || !b || !x) { set_error("null argument"); return OCTMG_E_INVALID; }
@@ -887,6 +961,36 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   if (!std::isfinite(hs->sum_rr)) { set_error("non-finite right-hand side"); return fill(OCTMG_E_NONFINITE, 0, false, 0, 0); }
   const double bn = std::sqrt(hs->sum_rr);
   if (bn == 0.0) return fill(OCTMG_OK, 0, true, 0.0, 0.0);
+  const char* gl = getenv("OCTMG_GRAPH_LOOP");  // default on for single-part hierarchies; 0: host loop
+  if (!(gl && atoi(gl) == 0) && np == 1 && !g.comm && !profiling(g)) {
+    // the device-side loop: one graph launch, one synchronisation per solve
+    if (!g.loop_graph || g.loop_ns != (ns ? 1 : 0)) OCTMG_TRY(build_loop_graph(g, ns));
+    LoopState* L = g.loop_host;
+    L->bn = bn;
+    L->rtol = prm.rtol;
+    L->rel = 1.0;
+    L->k = 0;
+    L->max_iters = prm.max_iters;
+    L->status = 0;
+    L->converged = 0;
+    OCTMG_CUDA(cudaMemcpyAsync(g.loop, L, offsetof(LoopState, hist), cudaMemcpyHostToDevice, s));
+    // beta = 0 on the first iteration: rho = inf, p = 0
+    const double inf = INFINITY;
+    OCTMG_CUDA(cudaMemcpyAsync(&h0.sc->rho, &inf, sizeof(double), cudaMemcpyHostToDevice, s));
+    OCTMG_CUDA(cudaMemsetAsync(h0.p0, 0, sizeof(float) * (size_t)h0.tree->NL * TB3, s));
+    OCTMG_CUDA(cudaGraphLaunch(g.loop_graph, s));
+    OCTMG_CUDA(cudaMemcpyAsync(L, g.loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+    OCTMG_CUDA(cudaStreamSynchronize(s));
+    const int kk = L->k;
+    g.launches += (int64_t)kk * (schedule_kernels(g) + 7);
+    if (report && report->history)
+      for (int i = 0; i < kk && i < report->history_cap && i < LOOP_HCAP; ++i) report->history[i] = L->hist[i];
+    if (L->status == 9) { set_error("PCG breakdown: p.Ap <= 0"); return fill(OCTMG_E_BREAKDOWN, kk - 1, false, L->rel, bn); }
+    if (L->status == 8) { set_error("non-finite PCG scalar"); return fill(OCTMG_E_NONFINITE, kk - 1, false, L->rel, bn); }
+    if (L->converged) return fill(OCTMG_OK, kk, true, L->rel, bn);
+    set_error("PCG did not converge within max_iters");
+    return fill(OCTMG_E_MAXITER, kk, false, L->rel, bn);
+  }
   OCTMG_TRY(run_M(g, s));
   OCTMG_TRY(dot_rz());
   int k = 0;

@@ -495,6 +495,25 @@ __global__ __launch_bounds__(256) void k_pupdate(const float* __restrict__ z, fl
   }
 }
 
+// the stopping test of the device-side PCG loop (Alg. 1 line 8): records ||r_k|| / ||r_0||,
+// and sets the while-node's condition to "continue" unless converged, broken down,
+// non-finite or at max_iters
+__global__ void k_pcg_check(Scalars* sc, LoopState* ls, cudaGraphConditionalHandle h) {
+  const double rr = sc->sum_rr;
+  const int k = ++ls->k;
+  const double rel = sqrt(rr) / ls->bn;
+  if (k - 1 < LOOP_HCAP) ls->hist[k - 1] = rel;
+  ls->rel = rel;
+  int st = 0;
+  if (sc->flags & 1) st = 9;
+  else if (!isfinite(rr)) st = 8;
+  const bool conv = st == 0 && rel <= ls->rtol;
+  if (!conv && st == 0 && k >= ls->max_iters) st = 10;
+  ls->status = st;
+  ls->converged = conv ? 1 : 0;
+  cudaGraphSetConditional(h, (conv || st) ? 0u : 1u);
+}
+
 __global__ void k_set_beta(Scalars* sc) { sc->beta_f = (float)(sc->sum_rz / sc->rho); }
 
 __global__ void k_copy_ranges(const float* src, float* dst, Ranges R) {
@@ -577,6 +596,9 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
   k_dot_rz<<<grid, 256, 0, s>>>(r, z, R, partial, counter, sc);
 }
 void launch_set_beta(Scalars* sc, cudaStream_t s) { k_set_beta<<<1, 1, 0, s>>>(sc); }
+void launch_pcg_check(Scalars* sc, LoopState* ls, unsigned long long handle, cudaStream_t s) {
+  k_pcg_check<<<1, 1, 0, s>>>(sc, ls, (cudaGraphConditionalHandle)handle);
+}
 void launch_pupdate(const float* z, float* p, const Ranges& R, const Scalars* sc, bool use_beta, cudaStream_t s,
                     int grid) {
   k_pupdate<<<grid, 256, 0, s>>>(z, p, R, sc, use_beta ? 1 : 0);

@@ -325,6 +325,17 @@ struct Comm;
 
 // A solver instance: one part (single GPU, or one rank of an NCCL job) or several parts
 // in one process (loopback partition on one GPU, for testing the distributed path).
+// state of the device-side PCG loop (OCTMG_GRAPH_LOOP=1): written by the loop's check
+// kernel, read by the host once per solve
+constexpr int LOOP_HCAP = 512;
+struct LoopState {
+  double bn, rtol, rel;
+  int k, max_iters, status;  // status: 0 running/converged, 9 breakdown, 8 non-finite, 10 max iters
+  int converged;
+  double hist[LOOP_HCAP];
+};
+void launch_pcg_check(Scalars* sc, LoopState* ls, unsigned long long handle, cudaStream_t s);
+
 struct Group {
   std::vector<Hier*> parts;
   Comm* comm = nullptr;
@@ -332,6 +343,10 @@ struct Group {
   std::vector<Op> ops;                 // identical for every part
   cudaGraphExec_t graph = nullptr;
   cudaStream_t graph_stream = nullptr;
+  cudaGraphExec_t loop_graph = nullptr;  // the whole PCG loop as a conditional-while graph
+  LoopState* loop = nullptr;             // device
+  LoopState* loop_host = nullptr;        // pinned
+  int loop_ns = -1;                      // null-space flag the loop graph was built with
   int64_t launches = 0;
   ~Group();
 };

@@ -187,7 +187,9 @@ def test_pcg_random_rhs_and_deterministic(om):
     assert _rel(x1.cpu().numpy().astype(np.float64), ref["x"]) <= 1e-5
 
 
-def test_pcg_edge_cases(om):
+@pytest.mark.parametrize("loop", ["0", "1"])
+def test_pcg_edge_cases(om, loop, monkeypatch):
+    monkeypatch.setenv("OCTMG_GRAPH_LOOP", loop)  # host-driven loop / device-side graph loop
     cfg = make_config("cfg1_octant")
     tree, h, o = _setup(om, cfg)
     b = torch.zeros(o.N, device=DEV)
@@ -248,7 +250,8 @@ def test_full_size_cfg2_parity(om):
 # ---------------------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
                                  {"OCTMG_GRID": "1"}, {"OCTMG_GRID": "1", "OCTMG_SUBCYCLE": "0"},
-                                 {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_PCG_FUSED": "1"}])
+                                 {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_PCG_FUSED": "1"},
+                                 {"OCTMG_GRAPH_LOOP": "0"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     for k, v in env.items():
