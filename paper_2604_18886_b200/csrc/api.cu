@@ -197,7 +197,9 @@ void read_env(Hier& h) {
   const char* pv = getenv("OCTMG_PASS_V");
   h.pass_v2 = !(pv && std::string(pv) == "1");
   const char* rv = getenv("OCTMG_RESTRICT_V");
-  h.restrict_v2 = !(rv && std::string(rv) == "1");  // k_restrict_v2 (vectorised regular tiles) by default
+  h.restrict_v2 = !rv ? 6 : (std::string(rv) == "1" ? 0 : (std::string(rv) == "8" ? 8 : 6));  // 8: measured no faster
+  const char* av = getenv("OCTMG_APPLY_V");
+  h.apply_v = av && (std::string(av) == "4" || std::string(av) == "6") ? atoi(av) : 5;
   const Tree& T = *h.tree;
   const char* gv = getenv("OCTMG_GRID");
   const bool grid = gv && std::string(gv) == "1";
@@ -875,7 +877,7 @@ octmg_status build_loop_graph(Group& g, bool ns) {
     a.partial = h.partial;
     a.counter = h.counter + 3;
     a.use_beta = 0;
-    if (a.v2) a.v2 = 4;
+    if (a.v2) a.v2 = h.apply_v;
     launch_apply(a, cs);                                                           // q = A p, p.q
     launch_update(h.xs, h.r, h.p0, h.q, h.own_cells, h.partial, h.counter + 4, h.sc, cs, G);
     if (ns) launch_project(h.r, h.act, h.own_cells, h.partial, h.counter + 1, h.sc, cs, G);
@@ -1023,7 +1025,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       a.partial = h->partial;
       a.counter = h->counter + 3;
       a.use_beta = fused && k > 0;
-      if (!fused && a.v2) a.v2 = 4;  // p precomputed: the colour-layout apply (k_apply_v4)
+      if (!fused && a.v2) a.v2 = h->apply_v;  // p precomputed: the colour-layout apply (k_apply_v5 / v4)
       {
         // fused: read z, p_old, record (24 B/leaf), write p, q (8); split: read p, record, write q
         ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * (fused ? 32.0 : 24.0));

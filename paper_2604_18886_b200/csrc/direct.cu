@@ -215,7 +215,8 @@ __global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
 // Residual + restriction + Avg with the neighbour entries prefetched and, on tiles without a
 // ghost face, the branch-free face sum (every load in flight at once, in-tile neighbours
 // from L1).  Same thread layout and outputs as k_restrict_direct.
-__global__ __launch_bounds__(NT, 6) void k_restrict_v2(SmoothArgs a) {
+template <int MINB>
+__global__ __launch_bounds__(NT, MINB) void k_restrict_v2(SmoothArgs a) {
   const int t = a.order[blockIdx.x];
   int nb[6];
   {
@@ -353,9 +354,10 @@ void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt) {
   else launch_pass_cpt<1>(a, mode, s, v2);
 }
 
-void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, bool v2) {
+void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2) {
   if (!a.n) return;
-  if (v2) k_restrict_v2<<<a.n, NT, 0, s>>>(a);
+  if (v2 == 8) k_restrict_v2<8><<<a.n, NT, 0, s>>>(a);
+  else if (v2) k_restrict_v2<6><<<a.n, NT, 0, s>>>(a);
   else k_restrict_direct<<<a.n, NT, 0, s>>>(a);
 }
 

@@ -310,6 +310,90 @@ __global__ __launch_bounds__(NT, 6) void k_apply_v4(ApplyArgs a) {
   }
 }
 
+// k_apply_v4 with vector loads: thread j owns the two colour cells of slots 2jj, 2jj + 1 of
+// colour j >> 7 (jj = j & 127: one half of a colour row, elements m = 2h, 2h + 1 of row
+// (y, z), x_m = 2m + p, p = (colour + y + z) & 1).  The other colour's row at the same slots
+// holds both cells' x-neighbours but one (element m + p - 1 / m + p: one extra scalar, in the
+// tile or the x-neighbour tile), and its rows 4 / 32 slots away are the y / z neighbours
+// (wrapped: -28 / +28, -224 / +224 into the neighbour tile), so a cell pair costs 15 float2 /
+// scalar loads instead of 28.  The y / z side tests are uniform per thread.  Same per-cell
+// fmaf order as k_apply_v4 (c p, then x-, x+, y-, y+, z-, z+), so q is bit-identical.
+template <bool DOT, int MINB>
+__global__ __launch_bounds__(NT, MINB) void k_apply_v5(ApplyArgs a) {
+  __shared__ double sred[NT / 32];
+  const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
+  int nb[6];
+  {
+    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
+    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
+    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
+  }
+  bool regular = true;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) regular &= nb[f] >= -1 && nb[f] < a.NL;
+  if (!regular) {
+    apply_general<DOT>(a, t, sred);
+    return;
+  }
+  const int j = threadIdx.x;
+  const int colour = j >> 7, jj = j & 127;
+  const int row = jj >> 1, h = jj & 1;
+  const int y = row & 7, z = row >> 3;
+  const int p = (colour + y + z) & 1;
+  const int own = (colour << 8) + 2 * jj;  // slots of elements 2h, 2h + 1
+  const int oth = own ^ 256;               // the other colour's row, same elements
+  const float* pt = a.z + ((size_t)t << 9);
+  const float* ct = a.coef + ((size_t)t << 11);
+  auto tz = [&](int n) { return n >= 0 ? a.z + ((size_t)n << 9) : pt; };
+  auto tc = [&](int n) { return n >= 0 ? a.coef + ((size_t)n << 11) : ct; };
+  const float2 pc = __ldg(reinterpret_cast<const float2*>(pt + own));
+  const float2 c0 = __ldg(reinterpret_cast<const float2*>(ct + own));
+  const float2 cxm = __ldg(reinterpret_cast<const float2*>(ct + 512 + own));
+  const float2 cym = __ldg(reinterpret_cast<const float2*>(ct + 1024 + own));
+  const float2 czm = __ldg(reinterpret_cast<const float2*>(ct + 1536 + own));
+  // x: the other row's elements 2h, 2h + 1 and the one outside them (p = 0: element 2h - 1,
+  // p = 1: element 2h + 2), in the tile or the x-neighbour tile (element 3 / 0 of its row)
+  const float2 ox = __ldg(reinterpret_cast<const float2*>(pt + oth));
+  const float2 cxo = __ldg(reinterpret_cast<const float2*>(ct + 512 + oth));
+  const bool xin = p ? h == 0 : h == 1;
+  const int nx = p ? nb[1] : nb[0];  // the tile across the face the extra element lies beyond
+  const int xo = p ? (xin ? oth + 2 : oth - 2) : (xin ? oth - 1 : oth + 3);
+  float xs = __ldg((xin ? pt : tz(nx)) + xo);
+  const float xsc = __ldg((xin ? ct : tc(nx)) + 512 + xo);  // its c_x- (used when p = 1)
+  if (!xin && nx < 0) xs = 0.0f;
+  // y / z: the other row 4 / 32 slots away (wrapped into the neighbour tile at the sides)
+  const bool yl = y > 0, yh = y < 7, zl = z > 0, zh = z < 7;
+  float2 ym = __ldg(reinterpret_cast<const float2*>((yl ? pt : tz(nb[2])) + oth + (yl ? -4 : 28)));
+  float2 yp = __ldg(reinterpret_cast<const float2*>((yh ? pt : tz(nb[3])) + oth + (yh ? 4 : -28)));
+  float2 zm = __ldg(reinterpret_cast<const float2*>((zl ? pt : tz(nb[4])) + oth + (zl ? -32 : 224)));
+  float2 zp = __ldg(reinterpret_cast<const float2*>((zh ? pt : tz(nb[5])) + oth + (zh ? 32 : -224)));
+  const float2 cyp = __ldg(reinterpret_cast<const float2*>((yh ? ct : tc(nb[3])) + 1024 + oth + (yh ? 4 : -28)));
+  const float2 czp = __ldg(reinterpret_cast<const float2*>((zh ? ct : tc(nb[5])) + 1536 + oth + (zh ? 32 : -224)));
+  if (!yl && nb[2] < 0) ym = make_float2(0.0f, 0.0f);
+  if (!yh && nb[3] < 0) yp = make_float2(0.0f, 0.0f);
+  if (!zl && nb[4] < 0) zm = make_float2(0.0f, 0.0f);
+  if (!zh && nb[5] < 0) zp = make_float2(0.0f, 0.0f);
+  // per element e: x- / x+ values and the x+ coupling
+  const float xm0 = p ? ox.x : xs, xm1 = p ? ox.y : ox.x;
+  const float xp0 = p ? ox.y : ox.x, xp1 = p ? xs : ox.y;
+  const float cxp0 = p ? cxo.y : cxo.x, cxp1 = p ? xsc : cxo.y;
+  const float pv0 = c0.x != 0.0f ? pc.x : 0.0f, pv1 = c0.y != 0.0f ? pc.y : 0.0f;
+  float s0 = c0.x * pv0, s1 = c0.y * pv1;
+  s0 = fmaf(cxm.x, xm0, s0); s1 = fmaf(cxm.y, xm1, s1);
+  s0 = fmaf(cxp0, xp0, s0);  s1 = fmaf(cxp1, xp1, s1);
+  s0 = fmaf(cym.x, ym.x, s0); s1 = fmaf(cym.y, ym.y, s1);
+  s0 = fmaf(cyp.x, yp.x, s0); s1 = fmaf(cyp.y, yp.y, s1);
+  s0 = fmaf(czm.x, zm.x, s0); s1 = fmaf(czm.y, zm.y, s1);
+  s0 = fmaf(czp.x, zp.x, s0); s1 = fmaf(czp.y, zp.y, s1);
+  const float r0 = c0.x != 0.0f ? s0 : 0.0f, r1 = c0.y != 0.0f ? s1 : 0.0f;
+  *reinterpret_cast<float2*>(a.q + ((size_t)t << 9) + own) = make_float2(r0, r1);
+  if (DOT) {
+    const double d = (double)pv0 * (double)r0 + (double)pv1 * (double)r1;
+    double bs = block_reduce_d(d, sred);
+    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
+  }
+}
+
 template <bool DOT>
 __global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
   __shared__ double sred[NT / 32];
@@ -568,12 +652,16 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
     return;
   }
   if (a.partial) {
-    if (a.v2 == 4) k_apply_v4<true><<<a.ntiles, NT, 0, s>>>(a);
+    if (a.v2 == 5) k_apply_v5<true, 8><<<a.ntiles, NT, 0, s>>>(a);
+    else if (a.v2 == 6) k_apply_v5<true, 6><<<a.ntiles, NT, 0, s>>>(a);
+    else if (a.v2 == 4) k_apply_v4<true><<<a.ntiles, NT, 0, s>>>(a);
     else if (a.v2) k_apply_v2<true><<<a.ntiles, NT, 0, s>>>(a);
     else k_apply<true><<<a.ntiles, NT, 0, s>>>(a);
     k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.ntiles, a.sc);
   } else {
-    if (a.v2 == 4) k_apply_v4<false><<<a.ntiles, NT, 0, s>>>(a);
+    if (a.v2 == 5) k_apply_v5<false, 8><<<a.ntiles, NT, 0, s>>>(a);
+    else if (a.v2 == 6) k_apply_v5<false, 6><<<a.ntiles, NT, 0, s>>>(a);
+    else if (a.v2 == 4) k_apply_v4<false><<<a.ntiles, NT, 0, s>>>(a);
     else if (a.v2) k_apply_v2<false><<<a.ntiles, NT, 0, s>>>(a);
     else k_apply<false><<<a.ntiles, NT, 0, s>>>(a);
   }

@@ -166,7 +166,7 @@ struct ApplyArgs {
   Scalars* sc;          // beta = sum_rz / rho read from here; sum_pq written by the finish kernel
   int NL;
   int use_beta;
-  int v2;               // 4: k_apply_v4 (p precomputed), 1: k_apply_v2 (p formed inside), 0: k_apply
+  int v2;               // 5 / 4: k_apply_v5 / k_apply_v4 (p precomputed), 1: k_apply_v2 (p formed inside), 0: k_apply
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
@@ -213,7 +213,7 @@ struct SmoothArgs {
 };
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
-void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, bool v2);
+void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2);  // 0 staged, 6 / 8: k_restrict_v2 min CTAs/SM
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
 int subcycle_ctas();
 int subcycle_max_tiles(int ctas);
@@ -293,7 +293,8 @@ struct Hier {
   int lvl_n[MAXL + 1] = {};
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
-  bool restrict_v2 = true;       // k_restrict_v2: vectorised regular tiles (OCTMG_RESTRICT_V=1: staged k_restrict_direct)
+  int apply_v = 5;               // p-precomputed apply: 5 k_apply_v5 (float2 rows), 4 k_apply_v4 (OCTMG_APPLY_V=4)
+  int restrict_v2 = 6;           // k_restrict_v2 (vectorised regular tiles) at >= 6 (8: OCTMG_RESTRICT_V=8) CTAs/SM; 0: staged k_restrict_direct (OCTMG_RESTRICT_V=1)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)

@@ -251,7 +251,8 @@ def test_full_size_cfg2_parity(om):
 @pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
                                  {"OCTMG_GRID": "1"}, {"OCTMG_GRID": "1", "OCTMG_SUBCYCLE": "0"},
                                  {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_PCG_FUSED": "1"},
-                                 {"OCTMG_GRAPH_LOOP": "0"}])
+                                 {"OCTMG_GRAPH_LOOP": "0"}, {"OCTMG_APPLY_V": "4"}, {"OCTMG_RESTRICT_V": "8"},
+                                 {"OCTMG_RESTRICT_V": "1"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     for k, v in env.items():
@@ -268,6 +269,24 @@ def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     x = torch.zeros_like(b)
     rep = h.pcg_solve(b, x, rtol=1e-6)
     assert abs(rep["iters"] - o.pcg(cfg["b"].astype(np.float64), rtol=1e-6, mu=cfg["mu"])["iters"]) <= 1
+
+
+@pytest.mark.parametrize("name", ["uniform64_dir", "sphere_small", "tank_mid", "cfg1_octant"])
+def test_apply_row_vector_variant_bit_identical(om, name, monkeypatch):
+    """k_apply_v5 (float2 colour rows) keeps k_apply_v4's per-cell fmaf order: q identical."""
+    cfg = make_config(name)
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    kind = torch.from_numpy(cfg["kind"]).to(DEV)
+    frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(DEV)
+    x = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, tree.N).astype(np.float32)).to(DEV)
+    out = []
+    for v in ("5", "4"):
+        monkeypatch.setenv("OCTMG_APPLY_V", v)
+        h = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
+        y = torch.empty_like(x)
+        h.apply(x, y)
+        out.append(y)
+    assert torch.equal(out[0], out[1])
 
 
 # ---------------------------------------------------------------------------------------

@@ -10,7 +10,7 @@ fi
 # level-5 prolongation = 4th k_prolong launch, the rest: first launch
 for KS in k_pass_v2:2 k_apply:0 k_restrict:0 k_prolong:3 k_update:0; do
   K=${KS%%:*}; S=${KS##*:}
-  ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 -o gpurun_out/full_$K \
+  OCTMG_GRAPH_LOOP=0 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 -o gpurun_out/full_$K \
       python tools/prof_solve.py cfg2_uniform256 0 > /dev/null 2>&1
 done
 ls gpurun_out | tail -12

@@ -35,7 +35,8 @@ def launches():
     recs = [(short(r[ki]), r[gi], float(r[vi].replace(",", ""))) for r in rows[hi + 1:] if r[mi] == "gpu__time_duration.sum"]
     with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as f:
         f.write("# ncu --metrics gpu__time_duration.sum --clock-control none "
-                "python bench.py --steps 3 --warmup 3 --no-cpu-baseline (cold-cache, serialised)\n")
+                "OCTMG_GRAPH_LOOP=0 python bench.py --steps 3 --warmup 3 --no-cpu-baseline (cold-cache, serialised; "
+                "host-driven PCG loop so ncu lists the loop body)\n")
         f.write("idx,kernel,grid,ns\n")
         for i, (k, g, t) in enumerate(recs):
             f.write(f"{i},{k},\"{g}\",{t:.0f}\n")
