@@ -293,6 +293,15 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
   const float* cc = a.coef + ((size_t)t << 11);
   const float* uc = tptr(a.uc, P, a.NL);
   const float* us = a.ustar + (size_t)(P - a.NL) * TB3;
+  // the cells' u and activity do not depend on the parent: loaded before the parent values
+  // arrive and unconditionally, so no load waits behind the activity branch
+  float uo[4], cv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int sl = threadIdx.x + 128 * k;
+    uo[k] = ut[sl];
+    cv[k] = __ldg(cc + sl);
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int sl = threadIdx.x + 128 * k;
@@ -300,7 +309,7 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
     slot_xyz(sl, x, y, z);
     const int pc = pcell_of(tv, x, y, z);
     const float c = a.pro_scale * (__ldg(uc + pc) - __ldg(us + pc));
-    if (__ldg(cc + sl) != 0.0f) ut[sl] += c;
+    if (cv[k] != 0.0f) ut[sl] = uo[k] + c;
   }
 }
 
