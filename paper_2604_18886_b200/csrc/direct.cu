@@ -224,6 +224,10 @@ __global__ __launch_bounds__(NT, MINB) void k_restrict_v2(SmoothArgs a) {
     const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
     nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
   }
+  // the tile's origin and parent (for the parent-cell stores at the end) are loaded up front,
+  // with the neighbour entries, not after the face sums
+  const int4 tv = __ldg(a.tile + t);
+  const int P = __ldg(a.parent + t);
   const int j = threadIdx.x;
   const int x2 = j & 3;
   const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
@@ -271,8 +275,6 @@ __global__ __launch_bounds__(NT, MINB) void k_restrict_v2(SmoothArgs a) {
   rs += __shfl_xor_sync(0xffffffffu, rs, 4);
   rs += __shfl_xor_sync(0xffffffffu, rs, 8);
   if (((j >> 2) & 3) == 0) {
-    const int4 tv = __ldg(a.tile + t);
-    const int P = __ldg(a.parent + t);
     const int pc = pcell_of(tv, x0, y, z);
     const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
     a.u.inner[pi] = a.std_form ? 0.0f : mP;  // Alg. 2: zero coarse guess, u* = 0
