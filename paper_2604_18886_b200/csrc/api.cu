@@ -194,6 +194,8 @@ struct Builder {
 void read_env(Hier& h) {
   const char* pc = getenv("OCTMG_PASS_CPT");
   h.pass_cpt = pc ? (atoi(pc) >= 4 ? 4 : std::max(1, std::min(2, atoi(pc)))) : 4;
+  const char* pb = getenv("OCTMG_PASS_BIG");
+  h.pass_big = pb ? std::max(1, atoi(pb)) : 1024;  // levels with >= this many tiles take pass_cpt
   const char* pv = getenv("OCTMG_PASS_V");
   h.pass_v2 = !(pv && std::string(pv) == "1");
   const char* rv = getenv("OCTMG_RESTRICT_V");
@@ -343,7 +345,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   if (mode == SM_RESTRICT) {
     launch_restrict_direct(a, s, h.restrict_v2);
   } else {
-    launch_pass_direct(a, s, (a.n >= 1024 ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0));
+    launch_pass_direct(a, s, (a.n >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0));
   }
 }
 

@@ -293,6 +293,7 @@ struct Hier {
   int lvl_n[MAXL + 1] = {};
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
+  int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
   int apply_v = 5;               // p-precomputed apply: 5 k_apply_v5 (float2 rows), 4 k_apply_v4 (OCTMG_APPLY_V=4)
   int restrict_v2 = 6;           // k_restrict_v2 (vectorised regular tiles) at >= 6 (8: OCTMG_RESTRICT_V=8) CTAs/SM; 0: staged k_restrict_direct (OCTMG_RESTRICT_V=1)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
