@@ -10,7 +10,8 @@ Table 1 (reading #14).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
 
-N > 1 (torchrun): the same workload is partitioned across the ranks by contiguous Morton
+N > 1: launched by torchrun (one process per GPU), or, when WORLD_SIZE is unset, bench.py
+re-launches itself under torch.distributed.run with N processes.  The same workload is partitioned across the ranks by contiguous Morton
 ranges: NCCL halo exchange after every kernel that
 changes a partitioned level, fp64 allreduce for every PCG scalar.  value = total cells /
 max-over-ranks time, "scaling": "strong".  --replicas instead solves one independent
@@ -57,7 +58,32 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--replicas", action="store_true", help="N>1: independent instance per rank")
+    ap.add_argument("--no-wcycle", action="store_true",
+                    help="skip the W-cycle configs 4/5 timed beside the headline (extra keys)")
+    ap.add_argument("--wcycle-steps", type=int, default=5)
     return ap.parse_args()
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 without a torchrun environment: re-launch this script under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1); rank 0 prints the
+    line.  Returns the launcher's exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def check_solve(rep, what):
+    """Every timed / warm-up solve must converge: a MAXITER or failed solve
+    never becomes a throughput number."""
+    if not rep["converged"] or rep["status"] != "OK":
+        raise RuntimeError(f"{what}: solve did not converge (status {rep['status']}, iters {rep['iters']}, "
+                           f"rel residual {rep['rel_residual']:.3e})")
+    return rep
 
 
 def dist_env():
@@ -112,12 +138,22 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(seconds: float):
-    """The fp64 oracle as it stands, on the host cores, on a bounded sample of the same
-    workload recipe (64^3): repeated full solves to 1e-6 for >= `seconds`."""
+def cpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _oracle_solves(name, seconds, threads, max_solves=None):
+    """Full fp64 oracle solves of workload `name` for >= `seconds` (at least one), with
+    `threads` OpenMP threads (set before the oracle library is first loaded)."""
     from octgen import make_config
     from oracle.oracle import Oracle
-    cfg = make_config(CPU_SAMPLE)
+    cfg = make_config(name)
     o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
     o.setup(cfg["kind"], cfg["w"])
     b = cfg["b"].astype(np.float64)
@@ -127,12 +163,38 @@ def cpu_baseline(seconds: float):
         n += 1
         iters = r["iters"]
         el = time.perf_counter() - t0
-        if el >= seconds:
+        if el >= seconds or (max_solves and n >= max_solves):
             break
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": n * o.N / el, "unit": "cells/s", "cores": cores, "kind": "oracle",
-            "sample": f"{CPU_SAMPLE} (64^3, same recipe as cfg2): {n} full fp64 solves to 1e-6 "
-                      f"({iters} PCG iterations each) in {el:.1f} s"}
+    return {"cells_per_s": n * o.N / el, "solves": n, "seconds": el, "iters": iters, "cells": o.N,
+            "threads": threads}
+
+
+def _oracle_leg(name, seconds, threads, max_solves=None):
+    """One oracle timing leg in a child process (OMP_NUM_THREADS must be fixed before the
+    OpenMP runtime starts)."""
+    code = ("import json, sys; sys.path.insert(0, %r); import bench; "
+            "print(json.dumps(bench._oracle_solves(%r, %r, %d, %r)))" % (ROOT, name, seconds, threads, max_solves))
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr[-2000:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(seconds: float, config: str):
+    """The fp64 oracle as it stands, timed on the host cores: one full solve of the headline
+    workload itself at all cores (same_config), and a single-thread leg on a bounded 64^3
+    sample of the same recipe."""
+    ncores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    full = _oracle_leg(config, 0.0, ncores, max_solves=1)
+    one = _oracle_leg(CPU_SAMPLE, seconds, 1)
+    return {"value": full["cells_per_s"], "unit": "cells/s", "cores": ncores, "kind": "oracle",
+            "same_config": True, "cpu_model": cpu_model(),
+            "sample": f"{config} itself: {full['solves']} full fp64 solve to 1e-6 ({full['iters']} PCG iterations, "
+                      f"{full['cells']} leaf cells) in {full['seconds']:.1f} s on {ncores} threads",
+            "single_thread": {"value": one["cells_per_s"], "unit": "cells/s", "cores": 1,
+                              "sample": f"{CPU_SAMPLE} (64^3, same recipe): {one['solves']} full fp64 solves "
+                                        f"({one['iters']} PCG iterations each) in {one['seconds']:.1f} s"}}
 
 
 def run_reference(args):
@@ -168,6 +230,54 @@ def run_reference(args):
     return 0
 
 
+def time_config(om, torch, name, steps, warmup, rtol):
+    """ms per solve of one more BASELINE config on this GPU (device-resident inputs, same
+    timing rules as the headline), plus its per-class profile (separate pass)."""
+    from octgen import make_config
+    cfg = make_config(name, with_fields=False)
+    tank = cfg["bc"] == "tank"
+    if not tank:
+        cfg = make_config(name)
+    t0 = time.perf_counter()
+    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    if tank:
+        kind, frac, b = om.tank_fields(tree, (0.5, 0.5, 0.5), cfg["radius"])
+    else:
+        kind = torch.from_numpy(cfg["kind"]).cuda()
+        frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).cuda()
+        b = torch.from_numpy(cfg["b"]).cuda()
+    h = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
+    del frac, kind
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    x = torch.zeros_like(b)
+    for _ in range(warmup):
+        check_solve(h.pcg_solve(b, x, rtol=rtol), name + " warm-up")
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    reps = [h.pcg_solve(b, x, rtol=rtol) for _ in range(steps)]
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    for rep in reps:
+        check_solve(rep, name)
+    ms = ev0.elapsed_time(ev1) / steps
+    h.profile(True)
+    check_solve(h.pcg_solve(b, x, rtol=rtol), name + " profiling")
+    prof = h.profile_read()
+    h.profile(False)
+    top = sorted(((k, v["ms"]) for k, v in prof.items() if v["launches"]), key=lambda kv: -kv[1])[:4]
+    out = {"workload": WORKLOADS.get(name, name), "leaf_cells": tree.N, "mu": cfg["mu"], "steps": steps,
+           "warmup": warmup, "ms_per_solve": ms, "cells_per_s": tree.N / (ms * 1e-3), "pcg_iters": reps[-1]["iters"],
+           "setup_s": setup_s, "profile_top_ms": {k: v for k, v in top},
+           "profile_note": "per-class ms of one solve with CUDA events around every launch (graph replay off)"}
+    del h, tree, b, x
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
 def traffic_from_profiles(config):
     """ncu dram bytes per launch of the dominant kernel, from the committed summary."""
     p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -180,10 +290,14 @@ def traffic_from_profiles(config):
 
 def main():
     args = parse()
+    rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one process per GPU")
     if args.impl == "reference":
         return run_reference(args)
     import torch
-    rank, world, local = dist_env()
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -249,7 +363,7 @@ def main():
 
     # ---- device-resident timing --------------------------------------------------------
     for _ in range(args.warmup):
-        rep = h.pcg_solve(b, x, rtol=args.rtol)
+        rep = check_solve(h.pcg_solve(b, x, rtol=args.rtol), "warm-up")
     torch.cuda.synchronize()
     barrier()
     sampler = ClockSampler(dev.index)
@@ -258,14 +372,18 @@ def main():
     ev0.record(stream)
     launches = 0
     iters = []
+    reps = []
     for _ in range(args.steps):
         rep = h.pcg_solve(b, x, rtol=args.rtol)
+        reps.append(rep)
         launches += rep["kernel_launches"]
         iters.append(rep["iters"])
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
     clocks = sampler.stop()
+    for rep in reps:
+        check_solve(rep, "timed")
     ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     units = N if partitioned else world * N  # cells solved by the whole job per step
     value = units / (ms * 1e-3)
@@ -283,6 +401,8 @@ def main():
     e_x = [torch.cuda.Event(), torch.cuda.Event()]
     e_d = [torch.cuda.Event(), torch.cuda.Event()]
 
+    e2e_reps = []
+
     def run_e2e(n):
         s_in.wait_stream(stream)
         s_out.wait_stream(stream)
@@ -299,7 +419,7 @@ def main():
                 e_b[1 - i].record(s_in)
             stream.wait_event(e_b[i])
             stream.wait_event(e_d[i])  # the download of x2[i] from step k-2 is done
-            h.pcg_solve(b2[i], x2[i], rtol=args.rtol, stream=stream)
+            e2e_reps.append(h.pcg_solve(b2[i], x2[i], rtol=args.rtol, stream=stream))
             e_x[i].record(stream)
             s_out.wait_event(e_x[i])
             with torch.cuda.stream(s_out):
@@ -317,11 +437,13 @@ def main():
     torch.cuda.synchronize()
     barrier()
     ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    for rep in e2e_reps:
+        check_solve(rep, "e2e")
 
     # ---- per-kernel device time (profiling pass: events around every launch) -----------
     h.profile(True)
     for _ in range(2):
-        h.pcg_solve(b, x, rtol=args.rtol)
+        check_solve(h.pcg_solve(b, x, rtol=args.rtol), "profiling")
     prof = h.profile_read()
     h.profile(False)
     dom = max((k for k in prof if prof[k]["launches"]), key=lambda k: prof[k]["ms"])
@@ -337,6 +459,7 @@ def main():
     solve_bytes = sum(v["bytes"] for v in prof.values()) / 2
     traffic = traffic_from_profiles(args.config)
 
+    line = {}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world, "steps": args.steps,
@@ -351,6 +474,8 @@ def main():
                              % (tree.T * 512 * 16 / 1e6)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "committed ncu --set full capture (profiles/roofline_traffic.json), "
+                                           "not measured in this run",
                          "share_of_step": d["ms"] / tot_ms if tot_ms else None,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
             "model_gbs_solve": solve_bytes / (ms * 1e-3) / 1e9,
@@ -365,8 +490,18 @@ def main():
             "paper_context": "RTX 4090: uniform (5-5) 256^3 = 2.41e8 cells/s (Table 1, P:L1797, M = 2^20)",
             "setup_note": setup_note,
         }
+    if world == 1 and not args.no_wcycle and args.config == "cfg2_uniform256":
+        # the W-cycle configs (BASELINE configs 4, 5) timed in the same run, as extra keys
+        del h, tree, b, x, b2, x2, kind
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        extra = {}
+        for name in ("cfg4_tank", "cfg5_tank"):
+            extra[name] = time_config(om, torch, name, args.wcycle_steps, 3, args.rtol)
+        line["wcycle_configs"] = extra
+    if rank == 0:
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, args.config)
         print(json.dumps(line), flush=True)
     if world > 1:
         del h, tree

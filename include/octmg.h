@@ -111,7 +111,7 @@ octmg_status octmg_tree_export(const octmg_tree* tree, int32_t what, void* host_
 
 typedef struct {
   float alpha;          /* restriction scaling, R = P^T / alpha; 2   */
-  float beta;           /* overshoot, applied at restriction (Alg. 4 line 10); 2   */
+  float beta_overshoot; /* MG overshoot beta (not the PDE face_beta), at restriction (Alg. 4 line 10); 2   */
   int32_t mu;           /* cycle index: 1 V-cycle, 2 W-cycle                   */
   int32_t nu_pre;       /* RBGS iterations (red+black) before coarsening: 2        */
   int32_t nu_post;      /* RBGS iterations after (opposite colour order): 2                 */
@@ -279,13 +279,19 @@ typedef struct {
   double* history;      /* optional host array: relative residual after each iteration   */
   int32_t history_cap;
   int64_t kernel_launches; /* device kernels launched by this solve (graph nodes counted) */
+  int32_t history_len;  /* entries of history written: min(iters, history_cap), and at most
+                           512 in the device-side loop                                    */
 } octmg_solve_report;
 
 /*
  * Alg. 1: x0 = 0, r0 = b (masked to active cells, projected if nullspace),
- * z = M r, CG recurrences with fp64 scalars kept on the device; one 8-byte device->host
- * read per iteration for the stopping test.  b (read-only) and x (overwritten) are
- * device f32[N].  Synchronises `stream` before returning.  report may be NULL.
+ * z = M r, CG recurrences with fp64 scalars kept on the device.  Single-part hierarchies
+ * run the whole loop as ONE CUDA graph with a conditional while node whose stopping test
+ * (Alg. 1 line 8) runs on the device: one host synchronisation per solve (environment
+ * OCTMG_GRAPH_LOOP=0, profiling, or a driver without conditional nodes: the host-driven
+ * loop, one 8-byte scalar read per iteration; partitioned hierarchies also use it).
+ * b (read-only) and x (overwritten) are device f32[N].  Synchronises `stream` before
+ * returning.  report may be NULL.
  */
 octmg_status octmg_pcg_solve(octmg_hier* h, const float* b, float* x, const octmg_solve_params* params,
                              octmg_solve_report* report, octmg_stream stream);

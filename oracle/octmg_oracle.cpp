@@ -80,7 +80,7 @@ struct Oracle {
 
   // inputs and coefficients
   std::vector<uint8_t> kind;         // leaf cells
-  std::vector<double> w[6];          // leaf cells
+  std::vector<float> w[6];           // leaf cells (the fp32 inputs, read as exact doubles)
   std::vector<double> c, cm[3];      // all tiles' cells
   std::unordered_map<uint64_t, std::array<double, 3>> gcoef;  // ghost-cell -face coefficients
   double alpha = 2.0;
@@ -88,6 +88,14 @@ struct Oracle {
 
   // multigrid work arrays (all tiles' cells)
   std::vector<double> u, b, ustar;
+  // scratch (all tiles' cells): the pass-start snapshot of an RBGS pass (only the level's
+  // cells and the coarse leaves its ghosts read are refreshed) and A^{l-1} u* of the FAS
+  // restriction (only level l-1's cells are written and read)
+  std::vector<double> snap, Au;
+  // Eq. 14 check: after each prolongation, the largest |mean of the active
+  // children - coarse value| and the largest |coarse value| seen (off unless enabled)
+  bool check_eq14 = false;
+  double eq14_dev = 0.0, eq14_scale = 0.0;
 
   int levels() const { return L + 1; }
   int tlev(int t) const { return tile[t][0]; }
@@ -144,7 +152,7 @@ struct Oracle {
     return false;
   }
   uint8_t leaf_kind(size_t i) const { return kind[i]; }
-  double wf(int f, size_t i) const { return w[f][i]; }
+  double wf(int f, size_t i) const { return (double)w[f][i]; }
 };
 
 // -------------------------------------------------------------------------------------
@@ -318,9 +326,16 @@ int assemble(Oracle& o) {
   o.c.assign(NC, 0.0);
   for (int a = 0; a < 3; ++a) o.cm[a].assign(NC, 0.0);
   o.gcoef.clear();
-  std::vector<size_t> subs;
+  int err = S_OK;  // first error seen by any thread (each cell's outputs are independent)
+  std::string err_msg;
+  auto fail = [&](int st, const char* msg) {
+#pragma omp critical(orc_assemble_err)
+    if (err == S_OK) { err = st; err_msg = msg; }
+  };
   // pass 1: diagonals of leaf cells from geometry
+#pragma omp parallel for schedule(dynamic, 64)
   for (int t = 0; t < o.NL; ++t) {
+    std::vector<size_t> subs;
     int l = o.tlev(t);
     double h = o.hcell(l);
     for (int off = 0; off < B3; ++off) {
@@ -342,21 +357,26 @@ int assemble(Oracle& o) {
         } else if (n.what == L_CELL) {
           fine_subcells(o, l, n, f, subs);
           for (size_t sidx : subs) {
-            if (sidx == (size_t)-1) { g_err = "fine sub-cell is not a leaf"; return S_NOT_GRADED; }
+            if (sidx == (size_t)-1) { fail(S_NOT_GRADED, "fine sub-cell is not a leaf"); continue; }
             if (o.kind[sidx] != K_NEUMANN) s += 0.5 * o.wf(f ^ 1, sidx) * (0.5 * h);
           }
         } else if (n.what == L_GHOST) {
           if (o.kind[o.idx(n.tile, n.off)] != K_NEUMANN) s += o.wf(f, i) * h;
         } else {
-          g_err = "uncovered neighbour";
-          return S_NOT_GRADED;
+          fail(S_NOT_GRADED, "uncovered neighbour");
         }
       }
       o.c[i] = s;  // a fluid cell with c == 0 is isolated and therefore inactive
     }
   }
-  // pass 2: -face off-diagonals and ghost-cell coefficients of the + faces
+  if (err) { g_err = err_msg; return err; }
+  // pass 2: -face off-diagonals and ghost-cell coefficients of the + faces (the ghost
+  // entries are collected per tile and inserted in tile order afterwards)
+  struct GEntry { uint64_t key; int a; double v; };
+  std::vector<std::vector<GEntry>> gent(o.NL);
+#pragma omp parallel for schedule(dynamic, 64)
   for (int t = 0; t < o.NL; ++t) {
+    std::vector<size_t> subs;
     int l = o.tlev(t);
     double h = o.hcell(l);
     for (int off = 0; off < B3; ++off) {
@@ -388,11 +408,13 @@ int assemble(Oracle& o) {
         Loc g = o.locate(l, p[0], p[1], p[2]);
         if (g.what == L_GHOST) {
           double gv = o.kind[o.idx(g.tile, g.off)] != K_NEUMANN ? -o.wf(f + 1, i) * h : 0.0;
-          o.gcoef[gkey(l, p[0], p[1], p[2])][a] = gv;
+          gent[t].push_back({gkey(l, p[0], p[1], p[2]), a, gv});
         }
       }
     }
   }
+  for (int t = 0; t < o.NL; ++t)
+    for (const GEntry& e : gent[t]) o.gcoef[e.key][e.a] = e.v;
   return S_OK;
 }
 
@@ -403,6 +425,7 @@ int assemble(Oracle& o) {
 void coarsen_level(Oracle& o, int l, bool literal) {
   const double al = o.alpha;
   int lc = l - 1;
+#pragma omp parallel for schedule(dynamic, 16)
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t) {
     for (int off = 0; off < o.B3; ++off) {
       int64_t IX, IY, IZ;
@@ -441,8 +464,8 @@ int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha, bool lit
   size_t N = (size_t)o.NL * o.B3;
   o.kind.assign(kind, kind + N);
   for (int f = 0; f < 6; ++f) {
-    o.w[f].resize(N);
-    for (size_t i = 0; i < N; ++i) o.w[f][i] = w ? (double)w[(size_t)f * N + i] : 1.0;
+    if (w) o.w[f].assign(w + (size_t)f * N, w + (size_t)(f + 1) * N);
+    else o.w[f].assign(N, 1.0f);
   }
   for (size_t i = 0; i < N; ++i)
     if (o.kind[i] > 2) { g_err = "bad cell kind"; return S_INVALID; }
@@ -453,6 +476,7 @@ int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha, bool lit
   o.setup = true;
   size_t NC = (size_t)o.T * o.B3;
   o.u.assign(NC, 0.0); o.b.assign(NC, 0.0); o.ustar.assign(NC, 0.0);
+  o.snap.assign(NC, 0.0); o.Au.assign(NC, 0.0);
   return S_OK;
 }
 
@@ -594,7 +618,15 @@ void apply_level(const Oracle& o, int l, const double* u, double* y) {
 // the global level-l cell coordinates (0 = red).  Ghost values and m_P come from the
 // state at the start of the pass (SURVEY c-5 / c-8 #1).
 void rbgs_pass(Oracle& o, int l, int colour, double* u, const double* b) {
-  std::vector<double> snap(u, u + (size_t)o.T * o.B3);
+  // pass-start snapshot of what the pass reads: level l's cells (leaf and inner segments)
+  // and the level-(l-1) leaf cells behind its ghosts (not written by the pass)
+  std::vector<double>& snap = o.snap;
+  auto keep = [&](int first, int count) {
+    std::copy(u + o.idx(first, 0), u + o.idx(first + count, 0), snap.begin() + o.idx(first, 0));
+  };
+  keep(o.lb[l], o.lc[l]);
+  keep(o.ib[l], o.ic[l]);
+  if (l >= 1) keep(o.lb[l - 1], o.lc[l - 1]);
   for_level_tiles(o, l, [&](int t) {
     for (int off = 0; off < o.B3; ++off) {
       int64_t X, Y, Z;
@@ -640,6 +672,25 @@ void children_of(const Oracle& o, int lc, int t, int off, size_t out[8]) {
   }
 }
 
+// Eq. 14 as a check: after the prolongation of the inner cells of level lc,
+// the mean of each inner cell's active children equals its coarse value u^{lc}_I.  Records
+// the largest deviation and the largest |u^{lc}_I| (serial, inner-cell order).
+void eq14_check(Oracle& o, int lc) {
+  for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
+    for (int off = 0; off < o.B3; ++off) {
+      size_t ch[8];
+      children_of(o, lc, t, off, ch);
+      double s = 0.0;
+      int n = 0;
+      for (int d = 0; d < 8; ++d)
+        if (o.c[ch[d]] != 0.0) { s += o.u[ch[d]]; n++; }
+      if (!n) continue;
+      size_t I = o.idx(t, off);
+      o.eq14_dev = std::max(o.eq14_dev, std::fabs(s / n - o.u[I]));
+      o.eq14_scale = std::max(o.eq14_scale, std::fabs(o.u[I]));
+    }
+}
+
 // Alg. 4, FAS-style mu-cycle, readings SURVEY c-6.
 void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
   if (l == 0) { smooth_coarsest(o, p); return; }
@@ -647,6 +698,7 @@ void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
   residual(o, l, r);                             // r^l = b^l - A^l u^l
   int lc = l - 1;
   // u*_I = Avg(u^l) over active children; u^{l-1}_I := u*_I  (inner cells of level l-1)
+#pragma omp parallel for schedule(dynamic, 16)
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
     for (int off = 0; off < o.B3; ++off) {
       size_t ch[8];
@@ -660,8 +712,9 @@ void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
       o.u[I] = o.ustar[I];
     }
   // b^{l-1}_I = beta R r^l + (A^{l-1} u^{l-1})_I  on inner rows; leaf(l-1) rows keep b
-  std::vector<double> Au((size_t)o.T * o.B3, 0.0);
+  std::vector<double>& Au = o.Au;  // only level l-1's entries are written and read
   apply_level(o, lc, o.u.data(), Au.data());
+#pragma omp parallel for schedule(dynamic, 16)
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
     for (int off = 0; off < o.B3; ++off) {
       size_t ch[8];
@@ -674,6 +727,7 @@ void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
     }
   for (int k = 0; k < p.mu; ++k) fas(o, lc, p, r);
   // prolongation of the update u^{l-1} - u* (no beta)
+#pragma omp parallel for schedule(dynamic, 16)
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
     for (int off = 0; off < o.B3; ++off) {
       size_t ch[8];
@@ -683,6 +737,7 @@ void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
       for (int d = 0; d < 8; ++d)
         if (o.c[ch[d]] != 0.0) o.u[ch[d]] += corr;
     }
+  if (o.check_eq14) eq14_check(o, lc);
   smooth(o, l, p.nu_post, false);                // post-smoothing (B,R)
 }
 
@@ -693,6 +748,7 @@ void mucycle_std(Oracle& o, int l, const MG& p, std::vector<double>& r) {
   smooth(o, l, p.nu_pre, true);
   residual(o, l, r);
   int lc = l - 1;
+#pragma omp parallel for schedule(dynamic, 16)
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
     for (int off = 0; off < o.B3; ++off) {
       size_t ch[8];
@@ -705,6 +761,7 @@ void mucycle_std(Oracle& o, int l, const MG& p, std::vector<double>& r) {
       o.u[I] = 0.0;
     }
   for (int k = 0; k < p.mu; ++k) mucycle_std(o, lc, p, r);
+#pragma omp parallel for schedule(dynamic, 16)
   for (int t = o.ib[lc]; t < o.ib[lc] + o.ic[lc]; ++t)
     for (int off = 0; off < o.B3; ++off) {
       size_t ch[8];
@@ -744,6 +801,7 @@ void project_mean(const Oracle& o, double* r) {
     if (o.c[i] != 0.0) { s += r[i]; n++; }
   if (!n) return;
   double m = s / (double)n;
+#pragma omp parallel for schedule(static)
   for (size_t i = 0; i < N; ++i)
     if (o.c[i] != 0.0) r[i] -= m;
 }
@@ -781,6 +839,7 @@ int pcg(Oracle& o, const MG& p, int precond_kind, const double* bin, double* x, 
     double sigma = dot(o, pv.data(), q.data());
     if (!(sigma > 0.0)) { *iters_out = k; return S_BREAKDOWN; }
     double alpha = rho / sigma;
+#pragma omp parallel for schedule(static)
     for (size_t i = 0; i < N; ++i) { x[i] += alpha * pv[i]; r[i] -= alpha * q[i]; }
     if (ns) project_mean(o, r.data());
     k++;
@@ -794,6 +853,7 @@ int pcg(Oracle& o, const MG& p, int precond_kind, const double* bin, double* x, 
     double rho2 = dot(o, r.data(), z.data());
     double beta = rho2 / rho;
     rho = rho2;
+#pragma omp parallel for schedule(static)
     for (size_t i = 0; i < N; ++i) pv[i] = z[i] + beta * pv[i];
   }
 }
@@ -989,6 +1049,7 @@ double face_fraction(const double phi[4], double phi_centre) {
 void tank_fields(const int32_t* tiles, int64_t n, int B, const double* ext, const double* c, double r,
                  uint8_t* kind, float* w, float* bout) {
   const int64_t B3 = (int64_t)B * B * B, N = n * B3;
+#pragma omp parallel for schedule(static)
   for (int64_t t = 0; t < n; ++t) {
     const int l = tiles[4 * t];
     const double h = std::ldexp(1.0, -l) / B;
@@ -1100,6 +1161,12 @@ void orc_coefs(void* h, double* out) {
   }
 }
 
+// out: the diagonal c of the leaf cells (NL*B3 doubles; c == 0: inactive)
+void orc_leaf_diag(void* h, double* out) {
+  auto* o = (Oracle*)h;
+  std::memcpy(out, o->c.data(), sizeof(double) * (size_t)o->NL * o->B3);
+}
+
 // ghost cell (level, X, Y, Z): its -face coefficients; returns 1 if such a ghost exists
 int32_t orc_ghost_coef(void* h, int32_t l, int64_t X, int64_t Y, int64_t Z, double* out) {
   auto* o = (Oracle*)h;
@@ -1110,6 +1177,19 @@ int32_t orc_ghost_coef(void* h, int32_t l, int64_t X, int64_t Y, int64_t Z, doub
 }
 
 void orc_apply(void* h, const double* x, double* y) { apply_composite(*(Oracle*)h, x, y); }
+
+// Eq. 14 check: enable / reset; read [max deviation, max |coarse value|]
+void orc_set_check_eq14(void* h, int32_t on) {
+  auto* o = (Oracle*)h;
+  o->check_eq14 = on != 0;
+  o->eq14_dev = 0.0;
+  o->eq14_scale = 0.0;
+}
+void orc_eq14(void* h, double* out) {
+  auto* o = (Oracle*)h;
+  out[0] = o->eq14_dev;
+  out[1] = o->eq14_scale;
+}
 
 void orc_apply_level(void* h, int32_t l, const double* u, double* y) {
   apply_level(*(Oracle*)h, l, u, y);

@@ -59,6 +59,9 @@ def lib():
         _lib.orc_face_fraction.restype = D
         _lib.orc_face_fraction.argtypes = [P, D]
         _lib.orc_tank_fields.argtypes = [P, I64, I32, P, P, D, P, P, P]
+        _lib.orc_leaf_diag.argtypes = [P, P]
+        _lib.orc_set_check_eq14.argtypes = [P, I32]
+        _lib.orc_eq14.argtypes = [P, P]
         _lib.orc_mg_solve.restype = I32
         _lib.orc_mg_solve.argtypes = [P, P, I32, P, P, D, I32, I32, P, P, P, P, I32]
     return _lib
@@ -161,6 +164,12 @@ class Oracle:
         lib().orc_coefs(self._h, _p(out))
         return out
 
+    def coefs_diag_leaf(self):
+        """The diagonal c of the leaf cells (c == 0: inactive), without the full export."""
+        out = np.zeros(self.N)
+        lib().orc_leaf_diag(self._h, _p(out))
+        return out
+
     def ghost_coef(self, level, X, Y, Z):
         out = np.zeros(3)
         ok = lib().orc_ghost_coef(self._h, level, X, Y, Z, _p(out))
@@ -221,6 +230,16 @@ class Oracle:
         n = int(it[0])
         return dict(x=x, iters=n, rel_residual=float(rr[0]), bnorm=float(bn[0]),
                     status=STATUS.get(st, st), history=hist[:min(n, hcap)].copy())
+
+    def eq14_check(self, on: bool = True):
+        """Enable (and reset) the Eq. 14 check inside the FAS cycle."""
+        lib().orc_set_check_eq14(self._h, int(on))
+
+    def eq14_result(self):
+        """(max |mean of active children - coarse value| after a prolongation, max |coarse value|)."""
+        out = np.zeros(2)
+        lib().orc_eq14(self._h, _p(out))
+        return float(out[0]), float(out[1])
 
     # ---- projection (P:L1610-1613) ---------------------------------------------------
     def divergence(self, frac, u6):

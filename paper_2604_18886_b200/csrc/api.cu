@@ -81,15 +81,19 @@ static octmg_status halloc(std::vector<void*>& list, T** p, size_t count) {
 }
 
 Hier::~Hier() {
+  // work issued on any stream may still read these buffers; a caching allocator hook (unlike
+  // cudaFree) would hand them out again at once
+  if (!allocs.empty()) cudaDeviceSynchronize();
   for (auto e : event_pool) cudaEventDestroy(e);
   for (void* p : allocs) dev_free(p);
   if (sc_host) cudaFreeHost(sc_host);
 }
 
 Group::~Group() {
+  cudaDeviceSynchronize();
   if (graph) cudaGraphExecDestroy(graph);
   if (loop_graph) cudaGraphExecDestroy(loop_graph);
-  if (loop) cudaFree(loop);
+  if (loop) dev_free(loop);
   if (loop_host) cudaFreeHost(loop_host);
   if (graph_stream) cudaStreamDestroy(graph_stream);
   for (Hier* h : parts) delete h;
@@ -132,8 +136,7 @@ octmg_status build_orders(Hier& h) {
     order.insert(order.end(), ts.begin(), ts.end());
   }
   int* d;
-  OCTMG_CUDA(cudaMalloc(&d, sizeof(int) * std::max<size_t>(order.size(), 1)));
-  h.allocs.push_back(d);
+  OCTMG_TRY(halloc(h.allocs, &d, order.size()));
   OCTMG_CUDA(cudaMemcpy(d, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
   h.order = d;
   return OCTMG_OK;
@@ -299,8 +302,8 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   // FAS form (Alg. 4): beta at restriction, prolongation of u^{l-1} - u*; standard form
   // (Alg. 2): R r as the coarse rhs, zero coarse guess (u* = 0), beta at prolongation
   a.std_form = h.prm.form == 1;
-  a.beta = a.std_form ? 1.0f : h.prm.beta;
-  a.pro_scale = a.std_form ? h.prm.beta : 1.0f;
+  a.beta = a.std_form ? 1.0f : h.prm.beta_overshoot;
+  a.pro_scale = a.std_form ? h.prm.beta_overshoot : 1.0f;
   a.order = h.order + h.lvl_order_off[l];
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
@@ -845,7 +848,8 @@ octmg_status build_loop_graph(Group& g, bool ns) {
   Hier& h = *g.parts[0];
   if (!g.graph_stream) OCTMG_CUDA(cudaStreamCreateWithFlags(&g.graph_stream, cudaStreamNonBlocking));
   if (!g.loop) {
-    OCTMG_CUDA(cudaMalloc(&g.loop, sizeof(LoopState)));
+    g.loop = (LoopState*)dev_malloc(sizeof(LoopState));
+    if (!g.loop) { set_error("device allocation failed (PCG loop state)"); return OCTMG_E_OOM; }
     OCTMG_CUDA(cudaMallocHost(&g.loop_host, sizeof(LoopState)));
   }
   if (g.loop_graph) {
@@ -914,6 +918,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   const int64_t launches0 = g.launches;
   const int np = (int)g.parts.size();
   Scalars* hs = h0.sc_host;
+  int hist_lim = 1 << 30;  // the device-side loop records LOOP_HCAP entries at most
   auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
     // the iterate (slot order) -> the caller's x (natural order), owned cells of each part
     for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
@@ -925,6 +930,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       report->bnorm = bn;
       report->status = st;
       report->kernel_launches = g.launches - launches0;
+      report->history_len = report->history ? std::min(std::min(iters, (int)report->history_cap), hist_lim) : 0;
     }
     return st;
   };
@@ -966,9 +972,19 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   const double bn = std::sqrt(hs->sum_rr);
   if (bn == 0.0) return fill(OCTMG_OK, 0, true, 0.0, 0.0);
   const char* gl = getenv("OCTMG_GRAPH_LOOP");  // default on for single-part hierarchies; 0: host loop
-  if (!(gl && atoi(gl) == 0) && np == 1 && !g.comm && !profiling(g)) {
+  bool device_loop = !(gl && atoi(gl) == 0) && np == 1 && !g.comm && !profiling(g) && !g.loop_unavailable;
+  if (device_loop && (!g.loop_graph || g.loop_ns != (ns ? 1 : 0))) {
+    // a driver without conditional nodes, or a schedule variant whose launches a
+    // conditional body cannot hold (cooperative / cluster launches): fall back to the
+    // host-driven loop for this hierarchy from now on
+    if (build_loop_graph(g, ns) != OCTMG_OK) {
+      cudaGetLastError();
+      g.loop_unavailable = true;
+      device_loop = false;
+    }
+  }
+  if (device_loop) {
     // the device-side loop: one graph launch, one synchronisation per solve
-    if (!g.loop_graph || g.loop_ns != (ns ? 1 : 0)) OCTMG_TRY(build_loop_graph(g, ns));
     LoopState* L = g.loop_host;
     L->bn = bn;
     L->rtol = prm.rtol;
@@ -986,9 +1002,13 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     OCTMG_CUDA(cudaMemcpyAsync(L, g.loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
-    g.launches += (int64_t)kk * (schedule_kernels(g) + 7);
-    if (report && report->history)
-      for (int i = 0; i < kk && i < report->history_cap && i < LOOP_HCAP; ++i) report->history[i] = L->hist[i];
+    // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
+    g.launches += (int64_t)kk * (schedule_kernels(g) + 6 + (ns ? 1 : 0));
+    hist_lim = LOOP_HCAP;
+    if (report && report->history) {
+      const int nh = std::min(kk, std::min((int)report->history_cap, LOOP_HCAP));
+      for (int i = 0; i < nh; ++i) report->history[i] = L->hist[i];
+    }
     if (L->status == 9) { set_error("PCG breakdown: p.Ap <= 0"); return fill(OCTMG_E_BREAKDOWN, kk - 1, false, L->rel, bn); }
     if (L->status == 8) { set_error("non-finite PCG scalar"); return fill(OCTMG_E_NONFINITE, kk - 1, false, L->rel, bn); }
     if (L->converged) return fill(OCTMG_OK, kk, true, L->rel, bn);
@@ -1090,6 +1110,7 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
       report->bnorm = bn;
       report->status = st;
       report->kernel_launches = g.launches - launches0;
+      report->history_len = report->history ? std::min(iters, (int)report->history_cap) : 0;
     }
     return st;
   };

@@ -109,7 +109,7 @@ void levels_of(const Group& g, int level, int field, int* l0, int* l1) {
 struct LoopbackComm : Comm {
   Scalars** d_scs = nullptr;
   ~LoopbackComm() override {
-    if (d_scs) cudaFree(d_scs);
+    if (d_scs) { cudaDeviceSynchronize(); dev_free(d_scs); }
   }
   const char* name() const override { return "loopback"; }
   octmg_status exchange(Group& g, int level, int field, const std::vector<Fld>& f, cudaStream_t s) override {
@@ -149,7 +149,8 @@ struct LoopbackComm : Comm {
     if (!d_scs) {
       std::vector<Scalars*> v;
       for (Hier* h : g.parts) v.push_back(h->sc);
-      OCTMG_CUDA(cudaMalloc(&d_scs, sizeof(Scalars*) * n));
+      d_scs = (Scalars**)dev_malloc(sizeof(Scalars*) * n);
+      if (!d_scs) { set_error("device allocation failed (loopback scalars)"); return OCTMG_E_OOM; }
       OCTMG_CUDA(cudaMemcpy(d_scs, v.data(), sizeof(Scalars*) * n, cudaMemcpyHostToDevice));
     }
     k_sum_scalars<<<1, 32, 0, s>>>(d_scs, n, first, count);

@@ -18,8 +18,15 @@ void set_error(const std::string& msg);
 
 namespace {
 
+// 19 bits per axis (the tree's own limit, tree.cu: ext << level <= 2^19) and the level
 inline uint64_t key(int l, int64_t i, int64_t j, int64_t k) {
   return ((uint64_t)l << 57) | ((uint64_t)i << 38) | ((uint64_t)j << 19) | (uint64_t)k;
+}
+constexpr int64_t KEY_AXIS = int64_t(1) << 19;
+inline bool key_fits(const int32_t* ext, int level) {
+  for (int a = 0; a < 3; ++a)
+    if (ext[a] < 1 || ((int64_t)ext[a] << level) > KEY_AXIS) return false;
+  return true;
 }
 
 }  // namespace
@@ -32,6 +39,10 @@ octmg_status grade_repair(const octmg_tile* in, int64_t n, const int32_t* ext, s
         ((int64_t)t.i >> t.level) >= ext[0] || ((int64_t)t.j >> t.level) >= ext[1] ||
         ((int64_t)t.k >> t.level) >= ext[2]) {
       set_error("leaf tile out of range");
+      return OCTMG_E_INVALID;
+    }
+    if (!key_fits(ext, t.level)) {
+      set_error("domain too fine: ext << level exceeds 2^19 tiles per axis");
       return OCTMG_E_INVALID;
     }
     set.insert(key(t.level, t.i, t.j, t.k));
@@ -63,7 +74,7 @@ octmg_status grade_repair(const octmg_tile* in, int64_t n, const int32_t* ext, s
       if (!marked.count(key(t.level, t.i, t.j, t.k))) next.push_back(t);
     for (const octmg_tile& t : refine) {
       set.erase(key(t.level, t.i, t.j, t.k));
-      if (t.level + 1 >= OCTMG_MAX_LEVELS) {
+      if (t.level + 1 >= OCTMG_MAX_LEVELS || !key_fits(ext, t.level + 1)) {
         set_error("grading repair exceeds the maximum level");
         return OCTMG_E_INVALID;
       }

@@ -349,6 +349,7 @@ struct Group {
   LoopState* loop = nullptr;             // device
   LoopState* loop_host = nullptr;        // pinned
   int loop_ns = -1;                      // null-space flag the loop graph was built with
+  bool loop_unavailable = false;         // building the loop graph failed: host-driven loop
   int64_t launches = 0;
   ~Group();
 };

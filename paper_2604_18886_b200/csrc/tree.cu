@@ -181,6 +181,7 @@ static octmg_status dalloc(std::vector<void*>& list, T** p, size_t count) {
 }
 
 Tree::~Tree() {
+  if (!allocs.empty()) cudaDeviceSynchronize();  // see Hier::~Hier
   for (void* p : allocs) dev_free(p);
 }
 

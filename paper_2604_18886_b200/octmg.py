@@ -38,7 +38,7 @@ class TreeInfo(C.Structure):
 
 
 class MGParams(C.Structure):
-    _fields_ = [("alpha", C.c_float), ("beta", C.c_float), ("mu", C.c_int32), ("nu_pre", C.c_int32),
+    _fields_ = [("alpha", C.c_float), ("beta_overshoot", C.c_float), ("mu", C.c_int32), ("nu_pre", C.c_int32),
                 ("nu_post", C.c_int32), ("nu_coarsest", C.c_int32), ("form", C.c_int32),
                 ("coarsen_literal", C.c_int32)]
 
@@ -50,7 +50,7 @@ class SolveParams(C.Structure):
 class SolveReport(C.Structure):
     _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
                 ("bnorm", C.c_double), ("status", C.c_int32), ("history", C.POINTER(C.c_double)),
-                ("history_cap", C.c_int32), ("kernel_launches", C.c_int64)]
+                ("history_cap", C.c_int32), ("kernel_launches", C.c_int64), ("history_len", C.c_int32)]
 
 
 EXPORT_TILES, EXPORT_NBR, EXPORT_PARENT, EXPORT_CHILD = 0, 1, 2, 3
@@ -288,7 +288,7 @@ class Hierarchy:
         st = fn(self._h, _ptr(b), _ptr(x), C.byref(prm), C.byref(rep), _stream(stream))
         out = dict(iters=rep.iters, converged=bool(rep.converged), rel_residual=rep.rel_residual,
                    bnorm=rep.bnorm, status=STATUS.get(st, st), kernel_launches=int(rep.kernel_launches),
-                   history=np.array(hist[:min(rep.iters, history_cap)]))
+                   history=np.array(hist[:rep.history_len]))
         if raise_on_error and st not in (0, 10):
             _check(st)
         return out
