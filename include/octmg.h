@@ -124,6 +124,20 @@ typedef struct {
                            branch without the activity test); 0 (default): with the test,
                            so that Alg. 3 equals R A P over the fluid unknowns (DESIGN.md
                            reading 3)                                                        */
+  int32_t coarsest;     /* level-0 step of the cycle (Alg. 4 line 4): 0 (default)
+                           nu_coarsest RBGS iterations; 1 "or direct solve":
+                           u^0 = M0 b^0 with M0 the solution operator of the level-0
+                           system over its active cells, precomputed at setup (exact
+                           inverse on components coupled to a Dirichlet cell or wall; the
+                           minimum-norm solution on floating pure-Neumann components,
+                           DESIGN.md reading 9b).  Needs <= 4096 level-0 cells (ext product
+                           <= 8), else OCTMG_E_INVALID                                       */
+  int32_t reserved0;
+  int64_t gather_below_cells; /* multi-GPU: levels whose total cell count is
+                           below this are not partitioned — every rank holds and smooths
+                           them redundantly after an all-gather of the restricted partition
+                           parents (0 = the default threshold, 2^21 cells; single part:
+                           ignored)                                                          */
 } octmg_mg_params;
 
 /*

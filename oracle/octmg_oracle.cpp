@@ -65,6 +65,7 @@ uint64_t morton(int64_t i, int64_t j, int64_t k) {
 struct MG {
   double alpha = 2.0, beta = 2.0;
   int mu = 1, nu_pre = 2, nu_post = 2, nu_coarsest = 10;
+  int coarsest = 0;  // 0: nu_b RBGS iterations at level 0; 1: direct solve (Alg. 4 line 4)
 };
 
 struct Oracle {
@@ -96,6 +97,10 @@ struct Oracle {
   // children - coarse value| and the largest |coarse value| seen (off unless enabled)
   bool check_eq14 = false;
   double eq14_dev = 0.0, eq14_scale = 0.0;
+  // direct coarsest solve (built on first use after setup): the level-0 cells (all-tile
+  // indices, leaf segment then inner segment) and the dense solution operator M0 (row-major)
+  std::vector<size_t> c0_cells;
+  std::vector<double> M0;
 
   int levels() const { return L + 1; }
   int tlev(int t) const { return tile[t][0]; }
@@ -477,6 +482,7 @@ int setup(Oracle& o, const uint8_t* kind, const float* w, double alpha, bool lit
   size_t NC = (size_t)o.T * o.B3;
   o.u.assign(NC, 0.0); o.b.assign(NC, 0.0); o.ustar.assign(NC, 0.0);
   o.snap.assign(NC, 0.0); o.Au.assign(NC, 0.0);
+  o.M0.clear(); o.c0_cells.clear();
   return S_OK;
 }
 
@@ -653,6 +659,130 @@ void smooth_coarsest(Oracle& o, const MG& p) {
   smooth(o, 0, p.nu_coarsest - p.nu_coarsest / 2, false);
 }
 
+// Direct solve at the coarsest level (Alg. 4 line 4, "Or direct solve"; DESIGN
+// reading 9b).  A0 = the level-0 operator over the cells of C_0, assembled column by column
+// with apply_level (a symmetric matrix: level 0 has no ghosts, and a same-level coupling is
+// the +side cell's -face entry in both rows).  Over the active cells:
+//  * a connected component (coupling graph A0_ij != 0) is FLOATING when every row sum
+//    |sum_j A0_ij| <= 1e-5 A0_ii (no Dirichlet coupling: A0 1_C = 0);
+//  * M0 = R^{-1} P: R = A0 + sum_{floating C} (s_C / |C|) 1_C 1_C^T (s_C = mean diagonal of
+//    C), P removes the mean of b over each floating component — so M0 b is the exact
+//    solution on nonsingular components and the minimum-norm (pseudo-inverse) solution on
+//    floating ones;
+//  * R^{-1} by Gauss-Jordan elimination with partial pivoting (textbook), fp64.
+// Inactive cells keep u = 0.
+void build_direct_coarsest(Oracle& o) {
+  std::vector<size_t>& cells = o.c0_cells;
+  cells.clear();
+  for (int t = o.lb[0]; t < o.lb[0] + o.lc[0]; ++t)
+    for (int off = 0; off < o.B3; ++off) cells.push_back(o.idx(t, off));
+  for (int t = o.ib[0]; t < o.ib[0] + o.ic[0]; ++t)
+    for (int off = 0; off < o.B3; ++off) cells.push_back(o.idx(t, off));
+  const size_t n = cells.size();
+  // unit vectors and columns in the level-local scratch arrays (apply_level at level 0 reads
+  // and writes only level-0 cells)
+  std::vector<double>& e = o.snap;
+  std::vector<double>& y = o.Au;
+  std::vector<double> A(n * n, 0.0);
+  for (size_t j = 0; j < n; ++j) e[cells[j]] = 0.0;
+  for (size_t j = 0; j < n; ++j) {
+    e[cells[j]] = 1.0;
+    apply_level(o, 0, e.data(), y.data());
+    for (size_t i = 0; i < n; ++i) A[i * n + j] = y[cells[i]];
+    e[cells[j]] = 0.0;
+  }
+  std::vector<char> act(n);
+  for (size_t i = 0; i < n; ++i) act[i] = o.c[cells[i]] != 0.0;
+  // connected components of the active cells (breadth-first)
+  std::vector<int> comp(n, -1);
+  int ncomp = 0;
+  for (size_t s0 = 0; s0 < n; ++s0) {
+    if (!act[s0] || comp[s0] >= 0) continue;
+    std::vector<size_t> q{s0};
+    comp[s0] = ncomp;
+    for (size_t k = 0; k < q.size(); ++k)
+      for (size_t j = 0; j < n; ++j)
+        if (act[j] && comp[j] < 0 && (A[q[k] * n + j] != 0.0 || A[j * n + q[k]] != 0.0)) {
+          comp[j] = ncomp;
+          q.push_back(j);
+        }
+    ncomp++;
+  }
+  std::vector<char> floating(ncomp, 1);
+  std::vector<double> csum(ncomp, 0.0);
+  std::vector<int> csize(ncomp, 0);
+  for (size_t i = 0; i < n; ++i) {
+    if (!act[i]) continue;
+    double rs = 0.0;
+    for (size_t j = 0; j < n; ++j) rs += A[i * n + j];
+    if (std::fabs(rs) > 1e-5 * A[i * n + i]) floating[comp[i]] = 0;
+    csum[comp[i]] += A[i * n + i];
+    csize[comp[i]]++;
+  }
+  // R = A0 on the active block + the floating components' rank-one terms; identity rows
+  // and columns for inactive cells
+  std::vector<double> R(n * n, 0.0);
+  for (size_t i = 0; i < n; ++i)
+    for (size_t j = 0; j < n; ++j) {
+      if (!act[i] || !act[j]) { R[i * n + j] = i == j ? 1.0 : 0.0; continue; }
+      R[i * n + j] = A[i * n + j];
+      if (comp[i] == comp[j] && floating[comp[i]]) R[i * n + j] += (csum[comp[i]] / csize[comp[i]]) / csize[comp[i]];
+    }
+  // Gauss-Jordan with partial pivoting: [R | I] -> [I | R^{-1}]
+  std::vector<double> Ri(n * n, 0.0);
+  for (size_t i = 0; i < n; ++i) Ri[i * n + i] = 1.0;
+  for (size_t k = 0; k < n; ++k) {
+    size_t piv = k;
+    for (size_t i = k + 1; i < n; ++i)
+      if (std::fabs(R[i * n + k]) > std::fabs(R[piv * n + k])) piv = i;
+    if (piv != k)
+      for (size_t j = 0; j < n; ++j) { std::swap(R[k * n + j], R[piv * n + j]); std::swap(Ri[k * n + j], Ri[piv * n + j]); }
+    const double d = R[k * n + k];
+    for (size_t j = 0; j < n; ++j) { R[k * n + j] /= d; Ri[k * n + j] /= d; }
+    for (size_t i = 0; i < n; ++i) {
+      if (i == k) continue;
+      const double f = R[i * n + k];
+      if (f == 0.0) continue;
+      for (size_t j = 0; j < n; ++j) { R[i * n + j] -= f * R[k * n + j]; Ri[i * n + j] -= f * Ri[k * n + j]; }
+    }
+  }
+  // M0 = R^{-1} P (P: mean removal over each floating component), zero for inactive cells
+  o.M0.assign(n * n, 0.0);
+  std::vector<double> rowmean(ncomp);
+  for (size_t i = 0; i < n; ++i) {
+    if (!act[i]) continue;
+    std::fill(rowmean.begin(), rowmean.end(), 0.0);
+    for (size_t j = 0; j < n; ++j)
+      if (act[j] && floating[comp[j]]) rowmean[comp[j]] += Ri[i * n + j];
+    for (size_t j = 0; j < n; ++j) {
+      if (!act[j]) continue;
+      double v = Ri[i * n + j];
+      if (floating[comp[j]]) v -= rowmean[comp[j]] / csize[comp[j]];
+      o.M0[i * n + j] = v;
+    }
+  }
+}
+
+void direct_coarsest(Oracle& o) {
+  if (o.M0.empty()) build_direct_coarsest(o);
+  const std::vector<size_t>& cells = o.c0_cells;
+  const size_t n = cells.size();
+  std::vector<double> bb(n), uu(n, 0.0);
+  for (size_t j = 0; j < n; ++j) bb[j] = o.b[cells[j]];
+  for (size_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (size_t j = 0; j < n; ++j) s += o.M0[i * n + j] * bb[j];
+    uu[i] = s;
+  }
+  for (size_t i = 0; i < n; ++i)
+    if (o.c[cells[i]] != 0.0) o.u[cells[i]] = uu[i];
+}
+
+void coarsest(Oracle& o, const MG& p) {
+  if (p.coarsest == 1) direct_coarsest(o);
+  else smooth_coarsest(o, p);
+}
+
 void residual(const Oracle& o, int l, std::vector<double>& r) {
   for_level_tiles(o, l, [&](int t) {
     for (int off = 0; off < o.B3; ++off) {
@@ -693,7 +823,7 @@ void eq14_check(Oracle& o, int lc) {
 
 // Alg. 4, FAS-style mu-cycle, readings SURVEY c-6.
 void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
-  if (l == 0) { smooth_coarsest(o, p); return; }
+  if (l == 0) { coarsest(o, p); return; }
   smooth(o, l, p.nu_pre, true);                  // pre-smoothing (R,B)
   residual(o, l, r);                             // r^l = b^l - A^l u^l
   int lc = l - 1;
@@ -744,7 +874,7 @@ void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
 // Alg. 2, standard mu-cycle with beta at prolongation.  Only meaningful on
 // uniform trees (no leaves below the finest level); used as an equivalence check.
 void mucycle_std(Oracle& o, int l, const MG& p, std::vector<double>& r) {
-  if (l == 0) { smooth_coarsest(o, p); return; }
+  if (l == 0) { coarsest(o, p); return; }
   smooth(o, l, p.nu_pre, true);
   residual(o, l, r);
   int lc = l - 1;
@@ -1098,7 +1228,7 @@ MG mg_from(const double* prm) {
   MG p;
   if (prm) {
     p.alpha = prm[0]; p.beta = prm[1]; p.mu = (int)prm[2]; p.nu_pre = (int)prm[3];
-    p.nu_post = (int)prm[4]; p.nu_coarsest = (int)prm[5];
+    p.nu_post = (int)prm[4]; p.nu_coarsest = (int)prm[5]; p.coarsest = (int)prm[6];
   }
   return p;
 }
@@ -1199,7 +1329,18 @@ void orc_rbgs_pass(void* h, int32_t l, int32_t colour, double* u, const double* 
   rbgs_pass(*(Oracle*)h, l, colour, u, b);
 }
 
-// prm: [alpha, beta, mu, nu_pre, nu_post, nu_coarsest]; form: 1 = Alg. 4 (FAS), 0 = Alg. 2
+// direct coarsest solve of level 0 alone (Alg. 4 line 4): u <- M0 b on the level-0 cells of
+// the all-tile arrays (other entries untouched)
+void orc_direct_coarsest(void* h, const double* b_all, double* u_all) {
+  auto* o = (Oracle*)h;
+  size_t NC = (size_t)o->T * o->B3;
+  std::copy(b_all, b_all + NC, o->b.begin());
+  std::copy(u_all, u_all + NC, o->u.begin());
+  direct_coarsest(*o);
+  std::copy(o->u.begin(), o->u.end(), u_all);
+}
+
+// prm: [alpha, beta, mu, nu_pre, nu_post, nu_coarsest, coarsest]; form: 1 = Alg. 4 (FAS), 0 = Alg. 2
 void orc_vcycle(void* h, const double* prm, const double* r, double* z, int32_t form) {
   precond(*(Oracle*)h, mg_from(prm), r, z, form == 1);
 }

@@ -60,6 +60,7 @@ def lib():
         _lib.orc_face_fraction.argtypes = [P, D]
         _lib.orc_tank_fields.argtypes = [P, I64, I32, P, P, D, P, P, P]
         _lib.orc_leaf_diag.argtypes = [P, P]
+        _lib.orc_direct_coarsest.argtypes = [P, P, P]
         _lib.orc_set_check_eq14.argtypes = [P, I32]
         _lib.orc_eq14.argtypes = [P, P]
         _lib.orc_mg_solve.restype = I32
@@ -96,8 +97,10 @@ class OracleError(RuntimeError):
         self.status = STATUS.get(status, status)
 
 
-def mg_params(alpha=2.0, beta=2.0, mu=1, nu_pre=2, nu_post=2, nu_coarsest=10):
-    return np.array([alpha, beta, mu, nu_pre, nu_post, nu_coarsest], dtype=np.float64)
+def mg_params(alpha=2.0, beta=2.0, mu=1, nu_pre=2, nu_post=2, nu_coarsest=10, coarsest="smooth"):
+    """coarsest: 'smooth' (nu_coarsest RBGS iterations) or 'direct' (Alg. 4 line 4)."""
+    c = {"smooth": 0, "direct": 1}[coarsest]
+    return np.array([alpha, beta, mu, nu_pre, nu_post, nu_coarsest, c], dtype=np.float64)
 
 
 class Oracle:
@@ -187,6 +190,13 @@ class Oracle:
         y = np.zeros(self.T * self.B3)
         lib().orc_apply_level(self._h, level, _p(u), _p(y))
         return y
+
+    def direct_coarsest(self, b_all, u_all):
+        """Alg. 4 line 4 'or direct solve': u^0 = M0 b^0 on the level-0 cells (all-tile arrays)."""
+        u = np.array(u_all, dtype=np.float64, copy=True)
+        b = np.ascontiguousarray(b_all, dtype=np.float64)
+        lib().orc_direct_coarsest(self._h, _p(b), _p(u))
+        return u
 
     def rbgs_pass(self, level, colour, u_all, b_all):
         u = np.array(u_all, dtype=np.float64, copy=True)

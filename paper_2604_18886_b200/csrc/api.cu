@@ -177,6 +177,10 @@ struct Builder {
     }
     if (l < T.L && fas_first && T.ic[l] > 0 && h.prm.form == 0) push(Op{1, l, 0});
     const bool finest = l == T.L;
+    if (l == 0 && h.c0n > 0) {  // direct coarsest solve (Alg. 4 line 4)
+      push(Op{10, 0, 0});
+      return;
+    }
     if (l == 0) {
       int nb = h.prm.nu_coarsest;
       int h1 = nb / 2;
@@ -308,6 +312,15 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
   a.stage[0] = op.stage;
+  a.c0M = h.c0M;
+  a.c0tile = h.c0tile;
+  a.c0n = h.c0n;
+  if (op.kind == 10) {
+    // read M0 (4 n0^2 B) and b^0, write u^0
+    ProfScope ps(h, KC_COARSEST, s, 4.0 * (double)h.c0n * h.c0n + 8.0 * h.c0n);
+    launch_coarse_direct(a, s);
+    return;
+  }
   if (op.kind == 9) {
     ProfScope ps(h, KC_COARSE_GRID, s, 0.0);
     cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
@@ -524,6 +537,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_TRY(assemble_leaf_coefs(h, kind, fbeta, ffrac, s));
   OCTMG_TRY(coarsen_all(h, s));
   launch_build_mask(h.coef, (int64_t)NLc, h.act, s);
+  if (prm.coarsest == 1) OCTMG_TRY(build_coarse_direct(h, s));  // M0 of level 0 (Alg. 4 line 4)
   OCTMG_CUDA(cudaStreamSynchronize(s));
   Scalars init{};
   init.n_active = h.n_active;
@@ -596,14 +610,15 @@ octmg_status set_ownership(Hier& h, const PartPlan* P) {
 
 bool valid_params(const octmg_mg_params& prm) {
   return prm.alpha > 0.0f && prm.mu >= 1 && prm.mu <= 4 && prm.nu_pre >= 1 && prm.nu_post >= 1 &&
-         prm.nu_coarsest >= 1 && (prm.form == 0 || prm.form == 1) && (prm.coarsen_literal == 0 || prm.coarsen_literal == 1);
+         prm.nu_coarsest >= 1 && (prm.form == 0 || prm.form == 1) && (prm.coarsen_literal == 0 || prm.coarsen_literal == 1) &&
+         (prm.coarsest == 0 || prm.coarsest == 1) && prm.gather_below_cells >= 0;
 }
 
 // a Group of `nparts` parts (1 = single GPU / one NCCL rank; >1 = loopback partition)
 octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void* nccl_comm, const uint8_t* kind,
                         const float* fbeta, const float* ffrac, const octmg_mg_params* params, cudaStream_t s,
                         octmg_hier** out) {
-  octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10, 0, 0};
+  octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10, 0, 0, 0, 0, 0};
   if (params) prm = *params;
   if (!valid_params(prm)) {
     set_error("invalid multigrid parameters (need alpha > 0, 1 <= mu <= 4, nu_* >= 1, form and coarsen_literal 0/1)");
@@ -633,6 +648,10 @@ octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void
     octmg_status st = plan_input(tree->t, in);
     if (st) return fail(st);
     const int lg = choose_partition_level(in, nranks);
+    if (lg == 0 && prm.coarsest == 1) {
+      set_error("direct coarsest solve needs a replicated level 0 (partition level >= 1)");
+      return fail(OCTMG_E_INVALID);
+    }
     build_partition(in, nranks, lg, g.plan->plan);
     P = &g.plan->plan;
     for (Hier* h : g.parts) h->lg = lg;

@@ -210,6 +210,11 @@ struct SmoothArgs {
   int n;                // tiles in the level
   int first_tile;       // k_fasrhs: first inner tile of the level
   int stage[1];         // bit0 colour, bits1.. mode
+  // direct coarsest solve (coarsest = 1): u^0 = M0 b^0 over the c0n level-0 cells (cell
+  // k*512 + slot of level-0 tile c0tile[k]); M0 row-major f32 [c0n][c0n]; c0n = 0: smoothing
+  const float* c0M;
+  const int* c0tile;
+  int c0n;
 };
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
@@ -227,6 +232,11 @@ cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int
 void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
                      const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
                      int ctas, cudaStream_t s);
+
+// direct coarsest solve (coarsest.cu)
+constexpr int C0_MAX_CELLS = 4096;
+octmg_status build_coarse_direct(Hier& h, cudaStream_t s);  // M0 of level 0 (setup)
+void launch_coarse_direct(const SmoothArgs& a, cudaStream_t s);  // u^0 = M0 b^0 (one launch)
 
 // setup kernels (setup.cu)
 struct SetupArgs;
@@ -299,6 +309,9 @@ struct Hier {
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
+  float* c0M = nullptr;          // direct coarsest solve: M0 [c0n][c0n] (coarsest = 1)
+  int* c0tile = nullptr;         // its level-0 tiles
+  int c0n = 0;
   unsigned* bar = nullptr;       // its grid barrier counter
   // profiling
   bool profiling = false;

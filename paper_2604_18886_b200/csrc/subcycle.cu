@@ -276,9 +276,44 @@ __device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch
   phase_end<PM>(A, epoch);
 }
 
-// smoothing at the coarsest level: nu_b/2 x (R,B) then nu_b/2 x (B,R)
+// direct coarsest solve u^0 = M0 b^0 (Alg. 4 line 4; coarsest.cu): every CTA stages
+// b^0 in shared memory, then one warp per row over all warps of the phase
+template <int PM, int M>
+__device__ __noinline__ void sc_direct(const SubArgs& A, unsigned& epoch) {
+  __shared__ __align__(16) float sb[C0_MAX_CELLS];
+  const SmoothArgs& a = A.a;
+  const int n = a.c0n;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) sb[j] = ldv<M>(tptr(a.b, a.c0tile[j >> 9], a.NL) + (j & 511));
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int i = ph_tid<PM>() >> 5; i < n; i += ph_nthreads<PM>() >> 5) {
+    const float4* row = reinterpret_cast<const float4*>(a.c0M + (size_t)i * n);
+    float s = 0.0f;
+    for (int q = lane; q < n / 4; q += 32) {
+      const float4 m = __ldg(row + q);
+      const float4 v = *reinterpret_cast<const float4*>(sb + 4 * q);
+      s = fmaf(m.x, v.x, s);
+      s = fmaf(m.y, v.y, s);
+      s = fmaf(m.z, v.z, s);
+      s = fmaf(m.w, v.w, s);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int t = a.c0tile[i >> 9], sl = i & 511;
+      if (__ldg(a.coef + cidx((size_t)t * TB3 + sl, 0)) != 0.0f) tptr(a.u, t, a.NL)[sl] = s;
+    }
+  }
+  phase_end<PM>(A, epoch);
+}
+
+// smoothing at the coarsest level: nu_b/2 x (R,B) then nu_b/2 x (B,R), or the
+// direct solve
 template <int PM, int M>
 __device__ void sc_coarsest(const SubArgs& A, bool finest, unsigned& epoch) {
+  if (A.a.c0n > 0) {
+    sc_direct<PM, M>(A, epoch);
+    return;
+  }
   const int h1 = A.nu_coarsest / 2;
   sc_passes<PM, M>(A, 0, h1, true, finest ? SM_ZERO1 : SM_PLAIN, finest ? SM_ZERO2 : SM_PLAIN, epoch);
   const bool zz = finest && h1 == 0;

@@ -40,7 +40,8 @@ class TreeInfo(C.Structure):
 class MGParams(C.Structure):
     _fields_ = [("alpha", C.c_float), ("beta_overshoot", C.c_float), ("mu", C.c_int32), ("nu_pre", C.c_int32),
                 ("nu_post", C.c_int32), ("nu_coarsest", C.c_int32), ("form", C.c_int32),
-                ("coarsen_literal", C.c_int32)]
+                ("coarsen_literal", C.c_int32), ("coarsest", C.c_int32), ("reserved0", C.c_int32),
+                ("gather_below_cells", C.c_int64)]
 
 
 class SolveParams(C.Structure):
@@ -237,10 +238,10 @@ class Hierarchy:
 
     def __init__(self, tree: Tree, kind, face_beta=None, face_frac=None, alpha=2.0, beta=2.0, mu=1,
                  nu_pre=2, nu_post=2, nu_coarsest=10, stream=None, loopback_parts: int = 0, form="fas",
-                 coarsen_literal=False):
+                 coarsen_literal=False, coarsest="smooth", gather_below_cells=0):
         self.tree = tree
         p = MGParams(alpha, beta, mu, nu_pre, nu_post, nu_coarsest, {"fas": 0, "alg2": 1}[form],
-                     int(coarsen_literal))
+                     int(coarsen_literal), {"smooth": 0, "direct": 1}[coarsest], 0, int(gather_below_cells))
         h = C.c_void_p()
         if loopback_parts:
             _check(lib().octmg_setup_hierarchy_loopback(tree._h, loopback_parts, _ptr(kind), _ptr(face_beta),

@@ -110,3 +110,60 @@ def test_standalone_mg_matches_oracle(om, name, mu):
     # the per-iteration residual history follows the oracle's
     n = min(len(rep["history"]), len(ref["history"]))
     assert np.allclose(rep["history"][:n], ref["history"][:n], rtol=1e-3, atol=1e-7)
+
+
+# ---------------------------------------------------------------------------------------
+# direct coarsest solve (Alg. 4 line 4; DESIGN reading 9b)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("env", [{}, {"OCTMG_SUBCYCLE": "0"}])
+@pytest.mark.parametrize("name,mu", [("cfg1_octant", 1), ("sphere_small_dir", 2), ("tank_small", 2),
+                                     ("uniform32", 1), ("sphere_small", 2)])
+def test_direct_coarsest_cycle_and_pcg_match_oracle(om, name, mu, env, monkeypatch):
+    """The cycle with the direct level-0 solve (on chip in the sub-cycle, or the standalone
+    k_coarse_direct launch with OCTMG_SUBCYCLE=0) against the oracle's: Dirichlet problems
+    (nonsingular level 0) and pure-Neumann ones (one floating component: the minimum-norm
+    solution), mu = 1, 2; the cycle <= 1e-5 and PCG within +-1 iterations, <= 1e-5."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = make_config(name)
+    tree, h, o = _pair(om, cfg, mu=mu, coarsest="direct")
+    rng = np.random.default_rng(21)
+    act = o.coefs_diag_leaf() != 0
+    r = (rng.standard_normal(o.N) * act).astype(np.float32)
+    z = torch.zeros(o.N, device=DEV)
+    h.vcycle(torch.from_numpy(r).to(DEV), z)
+    zr = o.vcycle(r.astype(np.float64), mu=mu, coarsest="direct")
+    assert _rel(z.cpu().numpy().astype(np.float64), zr) <= 1e-5
+    b = torch.from_numpy(cfg["b"]).to(DEV)
+    x = torch.zeros_like(b)
+    rep = h.pcg_solve(b, x, rtol=1e-6)
+    ref = o.pcg(cfg["b"].astype(np.float64), rtol=1e-6, mu=mu, coarsest="direct")
+    assert rep["converged"] and abs(rep["iters"] - ref["iters"]) <= 1
+    xg, xr = x.cpu().numpy().astype(np.float64), ref["x"]
+    if not any(cfg["wall_bc"]):
+        xg, xr = xg - xg[act].mean() * act, xr - xr[act].mean() * act
+    assert _rel(xg, xr) <= 1e-5
+
+
+def test_direct_coarsest_single_level_one_iteration(om):
+    """One-level tree: M = A^{-1} (to fp32 rounding), so PCG reaches 1e-6 in one iteration."""
+    rng = np.random.default_rng(8)
+    tiles = np.array([[0, 0, 0, 0]], dtype=np.int32)
+    tree = om.Tree(tiles)
+    kind = rng.choice([0, 1, 2], size=512, p=[0.9, 0.05, 0.05]).astype(np.uint8)
+    h = om.Hierarchy(tree, torch.from_numpy(kind).to(DEV), coarsest="direct")
+    b = torch.from_numpy((rng.standard_normal(512) * (kind == 0)).astype(np.float32)).to(DEV)
+    x = torch.zeros_like(b)
+    rep = h.pcg_solve(b, x, rtol=1e-5)
+    assert rep["converged"] and rep["iters"] == 1
+
+
+def test_direct_coarsest_rejects_large_level0(om):
+    """More than 4096 level-0 cells (ext product > 8): OCTMG_E_INVALID."""
+    from octgen import uniform_tiles, canonical_order
+    ext = (3, 3, 1)
+    tiles = uniform_tiles(0, ext)
+    tiles = tiles[canonical_order(tiles)]
+    tree = om.Tree(tiles, ext)
+    with pytest.raises(Exception):
+        om.Hierarchy(tree, torch.zeros(tree.N, dtype=torch.uint8, device=DEV), coarsest="direct")

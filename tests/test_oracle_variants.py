@@ -104,3 +104,95 @@ def test_standalone_mg_first_iterate_is_one_cycle():
     assert r["status"] == "MAXITER" and r["iters"] == 1
     z = o.vcycle(b, beta=1.0)
     assert np.array_equal(r["x"], z)
+
+
+# ---------------------------------------------------------------------------------------
+# direct coarsest solve (Alg. 4 line 4, "Or direct solve"; DESIGN reading 9b)
+# ---------------------------------------------------------------------------------------
+def _level0(o):
+    """all-tile indices of the level-0 cells (leaf segment, then inner segment)"""
+    segs = []
+    for b, c in ((o.leaf_begin[0], o.leaf_count[0]), (o.inner_begin[0], o.inner_count[0])):
+        segs.append(np.arange(b * o.B3, (b + c) * o.B3))
+    return np.concatenate(segs)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_direct_coarsest_is_exact_level0_solve(seed):
+    """Dirichlet walls (nonsingular A^0): the direct coarsest solve returns the exact solution of
+    A^0 u = b^0 over the active level-0 cells — checked against numpy's dense solve of the level
+    operator assembled column by column (random graded trees, non-cubic level 0, random masks
+    and face weights)."""
+    from tests.helpers import dense_level
+    rng = np.random.default_rng(40 + seed)
+    ext = [(1, 1, 1), (2, 1, 1), (1, 2, 2)][seed]
+    t = random_graded_tree(rng, 1, 2, 0.3, ext=ext)
+    o = Oracle(t, ext=ext, B=4)
+    kind = rng.choice([0, 1, 2], size=o.N, p=[0.85, 0.05, 0.1]).astype(np.uint8)
+    w = (0.1 + 0.9 * rng.random((6, o.N))).astype(np.float32)
+    o.setup(kind, w)
+    cells = _level0(o)
+    cf = o.coefs()
+    act = cells[cf[cells, 0] != 0]
+    A = dense_level(o, 0, act)
+    b = np.zeros(o.T * o.B3)
+    b[cells] = rng.standard_normal(len(cells))
+    u = o.direct_coarsest(b, np.zeros(o.T * o.B3))
+    ref = np.linalg.solve(A, b[act])
+    assert np.abs(u[act] - ref).max() <= 1e-10 * np.abs(ref).max()
+    inact = cells[cf[cells, 0] == 0]
+    assert np.all(u[inact] == 0.0)
+
+
+def test_direct_coarsest_floating_components_pseudo_inverse():
+    """Singular level 0: one level-0 tile (L = 0, B = 8), Dirichlet walls, a Neumann shell
+    that seals a 2x2x2 fluid pocket off from the rest (a floating component: A^0 1 = 0 on it,
+    P:L343) — the direct solve equals the minimum-norm solution pinv(A^0) b (numpy), i.e. the
+    exact inverse on the wall-connected component and the zero-mean solution of the
+    mean-free rhs on the pocket."""
+    from tests.helpers import dense_level
+    rng = np.random.default_rng(3)
+    o = Oracle(np.array([[0, 0, 0, 0]], dtype=np.int32))
+    X, Y, Z = np.meshgrid(np.arange(8), np.arange(8), np.arange(8), indexing="ij")
+    X, Y, Z = (a.transpose(2, 1, 0).ravel() for a in (X, Y, Z))  # natural order x + 8y + 64z
+    shell = (np.maximum(np.maximum(np.abs(X - 3.5), np.abs(Y - 3.5)), np.abs(Z - 3.5)) == 1.5)
+    kind = np.where(shell, 2, 0).astype(np.uint8)
+    o.setup(kind)
+    cells = _level0(o)
+    act = cells[o.coefs()[cells, 0] != 0]
+    A = dense_level(o, 0, act)
+    assert np.linalg.matrix_rank(A) == len(act) - 1  # exactly one floating component
+    b = np.zeros(o.T * o.B3)
+    b[act] = rng.standard_normal(len(act))
+    u = o.direct_coarsest(b, np.zeros(o.T * o.B3))
+    ref = np.linalg.pinv(A) @ b[act]
+    assert np.abs(u[act] - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_direct_coarsest_single_level_pcg_one_iteration():
+    """A one-level tree (L = 0): the FAS cycle with a direct coarsest solve is A^{-1}, so PCG
+    converges in one iteration (Alg. 1), while the smoothing-only cycle needs several."""
+    rng = np.random.default_rng(8)
+    o = Oracle(np.array([[0, 0, 0, 0]], dtype=np.int32))
+    kind = rng.choice([0, 1, 2], size=o.N, p=[0.9, 0.05, 0.05]).astype(np.uint8)
+    o.setup(kind)
+    b = rng.standard_normal(o.N) * (kind == 0)
+    d = o.pcg(b, rtol=1e-10, coarsest="direct")
+    s = o.pcg(b, rtol=1e-10)
+    assert d["status"] == "OK" and d["iters"] == 1
+    assert s["iters"] > 1
+
+
+@pytest.mark.parametrize("mu", [1, 2])
+def test_direct_coarsest_cycle_converges_no_slower(mu):
+    """On an adaptive Dirichlet problem the cycle with the exact coarsest solve is at least as
+    good a preconditioner as the 10-iteration smoother: PCG iterations no larger, solutions
+    equal within the solve tolerance."""
+    cfg = make_config("sphere_small_dir")
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    o.setup(cfg["kind"], cfg["w"])
+    b = cfg["b"].astype(np.float64)
+    d = o.pcg(b, rtol=1e-8, mu=mu, coarsest="direct")
+    s = o.pcg(b, rtol=1e-8, mu=mu)
+    assert d["iters"] <= s["iters"]
+    assert np.linalg.norm(d["x"] - s["x"]) <= 1e-6 * np.linalg.norm(s["x"])
