@@ -206,9 +206,8 @@ void read_env(Hier& h) {
   const char* pv = getenv("OCTMG_PASS_V");
   h.pass_v2 = !(pv && std::string(pv) == "1");
   const char* rv = getenv("OCTMG_RESTRICT_V");
-  h.restrict_v2 = !rv ? 6 : (std::string(rv) == "1" ? 0 : (std::string(rv) == "8" ? 8 : 6));  // 8: measured no faster
-  const char* av = getenv("OCTMG_APPLY_V");
-  h.apply_v = av && (std::string(av) == "4" || std::string(av) == "6") ? atoi(av) : 5;
+  // 6 / 8: k_restrict_v2 at >= 6 / 8 CTAs/SM; 1: staged k_restrict_direct
+  h.restrict_v2 = !rv ? 6 : (std::string(rv) == "1" ? 0 : (std::string(rv) == "8" ? 8 : 6));
   const Tree& T = *h.tree;
   const char* gv = getenv("OCTMG_GRID");
   const bool grid = gv && std::string(gv) == "1";
@@ -361,7 +360,10 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   if (mode == SM_RESTRICT) {
     launch_restrict_direct(a, s, h.restrict_v2);
   } else {
-    launch_pass_direct(a, s, (a.n >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0));
+    // kernel chosen by the level's total tile count, so every part of a partitioned solve runs
+    // the same per-tile arithmetic as the single-part solve
+    const int level_tiles = T.lc[l] + T.ic[l];
+    launch_pass_direct(a, s, (level_tiles >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0));
   }
 }
 
@@ -534,8 +536,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_CUDA(cudaMemsetAsync(h.p0, 0, NLc * sizeof(float), s));
   OCTMG_CUDA(cudaMemsetAsync(h.p1, 0, NLc * sizeof(float), s));
   OCTMG_CUDA(cudaMemsetAsync(h.sc, 0, sizeof(Scalars), s));
-  OCTMG_TRY(assemble_leaf_coefs(h, kind, fbeta, ffrac, s));
-  OCTMG_TRY(coarsen_all(h, s));
+  OCTMG_TRY(assemble_leaf_coefs(h, kind, fbeta, ffrac, s));  // + Alg. 3 coarsening and leaf row sums
   launch_build_mask(h.coef, (int64_t)NLc, h.act, s);
   if (prm.coarsest == 1) OCTMG_TRY(build_coarse_direct(h, s));  // M0 of level 0 (Alg. 4 line 4)
   OCTMG_CUDA(cudaStreamSynchronize(s));
@@ -677,9 +678,8 @@ ApplyArgs apply_args(const Hier& h) {
   a.tiles = h.apply_tiles; a.ntiles = h.n_apply_tiles;
   if (h.nranks == 1 && h.n_apply_tiles == h.tree->NL) a.tiles = nullptr;  // identity: skip the indirection
   a.tile = T.tile; a.nbr = T.nbr; a.child = T.child; a.coef = h.coef; a.glayer_val = h.glayer_val;
-  a.glayer = T.glayer; a.z = nullptr; a.pold = nullptr; a.pnew = nullptr; a.q = nullptr;
-  a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL; a.use_beta = 0;
-  a.v2 = h.pass_v2 ? 1 : 0;
+  a.glayer = T.glayer; a.dtile = h.dtile; a.dval = h.dval; a.z = nullptr; a.q = nullptr;
+  a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL;
   return a;
 }
 
@@ -896,13 +896,9 @@ octmg_status build_loop_graph(Group& g, bool ns) {
     launch_pupdate(h.z, h.p0, h.own_cells, h.sc, true, cs, G);                     // p = z + beta p
     ApplyArgs a = apply_args(h);
     a.z = h.p0;
-    a.pold = nullptr;
-    a.pnew = nullptr;
     a.q = h.q;
     a.partial = h.partial;
     a.counter = h.counter + 3;
-    a.use_beta = 0;
-    if (a.v2) a.v2 = h.apply_v;
     launch_apply(a, cs);                                                           // q = A p, p.q
     launch_update(h.xs, h.r, h.p0, h.q, h.own_cells, h.partial, h.counter + 4, h.sc, cs, G);
     if (ns) launch_project(h.r, h.act, h.own_cells, h.partial, h.counter + 1, h.sc, cs, G);
@@ -1039,48 +1035,33 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   int k = 0;
   double rel = 1.0;
   // direction update p = z + beta p (own cells, in place), halo of p, then q = A p with
-  // the fp64 p.q (OCTMG_PCG_FUSED=1: the older fused form, p formed inside the apply from
-  // z and the previous p of a ping-pong pair)
-  const char* fu = getenv("OCTMG_PCG_FUSED");
-  const bool fused = fu && atoi(fu) == 1;
-  int cur = 0;  // fused form: p0/p1 ping-pong, p_new in (cur ? p1 : p0)
+  // the fp64 p.q
   while (true) {
     std::vector<Fld> pf;
-    if (!fused) {
-      for (Hier* h : g.parts) {
-        ProfScope ps(*h, KC_PUPDATE, s, (double)h->n_apply_tiles * TB3 * (k > 0 ? 12.0 : 8.0));  // read z, p; write p
-        launch_pupdate(h->z, h->p0, h->own_cells, h->sc, k > 0, s, G);
-        pf.push_back(Fld{h->p0, nullptr});
-      }
-      g.launches += np;
-      if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
-    }
     for (Hier* h : g.parts) {
-      float* pcur = fused ? (cur ? h->p1 : h->p0) : h->p0;
-      float* pprev = cur ? h->p0 : h->p1;
+      ProfScope ps(*h, KC_PUPDATE, s, (double)h->n_apply_tiles * TB3 * (k > 0 ? 12.0 : 8.0));  // read z, p; write p
+      launch_pupdate(h->z, h->p0, h->own_cells, h->sc, k > 0, s, G);
+      pf.push_back(Fld{h->p0, nullptr});
+    }
+    g.launches += np;
+    if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
+    for (Hier* h : g.parts) {
       ApplyArgs a = apply_args(*h);
-      a.z = fused ? h->z : h->p0;
-      a.pold = (fused && k > 0) ? pprev : nullptr;
-      a.pnew = fused ? pcur : nullptr;
+      a.z = h->p0;
       a.q = h->q;
       a.partial = h->partial;
       a.counter = h->counter + 3;
-      a.use_beta = fused && k > 0;
-      if (!fused && a.v2) a.v2 = h->apply_v;  // p precomputed: the colour-layout apply (k_apply_v5 / v4)
       {
-        // fused: read z, p_old, record (24 B/leaf), write p, q (8); split: read p, record, write q
-        ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * (fused ? 32.0 : 24.0));
+        // read p, record; write q
+        ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 24.0);
         launch_apply(a, s);
       }
-      if (fused) pf.push_back(Fld{pcur, nullptr});
     }
     g.launches += 2 * np;
     OCTMG_TRY(allreduce(g, SF_PQ, 1, s));
-    if (g.comm && fused) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, s));  // p of the boundary tiles
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r
-      launch_update(h->xs, h->r, fused ? (cur ? h->p1 : h->p0) : h->p0, h->q, h->own_cells, h->partial,
-                    h->counter + 4, h->sc, s, G);
+      launch_update(h->xs, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G);
     }
     g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RR, 2, s));
@@ -1099,7 +1080,6 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     if (k >= prm.max_iters) { set_error("PCG did not converge within max_iters"); return fill(OCTMG_E_MAXITER, k, false, rel, bn); }
     OCTMG_TRY(run_M(g, s));
     OCTMG_TRY(dot_rz());
-    cur ^= 1;
   }
 }
 
@@ -1163,19 +1143,16 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
     OCTMG_TRY(run_M(g, s));  // z = M r (z = leaf part of the cycle's u)
     for (Hier* h : g.parts) {
       ApplyArgs a = apply_args(*h);
-      a.z = h->z;
-      a.pold = nullptr;
-      a.pnew = h->p0;  // z masked to the active cells
+      a.z = h->z;      // zero on inactive cells (the cycle writes active cells only, zeros the rest)
       a.q = h->q;      // A z
       a.partial = nullptr;
-      a.use_beta = 0;
-      ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 28.0);  // read z, record; write p, q
+      ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read z, record; write q
       launch_apply(a, s);
     }
     g.launches += np;
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);
-      launch_update(h->xs, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G, 1.0f);
+      launch_update(h->xs, h->r, h->z, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G, 1.0f);
     }
     g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RR, 2, s));

@@ -10,6 +10,7 @@
 
 #include "stencil.cuh"
 #include "rowstencil.cuh"
+#include "rowtile.cuh"
 
 namespace octmg {
 
@@ -166,117 +167,82 @@ __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
     if (act[k] || MODE == SM_ZERO1 || MODE == SM_ZERO2) ut[offs[k]] = unew[k];
 }
 
-__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ float e4(const float4& v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; }
 
-// The colour pass with 128-bit loads: thread j of a 64-thread tile CTA owns the colour row
-// (y, z) = (j & 7, j >> 3) of the pass colour — the four cells x = 2m + p (m = 0..3, p =
-// (colour + y + z) & 1) at the contiguous slots colour*256 + 4j + m.  In the colour-split
-// order the other colour's row at the same slots (xor 256) holds all x-neighbours but one
-// (p = 0: element -1 = element 3 of the x- tile's row; p = 1: element 4 = element 0 of the
-// x+ tile's row), its rows 4 / 32 slots away are the y / z neighbours (wrapped into the
-// neighbour tile: +28 / -28, +224 / -224), so a row of 4 cells costs 13 float4 + 2 scalar
-// loads instead of 56 scalar ones.  Regular tiles only read the other colour (and their own
-// colour's b and record), so no barrier is needed before the in-place store; ghost tiles
-// (T-junction faces, Eq. 12) take the general per-cell path of k_pass_v2 (4 cells per thread)
-// with its barrier.  Same per-cell fmaf order as face_sum_regular: bit-identical results.
-template <int MODE>
-__global__ __launch_bounds__(64, 16) void k_pass_v3(SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
-  int nb[6];
-  {
-    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
-    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
-    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
-  }
+// The colour pass, one colour row per thread (rowtile.cuh): thread j of a 64-thread tile
+// CTA owns row (y, z) = (j & 7, j >> 3) of the pass colour, 13 float4 + 2 scalar loads for 4
+// cells.  Regular tiles only read the other colour (and their own colour's b and record), so
+// no barrier is needed before the in-place store.  Tiles with a T-junction face take the
+// same row path with the Eq. 12 ghost values substituted (rowk::row_ghosts; snapshot reading
+// 1 of DESIGN.md): u_i and m_P come from the pass-start values of the own row and, by
+// shuffles of registers, of the rows y^1 / z^1 (lanes j^1 / j^8).  No thread reads another
+// row's own-colour cells from memory, so no barrier is needed here either.
+template <int MODE, bool GHOST>
+__device__ __forceinline__ void pass_row_body(const SmoothArgs& a, int t, const int (&nb)[6]) {
+  using namespace rowk;
   const int colour = a.stage[0] & 1;
-  const int j = threadIdx.x;
+  const RowGeo g = row_geo(colour, threadIdx.x);
   float* ut = tptr(a.u, t, a.NL);
-  const float* bt = tptr(a.b, t, a.NL);
   const float* ct = a.coef + ((size_t)t << 11);
-  bool ghost = false;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
-  if (MODE != SM_ZERO1 && ghost) {
-    // general path (T-junction tile): 4 colour cells per thread, slots colour*256 + j + 64k
-    const int y = (j >> 2) & 7, z0 = j >> 5;
-    float unew[4];
-    bool act[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int z = z0 + 2 * k;
-      const int x = 2 * (j & 3) + ((colour + y + z) & 1);
-      const int off = (colour << 8) + j + 64 * k;
-      const float4 q = make_float4(__ldg(ct + off), __ldg(ct + 512 + off), __ldg(ct + 1024 + off),
-                                   __ldg(ct + 1536 + off));
-      const float b = __ldg(bt + off);
-      act[k] = q.x != 0.0f;
-      const float ui = MODE == SM_ZERO2 ? 0.0f : __ldg(ut + off);
-      const float mP = block_mean<MODE == SM_ZERO2>(a, t, x, y, z, colour);
-      const float v = act[k] ? (b - face_sum<MODE == SM_ZERO2>(a, t, x, y, z, q, ui, mP, colour, 0.0f, nullptr,
-                                                                  nullptr, nb)) / q.x
-                             : 0.0f;
-      unew[k] = act[k] ? v : 0.0f;
-    }
-    __syncthreads();  // every pass-start read of this tile precedes the in-place writes
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (act[k] || MODE == SM_ZERO2) ut[(colour << 8) + j + 64 * k] = unew[k];
-    return;
-  }
-  const int y = j & 7, z = j >> 3;
-  const int p = (colour + y + z) & 1;
-  const int own = (colour << 8) + 4 * j, oth = own ^ 256;
-  const float4 q0 = ld4(ct + own);
-  const float4 bb = ld4(bt + own);
-  float4 r;
+  const float4 q0 = ld4(ct + g.own);
+  const float4 bb = ld4(tptr(a.b, t, a.NL) + g.own);
   if (MODE == SM_ZERO1) {  // first pass of the cycle: u = 0, so u = b / c
+    float4 r;
     r.x = q0.x != 0.0f ? bb.x / q0.x : 0.0f;
     r.y = q0.y != 0.0f ? bb.y / q0.y : 0.0f;
     r.z = q0.z != 0.0f ? bb.z / q0.z : 0.0f;
     r.w = q0.w != 0.0f ? bb.w / q0.w : 0.0f;
-    *reinterpret_cast<float4*>(ut + own) = r;
+    *reinterpret_cast<float4*>(ut + g.own) = r;
     return;
   }
-  const float4 qx = ld4(ct + 512 + own), qy = ld4(ct + 1024 + own), qz = ld4(ct + 1536 + own);
-  auto tu = [&](int n) { return n >= 0 ? tptr(a.u, n, a.NL) : ut; };
-  auto tc = [&](int n) { return n >= 0 ? a.coef + ((size_t)n << 11) : ct; };
-  const float4 ox = ld4(ut + oth);
-  const float4 cxo = ld4(ct + 512 + oth);
-  // the x element outside the row: p = 0 -> x- tile element 3; p = 1 -> x+ tile element 0
-  const int nx = p ? nb[1] : nb[0];
-  float xs = __ldg(tu(nx) + oth + (p ? 0 : 3));
-  const float xsc = __ldg(tc(nx) + 512 + oth);  // c_x- of the x+ tile's element 0 (p = 1)
-  if (nx < 0) xs = 0.0f;
-  const bool yl = y > 0, yh = y < 7, zl = z > 0, zh = z < 7;
-  float4 ym = ld4((yl ? ut : tu(nb[2])) + oth + (yl ? -4 : 28));
-  float4 yp = ld4((yh ? ut : tu(nb[3])) + oth + (yh ? 4 : -28));
-  float4 zm = ld4((zl ? ut : tu(nb[4])) + oth + (zl ? -32 : 224));
-  float4 zp = ld4((zh ? ut : tu(nb[5])) + oth + (zh ? 32 : -224));
-  const float4 cyp = ld4((yh ? ct : tc(nb[3])) + 1024 + oth + (yh ? 4 : -28));
-  const float4 czp = ld4((zh ? ct : tc(nb[5])) + 1536 + oth + (zh ? 32 : -224));
-  const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  if (!yl && nb[2] < 0) ym = Z4;
-  if (!yh && nb[3] < 0) yp = Z4;
-  if (!zl && nb[4] < 0) zm = Z4;
-  if (!zh && nb[5] < 0) zp = Z4;
-  float res[4];
-#pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    const float vxm = p ? e4(ox, m) : (m == 0 ? xs : e4(ox, m - 1));
-    const float vxp = p ? (m == 3 ? xs : e4(ox, m + 1)) : e4(ox, m);
-    const float cxp = p ? (m == 3 ? xsc : e4(cxo, m + 1)) : e4(cxo, m);
-    float sm = 0.0f;  // face_sum_regular's order: x-, x+, y-, y+, z-, z+
-    sm = fmaf(e4(qx, m), vxm, sm);
-    sm = fmaf(cxp, vxp, sm);
-    sm = fmaf(e4(qy, m), e4(ym, m), sm);
-    sm = fmaf(e4(cyp, m), e4(yp, m), sm);
-    sm = fmaf(e4(qz, m), e4(zm, m), sm);
-    sm = fmaf(e4(czp, m), e4(zp, m), sm);
-    const float c = e4(q0, m);
-    res[m] = c != 0.0f ? (e4(bb, m) - sm) / c : 0.0f;
+  const float4 qx = ld4(ct + 512 + g.own), qy = ld4(ct + 1024 + g.own), qz = ld4(ct + 1536 + g.own);
+  const Fld uf = a.u;
+  const int NL = a.NL;
+  auto tu = [uf, NL](int n) -> const float* { return tptr(uf, n, NL); };
+  RowSt s;
+  row_load(s, tu, a.coef, t, nb, g);
+  if (GHOST) {
+    const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    const float4 ui = MODE == SM_ZERO2 ? Z4 : ld4(ut + g.own);
+    const float4 co = ld4(ct + g.oth);
+    const float4 mP = row_block_mean<1, 8>(msk4(ui, q0), q0, msk4(s.ox, co), co);
+    const Fld ucf = a.uc;
+    auto uc_of = [ucf, NL](int C) -> const float* { return tptr(ucf, C, NL); };
+    row_ghosts<MODE == SM_ZERO2>(s, g, t, nb, __ldg(a.tile + t), a.coef, a.glayer_val, a.glayer, uc_of, ui, mP);
   }
-  *reinterpret_cast<float4*>(ut + own) = make_float4(res[0], res[1], res[2], res[3]);
+  const float4 f = row_sums(s, g, qx, qy, qz, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+  float4 r;
+  r.x = q0.x != 0.0f ? (bb.x - f.x) / q0.x : 0.0f;
+  r.y = q0.y != 0.0f ? (bb.y - f.y) / q0.y : 0.0f;
+  r.z = q0.z != 0.0f ? (bb.z - f.z) / q0.z : 0.0f;
+  r.w = q0.w != 0.0f ? (bb.w - f.w) / q0.w : 0.0f;
+  *reinterpret_cast<float4*>(ut + g.own) = r;
+}
+
+// the ghost-tile body out of line: its extra registers (spilled to L1-resident local memory
+// if need be) do not lower the occupancy of the regular-tile path
+template <int MODE>
+__device__ __noinline__ void pass_row_ghost(const SmoothArgs& a, int t, int n0, int n1, int n2, int n3, int n4,
+                                            int n5) {
+  const int nb[6] = {n0, n1, n2, n3, n4, n5};
+  pass_row_body<MODE, true>(a, t, nb);
+}
+
+// INL: the ghost body inlined, at 12 CTAs/SM (80 registers: no spills on either path)
+// instead of out of line at 16 (the regular path's occupancy; the ghost body spills)
+template <int MODE, bool INL>
+__global__ __launch_bounds__(64, INL ? 12 : 16) void k_pass_v3(const __grid_constant__ SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  int nb[6];
+  rowk::load_nb(a.nbr, t, nb);
+  bool ghost = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
+  if (MODE != SM_ZERO1 && ghost) {  // CTA-uniform
+    if (INL) pass_row_body<MODE, true>(a, t, nb);
+    else pass_row_ghost<MODE>(a, t, nb[0], nb[1], nb[2], nb[3], nb[4], nb[5]);
+    return;
+  }
+  pass_row_body<MODE, false>(a, t, nb);
 }
 
 // Residual r = b - A^l u and, per parent (inner, level l-1): u* = mean of the active
@@ -450,6 +416,16 @@ __global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
 
 }  // namespace
 
+// OCTMG_PASS_GHOST=inline: k_pass_v3's ghost body inlined (80 registers, 12 CTAs/SM)
+static bool pass_ghost_inline() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("OCTMG_PASS_GHOST");
+    on = e && std::string(e) == "inline";
+  }
+  return on == 1;
+}
+
 // OCTMG_PASS_V=2: the scalar k_pass_v2 on big levels instead of the 128-bit k_pass_v3
 static bool pass_v3_enabled() {
   static int on = -1;
@@ -469,9 +445,15 @@ static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool 
   const int grid = a.n;
   if (CPT == 4 && v2 && pass_v3_enabled()) {  // 128-bit row form (CPT 4 = 64 threads per tile)
     switch (mode) {
-      case SM_ZERO1: k_pass_v3<SM_ZERO1><<<grid, 64, 0, s>>>(a); break;
-      case SM_ZERO2: k_pass_v3<SM_ZERO2><<<grid, 64, 0, s>>>(a); break;
-      default: k_pass_v3<SM_PLAIN><<<grid, 64, 0, s>>>(a); break;
+      case SM_ZERO1: k_pass_v3<SM_ZERO1, false><<<grid, 64, 0, s>>>(a); break;
+      case SM_ZERO2:
+        if (pass_ghost_inline()) k_pass_v3<SM_ZERO2, true><<<grid, 64, 0, s>>>(a);
+        else k_pass_v3<SM_ZERO2, false><<<grid, 64, 0, s>>>(a);
+        break;
+      default:
+        if (pass_ghost_inline()) k_pass_v3<SM_PLAIN, true><<<grid, 64, 0, s>>>(a);
+        else k_pass_v3<SM_PLAIN, false><<<grid, 64, 0, s>>>(a);
+        break;
     }
     return;
   }

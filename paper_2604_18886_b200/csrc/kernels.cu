@@ -1,19 +1,14 @@
-// PCG kernels (sm_100a): the composite operator fused with p = z + beta p and the fp64 p.q
-// reduction, and the vector updates / dots.  One CTA per 8^3 tile for the operator; the
-// stencil is gathered directly through L1/L2 (see direct.cu); coefficient records are
-// float4 (c, c_x-, c_y-, c_z-) and the +face coefficient comes from the neighbour record or
-// the ghost layer.
+// PCG kernels (sm_100a): the composite leaf operator q = A p with the fp64 p.q reduction,
+// and the vector updates / dots.  One 128-thread CTA per 8^3 tile for the operator, one
+// colour row of 4 cells per thread (rowtile.cuh); the operator is evaluated in flux form
+// with the exact row sums of setup.cu (k_leaf_rowsum); the +face coupling comes from the
+// neighbour record or the ghost layer.
 #include "octmg_internal.cuh"
-#include "rowstencil.cuh"
+#include "rowtile.cuh"
 
 namespace octmg {
 
 namespace {
-
-constexpr int NT = 256;  // threads per tile CTA; thread -> cells (2*x2, y, z), (2*x2+1, y, z)
-
-__device__ __forceinline__ int loff(int x, int y, int z) { return cslot(x, y, z); }  // slot order
-__device__ __forceinline__ float comp(const float4& v, int a) { return a == 0 ? v.y : (a == 1 ? v.z : v.w); }
 
 
 __device__ __forceinline__ double block_reduce_d(double v, double* sred) {
@@ -50,354 +45,80 @@ __device__ __forceinline__ bool last_block_sum(double mine, double* partial, uns
   return threadIdx.x == 0;
 }
 
-// direction value p = z + beta p_old of cell i; z and p_old are zero on inactive cells (the
-// cycle never writes them, octmg_apply masks its input first), so no activity test
-__device__ __forceinline__ float pval(const ApplyArgs& a, float beta, size_t i) {
-  float v = __ldg(a.z + i);
-  if (a.pold) v = fmaf(beta, __ldg(a.pold + i), v);
-  return v;
-}
-
-// Composite operator row: same-level leaf neighbours give their value, a
-// same-level inner neighbour the mean of its active children (all leaves), a ghost
-// g = p_i + (p_C - m_P)/2 (Eq. 12), walls 0.  Face order x-, x+, y-, y+, z-, z+.
-__device__ __forceinline__ float composite_faces(const ApplyArgs& a, float beta, int t, int x, int y, int z,
-                                                 const float4& q, float pi, float mP, float s0, const float* sp,
-                                                 const float (*scm)[TB3]) {
-  const int c[3] = {x, y, z};
-  float s = s0;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    const int ax = f >> 1, sg = (f & 1) ? 1 : -1;
-    int nc[3] = {c[0], c[1], c[2]};
-    nc[ax] += sg;
-    float v = 0.0f, cf = (f & 1) ? 0.0f : comp(q, ax);
-    if (nc[ax] >= 0 && nc[ax] < 8) {
-      const int no = loff(nc[0], nc[1], nc[2]);
-      if (f & 1) cf = scm[ax][no];  // this tile's -face coefficients, staged (SoA)
-      v = sp[no];                   // this tile's p, staged in shared memory
-    } else {
-      const int n = __ldg(a.nbr + 6 * t + f);
-      nc[ax] &= 7;
-      const int no = loff(nc[0], nc[1], nc[2]);
-      if (n >= 0) {
-        if (f & 1) cf = comp(ldcoef(a.coef, (size_t)n * TB3 + no), ax);
-        if (n < a.NL) {
-          v = pval(a, beta, (size_t)n * TB3 + no);
-        } else {
-          const int ct = __ldg(a.child + 8 * (n - a.NL) + (nc[0] >> 2) + 2 * (nc[1] >> 2) + 4 * (nc[2] >> 2));
-          // the 8 children: activity and value loaded together (no load behind a branch)
-          float sm = 0.0f;
-          int k = 0;
-#pragma unroll
-          for (int d = 0; d < 8; ++d) {
-            const size_t ci = (size_t)ct * TB3 + loff((2 * nc[0] + (d & 1)) & 7, (2 * nc[1] + ((d >> 1) & 1)) & 7,
-                                                      (2 * nc[2] + (d >> 2)) & 7);
-            const float cc = __ldg(a.coef + cidx(ci, 0));
-            const float pv = pval(a, beta, ci);
-            if (cc != 0.0f) { sm += pv; k++; }
-          }
-          v = k ? sm / (float)k : 0.0f;
-        }
-      } else if (n <= -2) {
-        if (f & 1)
-          cf = __ldg(a.glayer_val + (size_t)__ldg(a.glayer + 3 * t + ax) * 64 +
-                     (ax == 0 ? y + 8 * z : (ax == 1 ? x + 8 * z : x + 8 * y)));
-        const int C = -2 - n;
-        const int4 tv = __ldg(a.tile + t);
-        int g[3] = {tv.y * 8 + c[0], tv.z * 8 + c[1], tv.w * 8 + c[2]};
-        g[ax] += sg;
-        const size_t ci = (size_t)C * TB3 + loff((g[0] >> 1) & 7, (g[1] >> 1) & 7, (g[2] >> 1) & 7);
-        const float cC = __ldg(a.coef + cidx(ci, 0));
-        const float pC = pval(a, beta, ci);
-        if (cC != 0.0f) v = pi + 0.5f * (pC - mP);
-      }
-    }
-    s = fmaf(cf, v, s);
-  }
-  return s;
-}
-
-// q = A p with p = z + beta p_old formed on the fly (and stored), plus the fp64 partial of
-// p.q with a deterministic last-block reduction that sets sigma and alpha = rho / sigma
-// (Alg. 1 lines 9-10; fp64 dots P:L1233).  Thread layout as the restriction: the
-// four lanes of a 2x2x2 block are xor 4 / xor 8 apart (ghost m_P by shuffles).
-template <bool DOT>
-__device__ __forceinline__ void apply_general(const ApplyArgs& a, int t, double* sred) {
-  const int j = threadIdx.x;
-  const int x2 = j & 3;
-  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
-  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
-  const int x0 = 2 * x2;
-  // beta = (r_k, z_k) / (r_{k-1}, z_{k-1}) (Alg. 1 line 12)
-  const float beta = (a.use_beta && a.pold) ? a.sc->beta_f : 0.0f;  // Alg. 1 line 12
-  const size_t base = (size_t)t * TB3;
-  const int off0 = loff(x0, y, z), off1 = off0 ^ 256;  // the pair: same q, opposite colours
-  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off1);
-  float p0 = 0.0f, p1 = 0.0f;
-  {
-    p0 = __ldg(a.z + base + off0);
-    p1 = __ldg(a.z + base + off1);
-    if (a.pold) {
-      p0 = fmaf(beta, __ldg(a.pold + base + off0), p0);
-      p1 = fmaf(beta, __ldg(a.pold + base + off1), p1);
-    }
-    if (q0.x == 0.0f) p0 = 0.0f;
-    if (q1.x == 0.0f) p1 = 0.0f;
-  }
-  if (a.pnew) {
-    a.pnew[base + off0] = p0;
-    a.pnew[base + off1] = p1;
-  }
-  __shared__ float sp[TB3];
-  __shared__ float scm[3][TB3];
-  sp[off0] = p0;
-  sp[off1] = p1;
-  scm[0][off0] = q0.y; scm[1][off0] = q0.z; scm[2][off0] = q0.w;
-  scm[0][off1] = q1.y; scm[1][off1] = q1.z; scm[2][off1] = q1.w;
-  float su = p0 + p1;
-  int na = (q0.x != 0.0f) + (q1.x != 0.0f);
-  su += __shfl_xor_sync(0xffffffffu, su, 4);
-  na += __shfl_xor_sync(0xffffffffu, na, 4);
-  su += __shfl_xor_sync(0xffffffffu, su, 8);
-  na += __shfl_xor_sync(0xffffffffu, na, 8);
-  const float mP = na ? su / (float)na : 0.0f;
-  __syncthreads();
-  const float r0 = q0.x != 0.0f ? composite_faces(a, beta, t, x0, y, z, q0, p0, mP, q0.x * p0, sp, scm) : 0.0f;
-  const float r1 = q1.x != 0.0f ? composite_faces(a, beta, t, x0 + 1, y, z, q1, p1, mP, q1.x * p1, sp, scm) : 0.0f;
-  a.q[base + off0] = r0;
-  a.q[base + off1] = r1;
-  if (DOT) {
-    // per-tile fp64 partial; k_finish_sigma sums them in tile order (no per-CTA fence)
-    double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
-    double bs = block_reduce_d(d, sred);
-    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
-  }
-}
-
-// q = A p as k_apply, on tiles whose six neighbours are all same-level leaves or walls (every
-// tile of a uniform tree): no shared-memory staging and no branches on the stencil path —
-// the neighbour entries are prefetched and the pair face sums are vectorised (row2_faces).
-// Other tiles take the general composite path of k_apply.
-template <bool DOT>
-__global__ __launch_bounds__(NT, 6) void k_apply_v2(ApplyArgs a) {
-  __shared__ double sred[NT / 32];
-  const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
-  int nb[6];
-  {
-    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
-    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
-    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
-  }
-  bool regular = true;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) regular &= nb[f] >= -1 && nb[f] < a.NL;
-  if (!regular) {
-    apply_general<DOT>(a, t, sred);
-    return;
-  }
-  const int j = threadIdx.x;
-  const int x2 = j & 3;
-  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
-  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
-  const int x0 = 2 * x2;
-  const float beta = (a.use_beta && a.pold) ? a.sc->beta_f : 0.0f;  // Alg. 1 line 12
-  const size_t base = (size_t)t * TB3;
-  const int off0 = loff(x0, y, z);
-  const float* cb = a.coef + ((size_t)t << 11);
-  const float2 c0 = ldpair(cb, off0), cxm = ldpair(cb + 512, off0), cym = ldpair(cb + 1024, off0),
-               czm = ldpair(cb + 1536, off0);
-  // p = z + beta p_old of any leaf cell (zero on inactive cells, see pval)
-  const RowTiles rt = row_tiles(t, nb, y, z);
-  DirVals vals;
-  vals.beta = beta;
-  vals.z = a.z;
-  vals.po = a.pold;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) vals.tf[f] = rt.tf[f];
-  float2 pp = ldpair(a.z + base, off0);
-  if (a.pold) {
-    const float2 w = ldpair(a.pold + base, off0);
-    pp.x = fmaf(beta, w.x, pp.x);
-    pp.y = fmaf(beta, w.y, pp.y);
-  }
-  const float p0 = c0.x != 0.0f ? pp.x : 0.0f, p1 = c0.y != 0.0f ? pp.y : 0.0f;
-  // same summation order as the general path: c*p, then the faces x-, x+, y-, y+, z-, z+
-  const float2 f = row2_faces(vals, rt, x2, y, z, pp, cxm, cym, czm, make_float2(c0.x * p0, c0.y * p1),
-                              a.coef + ((size_t)rt.tf[1] << 11) + 512, a.coef + ((size_t)rt.tf[3] << 11) + 1024,
-                              a.coef + ((size_t)rt.tf[5] << 11) + 1536);
-  const float r0 = c0.x != 0.0f ? f.x : 0.0f;
-  const float r1 = c0.y != 0.0f ? f.y : 0.0f;
-  if (a.pnew) {
-    a.pnew[base + off0] = p0;
-    a.pnew[base + (off0 ^ 256)] = p1;
-  }
-  a.q[base + off0] = r0;
-  a.q[base + (off0 ^ 256)] = r1;
-  if (DOT) {
-    double d = (double)p0 * (double)r0 + (double)p1 * (double)r1;
-    double bs = block_reduce_d(d, sred);
-    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
-  }
-}
-
-// q = A p for a precomputed p (split PCG form: a.z = p, no p_old), tiles without a ghost face
-// or inner neighbour: thread j < 128 owns red cells j, j + 128 of the tile, thread j >= 128
-// the black ones — the colour-pass layout: every neighbour of a cell is in the other colour
-// half at a fixed slot offset (see face_sum_regular in direct.cu), one load per neighbour.
-// Other tiles take the general composite path (same 256-thread CTA).
-template <bool DOT>
-__global__ __launch_bounds__(NT, 6) void k_apply_v4(ApplyArgs a) {
-  __shared__ double sred[NT / 32];
-  const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
-  int nb[6];
-#pragma unroll
-  for (int f = 0; f < 6; ++f) nb[f] = __ldg(a.nbr + 6 * (size_t)t + f);
-  bool regular = true;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) regular &= nb[f] >= -1 && nb[f] < a.NL;
-  if (!regular) {
-    apply_general<DOT>(a, t, sred);
-    return;
-  }
-  const int j = threadIdx.x;
-  const int colour = j >> 7, jj = j & 127;
-  const int y = (jj >> 2) & 7, z0 = jj >> 5;
-  const float* pt = a.z + ((size_t)t << 9);
+// q = A p (composite leaf operator; p precomputed by k_pupdate, split PCG form)
+// and the per-tile fp64 partial of p.q (Alg. 1 lines 9-10; fp64 dots P:L1233).  One
+// colour row per thread (rowtile.cuh): thread j of a 128-thread tile CTA owns row j >> 1 of
+// colour j & 1 (the two colours of a row in adjacent lanes, so a warp's float4 loads are two
+// contiguous 256-B half-rows).  Tiles with a T-junction face or a same-level inner neighbour
+// (IRR, CTA-uniform) take the same row loads and substitute the Eq. 12 ghost entries (m_P
+// by shuffles over the rows y^1, z^1 = lanes j^2, j^16) and the inner neighbours'
+// active-children means.  Flux form (A p)_i = d_i p_i + sum_f c_f (v_f - p_i) with the exact
+// row sums d (setup.cu k_leaf_rowsum, rowk::row_sums_flux); the ghost and inner entries are
+// formed directly as differences.  Algorithmic bytes: read p and the 4 record planes, write
+// q = 24 B per leaf cell (+4 B on tiles with a nonzero row sum).
+template <bool DOT, bool IRR>
+__device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const int (&nb)[6], double* sred) {
+  using namespace rowk;
+  const RowGeo g = row_geo(threadIdx.x & 1, threadIdx.x >> 1);
+  const float* pz = a.z;
   const float* ct = a.coef + ((size_t)t << 11);
-  const float* pn[6];
-  const float* cn[3];
-#pragma unroll
-  for (int f = 0; f < 6; ++f) pn[f] = nb[f] >= 0 ? a.z + ((size_t)nb[f] << 9) : pt;
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    const int n = nb[2 * ax + 1];
-    cn[ax] = (n >= 0 ? a.coef + ((size_t)n << 11) : ct) + ((1 + ax) << 9);
+  const int dk = __ldg(a.dtile + t);
+  const float4 pc = ld4(pz + ((size_t)t << 9) + g.own);
+  const float4 c0 = ld4(ct + g.own), cxm = ld4(ct + 512 + g.own), cym = ld4(ct + 1024 + g.own),
+               czm = ld4(ct + 1536 + g.own);
+  const int NL = a.NL;
+  // leaf values of tile n; an inner neighbour's entries are replaced below (row_inner), so
+  // its unconditional row load reads the own tile instead
+  auto tu = [pz, NL, t](int n) -> const float* { return pz + ((size_t)(n < NL ? n : t) << 9); };
+  RowSt s;
+  row_load<decltype(tu), true>(s, tu, a.coef, t, nb, g);
+  const float4 d = dk >= 0 ? ld4(a.dval + ((size_t)dk << 9) + g.own) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  const float4 pv = msk4(pc, c0);
+  RowRep rp{false, false, false, false, false};
+  if (IRR) {
+    const float4 co = ld4(ct + g.oth);
+    const float4 mP = row_block_mean<2, 16>(pv, c0, msk4(s.ox, co), co);
+    row_ghosts<false, decltype(tu), true>(s, g, t, nb, __ldg(a.tile + t), a.coef, a.glayer_val, a.glayer, tu, pv,
+                                          mP, &rp);
+    auto pvf = [pz](int tt, int sl) { return __ldg(pz + ((size_t)tt << 9) + sl); };
+    row_inner<decltype(pvf), true>(s, g, nb, NL, a.child, a.coef, pvf, pv, &rp);
   }
-  double d = 0.0;
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int z = z0 + 4 * k;
-    const int x = 2 * (jj & 3) + ((colour + y + z) & 1);
-    const int sl = (colour << 8) + jj + 128 * k;
-    const float c0 = __ldg(ct + sl), cxm = __ldg(ct + 512 + sl), cym = __ldg(ct + 1024 + sl),
-                czm = __ldg(ct + 1536 + sl);
-    const float pc = __ldg(pt + sl);
-    const int base = sl ^ 256;
-    const int p = x & 1;
-    const bool in[6] = {x > 0, x < 7, y > 0, y < 7, z > 0, z < 7};
-    const int dlt[6] = {in[0] ? p - 1 : 3, in[1] ? p : -3, in[2] ? -4 : 28, in[3] ? 4 : -28, in[4] ? -32 : 224,
-                        in[5] ? 32 : -224};
-    const float cm3[3] = {cxm, cym, czm};
-    const float pv = c0 != 0.0f ? pc : 0.0f;
-    float sm = c0 * pv;  // the general path's order: c*p, then x-, x+, y-, y+, z-, z+
-#pragma unroll
-    for (int f = 0; f < 6; ++f) {
-      const int ax = f >> 1;
-      const int no = base + dlt[f];
-      float v = __ldg((in[f] ? pt : pn[f]) + no);
-      const float cf = (f & 1) ? __ldg((in[f] ? ct + ((1 + ax) << 9) : cn[ax]) + no) : cm3[ax];
-      if (!in[f] && nb[f] < 0) v = 0.0f;
-      sm = fmaf(cf, v, sm);
-    }
-    const float r = c0 != 0.0f ? sm : 0.0f;
-    a.q[((size_t)t << 9) + sl] = r;
-    d += (double)pv * (double)r;
-  }
+  const float4 f = row_sums_flux(s, g, rp, cxm, cym, czm, pv, d);
+  const float4 r = make_float4(c0.x != 0.0f ? f.x : 0.0f, c0.y != 0.0f ? f.y : 0.0f, c0.z != 0.0f ? f.z : 0.0f,
+                               c0.w != 0.0f ? f.w : 0.0f);
+  *reinterpret_cast<float4*>(a.q + ((size_t)t << 9) + g.own) = r;
   if (DOT) {
-    double bs = block_reduce_d(d, sred);
+    const double dd = (double)pv.x * (double)r.x + (double)pv.y * (double)r.y + (double)pv.z * (double)r.z +
+                      (double)pv.w * (double)r.w;
+    double bs = block_reduce_d(dd, sred);
     if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
   }
 }
 
-// k_apply_v4 with vector loads: thread j owns the two colour cells of slots 2jj, 2jj + 1 of
-// colour j >> 7 (jj = j & 127: one half of a colour row, elements m = 2h, 2h + 1 of row
-// (y, z), x_m = 2m + p, p = (colour + y + z) & 1).  The other colour's row at the same slots
-// holds both cells' x-neighbours but one (element m + p - 1 / m + p: one extra scalar, in the
-// tile or the x-neighbour tile), and its rows 4 / 32 slots away are the y / z neighbours
-// (wrapped: -28 / +28, -224 / +224 into the neighbour tile), so a cell pair costs 15 float2 /
-// scalar loads instead of 28.  The y / z side tests are uniform per thread.  Same per-cell
-// fmaf order as k_apply_v4 (c p, then x-, x+, y-, y+, z-, z+), so q is bit-identical.
-template <bool DOT, int MINB>
-__global__ __launch_bounds__(NT, MINB) void k_apply_v5(ApplyArgs a) {
-  __shared__ double sred[NT / 32];
+// the irregular-tile body out of line (its registers do not lower the regular path's occupancy)
+template <bool DOT>
+__device__ __noinline__ void apply_row_irr(const ApplyArgs& a, int t, int n0, int n1, int n2, int n3, int n4, int n5,
+                                           double* sred) {
+  const int nb[6] = {n0, n1, n2, n3, n4, n5};
+  apply_row_body<DOT, true>(a, t, nb, sred);
+}
+
+// INL: the irregular body inlined, at 6 CTAs/SM (80 registers) instead of out of line at 8
+template <bool DOT, bool INL>
+__global__ __launch_bounds__(128, INL ? 6 : 8) void k_apply_v6(const __grid_constant__ ApplyArgs a) {
+  __shared__ double sred[4];
   const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
   int nb[6];
-  {
-    const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
-    const int2 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2);
-    nb[0] = n0.x; nb[1] = n0.y; nb[2] = n1.x; nb[3] = n1.y; nb[4] = n2.x; nb[5] = n2.y;
-  }
-  bool regular = true;
+  rowk::load_nb(a.nbr, t, nb);
+  bool irr = false;
 #pragma unroll
-  for (int f = 0; f < 6; ++f) regular &= nb[f] >= -1 && nb[f] < a.NL;
-  if (!regular) {
-    apply_general<DOT>(a, t, sred);
+  for (int f = 0; f < 6; ++f) irr |= nb[f] <= -2 || nb[f] >= a.NL;
+  if (irr) {  // CTA-uniform
+    if (INL) apply_row_body<DOT, true>(a, t, nb, sred);
+    else apply_row_irr<DOT>(a, t, nb[0], nb[1], nb[2], nb[3], nb[4], nb[5], sred);
     return;
   }
-  const int j = threadIdx.x;
-  const int colour = j >> 7, jj = j & 127;
-  const int row = jj >> 1, h = jj & 1;
-  const int y = row & 7, z = row >> 3;
-  const int p = (colour + y + z) & 1;
-  const int own = (colour << 8) + 2 * jj;  // slots of elements 2h, 2h + 1
-  const int oth = own ^ 256;               // the other colour's row, same elements
-  const float* pt = a.z + ((size_t)t << 9);
-  const float* ct = a.coef + ((size_t)t << 11);
-  auto tz = [&](int n) { return n >= 0 ? a.z + ((size_t)n << 9) : pt; };
-  auto tc = [&](int n) { return n >= 0 ? a.coef + ((size_t)n << 11) : ct; };
-  const float2 pc = __ldg(reinterpret_cast<const float2*>(pt + own));
-  const float2 c0 = __ldg(reinterpret_cast<const float2*>(ct + own));
-  const float2 cxm = __ldg(reinterpret_cast<const float2*>(ct + 512 + own));
-  const float2 cym = __ldg(reinterpret_cast<const float2*>(ct + 1024 + own));
-  const float2 czm = __ldg(reinterpret_cast<const float2*>(ct + 1536 + own));
-  // x: the other row's elements 2h, 2h + 1 and the one outside them (p = 0: element 2h - 1,
-  // p = 1: element 2h + 2), in the tile or the x-neighbour tile (element 3 / 0 of its row)
-  const float2 ox = __ldg(reinterpret_cast<const float2*>(pt + oth));
-  const float2 cxo = __ldg(reinterpret_cast<const float2*>(ct + 512 + oth));
-  const bool xin = p ? h == 0 : h == 1;
-  const int nx = p ? nb[1] : nb[0];  // the tile across the face the extra element lies beyond
-  const int xo = p ? (xin ? oth + 2 : oth - 2) : (xin ? oth - 1 : oth + 3);
-  float xs = __ldg((xin ? pt : tz(nx)) + xo);
-  const float xsc = __ldg((xin ? ct : tc(nx)) + 512 + xo);  // its c_x- (used when p = 1)
-  if (!xin && nx < 0) xs = 0.0f;
-  // y / z: the other row 4 / 32 slots away (wrapped into the neighbour tile at the sides)
-  const bool yl = y > 0, yh = y < 7, zl = z > 0, zh = z < 7;
-  float2 ym = __ldg(reinterpret_cast<const float2*>((yl ? pt : tz(nb[2])) + oth + (yl ? -4 : 28)));
-  float2 yp = __ldg(reinterpret_cast<const float2*>((yh ? pt : tz(nb[3])) + oth + (yh ? 4 : -28)));
-  float2 zm = __ldg(reinterpret_cast<const float2*>((zl ? pt : tz(nb[4])) + oth + (zl ? -32 : 224)));
-  float2 zp = __ldg(reinterpret_cast<const float2*>((zh ? pt : tz(nb[5])) + oth + (zh ? 32 : -224)));
-  const float2 cyp = __ldg(reinterpret_cast<const float2*>((yh ? ct : tc(nb[3])) + 1024 + oth + (yh ? 4 : -28)));
-  const float2 czp = __ldg(reinterpret_cast<const float2*>((zh ? ct : tc(nb[5])) + 1536 + oth + (zh ? 32 : -224)));
-  if (!yl && nb[2] < 0) ym = make_float2(0.0f, 0.0f);
-  if (!yh && nb[3] < 0) yp = make_float2(0.0f, 0.0f);
-  if (!zl && nb[4] < 0) zm = make_float2(0.0f, 0.0f);
-  if (!zh && nb[5] < 0) zp = make_float2(0.0f, 0.0f);
-  // per element e: x- / x+ values and the x+ coupling
-  const float xm0 = p ? ox.x : xs, xm1 = p ? ox.y : ox.x;
-  const float xp0 = p ? ox.y : ox.x, xp1 = p ? xs : ox.y;
-  const float cxp0 = p ? cxo.y : cxo.x, cxp1 = p ? xsc : cxo.y;
-  const float pv0 = c0.x != 0.0f ? pc.x : 0.0f, pv1 = c0.y != 0.0f ? pc.y : 0.0f;
-  float s0 = c0.x * pv0, s1 = c0.y * pv1;
-  s0 = fmaf(cxm.x, xm0, s0); s1 = fmaf(cxm.y, xm1, s1);
-  s0 = fmaf(cxp0, xp0, s0);  s1 = fmaf(cxp1, xp1, s1);
-  s0 = fmaf(cym.x, ym.x, s0); s1 = fmaf(cym.y, ym.y, s1);
-  s0 = fmaf(cyp.x, yp.x, s0); s1 = fmaf(cyp.y, yp.y, s1);
-  s0 = fmaf(czm.x, zm.x, s0); s1 = fmaf(czm.y, zm.y, s1);
-  s0 = fmaf(czp.x, zp.x, s0); s1 = fmaf(czp.y, zp.y, s1);
-  const float r0 = c0.x != 0.0f ? s0 : 0.0f, r1 = c0.y != 0.0f ? s1 : 0.0f;
-  *reinterpret_cast<float2*>(a.q + ((size_t)t << 9) + own) = make_float2(r0, r1);
-  if (DOT) {
-    const double d = (double)pv0 * (double)r0 + (double)pv1 * (double)r1;
-    double bs = block_reduce_d(d, sred);
-    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
-  }
-}
-
-template <bool DOT>
-__global__ __launch_bounds__(NT, 5) void k_apply(ApplyArgs a) {
-  __shared__ double sred[NT / 32];
-  apply_general<DOT>(a, a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x, sred);
+  apply_row_body<DOT, false>(a, t, nb, sred);
 }
 
 // sigma = p.q from the per-tile partials (fixed order => deterministic)
@@ -651,19 +372,18 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
     if (a.partial) cudaMemsetAsync(&a.sc->sum_pq, 0, sizeof(double), s);
     return;
   }
+  static int inl = -1;  // OCTMG_APPLY_IRR=inline: the irregular body inlined
+  if (inl < 0) {
+    const char* e = getenv("OCTMG_APPLY_IRR");
+    inl = e && e[0] == 'i';
+  }
   if (a.partial) {
-    if (a.v2 == 5) k_apply_v5<true, 8><<<a.ntiles, NT, 0, s>>>(a);
-    else if (a.v2 == 6) k_apply_v5<true, 6><<<a.ntiles, NT, 0, s>>>(a);
-    else if (a.v2 == 4) k_apply_v4<true><<<a.ntiles, NT, 0, s>>>(a);
-    else if (a.v2) k_apply_v2<true><<<a.ntiles, NT, 0, s>>>(a);
-    else k_apply<true><<<a.ntiles, NT, 0, s>>>(a);
+    if (inl) k_apply_v6<true, true><<<a.ntiles, 128, 0, s>>>(a);
+    else k_apply_v6<true, false><<<a.ntiles, 128, 0, s>>>(a);
     k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.ntiles, a.sc);
   } else {
-    if (a.v2 == 5) k_apply_v5<false, 8><<<a.ntiles, NT, 0, s>>>(a);
-    else if (a.v2 == 6) k_apply_v5<false, 6><<<a.ntiles, NT, 0, s>>>(a);
-    else if (a.v2 == 4) k_apply_v4<false><<<a.ntiles, NT, 0, s>>>(a);
-    else if (a.v2) k_apply_v2<false><<<a.ntiles, NT, 0, s>>>(a);
-    else k_apply<false><<<a.ntiles, NT, 0, s>>>(a);
+    if (inl) k_apply_v6<false, true><<<a.ntiles, 128, 0, s>>>(a);
+    else k_apply_v6<false, false><<<a.ntiles, 128, 0, s>>>(a);
   }
 }
 

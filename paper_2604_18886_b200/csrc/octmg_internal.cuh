@@ -157,16 +157,14 @@ struct ApplyArgs {
   const float* coef;    // SoA per tile: planes c, c_x-, c_y-, c_z- (cidx)
   const float* glayer_val;
   const int* glayer;
-  const float* z;       // direction source (user x for octmg_apply)
-  const float* pold;    // previous p (nullptr: beta = 0)
-  float* pnew;          // written p = z + beta p (nullptr: not written)
+  const int* dtile;     // leaf row sums (flux form): tile -> row of dval, -1 = all zero
+  const float* dval;
+  const float* z;       // p (user x for octmg_apply), zero on inactive cells
   float* q;             // A p
   double* partial;      // per-tile fp64 partial of p.q (nullptr: no dot)
   unsigned* counter;
-  Scalars* sc;          // beta = sum_rz / rho read from here; sum_pq written by the finish kernel
+  Scalars* sc;          // sum_pq written by the finish kernel
   int NL;
-  int use_beta;
-  int v2;               // 5 / 4: k_apply_v5 / k_apply_v4 (p precomputed), 1: k_apply_v2 (p formed inside), 0: k_apply
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
@@ -241,7 +239,7 @@ void launch_coarse_direct(const SmoothArgs& a, cudaStream_t s);  // u^0 = M0 b^0
 // setup kernels (setup.cu)
 struct SetupArgs;
 octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
-                                 cudaStream_t s);
+                                 cudaStream_t s);  // + coarsen_all + the leaf row sums d
 octmg_status coarsen_all(Hier& h, cudaStream_t s);  // literal Alg. 3 if h.prm.coarsen_literal
 
 // projection operators (projection.cu)
@@ -279,6 +277,9 @@ struct Hier {
   float* coef = nullptr;         // [T*2048] SoA per tile: c, cxm, cym, czm planes (cidx)
   uint32_t* act = nullptr;       // [NL*512/32] activity bitmask of the leaf cells
   float* glayer_val = nullptr;   // [n_glayers*64]
+  int* dtile = nullptr;          // [NL] leaf row sums d (flux-form apply): tile's row in dval, or -1 (all d = 0)
+  float* dval = nullptr;         // [n_dtiles*512] d of those tiles (slot order)
+  int n_dtiles = 0;
   // multigrid buffers
   float* z = nullptr;            // [NL*512] leaf part of the cycle's u (buffer A) = M output
   float* uinA = nullptr;         // [NI*512] inner part of u (buffer A)
@@ -304,7 +305,6 @@ struct Hier {
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
-  int apply_v = 5;               // p-precomputed apply: 5 k_apply_v5 (float2 rows), 4 k_apply_v4 (OCTMG_APPLY_V=4)
   int restrict_v2 = 6;           // k_restrict_v2 (vectorised regular tiles) at >= 6 (8: OCTMG_RESTRICT_V=8) CTAs/SM; 0: staged k_restrict_direct (OCTMG_RESTRICT_V=1)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)

@@ -2,6 +2,7 @@
 // T-junction faces Eqs. 9-10) and Galerkin coarsening (Alg. 3)
 // of the compact record (c, c_x-, c_y-, c_z-) held as one float4 per cell.
 #include <algorithm>
+#include <vector>
 
 #include "nbref.cuh"
 
@@ -99,6 +100,75 @@ __global__ __launch_bounds__(256) void k_assemble_offdiag(AsmArgs a) {
     a.coef[cidx(i, 2)] = cm[1];
     a.coef[cidx(i, 3)] = cm[2];
   }
+}
+
+// Row sums of the leaf operator as the apply evaluates it, d_i = c_i + sum_f c_f (the
+// exact, fp64 diagonal of Eq. 3 plus the six stored fp32 couplings the apply uses: own -face
+// entries, the +face neighbour's -face entry (same-level leaf or inner cell), the ghost
+// layer toward a coarse leaf, 0 at a domain wall).  The apply evaluates the operator in
+// flux form, (A p)_i = d_i p_i + sum_f c_f (v_f - p_i) (kernels.cu k_apply_v6), so its
+// diagonal is the exact c_i even though the stored c is fp32, and the operator's rows sum
+// exactly to d_i (0 away from Dirichlet walls).  Runs after the coarsening (the +faces of
+// inner neighbours are their Alg. 3 records).  flag[t] = 1 if any d of tile t is nonzero.
+__global__ __launch_bounds__(256) void k_leaf_rowsum(AsmArgs a, float* d, int* flag) {
+  const int t = blockIdx.x;
+  const int4 tv = a.tile[t];
+  const double h = ldexp(1.0, -tv.x) * 0.125;
+  int any = 0;
+  for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
+    int x, y, z;
+    slot_xyz(off, x, y, z);
+    const size_t i = (size_t)t * TB3 + off;
+    double dv = 0.0;
+    if (a.coef[cidx(i, 0)] != 0.0f) {
+      // the exact diagonal (k_assemble_diag's terms in fp64)
+      double c = 0.0;
+      for (int f = 0; f < 6; ++f) {
+        NbRef nb = nb_ref(a.nbr, tv, t, a.NL, x, y, z, f);
+        if (nb.what == NB_WALL) {
+          if (a.wall[f]) c += (double)a.w.w(f, i) * h;
+        } else if (nb.what == NB_LEAF) {
+          size_t j = (size_t)nb.tile * TB3 + nb.off;
+          if (a.kind[j] != KN) c += (double)((f & 1) ? a.w.w(f ^ 1, j) : a.w.w(f, i)) * h;
+        } else if (nb.what == NB_INNER) {
+          size_t sub[4];
+          fine_subs(a.child, a.NL, nb, f, sub);
+          for (int k = 0; k < 4; ++k)
+            if (a.kind[sub[k]] != KN) c += 0.5 * (double)a.w.w(f ^ 1, sub[k]) * (0.5 * h);
+        } else {
+          size_t C = (size_t)nb.tile * TB3 + nb.off;
+          if (a.kind[C] != KN) c += (double)a.w.w(f, i) * h;
+        }
+      }
+      // + the couplings the apply uses
+      for (int f = 0; f < 6; ++f) {
+        const int ax = f >> 1;
+        if (!(f & 1)) {
+          c += (double)a.coef[cidx(i, 1 + ax)];
+          continue;
+        }
+        NbRef nb = nb_ref(a.nbr, tv, t, a.NL, x, y, z, f);
+        if (nb.what == NB_LEAF || nb.what == NB_INNER) {
+          c += (double)a.coef[cidx((size_t)nb.tile * TB3 + nb.off, 1 + ax)];
+        } else if (nb.what == NB_GHOST) {
+          const int p = ax == 0 ? y + 8 * z : (ax == 1 ? x + 8 * z : x + 8 * y);
+          c += (double)a.glayer_val[(size_t)a.glayer[3 * t + ax] * 64 + p];
+        }
+      }
+      dv = c;
+    }
+    d[i] = (float)dv;
+    any |= (float)dv != 0.0f;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) flag[t] = any;
+}
+
+__global__ void k_compact_rowsum(const float* d, const int* dtile, int NL, float* dval) {
+  const int t = blockIdx.x;
+  const int k = dtile[t];
+  if (k < 0) return;
+  for (int o = threadIdx.x; o < TB3; o += blockDim.x) dval[(size_t)k * TB3 + o] = d[(size_t)t * TB3 + o];
 }
 
 struct CoarsenArgs {
@@ -199,6 +269,36 @@ octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbet
   k_assemble_diag<<<T.NL, 256, 0, s>>>(a);
   k_assemble_offdiag<<<T.NL, 256, 0, s>>>(a);
   OCTMG_CUDA(cudaGetLastError());
+  OCTMG_TRY(coarsen_all(h, s));  // Alg. 3 (the +face records of inner neighbours feed the row sums)
+  {
+    // leaf row sums d (flux-form apply), kept for the tiles where some d != 0
+    float* dfull = nullptr;
+    int* dflag = nullptr;
+    OCTMG_CUDA(cudaMallocAsync(&dfull, sizeof(float) * std::max<int64_t>(Nc, 1), s));
+    OCTMG_CUDA(cudaMallocAsync(&dflag, sizeof(int) * std::max(T.NL, 1), s));
+    if (T.NL) k_leaf_rowsum<<<T.NL, 256, 0, s>>>(a, dfull, dflag);
+    OCTMG_CUDA(cudaGetLastError());
+    std::vector<int> fl(T.NL);
+    if (T.NL) OCTMG_CUDA(cudaMemcpyAsync(fl.data(), dflag, sizeof(int) * T.NL, cudaMemcpyDeviceToHost, s));
+    OCTMG_CUDA(cudaStreamSynchronize(s));
+    int nd = 0;
+    for (int t = 0; t < T.NL; ++t) fl[t] = fl[t] ? nd++ : -1;
+    OCTMG_CUDA(cudaMemcpyAsync(dflag, fl.data(), sizeof(int) * T.NL, cudaMemcpyHostToDevice, s));
+    h.dtile = (int*)dev_malloc(sizeof(int) * std::max(T.NL, 1));
+    h.dval = (float*)dev_malloc(sizeof(float) * (size_t)std::max(nd, 1) * TB3);
+    if (!h.dtile || !h.dval) {
+      set_error("device allocation failed (leaf row sums)");
+      return OCTMG_E_OOM;
+    }
+    h.allocs.push_back(h.dtile);
+    h.allocs.push_back(h.dval);
+    h.n_dtiles = nd;
+    OCTMG_CUDA(cudaMemcpyAsync(h.dtile, dflag, sizeof(int) * T.NL, cudaMemcpyDeviceToDevice, s));
+    if (T.NL) k_compact_rowsum<<<T.NL, 128, 0, s>>>(dfull, dflag, T.NL, h.dval);
+    OCTMG_CUDA(cudaGetLastError());
+    OCTMG_CUDA(cudaFreeAsync(dfull, s));
+    OCTMG_CUDA(cudaFreeAsync(dflag, s));
+  }
   // active leaf-cell count and whether any Dirichlet kind exists (null-space auto)
   unsigned long long* d_cnt;
   int* d_flag;

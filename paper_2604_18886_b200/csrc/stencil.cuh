@@ -89,29 +89,36 @@ __device__ __forceinline__ bool has_ghost(const SmoothArgs& a, int t) {
   return g;
 }
 
-// mean of the active cells of the 2x2x2 block holding (x,y,z) (pass-start values)
+// mean of the active cells of the 2x2x2 block holding (x,y,z) (pass-start values), summed
+// as ((x-pair at dy0,dz0 + x-pair at dy1,dz0) + (dy0,dz1 + dy1,dz1)) — the order of the
+// row kernels' shuffle sums (rowtile.cuh row_block_mean), so every kernel forms the same m_P
 template <bool ZERO_OWN, int NC = 1>
 __device__ __forceinline__ float block_mean(const SmoothArgs& a, int t, int x, int y, int z, int colour) {
   const size_t base = (size_t)t * TB3;
   const float* ut = tptr(a.u, t, a.NL);
-  float sm = 0.0f;
+  float pr[2][2];
   int nn = 0;
   // the block's cells: q0 + 4 dy + 32 dz in the half of colour (dx + dy + dz) & 1 (the
   // block corner (x&~1, y&~1, z&~1) has even coordinates, hence colour 0)
   const int q0 = (x >> 1) + 4 * (y & ~1) + 32 * (z & ~1);
+#pragma unroll
   for (int dz = 0; dz < 2; ++dz)
-    for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      float v[2];
+#pragma unroll
       for (int dx = 0; dx < 2; ++dx) {
         const int cb = (dx + dy + dz) & 1;
         const int bo = (cb << 8) + q0 + 4 * dy + 32 * dz;
         const float cc = __ldg(a.coef + cidx(base + bo, 0));
         float bv = ldv<NC>(ut + bo);  // loaded with the activity (no load behind a branch)
-        if (cc != 0.0f) {
-          if (ZERO_OWN && cb == colour) bv = 0.0f;
-          sm += bv;
-          nn++;
-        }
+        if (ZERO_OWN && cb == colour) bv = 0.0f;
+        v[dx] = cc != 0.0f ? bv : 0.0f;
+        nn += cc != 0.0f;
       }
+      pr[dz][dy] = v[0] + v[1];
+    }
+  const float sm = (pr[0][0] + pr[0][1]) + (pr[1][0] + pr[1][1]);
   return nn ? sm / (float)nn : 0.0f;
 }
 

@@ -250,11 +250,12 @@ def test_full_size_cfg2_parity(om):
 # ---------------------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
                                  {"OCTMG_GRID": "1"}, {"OCTMG_GRID": "1", "OCTMG_SUBCYCLE": "0"},
-                                 {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_PCG_FUSED": "1"},
-                                 {"OCTMG_GRAPH_LOOP": "0"}, {"OCTMG_APPLY_V": "4"}, {"OCTMG_RESTRICT_V": "8"},
+                                 {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_GRAPH_LOOP": "0"}, {"OCTMG_RESTRICT_V": "8"},
                                  {"OCTMG_RESTRICT_V": "1"}, {"OCTMG_PASS_V": "1"},
                                  {"OCTMG_SUBCYCLE_CTAS": "8", "OCTMG_SUBCYCLE_LD": "2"},
-                                 {"OCTMG_GRID": "1", "OCTMG_GRID_TILES": "64"}, {"OCTMG_PASS_BIG": "1"}])
+                                 {"OCTMG_GRID": "1", "OCTMG_GRID_TILES": "64"}, {"OCTMG_PASS_BIG": "1"},
+                                 {"OCTMG_PASS_V": "2"}, {"OCTMG_PASS_GHOST": "inline"},
+                                 {"OCTMG_APPLY_IRR": "inline"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     for k, v in env.items():
@@ -273,22 +274,23 @@ def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     assert abs(rep["iters"] - o.pcg(cfg["b"].astype(np.float64), rtol=1e-6, mu=cfg["mu"])["iters"]) <= 1
 
 
-@pytest.mark.parametrize("name", ["uniform64_dir", "sphere_small", "tank_mid", "cfg1_octant"])
-def test_apply_row_vector_variant_bit_identical(om, name, monkeypatch):
-    """k_apply_v5 (float2 colour rows) keeps k_apply_v4's per-cell fmaf order: q identical."""
+@pytest.mark.parametrize("name", ["uniform128", "sphere_small", "sphere_small_dir", "tank_mid", "cfg1_octant"])
+def test_apply_smooth_input_matches_oracle(om, name):
+    """The apply on a smooth input (the low modes the preconditioned CG leaves last), where
+    |A p| << |c| |p|: the flux-form evaluation (exact row sums, differences v_f - p_i) keeps
+    the north_star apply bar (<= 1e-5 relative L2 against the fp64 oracle) there too; a
+    c p + sum c_f v_f evaluation in fp32 loses ~eps |c| |p| per row to cancellation."""
+    from octgen.trees import leaf_cell_geometry
     cfg = make_config(name)
-    tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
-    kind = torch.from_numpy(cfg["kind"]).to(DEV)
-    frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(DEV)
-    x = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, tree.N).astype(np.float32)).to(DEV)
-    out = []
-    for v in ("5", "4"):
-        monkeypatch.setenv("OCTMG_APPLY_V", v)
-        h = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
-        y = torch.empty_like(x)
-        h.apply(x, y)
-        out.append(y)
-    assert torch.equal(out[0], out[1])
+    tree, h, o = _setup(om, cfg)
+    ctr, _ = leaf_cell_geometry(cfg["tiles"])
+    xs = 1.0 + 0.5 * np.cos(2.0 * ctr[:, 0] + 1.0) * np.cos(1.5 * ctr[:, 1]) + 0.25 * ctr[:, 2] ** 2
+    act = o.coefs()[:o.N, 0] != 0
+    xs = np.where(act, xs, 0.0).astype(np.float32)
+    y = torch.zeros(o.N, device=DEV)
+    h.apply(torch.from_numpy(xs).to(DEV), y)
+    ref = o.apply(xs.astype(np.float64))
+    assert _rel(y.cpu().numpy().astype(np.float64), ref) <= 1e-5
 
 
 # ---------------------------------------------------------------------------------------

@@ -1,0 +1,15 @@
+#!/bin/bash
+# build, fast GPU tests, A/B benches of the kernel variants on configs 2 and 3, cfg5 diagnostic
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { echo build failed; tail -30 gpurun_out/build.log; exit 1; }
+timeout 1500 python -m pytest tests -m "gpu and not slow" -q > gpurun_out/gputests.log 2>&1; echo "gpu tests rc=$?" >> gpurun_out/gputests.log
+tail -3 gpurun_out/gputests.log
+for cfg in cfg2_uniform256 cfg3_sphere; do
+  for v in "base:" "pass2:OCTMG_PASS_V=2" "restrict3:OCTMG_RESTRICT_V=3" "restrict36:OCTMG_RESTRICT_V=36"; do
+    tag=${v%%:*}; envs=${v#*:}
+    env $envs timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-wcycle --no-cpu-baseline > gpurun_out/ab_${cfg}_${tag}.json 2> gpurun_out/ab_${cfg}_${tag}.err
+    python -c "import json,sys; d=json.load(open('gpurun_out/ab_${cfg}_${tag}.json')); print('$cfg $tag', round(d['ms_per_step'],3), d['config']['pcg_iters'], {k:round(v['ms_per_solve'],3) for k,v in d['kernels'].items() if k in ('rbgs_pass','residual_restrict','apply','coarse_levels')})" || tail -3 gpurun_out/ab_${cfg}_${tag}.err
+  done
+done
+timeout 900 python tools/diag_cfg5.py > gpurun_out/diag5.log 2>&1; echo "diag rc=$?"
+tail -5 gpurun_out/diag5.log
