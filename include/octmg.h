@@ -331,6 +331,11 @@ octmg_status octmg_mg_solve(octmg_hier* h, const float* b, float* x, const octmg
 octmg_status octmg_profile_enable(octmg_hier* h, int32_t on);
 octmg_status octmg_profile_read(octmg_hier* h, const char** names, double* ms, int64_t* counts,
                                 double* bytes, int32_t cap, int32_t* n);
+/* The same restricted to the multigrid work of one level (0 = coarsest; the classes in
+ * octmg_profile_read's order; the PCG vector kernels have no level and are not counted).
+ * Accumulates since the last octmg_profile_enable, like octmg_profile_read.  Synchronises. */
+octmg_status octmg_profile_read_level(octmg_hier* h, int32_t level, double* ms, int64_t* counts, double* bytes,
+                                      int32_t cap, int32_t* n);
 
 void octmg_hier_destroy(octmg_hier* h);
 void octmg_tree_destroy(octmg_tree* tree);

@@ -116,6 +116,15 @@ octmg_status build_orders(Hier& h) {
   const Tree& T = *h.tree;
   std::vector<int4> tile(T.T);
   OCTMG_CUDA(cudaMemcpy(tile.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
+  {
+    // levels with a T-junction (ghost) face anywhere (all parts decide alike)
+    std::vector<int> nbr((size_t)T.T * 6);
+    OCTMG_CUDA(cudaMemcpy(nbr.data(), T.nbr, sizeof(int) * nbr.size(), cudaMemcpyDeviceToHost));
+    for (int l = 0; l <= MAXL; ++l) h.lvl_ghost[l] = false;
+    for (int t = 0; t < T.T; ++t)
+      for (int f = 0; f < 6; ++f)
+        if (nbr[6 * (size_t)t + f] <= -2) h.lvl_ghost[tile[t].x] = true;
+  }
   auto m2 = [](uint32_t x, uint32_t y) {
     uint64_t m = 0;
     for (int b = 0; b < 21; ++b) m |= ((uint64_t)((x >> b) & 1) << (2 * b)) | ((uint64_t)((y >> b) & 1) << (2 * b + 1));
@@ -275,12 +284,12 @@ struct ProfScope {
   int cls;
   cudaStream_t s;
   cudaEvent_t b = nullptr;
-  ProfScope(Hier& hh, int c, cudaStream_t ss, double bytes) : h(hh), cls(c), s(ss) {
+  ProfScope(Hier& hh, int c, cudaStream_t ss, double bytes, int level = -1) : h(hh), cls(c), s(ss) {
     if (h.profiling) {
       cudaEvent_t a = next_event(h);
       b = next_event(h);
       cudaEventRecord(a, s);
-      h.events.push_back({cls, bytes, a, b});
+      h.events.push_back({cls, bytes, a, b, level});
     }
   }
   ~ProfScope() {
@@ -292,7 +301,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   const Tree& T = *h.tree;
   if (op.kind == 2) {
     size_t first = (size_t)T.lc[T.L] * TB3;
-    ProfScope ps(h, KC_MEMSET, s, 4.0 * ((double)T.NL * TB3 - first));
+    ProfScope ps(h, KC_MEMSET, s, 4.0 * ((double)T.NL * TB3 - first), op.level);
     cudaMemsetAsync(h.z + first, 0, ((size_t)T.NL * TB3 - first) * sizeof(float), s);
     return;
   }
@@ -316,32 +325,32 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.c0n = h.c0n;
   if (op.kind == 10) {
     // read M0 (4 n0^2 B) and b^0, write u^0
-    ProfScope ps(h, KC_COARSEST, s, 4.0 * (double)h.c0n * h.c0n + 8.0 * h.c0n);
+    ProfScope ps(h, KC_COARSEST, s, 4.0 * (double)h.c0n * h.c0n + 8.0 * h.c0n, op.level);
     launch_coarse_direct(a, s);
     return;
   }
   if (op.kind == 9) {
-    ProfScope ps(h, KC_COARSE_GRID, s, 0.0);
+    ProfScope ps(h, KC_COARSE_GRID, s, 0.0, op.level);
     cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
                                        T.ic, h.bar, s);
     if (e != cudaSuccess) set_error(std::string("k_coarse_grid launch: ") + cudaGetErrorString(e));
     return;
   }
   if (op.kind == 4) {
-    ProfScope ps(h, KC_SUBCYCLE, s, 0.0);
+    ProfScope ps(h, KC_SUBCYCLE, s, 0.0, op.level);
     launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, h.sub_ctas, s);
     return;
   }
   if (op.kind == 3) {
     // read u and the c plane, write u (12 B/cell) + the parents' u, u* (1 B/cell)
-    ProfScope ps(h, KC_PROLONG, s, 13.0 * a.n * TB3);
+    ProfScope ps(h, KC_PROLONG, s, 13.0 * a.n * TB3, op.level);
     launch_prolong(a, s);
     return;
   }
   if (op.kind == 1) {
     // read u, b, record; write b (inner cells of the level, this part's)
     a.first_tile = h.own_ib[l];
-    ProfScope ps(h, KC_FASRHS, s, 28.0 * h.own_ic[l] * TB3);
+    ProfScope ps(h, KC_FASRHS, s, 28.0 * h.own_ic[l] * TB3, op.level);
     launch_fasrhs(a, h.own_ic[l], s);
     return;
   }
@@ -356,14 +365,15 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   if (mode == SM_PRO1 || mode == SM_PRO2) bytes += cells;
   int cls = mode == SM_RESTRICT ? KC_RESTRICT
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
-  ProfScope ps(h, cls, s, bytes);
+  ProfScope ps(h, cls, s, bytes, op.level);
   if (mode == SM_RESTRICT) {
     launch_restrict_direct(a, s, h.restrict_v2);
   } else {
     // kernel chosen by the level's total tile count, so every part of a partitioned solve runs
     // the same per-tile arithmetic as the single-part solve
     const int level_tiles = T.lc[l] + T.ic[l];
-    launch_pass_direct(a, s, (level_tiles >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0));
+    launch_pass_direct(a, s, (level_tiles >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0) |
+                                 (h.lvl_ghost[l] ? 32 : 0));
   }
 }
 
@@ -1176,14 +1186,14 @@ octmg_status octmg_profile_enable(octmg_hier* hh, int32_t on) {
     h.events.clear();
     h.event_next = 0;
     for (int c = 0; c < KC_COUNT; ++c) { h.prof_ms[c] = 0.0; h.prof_cnt[c] = 0; h.prof_bytes[c] = 0.0; }
+    for (int l = 0; l <= MAXL; ++l)
+      for (int c = 0; c < KC_COUNT; ++c) { h.prof_lvl_ms[l][c] = 0.0; h.prof_lvl_cnt[l][c] = 0; h.prof_lvl_bytes[l][c] = 0.0; }
   }
   return OCTMG_OK;
 }
 
-octmg_status octmg_profile_read(octmg_hier* hh, const char** names, double* ms, int64_t* counts, double* bytes,
-                                int32_t cap, int32_t* n) {
-  if (!hh || !n) { set_error("null argument"); return OCTMG_E_INVALID; }
-  Hier& h = *hh->g.parts[0];
+namespace {
+octmg_status prof_collect(octmg::Hier& h) {
   OCTMG_CUDA(cudaDeviceSynchronize());
   for (auto& ev : h.events) {
     float t = 0.0f;
@@ -1191,9 +1201,38 @@ octmg_status octmg_profile_read(octmg_hier* hh, const char** names, double* ms, 
     h.prof_ms[ev.cls] += t;
     h.prof_cnt[ev.cls] += 1;
     h.prof_bytes[ev.cls] += ev.bytes;
+    if (ev.level >= 0 && ev.level <= octmg::MAXL) {
+      h.prof_lvl_ms[ev.level][ev.cls] += t;
+      h.prof_lvl_cnt[ev.level][ev.cls] += 1;
+      h.prof_lvl_bytes[ev.level][ev.cls] += ev.bytes;
+    }
   }
   h.events.clear();
   h.event_next = 0;
+  return OCTMG_OK;
+}
+}  // namespace
+
+octmg_status octmg_profile_read_level(octmg_hier* hh, int32_t level, double* ms, int64_t* counts, double* bytes,
+                                      int32_t cap, int32_t* n) {
+  if (!hh || !n || level < 0 || level > octmg::MAXL) { set_error("null argument or level out of range"); return OCTMG_E_INVALID; }
+  Hier& h = *hh->g.parts[0];
+  OCTMG_TRY(prof_collect(h));
+  int k = 0;
+  for (int c = 0; c < KC_COUNT && k < cap; ++c, ++k) {
+    if (ms) ms[k] = h.prof_lvl_ms[level][c];
+    if (counts) counts[k] = h.prof_lvl_cnt[level][c];
+    if (bytes) bytes[k] = h.prof_lvl_bytes[level][c];
+  }
+  *n = k;
+  return OCTMG_OK;
+}
+
+octmg_status octmg_profile_read(octmg_hier* hh, const char** names, double* ms, int64_t* counts, double* bytes,
+                                int32_t cap, int32_t* n) {
+  if (!hh || !n) { set_error("null argument"); return OCTMG_E_INVALID; }
+  Hier& h = *hh->g.parts[0];
+  OCTMG_TRY(prof_collect(h));
   int k = 0;
   for (int c = 0; c < KC_COUNT && k < cap; ++c, ++k) {
     if (names) names[k] = kclass_name[c];

@@ -416,14 +416,17 @@ __global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
 
 }  // namespace
 
-// OCTMG_PASS_GHOST=inline: k_pass_v3's ghost body inlined (80 registers, 12 CTAs/SM)
-static bool pass_ghost_inline() {
-  static int on = -1;
-  if (on < 0) {
+// k_pass_v3's ghost body: inlined (80 registers, 12 CTAs/SM) on levels with ghost tiles,
+// out of line (the regular path at 16 CTAs/SM) elsewhere; OCTMG_PASS_GHOST=inline / call
+// forces one form on every level (measured: inline 10.2 vs 11.3 ms of passes per config-3
+// solve; out of line 2.72 vs 3.15 ms on config 2, which has no ghost tile)
+static bool pass_ghost_inline(bool level_has_ghosts) {
+  static int mode = -1;
+  if (mode < 0) {
     const char* e = getenv("OCTMG_PASS_GHOST");
-    on = e && std::string(e) == "inline";
+    mode = !e ? 0 : (std::string(e) == "inline" ? 1 : (std::string(e) == "call" ? 2 : 0));
   }
-  return on == 1;
+  return mode == 1 || (mode == 0 && level_has_ghosts);
 }
 
 // OCTMG_PASS_V=2: the scalar k_pass_v2 on big levels instead of the 128-bit k_pass_v3
@@ -441,17 +444,17 @@ void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s) {
 }
 
 template <int CPT>
-static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool v2) {
+static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool v2, bool ghosts) {
   const int grid = a.n;
   if (CPT == 4 && v2 && pass_v3_enabled()) {  // 128-bit row form (CPT 4 = 64 threads per tile)
     switch (mode) {
       case SM_ZERO1: k_pass_v3<SM_ZERO1, false><<<grid, 64, 0, s>>>(a); break;
       case SM_ZERO2:
-        if (pass_ghost_inline()) k_pass_v3<SM_ZERO2, true><<<grid, 64, 0, s>>>(a);
+        if (pass_ghost_inline(ghosts)) k_pass_v3<SM_ZERO2, true><<<grid, 64, 0, s>>>(a);
         else k_pass_v3<SM_ZERO2, false><<<grid, 64, 0, s>>>(a);
         break;
       default:
-        if (pass_ghost_inline()) k_pass_v3<SM_PLAIN, true><<<grid, 64, 0, s>>>(a);
+        if (pass_ghost_inline(ghosts)) k_pass_v3<SM_PLAIN, true><<<grid, 64, 0, s>>>(a);
         else k_pass_v3<SM_PLAIN, false><<<grid, 64, 0, s>>>(a);
         break;
     }
@@ -475,10 +478,10 @@ static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool 
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt) {
   if (a.n == 0) return;
   const int mode = a.stage[0] >> 1;
-  const bool v2 = cpt & 16;
-  if ((cpt & 15) == 4) launch_pass_cpt<4>(a, mode, s, v2);
-  else if ((cpt & 15) == 2) launch_pass_cpt<2>(a, mode, s, v2);
-  else launch_pass_cpt<1>(a, mode, s, v2);
+  const bool v2 = cpt & 16, gh = cpt & 32;
+  if ((cpt & 15) == 4) launch_pass_cpt<4>(a, mode, s, v2, gh);
+  else if ((cpt & 15) == 2) launch_pass_cpt<2>(a, mode, s, v2, gh);
+  else launch_pass_cpt<1>(a, mode, s, v2, gh);
 }
 
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2) {

@@ -302,6 +302,7 @@ struct Hier {
   int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
+  bool lvl_ghost[MAXL + 1] = {};  // the level has T-junction (ghost) tiles (anywhere, all parts)
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
@@ -315,13 +316,16 @@ struct Hier {
   unsigned* bar = nullptr;       // its grid barrier counter
   // profiling
   bool profiling = false;
-  struct Ev { int cls; double bytes; cudaEvent_t a, b; };
+  struct Ev { int cls; double bytes; cudaEvent_t a, b; int level; };
   std::vector<Ev> events;
   std::vector<cudaEvent_t> event_pool;
   size_t event_next = 0;
   double prof_ms[KC_COUNT] = {};
   int64_t prof_cnt[KC_COUNT] = {};
   double prof_bytes[KC_COUNT] = {};
+  double prof_lvl_ms[MAXL + 1][KC_COUNT] = {};   // the same per level of the multigrid op
+  int64_t prof_lvl_cnt[MAXL + 1][KC_COUNT] = {};
+  double prof_lvl_bytes[MAXL + 1][KC_COUNT] = {};
   // partition (multi-part): this part's rank, owned ranges
   int rank = 0, nranks = 1;
   int lg = 0;                          // partition level (levels < lg replicated)

@@ -64,7 +64,7 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
                "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields",
                "octmg_divergence", "octmg_subtract_gradient",
-               "octmg_grade_repair_host", "octmg_set_allocator"]
+               "octmg_grade_repair_host", "octmg_set_allocator", "octmg_profile_read_level"]
 
 _lib = None
 
@@ -101,6 +101,8 @@ def lib():
         L.octmg_subtract_gradient.restype = C.c_int
         L.octmg_profile_enable.argtypes = [P, I32]
         L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
+        L.octmg_profile_read_level.argtypes = [P, I32, P, P, P, I32, C.POINTER(I32)]
+        L.octmg_profile_read_level.restype = C.c_int
         L.octmg_setup_hierarchy_loopback.argtypes = [P, I32, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
         L.octmg_partition_info.argtypes = [P, I32, P, P, P, P, P]
         L.octmg_nccl_unique_id.argtypes = [P]
@@ -321,6 +323,23 @@ class Hierarchy:
         _check(lib().octmg_profile_read(self._h, C.cast(names, C.c_void_p), C.cast(ms, C.c_void_p),
                                         C.cast(cnt, C.c_void_p), C.cast(byt, C.c_void_p), cap, C.byref(n)))
         return {names[k].decode(): dict(ms=ms[k], launches=int(cnt[k]), bytes=byt[k]) for k in range(n.value)}
+
+    def profile_read_levels(self, levels):
+        """{level: {class: dict(ms, launches, bytes)}} of the multigrid work per level."""
+        cap = 32
+        names = (C.c_char_p * cap)()
+        n = C.c_int32()
+        _check(lib().octmg_profile_read(self._h, C.cast(names, C.c_void_p), None, None, None, cap, C.byref(n)))
+        out = {}
+        for lv in levels:
+            ms = (C.c_double * cap)()
+            cnt = (C.c_int64 * cap)()
+            byt = (C.c_double * cap)()
+            _check(lib().octmg_profile_read_level(self._h, lv, C.cast(ms, C.c_void_p), C.cast(cnt, C.c_void_p),
+                                                  C.cast(byt, C.c_void_p), cap, C.byref(n)))
+            out[lv] = {names[k].decode(): dict(ms=ms[k], launches=int(cnt[k]), bytes=byt[k])
+                       for k in range(n.value) if cnt[k]}
+        return out
 
     def __del__(self):
         try:
