@@ -253,6 +253,14 @@ octmg_status build_schedule(Group& g) {
   for (Hier* p : g.parts) {
     OCTMG_TRY(build_orders(*p));
     read_env(*p);
+    // the on-chip sub-cycle levels as dense shared-memory grids when they are complete
+    // inner levels (coarse_dense.cu); otherwise the tile-layout k_subcycle
+    if (p->sub_K >= 0 && p->grid_K < 0 && p->c0n == 0) {
+      OCTMG_TRY(build_coarse_dense(*p, p->nranks > 1 ? p->lg - 1 : MAXL, nullptr));
+      OCTMG_CUDA(cudaDeviceSynchronize());
+      if (p->cd_K >= p->sub_K) p->sub_K = p->cd_K;
+      else p->cd_K = -1;
+    }
   }
   Hier& h = *g.parts[0];
   const Tree& T = *h.tree;
@@ -334,6 +342,11 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
                                        T.ic, h.bar, s);
     if (e != cudaSuccess) set_error(std::string("k_coarse_grid launch: ") + cudaGetErrorString(e));
+    return;
+  }
+  if (op.kind == 4 && h.cd_K >= 0) {
+    ProfScope ps(h, KC_SUBCYCLE, s, 0.0, op.level);
+    launch_coarse_dense(h, l, op.stage, h.uinA, h.binner, s);
     return;
   }
   if (op.kind == 4) {

@@ -1,0 +1,409 @@
+// The coarsest levels of the cycle as dense grids in shared memory (sm_100a).
+//
+// Below the coarsest leaf level every level of the tile octree is complete: level l is the
+// whole domain, an (8 ext_x 2^l) x (8 ext_y 2^l) x (8 ext_z 2^l) box of inner cells (the
+// leaves tile the domain, so each level-l tile has descendants and exists).  Their part of
+// Alg. 4 — pre-smoothing, residual + restriction + Avg, FAS rhs, the mu
+// recursive calls, the coarsest smoothing nu_b/2 x (R,B) + nu_b/2 x (B,R),
+// prolongation, post-smoothing — runs here in ONE CTA with every value in shared memory,
+// stored as a dense colour-split grid per level:
+//
+//   idx(x, y, z) = ((x + y + z) & 1) * n/2 + (z * ny + y) * nx/2 + (x >> 1),
+//
+// so a colour pass reads the other colour half at fixed offsets (x: -1 + p / +p, y: -+ nx/2,
+// z: -+ nx ny / 2, p = x & 1) and consecutive threads touch consecutive words (no bank
+// conflicts).  The coefficient records (c, c_x-, c_y-, c_z-) of these levels are converted
+// to the same dense layout once at setup (build_coarse_dense) and copied in per visit with
+// 128-bit loads; the +face coupling of a cell is its neighbour's -face entry.  The level-K
+// rhs b^K and iterate u^K = u* arrive in the tile layout (written by the level-(K+1)
+// restriction) and u^K (and b^K, which the first of the mu calls turns into the FAS rhs)
+// leave the same way.  Per-cell arithmetic as the tile kernels (face sums in the order x-,
+// x+, y-, y+, z-, z+ from 0, or from c u; block sums pair / y / z), so the replaced
+// k_subcycle and this kernel agree to rounding.
+//
+// A phase (one colour pass, a restriction half, ...) is a few shared-memory loads per cell
+// and one CTA barrier: ~0.1-0.3 us against the ~2 us of the global-memory sub-cycle, whose
+// phases are dependent L1/L2 round trips plus ~100 instructions of tile indexing per cell.
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "octmg_internal.cuh"
+
+namespace octmg {
+
+namespace {
+
+constexpr int CD_THREADS = 1024;
+
+struct CDLevel {
+  int nx, ny, nz;   // cells per axis
+  int n;            // nx * ny * nz
+  int off;          // first cell of the level in the concatenated dense arrays
+  int ntx, nty;     // tiles per axis (x, y)
+  const int* tmap;  // [ntz][nty][ntx] global tile index of each level tile
+};
+
+struct CDArgs {
+  CDLevel lv[CD_MAXL + 1];
+  int K;                 // top level (the cycle enters here)
+  int fas_first;         // form the FAS rhs of level K first
+  int mu, nu_pre, nu_post, nu_coarsest;
+  int std_form;          // Alg. 2: zero coarse guess, u* = 0, no FAS rhs, beta at prolongation
+  float alpha, beta, pro_scale;
+  const float* dcoef;    // dense coefficients: 4 planes per level, plane k of level l at 4 off_l + k n_l
+  // level-K fields in the tile layout (inner tiles): u (= u* on entry), b
+  float* u_inner;
+  float* b_inner;
+  int NL;
+  int total;             // cells of levels 0..K
+};
+
+// shared memory: coef[4 * total] | u[total] | b[total] | ustar[total] | scratch[n_K]
+struct CDMem {
+  float* coef;
+  float* u;
+  float* b;
+  float* us;
+  float* scr;
+};
+
+__device__ __forceinline__ int didx(const CDLevel& L, int x, int y, int z) {
+  return (((x + y + z) & 1) * (L.n >> 1)) + (z * L.ny + y) * (L.nx >> 1) + (x >> 1);
+}
+
+// coordinates of colour-c cell k of level L
+__device__ __forceinline__ void dcell(const CDLevel& L, int c, int k, int& x, int& y, int& z) {
+  const int hx = L.nx >> 1;
+  const int row = k / hx;
+  y = row % L.ny;
+  z = row / L.ny;
+  x = 2 * (k - row * hx) + ((c + y + z) & 1);
+}
+
+// 7-point face sum of cell (x, y, z) (dense index i) at level L starting from s0, in the
+// order x-, x+, y-, y+, z-, z+ (walls: value 0)
+__device__ __forceinline__ float dface_sum(const CDLevel& L, const CDMem& M, int x, int y, int z, int i, float s0) {
+  const int o = L.off;
+  const float* u = M.u + o;
+  const float* cx = M.coef + 4 * o + L.n;
+  const float* cy = cx + L.n;
+  const float* cz = cy + L.n;
+  const int hx = L.nx >> 1, hxy = hx * L.ny;
+  const int j = i < (L.n >> 1) ? i + (L.n >> 1) : i - (L.n >> 1);  // same (x>>1, y, z) in the other half
+  const int p = x & 1;
+  float s = s0;
+  // x-: cell x-1 at j - 1 + p; x+: x+1 at j + p
+  const bool xl = x > 0, xh = x < L.nx - 1, yl = y > 0, yh = y < L.ny - 1, zl = z > 0, zh = z < L.nz - 1;
+  s = fmaf(cx[i], xl ? u[j - 1 + p] : 0.0f, s);
+  s = fmaf(xh ? cx[j + p] : 0.0f, xh ? u[j + p] : 0.0f, s);
+  s = fmaf(cy[i], yl ? u[j - hx] : 0.0f, s);
+  s = fmaf(yh ? cy[j + hx] : 0.0f, yh ? u[j + hx] : 0.0f, s);
+  s = fmaf(cz[i], zl ? u[j - hxy] : 0.0f, s);
+  s = fmaf(zh ? cz[j + hxy] : 0.0f, zh ? u[j + hxy] : 0.0f, s);
+  return s;
+}
+
+// RBGS colour pass at level l, in place (reads only the other colour)
+__device__ __forceinline__ void cd_pass(const CDArgs& A, const CDMem& M, int l, int colour) {
+  const CDLevel& L = A.lv[l];
+  const int nh = L.n >> 1;
+  for (int k = threadIdx.x; k < nh; k += CD_THREADS) {
+    int x, y, z;
+    dcell(L, colour, k, x, y, z);
+    const int i = colour * nh + k;
+    const float c = M.coef[4 * L.off + i];
+    float v = 0.0f;
+    if (c != 0.0f) v = (M.b[L.off + i] - dface_sum(L, M, x, y, z, i, 0.0f)) / c;
+    M.u[L.off + i] = v;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cd_passes(const CDArgs& A, const CDMem& M, int l, int iters, bool red_first) {
+  for (int k = 0; k < iters; ++k) {
+    cd_pass(A, M, l, red_first ? 0 : 1);
+    cd_pass(A, M, l, red_first ? 1 : 0);
+  }
+}
+
+// residual r = b - A u (active cells) into scratch, then per parent: u* = mean of the active
+// children, u^{l-1} = u*, b^{l-1} = beta (R r) = beta sum(r) / alpha (Alg. 4 lines 8-10)
+__device__ __forceinline__ void cd_restrict(const CDArgs& A, const CDMem& M, int l) {
+  const CDLevel& L = A.lv[l];
+  const CDLevel& P = A.lv[l - 1];
+  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+    const int c = i >= (L.n >> 1);
+    int x, y, z;
+    dcell(L, c, i - c * (L.n >> 1), x, y, z);
+    const float cc = M.coef[4 * L.off + i];
+    const float u = M.u[L.off + i];
+    M.scr[i] = cc != 0.0f ? M.b[L.off + i] - dface_sum(L, M, x, y, z, i, cc * u) : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < P.n; i += CD_THREADS) {
+    const int c = i >= (P.n >> 1);
+    int X, Y, Z;
+    dcell(P, c, i - c * (P.n >> 1), X, Y, Z);
+    float rs[2][2], us[2][2];
+    int na = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        float r2 = 0.0f, u2 = 0.0f;
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const int ci = didx(L, 2 * X + dx, 2 * Y + dy, 2 * Z + dz);
+          const bool act = M.coef[4 * L.off + ci] != 0.0f;
+          const float uv = act ? M.u[L.off + ci] : 0.0f;
+          r2 = dx ? r2 + M.scr[ci] : M.scr[ci];
+          u2 = dx ? u2 + uv : uv;
+          na += act;
+        }
+        rs[dz][dy] = r2;
+        us[dz][dy] = u2;
+      }
+    const float rsum = (rs[0][0] + rs[0][1]) + (rs[1][0] + rs[1][1]);
+    const float usum = (us[0][0] + us[0][1]) + (us[1][0] + us[1][1]);
+    const float mP = na ? usum / (float)na : 0.0f;
+    M.u[P.off + i] = A.std_form ? 0.0f : mP;
+    M.us[P.off + i] = A.std_form ? 0.0f : mP;
+    M.b[P.off + i] = A.beta * (rsum / A.alpha);
+  }
+  __syncthreads();
+}
+
+// FAS rhs of level l: b += A^l u* (u holds u* here; Alg. 4 line 10)
+__device__ __forceinline__ void cd_fasrhs(const CDArgs& A, const CDMem& M, int l) {
+  const CDLevel& L = A.lv[l];
+  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+    const int c = i >= (L.n >> 1);
+    int x, y, z;
+    dcell(L, c, i - c * (L.n >> 1), x, y, z);
+    const float cc = M.coef[4 * L.off + i];
+    const float u = M.u[L.off + i];
+    // each thread reads and writes only its own b (the stencil reads u)
+    M.b[L.off + i] = cc != 0.0f ? M.b[L.off + i] + dface_sum(L, M, x, y, z, i, cc * u) : 0.0f;
+  }
+  __syncthreads();
+}
+
+// u^l += pro_scale (u^{l-1} - u*) on the active cells (Alg. 4 line 15)
+__device__ __forceinline__ void cd_prolong(const CDArgs& A, const CDMem& M, int l) {
+  const CDLevel& L = A.lv[l];
+  const CDLevel& P = A.lv[l - 1];
+  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+    if (M.coef[4 * L.off + i] == 0.0f) continue;
+    const int c = i >= (L.n >> 1);
+    int x, y, z;
+    dcell(L, c, i - c * (L.n >> 1), x, y, z);
+    const int pi = didx(P, x >> 1, y >> 1, z >> 1);
+    M.u[L.off + i] += A.pro_scale * (M.u[P.off + pi] - M.us[P.off + pi]);
+  }
+  __syncthreads();
+}
+
+// tile-layout cell of dense cell (x, y, z) of level L
+__device__ __forceinline__ size_t tile_cell(const CDLevel& L, int NL, int x, int y, int z) {
+  const int t = __ldg(L.tmap + ((z >> 3) * L.nty + (y >> 3)) * L.ntx + (x >> 3));
+  return (size_t)(t - NL) * TB3 + cslot(x & 7, y & 7, z & 7);
+}
+
+__global__ __launch_bounds__(CD_THREADS, 1) void k_coarse_dense(const __grid_constant__ CDArgs A) {
+  extern __shared__ __align__(16) float smem[];
+  CDMem M;
+  M.coef = smem;
+  M.u = M.coef + 4 * A.total;
+  M.b = M.u + A.total;
+  M.us = M.b + A.total;
+  M.scr = M.us + A.total;
+  // copy in: the dense coefficients of levels 0..K (128-bit), u^K and b^K from the tiles
+  {
+    const float4* src = reinterpret_cast<const float4*>(A.dcoef);
+    float4* dst = reinterpret_cast<float4*>(M.coef);
+    for (int i = threadIdx.x; i < A.total; i += CD_THREADS) dst[i] = __ldg(src + i);  // 4 * total floats
+    const CDLevel& L = A.lv[A.K];
+    for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+      const int c = i >= (L.n >> 1);
+      int x, y, z;
+      dcell(L, c, i - c * (L.n >> 1), x, y, z);
+      const size_t g = tile_cell(L, A.NL, x, y, z);
+      M.u[L.off + i] = A.u_inner[g];
+      M.b[L.off + i] = A.b_inner[g];
+    }
+  }
+  __syncthreads();
+  // Alg. 4 from level K down, iteratively (explicit per-level count of the mu coarse calls)
+  int done[CD_MAXL + 1];
+  int l = A.K;
+  bool ff = A.fas_first != 0;
+  bool entering = true;
+  while (true) {
+    if (entering) {
+      if (ff && !A.std_form) cd_fasrhs(A, M, l);
+      if (l == 0) {
+        const int h1 = A.nu_coarsest / 2;
+        cd_passes(A, M, 0, h1, true);
+        cd_passes(A, M, 0, A.nu_coarsest - h1, false);
+      } else {
+        cd_passes(A, M, l, A.nu_pre, true);
+        cd_restrict(A, M, l);
+        done[l] = 0;
+        l -= 1;
+        ff = true;
+        continue;
+      }
+      entering = false;
+    }
+    if (l == A.K) break;
+    const int p = l + 1;
+    if (++done[p] < A.mu) {  // the next coarse call starts from the previous one's u^l
+      l = p - 1;
+      ff = false;
+      entering = true;
+      continue;
+    }
+    cd_prolong(A, M, p);
+    cd_passes(A, M, p, A.nu_post, false);
+    l = p;
+  }
+  // copy out u^K and b^K (the FAS rhs persists across the mu calls from level K+1)
+  const CDLevel& L = A.lv[A.K];
+  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+    const int c = i >= (L.n >> 1);
+    int x, y, z;
+    dcell(L, c, i - c * (L.n >> 1), x, y, z);
+    const size_t g = tile_cell(L, A.NL, x, y, z);
+    A.u_inner[g] = M.u[L.off + i];
+    if (A.fas_first) A.b_inner[g] = M.b[L.off + i];
+  }
+}
+
+// setup: tile-layout coefficient records -> the dense colour-split planes of level l
+__global__ void k_dense_coef(const float* coef, CDLevel L, int NL, float* dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n) return;
+  const int c = i >= (L.n >> 1);
+  int x, y, z;
+  dcell(L, c, i - c * (L.n >> 1), x, y, z);
+  const int t = L.tmap[((z >> 3) * L.nty + (y >> 3)) * L.ntx + (x >> 3)];
+  const float* p = coef + ((size_t)t << 11) + cslot(x & 7, y & 7, z & 7);
+  for (int k = 0; k < 4; ++k) dst[(size_t)k * L.n + i] = p[k * 512];
+}
+
+}  // namespace
+
+size_t coarse_dense_smem(int total_cells, int nK) { return sizeof(float) * ((size_t)7 * total_cells + nK); }
+
+// Levels 0..K as dense grids if every tile of those levels is an inner tile (K below the
+// coarsest leaf level) and their fields fit the shared memory of one CTA.  Returns K, or -1.
+octmg_status build_coarse_dense(Hier& h, int Kmax, cudaStream_t s) {
+  const Tree& T = *h.tree;
+  h.cd_K = -1;
+  if (getenv("OCTMG_COARSE_DENSE") && std::string(getenv("OCTMG_COARSE_DENSE")) == "0") return OCTMG_OK;
+  int lmin = T.L;
+  for (int l = 0; l <= T.L; ++l)
+    if (T.lc[l] > 0) { lmin = l; break; }
+  int dev = 0, smem_optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int K = -1, total = 0;
+  for (int l = 0; l <= std::min({Kmax, lmin - 1, CD_MAXL}); ++l) {
+    const int n = T.ic[l] * TB3;
+    const int expect = T.ext[0] * T.ext[1] * T.ext[2] * (1 << (3 * l)) * TB3;
+    if (n != expect) break;  // not a complete level
+    if (coarse_dense_smem(total + n, n) > (size_t)smem_optin) break;
+    total += n;
+    K = l;
+  }
+  if (K < 0) return OCTMG_OK;
+  // tile maps (host) from the tile table
+  std::vector<int4> tile(T.T);
+  OCTMG_CUDA(cudaMemcpy(tile.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
+  std::vector<int> maps;
+  std::vector<int> moff(K + 1);
+  for (int l = 0; l <= K; ++l) {
+    const int ntx = T.ext[0] << l, nty = T.ext[1] << l, ntz = T.ext[2] << l;
+    moff[l] = (int)maps.size();
+    maps.resize(maps.size() + (size_t)ntx * nty * ntz, -1);
+    for (int t = T.ib[l]; t < T.ib[l] + T.ic[l]; ++t) {  // ib: global tile index of the level's first inner tile
+      const int4 v = tile[t];
+      if (v.x != l || v.y < 0 || v.y >= ntx || v.z < 0 || v.z >= nty || v.w < 0 || v.w >= ntz) return OCTMG_OK;
+      maps[moff[l] + ((size_t)v.w * nty + v.z) * ntx + v.y] = t;
+    }
+  }
+  for (int v : maps)
+    if (v < 0) return OCTMG_OK;  // (cannot happen for a complete level)
+  int* dmap = (int*)dev_malloc(sizeof(int) * maps.size());
+  float* dcoef = (float*)dev_malloc(sizeof(float) * 4 * (size_t)total);
+  if (!dmap || !dcoef) {
+    set_error("device allocation failed (dense coarse levels)");
+    return OCTMG_E_OOM;
+  }
+  h.allocs.push_back(dmap);
+  h.allocs.push_back(dcoef);
+  OCTMG_CUDA(cudaMemcpy(dmap, maps.data(), sizeof(int) * maps.size(), cudaMemcpyHostToDevice));
+  int off = 0;
+  for (int l = 0; l <= K; ++l) {
+    CDLevel L;
+    L.nx = T.ext[0] * 8 << l;
+    L.ny = T.ext[1] * 8 << l;
+    L.nz = T.ext[2] * 8 << l;
+    L.n = L.nx * L.ny * L.nz;
+    L.off = off;
+    L.ntx = T.ext[0] << l;
+    L.nty = T.ext[1] << l;
+    L.tmap = dmap + moff[l];
+    k_dense_coef<<<(L.n + 255) / 256, 256, 0, s>>>(h.coef, L, T.NL, dcoef + 4 * (size_t)off);
+    h.cd_lv[l][0] = L.nx; h.cd_lv[l][1] = L.ny; h.cd_lv[l][2] = L.nz; h.cd_lv[l][3] = off;
+    off += L.n;
+  }
+  OCTMG_CUDA(cudaGetLastError());
+  const size_t smem = coarse_dense_smem(total, T.ic[K] * TB3);
+  OCTMG_CUDA(cudaFuncSetAttribute(k_coarse_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  h.cd_K = K;
+  h.cd_total = total;
+  h.cd_map = dmap;
+  h.cd_moff = moff;
+  h.cd_coef = dcoef;
+  return OCTMG_OK;
+}
+
+void launch_coarse_dense(const Hier& h, int K, int fas_first, float* u_inner, float* b_inner, cudaStream_t s) {
+  const Tree& T = *h.tree;
+  CDArgs A;
+  for (int l = 0; l <= CD_MAXL; ++l) {
+    CDLevel& L = A.lv[l];
+    if (l <= K) {
+      L.nx = h.cd_lv[l][0]; L.ny = h.cd_lv[l][1]; L.nz = h.cd_lv[l][2];
+      L.n = L.nx * L.ny * L.nz;
+      L.off = h.cd_lv[l][3];
+      L.ntx = T.ext[0] << l;
+      L.nty = T.ext[1] << l;
+      L.tmap = h.cd_map + h.cd_moff[l];
+    } else {
+      L = CDLevel{0, 0, 0, 0, 0, 0, 0, nullptr};
+    }
+  }
+  A.K = K;
+  A.fas_first = fas_first;
+  A.mu = h.prm.mu;
+  A.nu_pre = h.prm.nu_pre;
+  A.nu_post = h.prm.nu_post;
+  A.nu_coarsest = h.prm.nu_coarsest;
+  A.std_form = h.prm.form == 1;
+  A.alpha = h.prm.alpha;
+  A.beta = A.std_form ? 1.0f : h.prm.beta_overshoot;
+  A.pro_scale = A.std_form ? h.prm.beta_overshoot : 1.0f;
+  A.dcoef = h.cd_coef;
+  A.u_inner = u_inner;
+  A.b_inner = b_inner;
+  A.NL = T.NL;
+  int total = 0;
+  for (int l = 0; l <= K; ++l) total += A.lv[l].n;
+  A.total = total;
+  k_coarse_dense<<<1, CD_THREADS, coarse_dense_smem(total, A.lv[K].n), s>>>(A);
+}
+
+}  // namespace octmg

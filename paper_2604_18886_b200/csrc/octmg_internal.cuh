@@ -231,6 +231,11 @@ void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const 
                      const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
                      int ctas, cudaStream_t s);
 
+// the coarsest complete levels as dense grids in shared memory (coarse_dense.cu)
+constexpr int CD_MAXL = 3;
+octmg_status build_coarse_dense(Hier& h, int Kmax, cudaStream_t s);  // sets h.cd_K (-1: not applicable)
+void launch_coarse_dense(const Hier& h, int K, int fas_first, float* u_inner, float* b_inner, cudaStream_t s);
+
 // direct coarsest solve (coarsest.cu)
 constexpr int C0_MAX_CELLS = 4096;
 octmg_status build_coarse_direct(Hier& h, cudaStream_t s);  // M0 of level 0 (setup)
@@ -308,6 +313,12 @@ struct Hier {
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
   int restrict_v2 = 6;           // k_restrict_v2 (vectorised regular tiles) at >= 6 (8: OCTMG_RESTRICT_V=8) CTAs/SM; 0: staged k_restrict_direct (OCTMG_RESTRICT_V=1)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
+  int cd_K = -1;                 // top level of the dense shared-memory coarse cycle (coarse_dense.cu; -1: none)
+  int cd_total = 0;              // its cells (levels 0..cd_K)
+  int cd_lv[CD_MAXL + 1][4] = {};  // per level: nx, ny, nz, first cell
+  int* cd_map = nullptr;         // tile maps of those levels
+  std::vector<int> cd_moff;      // per level: offset of its tile map
+  float* cd_coef = nullptr;      // dense coefficient planes
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
   float* c0M = nullptr;          // direct coarsest solve: M0 [c0n][c0n] (coarsest = 1)
