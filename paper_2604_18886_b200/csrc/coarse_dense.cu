@@ -34,11 +34,12 @@ namespace octmg {
 
 namespace {
 
-constexpr int CD_THREADS = 1024;
+
 
 struct CDLevel {
   int nx, ny, nz;   // cells per axis
   int n;            // nx * ny * nz
+  int shx, shy;     // log2(nx / 2), log2(ny) when powers of two, else -1 (division)
   int off;          // first cell of the level in the concatenated dense arrays
   int ntx, nty;     // tiles per axis (x, y)
   const int* tmap;  // [ntz][nty][ntx] global tile index of each level tile
@@ -51,15 +52,19 @@ struct CDArgs {
   int mu, nu_pre, nu_post, nu_coarsest;
   int std_form;          // Alg. 2: zero coarse guess, u* = 0, no FAS rhs, beta at prolongation
   float alpha, beta, pro_scale;
-  const float* dcoef;    // dense coefficients: 4 planes per level, plane k of level l at 4 off_l + k n_l
+  const float* dcoef;    // dense coefficients: NP planes per level (c, c_x-, c_y-, c_z-, 1/c or 0), plane k of level l at NP off_l + k n_l
   // level-K fields in the tile layout (inner tiles): u (= u* on entry), b
   float* u_inner;
   float* b_inner;
+  const int4* tile;      // tile table; level K's inner tiles are tK0 .. tK0 + n_K/512 - 1
+  int tK0;
   int NL;
   int total;             // cells of levels 0..K
 };
 
-// shared memory: coef[4 * total] | u[total] | b[total] | ustar[total] | scratch[n_K]
+constexpr int NP = 5;  // coefficient planes per level: c, c_x-, c_y-, c_z-, 1/c (0 where inactive)
+
+// shared memory: coef[NP * total] | u[total] | b[total] | ustar[total] | scratch[n_K]
 struct CDMem {
   float* coef;
   float* u;
@@ -75,9 +80,16 @@ __device__ __forceinline__ int didx(const CDLevel& L, int x, int y, int z) {
 // coordinates of colour-c cell k of level L
 __device__ __forceinline__ void dcell(const CDLevel& L, int c, int k, int& x, int& y, int& z) {
   const int hx = L.nx >> 1;
-  const int row = k / hx;
-  y = row % L.ny;
-  z = row / L.ny;
+  int row;
+  if (L.shx >= 0 && L.shy >= 0) {
+    row = k >> L.shx;
+    y = row & (L.ny - 1);
+    z = row >> L.shy;
+  } else {
+    row = k / hx;
+    y = row % L.ny;
+    z = row / L.ny;
+  }
   x = 2 * (k - row * hx) + ((c + y + z) & 1);
 }
 
@@ -86,7 +98,7 @@ __device__ __forceinline__ void dcell(const CDLevel& L, int c, int k, int& x, in
 __device__ __forceinline__ float dface_sum(const CDLevel& L, const CDMem& M, int x, int y, int z, int i, float s0) {
   const int o = L.off;
   const float* u = M.u + o;
-  const float* cx = M.coef + 4 * o + L.n;
+  const float* cx = M.coef + NP * o + L.n;
   const float* cy = cx + L.n;
   const float* cz = cy + L.n;
   const int hx = L.nx >> 1, hxy = hx * L.ny;
@@ -105,43 +117,45 @@ __device__ __forceinline__ float dface_sum(const CDLevel& L, const CDMem& M, int
 }
 
 // RBGS colour pass at level l, in place (reads only the other colour)
+template <int NT>
 __device__ __forceinline__ void cd_pass(const CDArgs& A, const CDMem& M, int l, int colour) {
   const CDLevel& L = A.lv[l];
   const int nh = L.n >> 1;
-  for (int k = threadIdx.x; k < nh; k += CD_THREADS) {
+#pragma unroll 4
+  for (int k = threadIdx.x; k < nh; k += NT) {
     int x, y, z;
     dcell(L, colour, k, x, y, z);
     const int i = colour * nh + k;
-    const float c = M.coef[4 * L.off + i];
-    float v = 0.0f;
-    if (c != 0.0f) v = (M.b[L.off + i] - dface_sum(L, M, x, y, z, i, 0.0f)) / c;
-    M.u[L.off + i] = v;
+    // u = (b - sum) / c with the precomputed 1/c (0 on inactive cells: u = 0 there)
+    M.u[L.off + i] = (M.b[L.off + i] - dface_sum(L, M, x, y, z, i, 0.0f)) * M.coef[NP * L.off + 4 * L.n + i];
   }
   __syncthreads();
 }
 
+template <int NT>
 __device__ __forceinline__ void cd_passes(const CDArgs& A, const CDMem& M, int l, int iters, bool red_first) {
   for (int k = 0; k < iters; ++k) {
-    cd_pass(A, M, l, red_first ? 0 : 1);
-    cd_pass(A, M, l, red_first ? 1 : 0);
+    cd_pass<NT>(A, M, l, red_first ? 0 : 1);
+    cd_pass<NT>(A, M, l, red_first ? 1 : 0);
   }
 }
 
 // residual r = b - A u (active cells) into scratch, then per parent: u* = mean of the active
 // children, u^{l-1} = u*, b^{l-1} = beta (R r) = beta sum(r) / alpha (Alg. 4 lines 8-10)
+template <int NT>
 __device__ __forceinline__ void cd_restrict(const CDArgs& A, const CDMem& M, int l) {
   const CDLevel& L = A.lv[l];
   const CDLevel& P = A.lv[l - 1];
-  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+  for (int i = threadIdx.x; i < L.n; i += NT) {
     const int c = i >= (L.n >> 1);
     int x, y, z;
     dcell(L, c, i - c * (L.n >> 1), x, y, z);
-    const float cc = M.coef[4 * L.off + i];
+    const float cc = M.coef[NP * L.off + i];
     const float u = M.u[L.off + i];
     M.scr[i] = cc != 0.0f ? M.b[L.off + i] - dface_sum(L, M, x, y, z, i, cc * u) : 0.0f;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < P.n; i += CD_THREADS) {
+  for (int i = threadIdx.x; i < P.n; i += NT) {
     const int c = i >= (P.n >> 1);
     int X, Y, Z;
     dcell(P, c, i - c * (P.n >> 1), X, Y, Z);
@@ -155,7 +169,7 @@ __device__ __forceinline__ void cd_restrict(const CDArgs& A, const CDMem& M, int
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
           const int ci = didx(L, 2 * X + dx, 2 * Y + dy, 2 * Z + dz);
-          const bool act = M.coef[4 * L.off + ci] != 0.0f;
+          const bool act = M.coef[NP * L.off + ci] != 0.0f;
           const float uv = act ? M.u[L.off + ci] : 0.0f;
           r2 = dx ? r2 + M.scr[ci] : M.scr[ci];
           u2 = dx ? u2 + uv : uv;
@@ -175,13 +189,14 @@ __device__ __forceinline__ void cd_restrict(const CDArgs& A, const CDMem& M, int
 }
 
 // FAS rhs of level l: b += A^l u* (u holds u* here; Alg. 4 line 10)
+template <int NT>
 __device__ __forceinline__ void cd_fasrhs(const CDArgs& A, const CDMem& M, int l) {
   const CDLevel& L = A.lv[l];
-  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
+  for (int i = threadIdx.x; i < L.n; i += NT) {
     const int c = i >= (L.n >> 1);
     int x, y, z;
     dcell(L, c, i - c * (L.n >> 1), x, y, z);
-    const float cc = M.coef[4 * L.off + i];
+    const float cc = M.coef[NP * L.off + i];
     const float u = M.u[L.off + i];
     // each thread reads and writes only its own b (the stencil reads u)
     M.b[L.off + i] = cc != 0.0f ? M.b[L.off + i] + dface_sum(L, M, x, y, z, i, cc * u) : 0.0f;
@@ -190,11 +205,12 @@ __device__ __forceinline__ void cd_fasrhs(const CDArgs& A, const CDMem& M, int l
 }
 
 // u^l += pro_scale (u^{l-1} - u*) on the active cells (Alg. 4 line 15)
+template <int NT>
 __device__ __forceinline__ void cd_prolong(const CDArgs& A, const CDMem& M, int l) {
   const CDLevel& L = A.lv[l];
   const CDLevel& P = A.lv[l - 1];
-  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
-    if (M.coef[4 * L.off + i] == 0.0f) continue;
+  for (int i = threadIdx.x; i < L.n; i += NT) {
+    if (M.coef[NP * L.off + i] == 0.0f) continue;
     const int c = i >= (L.n >> 1);
     int x, y, z;
     dcell(L, c, i - c * (L.n >> 1), x, y, z);
@@ -204,33 +220,53 @@ __device__ __forceinline__ void cd_prolong(const CDArgs& A, const CDMem& M, int 
   __syncthreads();
 }
 
-// tile-layout cell of dense cell (x, y, z) of level L
-__device__ __forceinline__ size_t tile_cell(const CDLevel& L, int NL, int x, int y, int z) {
-  const int t = __ldg(L.tmap + ((z >> 3) * L.nty + (y >> 3)) * L.ntx + (x >> 3));
-  return (size_t)(t - NL) * TB3 + cslot(x & 7, y & 7, z & 7);
-}
-
-__global__ __launch_bounds__(CD_THREADS, 1) void k_coarse_dense(const __grid_constant__ CDArgs A) {
+template <int NT>
+__global__ __launch_bounds__(NT, 1) void k_coarse_dense(const __grid_constant__ CDArgs A) {
   extern __shared__ __align__(16) float smem[];
   CDMem M;
   M.coef = smem;
-  M.u = M.coef + 4 * A.total;
+  M.u = M.coef + NP * A.total;
   M.b = M.u + A.total;
   M.us = M.b + A.total;
   M.scr = M.us + A.total;
-  // copy in: the dense coefficients of levels 0..K (128-bit), u^K and b^K from the tiles
+  // copy in: the dense coefficients of levels 0..K (128-bit, 8 loads in flight per thread),
+  // u^K and b^K from the level-K tiles (global inner tiles tK0.., coalesced slot runs)
   {
     const float4* src = reinterpret_cast<const float4*>(A.dcoef);
     float4* dst = reinterpret_cast<float4*>(M.coef);
-    for (int i = threadIdx.x; i < A.total; i += CD_THREADS) dst[i] = __ldg(src + i);  // 4 * total floats
+    const int nv = NP * A.total / 4;
+    for (int i0 = threadIdx.x; i0 < nv; i0 += 8 * NT) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k * NT < nv) v[k] = __ldg(src + i0 + k * NT);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k * NT < nv) dst[i0 + k * NT] = v[k];
+    }
     const CDLevel& L = A.lv[A.K];
-    for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
-      const int c = i >= (L.n >> 1);
-      int x, y, z;
-      dcell(L, c, i - c * (L.n >> 1), x, y, z);
-      const size_t g = tile_cell(L, A.NL, x, y, z);
-      M.u[L.off + i] = A.u_inner[g];
-      M.b[L.off + i] = A.b_inner[g];
+    for (int g0 = threadIdx.x; g0 < L.n; g0 += 4 * NT) {
+      float uv[4], bv[4];
+      int di[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int g = g0 + k * NT;
+        if (g >= L.n) break;
+        const int t = A.tK0 + (g >> 9), sl = g & 511;
+        const int4 tv = __ldg(A.tile + t);
+        int x, y, z;
+        slot_xyz(sl, x, y, z);
+        di[k] = didx(L, tv.y * 8 + x, tv.z * 8 + y, tv.w * 8 + z);
+        const size_t gi = (size_t)(t - A.NL) * TB3 + sl;
+        uv[k] = A.u_inner[gi];
+        bv[k] = A.b_inner[gi];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (g0 + k * NT >= L.n) break;
+        M.u[L.off + di[k]] = uv[k];
+        M.b[L.off + di[k]] = bv[k];
+      }
     }
   }
   __syncthreads();
@@ -241,14 +277,14 @@ __global__ __launch_bounds__(CD_THREADS, 1) void k_coarse_dense(const __grid_con
   bool entering = true;
   while (true) {
     if (entering) {
-      if (ff && !A.std_form) cd_fasrhs(A, M, l);
+      if (ff && !A.std_form) cd_fasrhs<NT>(A, M, l);
       if (l == 0) {
         const int h1 = A.nu_coarsest / 2;
-        cd_passes(A, M, 0, h1, true);
-        cd_passes(A, M, 0, A.nu_coarsest - h1, false);
+        cd_passes<NT>(A, M, 0, h1, true);
+        cd_passes<NT>(A, M, 0, A.nu_coarsest - h1, false);
       } else {
-        cd_passes(A, M, l, A.nu_pre, true);
-        cd_restrict(A, M, l);
+        cd_passes<NT>(A, M, l, A.nu_pre, true);
+        cd_restrict<NT>(A, M, l);
         done[l] = 0;
         l -= 1;
         ff = true;
@@ -264,19 +300,21 @@ __global__ __launch_bounds__(CD_THREADS, 1) void k_coarse_dense(const __grid_con
       entering = true;
       continue;
     }
-    cd_prolong(A, M, p);
-    cd_passes(A, M, p, A.nu_post, false);
+    cd_prolong<NT>(A, M, p);
+    cd_passes<NT>(A, M, p, A.nu_post, false);
     l = p;
   }
   // copy out u^K and b^K (the FAS rhs persists across the mu calls from level K+1)
   const CDLevel& L = A.lv[A.K];
-  for (int i = threadIdx.x; i < L.n; i += CD_THREADS) {
-    const int c = i >= (L.n >> 1);
+  for (int g = threadIdx.x; g < L.n; g += NT) {
+    const int t = A.tK0 + (g >> 9), sl = g & 511;
+    const int4 tv = __ldg(A.tile + t);
     int x, y, z;
-    dcell(L, c, i - c * (L.n >> 1), x, y, z);
-    const size_t g = tile_cell(L, A.NL, x, y, z);
-    A.u_inner[g] = M.u[L.off + i];
-    if (A.fas_first) A.b_inner[g] = M.b[L.off + i];
+    slot_xyz(sl, x, y, z);
+    const int di = didx(L, tv.y * 8 + x, tv.z * 8 + y, tv.w * 8 + z);
+    const size_t gi = (size_t)(t - A.NL) * TB3 + sl;
+    A.u_inner[gi] = M.u[L.off + di];
+    if (A.fas_first) A.b_inner[gi] = M.b[L.off + di];
   }
 }
 
@@ -290,11 +328,18 @@ __global__ void k_dense_coef(const float* coef, CDLevel L, int NL, float* dst) {
   const int t = L.tmap[((z >> 3) * L.nty + (y >> 3)) * L.ntx + (x >> 3)];
   const float* p = coef + ((size_t)t << 11) + cslot(x & 7, y & 7, z & 7);
   for (int k = 0; k < 4; ++k) dst[(size_t)k * L.n + i] = p[k * 512];
+  dst[(size_t)4 * L.n + i] = p[0] != 0.0f ? 1.0f / p[0] : 0.0f;
+}
+
+int shift_of(int v) {  // log2(v) for a power of two, else -1
+  for (int k = 0; k < 31; ++k)
+    if (v == (1 << k)) return k;
+  return -1;
 }
 
 }  // namespace
 
-size_t coarse_dense_smem(int total_cells, int nK) { return sizeof(float) * ((size_t)7 * total_cells + nK); }
+size_t coarse_dense_smem(int total_cells, int nK) { return sizeof(float) * ((size_t)(NP + 3) * total_cells + nK); }
 
 // Levels 0..K as dense grids if every tile of those levels is an inner tile (K below the
 // coarsest leaf level) and their fields fit the shared memory of one CTA.  Returns K, or -1.
@@ -336,7 +381,7 @@ octmg_status build_coarse_dense(Hier& h, int Kmax, cudaStream_t s) {
   for (int v : maps)
     if (v < 0) return OCTMG_OK;  // (cannot happen for a complete level)
   int* dmap = (int*)dev_malloc(sizeof(int) * maps.size());
-  float* dcoef = (float*)dev_malloc(sizeof(float) * 4 * (size_t)total);
+  float* dcoef = (float*)dev_malloc(sizeof(float) * NP * (size_t)total);
   if (!dmap || !dcoef) {
     set_error("device allocation failed (dense coarse levels)");
     return OCTMG_E_OOM;
@@ -355,13 +400,19 @@ octmg_status build_coarse_dense(Hier& h, int Kmax, cudaStream_t s) {
     L.ntx = T.ext[0] << l;
     L.nty = T.ext[1] << l;
     L.tmap = dmap + moff[l];
-    k_dense_coef<<<(L.n + 255) / 256, 256, 0, s>>>(h.coef, L, T.NL, dcoef + 4 * (size_t)off);
+    L.shx = shift_of(L.nx >> 1);
+    L.shy = shift_of(L.ny);
+    k_dense_coef<<<(L.n + 255) / 256, 256, 0, s>>>(h.coef, L, T.NL, dcoef + NP * (size_t)off);
     h.cd_lv[l][0] = L.nx; h.cd_lv[l][1] = L.ny; h.cd_lv[l][2] = L.nz; h.cd_lv[l][3] = off;
     off += L.n;
   }
   OCTMG_CUDA(cudaGetLastError());
   const size_t smem = coarse_dense_smem(total, T.ic[K] * TB3);
-  OCTMG_CUDA(cudaFuncSetAttribute(k_coarse_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  OCTMG_CUDA(cudaFuncSetAttribute(k_coarse_dense<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  OCTMG_CUDA(cudaFuncSetAttribute(k_coarse_dense<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  OCTMG_CUDA(cudaFuncSetAttribute(k_coarse_dense<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const char* ct = getenv("OCTMG_CD_THREADS");  // threads of the dense coarse CTA (256 / 512 / 1024)
+  h.cd_threads = ct ? atoi(ct) : 512;
   h.cd_K = K;
   h.cd_total = total;
   h.cd_map = dmap;
@@ -382,8 +433,10 @@ void launch_coarse_dense(const Hier& h, int K, int fas_first, float* u_inner, fl
       L.ntx = T.ext[0] << l;
       L.nty = T.ext[1] << l;
       L.tmap = h.cd_map + h.cd_moff[l];
+      L.shx = shift_of(L.nx >> 1);
+      L.shy = shift_of(L.ny);
     } else {
-      L = CDLevel{0, 0, 0, 0, 0, 0, 0, nullptr};
+      L = CDLevel{0, 0, 0, 0, -1, -1, 0, 0, 0, nullptr};
     }
   }
   A.K = K;
@@ -399,11 +452,18 @@ void launch_coarse_dense(const Hier& h, int K, int fas_first, float* u_inner, fl
   A.dcoef = h.cd_coef;
   A.u_inner = u_inner;
   A.b_inner = b_inner;
+  A.tile = T.tile;
+  A.tK0 = T.ib[K];
   A.NL = T.NL;
   int total = 0;
   for (int l = 0; l <= K; ++l) total += A.lv[l].n;
   A.total = total;
-  k_coarse_dense<<<1, CD_THREADS, coarse_dense_smem(total, A.lv[K].n), s>>>(A);
+  const size_t sm = coarse_dense_smem(total, A.lv[K].n);
+  switch (h.cd_threads) {
+    case 256: k_coarse_dense<256><<<1, 256, sm, s>>>(A); break;
+    case 512: k_coarse_dense<512><<<1, 512, sm, s>>>(A); break;
+    default: k_coarse_dense<1024><<<1, 1024, sm, s>>>(A); break;
+  }
 }
 
 }  // namespace octmg

@@ -319,6 +319,7 @@ struct Hier {
   int* cd_map = nullptr;         // tile maps of those levels
   std::vector<int> cd_moff;      // per level: offset of its tile map
   float* cd_coef = nullptr;      // dense coefficient planes
+  int cd_threads = 512;          // threads of its CTA
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
   float* c0M = nullptr;          // direct coarsest solve: M0 [c0n][c0n] (coarsest = 1)
