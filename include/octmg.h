@@ -133,11 +133,13 @@ typedef struct {
                            DESIGN.md reading 9b).  Needs <= 4096 level-0 cells (ext product
                            <= 8), else OCTMG_E_INVALID                                       */
   int32_t reserved0;
-  int64_t gather_below_cells; /* multi-GPU: levels whose total cell count is
-                           below this are not partitioned — every rank holds and smooths
-                           them redundantly after an all-gather of the restricted partition
-                           parents (0 = the default threshold, 2^21 cells; single part:
-                           ignored)                                                          */
+  int64_t gather_below_cells; /* multi-GPU: the partition level lg is the
+                           coarsest level (<= the coarsest leaf level) with >= 8 tiles per
+                           rank and >= gather_below_cells cells; the levels below it are not
+                           partitioned — every rank holds and smooths them redundantly after
+                           an all-gather of the restricted partition parents (0 = the default
+                           threshold, 2^21 cells; 1 = partition as deep as 8 tiles per rank
+                           allow; single part: ignored)                                      */
 } octmg_mg_params;
 
 /*
@@ -187,12 +189,13 @@ void octmg_nccl_comm_destroy(void* comm);
  * leaf_count, inner_begin, inner_count), the partition level lg, the owner rank of every
  * tile (-1 = replicated, level < lg) and the halo item lists: n_items_out[(l*nranks +
  * from)*nranks + to] items of (tile, kind) pairs concatenated in that order into items_out
- * (kind 0..5 = face layer of that face, 6 = whole tile).  items_cap = max item count. */
+ * (kind 0..5 = face layer of that face, 6 = whole tile).  items_cap = max item count.
+ * gather_below_cells: as octmg_mg_params.gather_below_cells (0 = the default threshold). */
 octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr, const int32_t* parent,
                                        const int32_t* child, int32_t NL, int32_t NI, int32_t L,
                                        const int32_t* level_counts, int32_t nranks, int32_t* lg_out,
                                        int32_t* owner_out, int32_t* n_items_out, int32_t* items_out,
-                                       int64_t items_cap);
+                                       int64_t items_cap, int64_t gather_below_cells);
 
 /*
  * Cut-cell fields of the static tank scene: a solid sphere
@@ -295,15 +298,18 @@ typedef struct {
   int64_t kernel_launches; /* device kernels launched by this solve (graph nodes counted) */
   int32_t history_len;  /* entries of history written: min(iters, history_cap), and at most
                            512 in the device-side loop                                    */
+  int32_t device_loop;  /* 1: the solve ran as the device-side conditional-graph loop;
+                           0: the host-driven loop                                        */
 } octmg_solve_report;
 
 /*
  * Alg. 1: x0 = 0, r0 = b (masked to active cells, projected if nullspace),
- * z = M r, CG recurrences with fp64 scalars kept on the device.  Single-part hierarchies
- * run the whole loop as ONE CUDA graph with a conditional while node whose stopping test
- * (Alg. 1 line 8) runs on the device: one host synchronisation per solve (environment
- * OCTMG_GRAPH_LOOP=0, profiling, or a driver without conditional nodes: the host-driven
- * loop, one 8-byte scalar read per iteration; partitioned hierarchies also use it).
+ * z = M r, CG recurrences with fp64 scalars kept on the device.  The whole loop runs as
+ * ONE CUDA graph with a conditional while node whose stopping test (Alg. 1 line 8) runs on
+ * the device: one host synchronisation per solve; a partitioned hierarchy captures its
+ * transport's halo exchanges and fp64 scalar allreduces into the same body.  Environment
+ * OCTMG_GRAPH_LOOP=0, profiling, or a transport / driver that cannot be captured: the
+ * host-driven loop (the same kernels, one scalar read per iteration).
  * b (read-only) and x (overwritten) are device f32[N].  Synchronises `stream` before
  * returning.  report may be NULL.
  */

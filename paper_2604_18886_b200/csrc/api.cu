@@ -671,7 +671,7 @@ octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void
     PartInput in;
     octmg_status st = plan_input(tree->t, in);
     if (st) return fail(st);
-    const int lg = choose_partition_level(in, nranks);
+    const int lg = choose_partition_level(in, nranks, prm.gather_below_cells);
     if (lg == 0 && prm.coarsest == 1) {
       set_error("direct coarsest solve needs a replicated level 0 (partition level >= 1)");
       return fail(OCTMG_E_INVALID);
@@ -759,7 +759,7 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
                                        const int32_t* child, int32_t NL, int32_t NI, int32_t L,
                                        const int32_t* level_counts, int32_t nranks, int32_t* lg_out,
                                        int32_t* owner_out, int32_t* n_items_out, int32_t* items_out,
-                                       int64_t items_cap) {
+                                       int64_t items_cap, int64_t gather_below_cells) {
   if (!tiles4 || !nbr || !parent || !level_counts || !lg_out || !owner_out || !n_items_out || nranks < 1 ||
       L < 0 || L > MAXL) {
     set_error("bad argument");
@@ -782,7 +782,8 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
   in.morton.resize(T);
   for (int t = 0; t < T; ++t) in.morton[t] = morton3h(in.tiles4[4 * t + 1], in.tiles4[4 * t + 2], in.tiles4[4 * t + 3]);
   PartPlan P;
-  const int lg = choose_partition_level(in, nranks);
+  if (gather_below_cells < 0) { set_error("gather_below_cells < 0"); return OCTMG_E_INVALID; }
+  const int lg = choose_partition_level(in, nranks, gather_below_cells);
   build_partition(in, nranks, lg, P);
   *lg_out = lg;
   std::memcpy(owner_out, P.owner.data(), sizeof(int32_t) * T);
@@ -884,8 +885,10 @@ namespace {
 // The whole PCG loop (Alg. 1 lines 8-13) as ONE CUDA graph with a conditional while node
 // (SURVEY 8(a) S12): each body iteration is z = M r, (r, z) and beta, p = z + beta p,
 // q = A p and p.q, the x / r update, the null-space projection, and the stopping test,
-// which sets the while condition on the device — no host round trip per iteration.
-// Single-part hierarchies (the NCCL / loopback transports stay on the host-driven loop).
+// which sets the while condition on the device — no host round trip per iteration.  A
+// partitioned group (loopback parts, or one NCCL rank) captures the same sequence with its
+// transport's halo exchanges and scalar allreduces in the body (every rank runs the same
+// number of iterations: the test reads the allreduced sums).
 octmg_status build_loop_graph(Group& g, bool ns) {
   Hier& h = *g.parts[0];
   if (!g.graph_stream) OCTMG_CUDA(cudaStreamCreateWithFlags(&g.graph_stream, cudaStreamNonBlocking));
@@ -913,20 +916,37 @@ octmg_status build_loop_graph(Group& g, bool ns) {
   cudaStream_t cs = g.graph_stream;
   const int G = vec_grid();
   OCTMG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  octmg_status st = launch_ops(g, cs);  // z = M r
-  if (st == OCTMG_OK) {
-    launch_dot_rz(h.r, h.z, h.own_cells, h.partial, h.counter + 2, h.sc, cs, G);  // (r, z), beta
-    launch_pupdate(h.z, h.p0, h.own_cells, h.sc, true, cs, G);                     // p = z + beta p
-    ApplyArgs a = apply_args(h);
-    a.z = h.p0;
-    a.q = h.q;
-    a.partial = h.partial;
-    a.counter = h.counter + 3;
-    launch_apply(a, cs);                                                           // q = A p, p.q
-    launch_update(h.xs, h.r, h.p0, h.q, h.own_cells, h.partial, h.counter + 4, h.sc, cs, G);
-    if (ns) launch_project(h.r, h.act, h.own_cells, h.partial, h.counter + 1, h.sc, cs, G);
-    launch_pcg_check(h.sc, g.loop, (unsigned long long)hd, cs);
-  }
+  auto seq = [&]() -> octmg_status {
+    OCTMG_TRY(launch_ops(g, cs));  // z = M r
+    for (Hier* p : g.parts) launch_dot_rz(p->r, p->z, p->own_cells, p->partial, p->counter + 2, p->sc, cs, G);
+    OCTMG_TRY(allreduce(g, SF_RZ, 1, cs));  // (r, z)
+    if (g.comm)
+      for (Hier* p : g.parts) launch_set_beta(p->sc, cs);  // beta from the summed (r, z)
+    std::vector<Fld> pf;
+    for (Hier* p : g.parts) {
+      launch_pupdate(p->z, p->p0, p->own_cells, p->sc, true, cs, G);  // p = z + beta p
+      pf.push_back(Fld{p->p0, nullptr});
+    }
+    if (g.comm) OCTMG_TRY(g.comm->exchange(g, 0, 1, pf, cs));  // p of the boundary tiles
+    for (Hier* p : g.parts) {
+      ApplyArgs a = apply_args(*p);
+      a.z = p->p0;
+      a.q = p->q;
+      a.partial = p->partial;
+      a.counter = p->counter + 3;
+      launch_apply(a, cs);  // q = A p, p.q
+    }
+    OCTMG_TRY(allreduce(g, SF_PQ, 1, cs));
+    for (Hier* p : g.parts) launch_update(p->xs, p->r, p->p0, p->q, p->own_cells, p->partial, p->counter + 4, p->sc, cs, G);
+    OCTMG_TRY(allreduce(g, SF_RR, 2, cs));
+    if (ns) {
+      for (Hier* p : g.parts) launch_project(p->r, p->act, p->own_cells, p->partial, p->counter + 1, p->sc, cs, G);
+      OCTMG_TRY(allreduce(g, SF_RR, 1, cs));
+    }
+    launch_pcg_check(h.sc, g.loop, (unsigned long long)hd, cs);  // the allreduced sums of part 0
+    return OCTMG_OK;
+  };
+  octmg_status st = seq();
   cudaError_t e = cudaStreamEndCapture(cs, &body);
   if (st != OCTMG_OK) { cudaGraphDestroy(graph); return st; }
   if (e != cudaSuccess) { cudaGraphDestroy(graph); return cuda_status(e, "cudaStreamEndCapture (PCG loop)"); }
@@ -969,6 +989,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       report->status = st;
       report->kernel_launches = g.launches - launches0;
       report->history_len = report->history ? std::min(std::min(iters, (int)report->history_cap), hist_lim) : 0;
+      report->device_loop = hist_lim == LOOP_HCAP ? 1 : 0;
     }
     return st;
   };
@@ -1010,7 +1031,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   const double bn = std::sqrt(hs->sum_rr);
   if (bn == 0.0) return fill(OCTMG_OK, 0, true, 0.0, 0.0);
   const char* gl = getenv("OCTMG_GRAPH_LOOP");  // default on for single-part hierarchies; 0: host loop
-  bool device_loop = !(gl && atoi(gl) == 0) && np == 1 && !g.comm && !profiling(g) && !g.loop_unavailable;
+  bool device_loop = !(gl && atoi(gl) == 0) && !profiling(g) && !g.loop_unavailable;
   if (device_loop && (!g.loop_graph || g.loop_ns != (ns ? 1 : 0))) {
     // a driver without conditional nodes, or a schedule variant whose launches a
     // conditional body cannot hold (cooperative / cluster launches): fall back to the
@@ -1033,15 +1054,17 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     L->converged = 0;
     OCTMG_CUDA(cudaMemcpyAsync(g.loop, L, offsetof(LoopState, hist), cudaMemcpyHostToDevice, s));
     // beta = 0 on the first iteration: rho = inf, p = 0
-    const double inf = INFINITY;
-    OCTMG_CUDA(cudaMemcpyAsync(&h0.sc->rho, &inf, sizeof(double), cudaMemcpyHostToDevice, s));
-    OCTMG_CUDA(cudaMemsetAsync(h0.p0, 0, sizeof(float) * (size_t)h0.tree->NL * TB3, s));
+    static const double inf = INFINITY;
+    for (Hier* h : g.parts) {
+      OCTMG_CUDA(cudaMemcpyAsync(&h->sc->rho, &inf, sizeof(double), cudaMemcpyHostToDevice, s));
+      OCTMG_CUDA(cudaMemsetAsync(h->p0, 0, sizeof(float) * (size_t)h->tree->NL * TB3, s));
+    }
     OCTMG_CUDA(cudaGraphLaunch(g.loop_graph, s));
     OCTMG_CUDA(cudaMemcpyAsync(L, g.loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
-    g.launches += (int64_t)kk * (schedule_kernels(g) + 6 + (ns ? 1 : 0));
+    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (5 + (ns ? 1 : 0) + (g.comm ? 1 : 0)) + 1);
     hist_lim = LOOP_HCAP;
     if (report && report->history) {
       const int nh = std::min(kk, std::min((int)report->history_cap, LOOP_HCAP));
@@ -1133,6 +1156,7 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
       report->status = st;
       report->kernel_launches = g.launches - launches0;
       report->history_len = report->history ? std::min(iters, (int)report->history_cap) : 0;
+      report->device_loop = 0;
     }
     return st;
   };

@@ -26,14 +26,21 @@ namespace octmg {
 
 static int tile_level(const std::vector<int>& tiles4, int t) { return tiles4[4 * (size_t)t]; }
 
-int choose_partition_level(const PartInput& in, int nranks) {
-  // coarsest leaf level
+int choose_partition_level(const PartInput& in, int nranks, int64_t gather_below_cells) {
+  // coarsest leaf level (every leaf must be owned, so lg <= lmin)
   int lmin = in.L;
   for (int l = 0; l <= in.L; ++l)
     if (in.lc[l] > 0) { lmin = l; break; }
-  // the coarsest level <= lmin with at least 8 tiles per rank
-  for (int l = 0; l <= lmin; ++l)
-    if (in.lc[l] + in.ic[l] >= 8 * nranks) return l;
+  // the coarsest level <= lmin with at least 8 tiles per rank and at least
+  // gather_below_cells cells: the levels below it are small enough that a rank solves them
+  // faster redundantly (after gathering the restricted parents) than partitioned with a
+  // halo exchange per pass (BASELINE north_star: "coarse levels below a size threshold are
+  // gathered")
+  const int64_t thr = gather_below_cells > 0 ? gather_below_cells : DEFAULT_GATHER_BELOW_CELLS;
+  for (int l = 0; l <= lmin; ++l) {
+    const int64_t tiles = (int64_t)in.lc[l] + in.ic[l];
+    if (tiles >= 8 * (int64_t)nranks && tiles * 512 >= thr) return l;
+  }
   return lmin;
 }
 

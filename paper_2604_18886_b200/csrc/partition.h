@@ -36,7 +36,10 @@ struct PartPlan {
   }
 };
 
-int choose_partition_level(const PartInput& in, int nranks);
+// levels with fewer cells are replicated (gathered) rather than partitioned unless the
+// caller sets octmg_mg_params.gather_below_cells (2^21 cells: one 128^3 level)
+constexpr int64_t DEFAULT_GATHER_BELOW_CELLS = (int64_t)1 << 21;
+int choose_partition_level(const PartInput& in, int nranks, int64_t gather_below_cells);
 void build_partition(const PartInput& in, int nranks, int lg, PartPlan& P);
 
 }  // namespace octmg

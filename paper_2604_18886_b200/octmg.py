@@ -51,7 +51,8 @@ class SolveParams(C.Structure):
 class SolveReport(C.Structure):
     _fields_ = [("iters", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
                 ("bnorm", C.c_double), ("status", C.c_int32), ("history", C.POINTER(C.c_double)),
-                ("history_cap", C.c_int32), ("kernel_launches", C.c_int64), ("history_len", C.c_int32)]
+                ("history_cap", C.c_int32), ("kernel_launches", C.c_int64), ("history_len", C.c_int32),
+                ("device_loop", C.c_int32)]
 
 
 EXPORT_TILES, EXPORT_NBR, EXPORT_PARENT, EXPORT_CHILD = 0, 1, 2, 3
@@ -111,7 +112,7 @@ def lib():
         L.octmg_nccl_comm_destroy.restype = None
         L.octmg_hier_destroy.argtypes = [P]
         L.octmg_tree_destroy.argtypes = [P]
-        L.octmg_partition_plan_host.argtypes = [P, P, P, P, I32, I32, I32, P, I32, P, P, P, P, I64]
+        L.octmg_partition_plan_host.argtypes = [P, P, P, P, I32, I32, I32, P, I32, P, P, P, P, I64, I64]
         for name in ABI_SYMBOLS[2:16] + ["octmg_partition_plan_host"]:
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -291,7 +292,7 @@ class Hierarchy:
         st = fn(self._h, _ptr(b), _ptr(x), C.byref(prm), C.byref(rep), _stream(stream))
         out = dict(iters=rep.iters, converged=bool(rep.converged), rel_residual=rep.rel_residual,
                    bnorm=rep.bnorm, status=STATUS.get(st, st), kernel_launches=int(rep.kernel_launches),
-                   history=np.array(hist[:rep.history_len]))
+                   history=np.array(hist[:rep.history_len]), device_loop=bool(rep.device_loop))
         if raise_on_error and st not in (0, 10):
             _check(st)
         return out
@@ -398,7 +399,7 @@ def grade_repair_host(tiles, ext=(1, 1, 1)):
         _check(st)
 
 
-def partition_plan_host(tables, L, NL, NI, level_counts, nranks):
+def partition_plan_host(tables, L, NL, NI, level_counts, nranks, gather_below_cells=0):
     """octmg_partition_plan_host on host tables (no GPU): (lg, owner[T], items) where items is
     a dict (level, from, to) -> int32 array (n, 2) of (tile, kind)."""
     T = NL + NI
@@ -416,7 +417,8 @@ def partition_plan_host(tables, L, NL, NI, level_counts, nranks):
     items = np.zeros(2 * cap, dtype=np.int32)
     vp = lambda a: a.ctypes.data_as(C.c_void_p)
     _check(lib().octmg_partition_plan_host(vp(t4), vp(nb), vp(par), vp(ch), NL, NI, L, vp(lcnt), nranks,
-                                           C.byref(lg), vp(owner), vp(nitems), vp(items), cap))
+                                           C.byref(lg), vp(owner), vp(nitems), vp(items), cap,
+                                           int(gather_below_cells)))
     out, k = {}, 0
     for l in range(L + 1):
         for a in range(nranks):

@@ -16,13 +16,13 @@ from oracle.oracle import Oracle
 B3 = 512
 
 
-def _plan(o, nranks):
+def _plan(o, nranks, gather=0):
     import paper_2604_18886_b200 as om
     tb = o.tables()
     counts = np.zeros(4 * (o.L + 1), dtype=np.int32)
     for l in range(o.L + 1):
         counts[4 * l:4 * l + 4] = [o.leaf_begin[l], o.leaf_count[l], o.inner_begin[l], o.inner_count[l]]
-    return om.partition_plan_host(tb, o.L, o.NL, o.NI, counts, nranks)
+    return om.partition_plan_host(tb, o.L, o.NL, o.NI, counts, nranks, gather)
 
 
 def _cells(kind):
@@ -56,12 +56,13 @@ def _fill(local, ref, items, leaf_only, NL):
 CASES = ["sphere_small", "tank_small", "uniform32"]
 
 
-@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("gather", [0, 1])
+@pytest.mark.parametrize("name", CASES + ["sphere_35"])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_partition_ownership(name, nranks):
+def test_partition_ownership(name, nranks, gather):
     cfg = make_config(name, with_fields=False)
     o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
-    lg, owner, items = _plan(o, nranks)
+    lg, owner, items = _plan(o, nranks, gather)
     tb = o.tables()
     lev = tb["tiles"][:, 0]
     assert np.all(owner[lev < lg] == -1) and np.all((owner[lev >= lg] >= 0) & (owner[lev >= lg] < nranks))
@@ -79,6 +80,26 @@ def test_partition_ownership(name, nranks):
     m = morton3(tb["tiles"][at, 1], tb["tiles"][at, 2], tb["tiles"][at, 3])
     seq = owner[at[np.argsort(m)]]
     assert np.all(np.diff(seq) >= 0)
+    # whole parents: the children of a level-(lg-1) tile belong to one rank
+    if lg >= 1:
+        for pt in np.unique(tb["parent"][at]):
+            assert len(np.unique(owner[at[tb["parent"][at] == pt]])) == 1
+
+
+def test_gather_threshold_chooses_partition_level():
+    """gather_below_cells (north_star: coarse levels below a size threshold are gathered): lg
+    is the coarsest level <= the coarsest leaf level with >= 8 tiles per rank and >= the
+    threshold in cells.  sphere_35: levels 0..3 have 1, 8, 64, 512 tiles, leaves from 3."""
+    cfg = make_config("sphere_35", with_fields=False)
+    o = Oracle(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
+    assert [int(c) for c in (np.asarray(o.leaf_count) + np.asarray(o.inner_count))[:4]] == [1, 8, 64, 512]
+    assert _plan(o, 2, 1)[0] == 2            # as deep as 8 tiles per rank allow (64 >= 16)
+    assert _plan(o, 8, 1)[0] == 2            # 64 >= 64
+    assert _plan(o, 9, 1)[0] == 3            # 64 < 72
+    assert _plan(o, 2, 64 * 512)[0] == 2     # level 2 holds exactly the threshold
+    assert _plan(o, 2, 64 * 512 + 1)[0] == 3
+    assert _plan(o, 2, 0)[0] == 3            # default 2^21 cells: nothing reaches it, lg = leaf level
+    assert _plan(o, 2, 1 << 40)[0] == 3      # never above the coarsest leaf level
 
 
 def _check_rank(o, owner, items, lg, rank, nranks, x, u_all, Ax, Au):
@@ -118,9 +139,10 @@ def test_halo_plan_covers_every_read(name):
     Ax = o.apply(x)
     Au = {l: o.apply_level(l, u_all) for l in range(o.L + 1)}
     for nranks in (2, 3):
-        lg, owner, items = _plan(o, nranks)
-        for rank in range(nranks):
-            _check_rank(o, owner, items, lg, rank, nranks, x, u_all, Ax, Au)
+        for gather in (0, 1):
+            lg, owner, items = _plan(o, nranks, gather)
+            for rank in range(nranks):
+                _check_rank(o, owner, items, lg, rank, nranks, x, u_all, Ax, Au)
     # negative control: the check notices one missing item of each kind class
     lg, owner, items = _plan(o, 2)
     for kinds in ((0, 1, 2, 3, 4, 5), (6,)):
@@ -181,6 +203,37 @@ def _worker(rank, world, port, name, q):
         dist.all_reduce(part)
         tot = float((x * o.apply(x)).sum())
         ok = ok and abs(part.item() - tot) <= 1e-12 * abs(tot)
+        # gather below the partition level: each rank restricts the residual of its level-lg
+        # tiles into their (whole, rank-owned) parents, R r = sum of the 8 children / alpha,
+        # and the all-gather leaves every rank with the full replicated level lg - 1
+        if lg >= 1:
+            tb = o.tables()
+            lev, par = tb["tiles"][:, 0], tb["parent"]
+            u_all = np.random.default_rng(5).standard_normal(o.T * B3) * (o.coefs()[:, 0] != 0)
+            r_all = -o.apply_level(lg, u_all)
+            def restrict(tiles_):
+                out = np.zeros(o.T * B3)
+                for t in tiles_:
+                    p, (i, j, k) = par[t], tb["tiles"][t, 1:4]
+                    for c in range(B3):
+                        x_, y_, z_ = c & 7, (c >> 3) & 7, c >> 6
+                        pc = ((i & 1) * 4 + (x_ >> 1)) + 8 * ((j & 1) * 4 + (y_ >> 1)) + 64 * ((k & 1) * 4 + (z_ >> 1))
+                        out[p * B3 + pc] += r_all[t * B3 + c] / 2.0
+                return out
+            at = np.where(lev == lg)[0]
+            full = restrict(at)
+            mine_p = restrict(at[owner[at] == rank])
+            parents = np.unique(par[at[owner[at] == rank]])
+            got = [None] * world
+            dist.all_gather_object(got, {int(p_): mine_p[p_ * B3:(p_ + 1) * B3] for p_ in parents})
+            gathered = np.zeros(o.T * B3)
+            for d in got:
+                for p_, v in d.items():
+                    assert not gathered[p_ * B3:(p_ + 1) * B3].any()  # each parent from one rank
+                    gathered[p_ * B3:(p_ + 1) * B3] = v
+            pall = np.unique(par[at])
+            idx = np.concatenate([np.arange(p_ * B3, (p_ + 1) * B3) for p_ in pall])
+            ok = ok and np.array_equal(gathered[idx], full[idx])
         q.put((rank, ok))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - surfaced through the queue

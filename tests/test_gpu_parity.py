@@ -299,15 +299,26 @@ def test_apply_smooth_input_matches_oracle(om, name):
 # partition in one process; halo exchanges / parent broadcasts / scalar sums are device
 # copies.  Same kernels and schedule as an NCCL job.
 # ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("gather", [0, 1])
 @pytest.mark.parametrize("parts", [2, 3, 4])
-@pytest.mark.parametrize("name", ["uniform64", "sphere_small", "tank_small", "sphere_small_dir"])
-def test_loopback_partition_matches_single(om, name, parts):
+@pytest.mark.parametrize("name", ["uniform64", "sphere_small", "tank_small", "sphere_small_dir", "sphere_35"])
+def test_loopback_partition_matches_single(om, name, parts, gather):
+    """P parts of a Morton-range partition in one process (loopback transport: the halo
+    exchanges, the gather of the restricted parents into the replicated levels below the
+    partition level and the scalar allreduces are device copies), with the default
+    gather_below_cells threshold (0) and partitioned as deep as 8 tiles per part allow (1):
+    the cycle and the apply bit-identical to the single-part solve; the PCG, run as the
+    device-side conditional-graph loop, within the parity bar."""
     cfg = make_config(name)
     tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
     kind = torch.from_numpy(cfg["kind"]).to(DEV)
     frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(DEV)
     h1 = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
-    hp = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"], loopback_parts=parts)
+    hp = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"], loopback_parts=parts, gather_below_cells=gather)
+    lcnt = tree.leaf_count + tree.inner_count
+    lmin = int(np.flatnonzero(tree.leaf_count)[0])
+    cand = [l for l in range(lmin + 1) if lcnt[l] >= 8 * parts and lcnt[l] * 512 >= (gather or (1 << 21))]
+    assert hp.partition(0)[0] == (cand[0] if cand else lmin)
     # ownership: every leaf tile owned by exactly one part
     owned = np.zeros(tree.NL, dtype=np.int64)
     for p in range(parts):
@@ -330,6 +341,7 @@ def test_loopback_partition_matches_single(om, name, parts):
     x1, xp = torch.zeros_like(b), torch.zeros_like(b)
     r1 = h1.pcg_solve(b, x1, rtol=1e-6)
     rp = hp.pcg_solve(b, xp, rtol=1e-6)
+    assert r1["device_loop"] and rp["device_loop"]
     assert rp["converged"] and abs(r1["iters"] - rp["iters"]) <= 1
     a1, ap = x1.cpu().numpy().astype(np.float64), xp.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(a1 - ap) <= 1e-5 * np.linalg.norm(a1)
