@@ -198,6 +198,24 @@ octmg_status octmg_partition_plan_host(const int32_t* tiles4, const int32_t* nbr
                                        int64_t items_cap, int64_t gather_below_cells);
 
 /*
+ * Narrow-band leaf tiles around a sphere surface on the device (P:L1224-1229,
+ * the Table 1 / Sec. 5.3-5.4 grids): starting from every level-l0 tile of the ext[0] x
+ * ext[1] x ext[2] domain, a tile whose box strictly intersects the sphere surface (distance
+ * from `centre3` to the box: d_min < radius < d_max; coordinates in level-0 tile units) is
+ * refined, down to level l0 + extra; the others stay leaves.  grade_repair = 1 then refines,
+ * to fixpoint, every leaf face-adjacent to a leaf two or more levels finer, the
+ * unique minimal 2:1-graded refinement.  Dense per-level occupancy bitmaps on the device
+ * (fp64 box test without FMA contraction: the same tile set as an IEEE host computation).
+ * out_host: cap entries of host memory receiving the leaves in unspecified order (feed them
+ * to octmg_build_tree), or NULL to count only; *n_out = the leaf count (OCTMG_E_INVALID if it
+ * exceeds cap).
+ * Synchronises `stream`.
+ */
+octmg_status octmg_band_tiles(const int32_t* ext3, int32_t l0, int32_t extra, const double* centre3, double radius,
+                             int32_t grade_repair, octmg_tile* out_host, int64_t cap, int64_t* n_out,
+                             octmg_stream stream);
+
+/*
  * Cut-cell fields of the static tank scene: a solid sphere
  * obstacle (centre, radius in level-0 tile units; radius <= 0: none) in a tank with solid
  * bottom and side walls and an open top y = ext_y.  For every leaf cell (leaf-slot order),

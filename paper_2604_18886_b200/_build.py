@@ -37,7 +37,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         for src in SOURCES:
             obj = os.path.join(objdir, os.path.basename(src) + ".o")
             objs.append(obj)
-            extra = ["-fmad=false"] if os.path.basename(src) == "geometry.cu" else []  # fp64 SDF = oracle's IEEE ops
+            # fp64 SDF / box tests = the host's IEEE operations (no FMA contraction)
+            extra = ["-fmad=false"] if os.path.basename(src) in ("geometry.cu", "band.cu") else []
             cmds.append([nvcc] + cflags + extra + ["-c", "-o", obj, src])
         if verbose:
             for c in cmds:

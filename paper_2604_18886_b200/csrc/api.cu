@@ -819,6 +819,12 @@ octmg_status octmg_subtract_gradient(const octmg_hier* hh, const uint8_t* kind, 
   return subtract_gradient(*hh->g.parts[0], kind, face_beta, face_frac, p, u6, (cudaStream_t)stream);
 }
 
+octmg_status octmg_band_tiles(const int32_t* ext3, int32_t l0, int32_t extra, const double* centre3, double radius,
+                             int32_t grade_repair, octmg_tile* out_host, int64_t cap, int64_t* n_out,
+                             octmg_stream stream) {
+  return band_tiles(ext3, l0, extra, centre3, radius, grade_repair, out_host, cap, n_out, (cudaStream_t)stream);
+}
+
 octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind,
                                float* face_frac, float* b, octmg_stream stream) {
   if (!tree || !centre3 || !kind || !face_frac || !b) { set_error("null argument"); return OCTMG_E_INVALID; }

@@ -256,6 +256,10 @@ octmg_status subtract_gradient(const Hier& h, const uint8_t* kind, const float* 
 octmg_status tank_fields(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac, float* b,
                          cudaStream_t s);
 
+// narrow-band refinement of the sphere-surface test grids on the device (band.cu)
+octmg_status band_tiles(const int32_t* ext, int l0, int extra, const double* centre, double radius, int repair,
+                        octmg_tile* out_host, int64_t cap, int64_t* n_out, cudaStream_t s);
+
 // 2:1 grading repair of a leaf-tile list (grade.cpp, host)
 octmg_status grade_repair(const octmg_tile* in, int64_t n, const int32_t* ext, std::vector<octmg_tile>& out);
 

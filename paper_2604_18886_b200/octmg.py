@@ -65,7 +65,8 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_nccl_comm_init", "octmg_nccl_comm_destroy", "octmg_partition_plan_host",
                "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields",
                "octmg_divergence", "octmg_subtract_gradient",
-               "octmg_grade_repair_host", "octmg_set_allocator", "octmg_profile_read_level"]
+               "octmg_grade_repair_host", "octmg_set_allocator", "octmg_profile_read_level",
+               "octmg_band_tiles"]
 
 _lib = None
 
@@ -104,6 +105,8 @@ def lib():
         L.octmg_profile_read.argtypes = [P, P, P, P, P, I32, C.POINTER(I32)]
         L.octmg_profile_read_level.argtypes = [P, I32, P, P, P, I32, C.POINTER(I32)]
         L.octmg_profile_read_level.restype = C.c_int
+        L.octmg_band_tiles.argtypes = [P, I32, I32, P, C.c_double, I32, P, I64, P, P]
+        L.octmg_band_tiles.restype = C.c_int
         L.octmg_setup_hierarchy_loopback.argtypes = [P, I32, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
         L.octmg_partition_info.argtypes = [P, I32, P, P, P, P, P]
         L.octmg_nccl_unique_id.argtypes = [P]
@@ -397,6 +400,21 @@ def grade_repair_host(tiles, ext=(1, 1, 1)):
             cap = n_out.value
             continue
         _check(st)
+
+
+def band_tiles(l0, extra, centre=(0.5, 0.5, 0.5), radius=0.25, ext=(1, 1, 1), grade_repair=True, stream=None):
+    """octmg_band_tiles: the narrow-band leaf tiles (n, 4) int32 (level, i, j, k), computed on
+    the device (unspecified order); centre / radius in level-0 tile units."""
+    e = (C.c_int32 * 3)(*ext)
+    c = (C.c_double * 3)(*centre)
+    n = C.c_int64()
+    _check(lib().octmg_band_tiles(C.cast(e, C.c_void_p), int(l0), int(extra), C.cast(c, C.c_void_p), float(radius),
+                                  1 if grade_repair else 0, None, 0, C.byref(n), _stream(stream)))
+    out = np.zeros((n.value, 4), dtype=np.int32)
+    _check(lib().octmg_band_tiles(C.cast(e, C.c_void_p), int(l0), int(extra), C.cast(c, C.c_void_p), float(radius),
+                                  1 if grade_repair else 0, out.ctypes.data_as(C.c_void_p), n.value, C.byref(n),
+                                  _stream(stream)))
+    return out
 
 
 def partition_plan_host(tables, L, NL, NI, level_counts, nranks, gather_below_cells=0):

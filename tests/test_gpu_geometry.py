@@ -75,3 +75,51 @@ def test_solve_on_device_fields_matches_oracle(om):
     assert rep["converged"] and abs(rep["iters"] - ref["iters"]) <= 1
     xg = x.cpu().numpy().astype(np.float64)
     assert np.linalg.norm(xg - ref["x"]) / np.linalg.norm(ref["x"]) <= 1e-5
+
+
+# ---------------------------------------------------------------------------------------
+# narrow-band refinement on the device (octmg_band_tiles)
+# ---------------------------------------------------------------------------------------
+def _sorted_rows(t):
+    t = np.asarray(t, dtype=np.int64)
+    return t[np.lexsort((t[:, 3], t[:, 2], t[:, 1], t[:, 0]))]
+
+
+@pytest.mark.parametrize("l0,extra,r,centre,repair", [(2, 2, 0.25, (0.5, 0.5, 0.5), True),
+                                                      (3, 2, 0.25, (0.5, 0.5, 0.5), False),
+                                                      (2, 3, 0.31, (0.45, 0.52, 0.5), True),
+                                                      (4, 3, 0.375, (0.5, 0.5, 0.5), True),   # config 3
+                                                      (4, 4, 0.30, (0.5, 0.5, 0.5), True)])   # config 4
+def test_band_tiles_match_generator(om, l0, extra, r, centre, repair):
+    """The device refinement yields exactly the input generator's tile set (octgen: strict
+    box test + grading repair to fixpoint, the same IEEE fp64 operations)."""
+    from octgen.trees import sphere_band_tiles, is_graded
+    ref = sphere_band_tiles(l0, extra, center=centre, r=r, repair=repair)
+    got = om.band_tiles(l0, extra, centre=centre, radius=r, grade_repair=repair)
+    assert np.array_equal(_sorted_rows(got), _sorted_rows(ref))
+    if repair:
+        assert is_graded(got)
+
+
+def test_band_tiles_table1_counts(om):
+    """Table 1's sphere grids (3368 / 15464 / 79080 leaf tiles,
+    tests/golden/table1_tiles.json) from the device refinement, and a tree builds on them."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table1_tiles.json")))
+    for row in gold["rows"]:
+        if "l0" not in row:
+            continue
+        t = om.band_tiles(row["l0"], 2, radius=gold["sphere_r"])
+        assert len(t) == row["tiles"], row
+    tree = om.Tree(t, (1, 1, 1), (0, 0, 0, 0, 0, 0))
+    assert tree.NL == 79080
+
+
+@pytest.mark.slow
+def test_band_tiles_full_size_cfg5(om):
+    """BASELINE config 5's tile list (l0 = 4, 5 extra levels, r = 0.35: 1.64M leaf tiles)
+    from the device equals the host generator's."""
+    cfg = make_config("cfg5_tank", with_fields=False)
+    got = om.band_tiles(4, 5, radius=cfg["radius"])
+    assert np.array_equal(_sorted_rows(got), _sorted_rows(cfg["tiles"]))
