@@ -48,7 +48,7 @@ def launches():
     tot = sum(t for _, _, t in seg)
     agg = collections.defaultdict(lambda: [0, 0.0])
     for k, g, t in seg:
-        key = k + ("  grid=" + g.strip() if k.startswith("k_pass") or k.startswith("k_restrict") or k.startswith("k_prolong") or k.startswith("k_fasrhs") else "")
+        key = k + ("  grid=" + g.strip() if k.startswith(("k_pass", "k_restrict", "k_prolong", "k_fasrhs")) else "")
         agg[key][0] += 1
         agg[key][1] += t
     lines = [f"# {tag}: launch shares of the bench's timed solves (ncu launch list, cold-cache, serialised)",
@@ -102,7 +102,7 @@ def full():
     open(os.path.join(PROF, f"{tag}_ncu_full.md"), "w").write("\n".join(out) + "\n")
     tj = os.path.join(PROF, "roofline_traffic.json")
     d = json.load(open(tj)) if os.path.exists(tj) else {}
-    for kname in ("k_pass_v2", "k_pass_direct"):
+    for kname in ("k_pass_v3", "k_pass_v2", "k_pass_direct"):
         if kname in traffic:
             # the bench's dominant kernel (rbgs_pass) at the finest level of config 2
             d["cfg2_uniform256"] = traffic[kname]
