@@ -5,9 +5,11 @@
 #include <cmath>
 #include <unordered_map>
 #include <algorithm>
-#include <cstdlib>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "comm.h"
 #include "octmg_internal.cuh"
@@ -287,6 +289,8 @@ cudaEvent_t next_event(Hier& h) {
   return h.event_pool[h.event_next++];
 }
 
+// CUDA events around a launch (and an NVTX range "class Ll" for nsys timelines) while the
+// hierarchy profiles; nothing otherwise
 struct ProfScope {
   Hier& h;
   int cls;
@@ -294,6 +298,10 @@ struct ProfScope {
   cudaEvent_t b = nullptr;
   ProfScope(Hier& hh, int c, cudaStream_t ss, double bytes, int level = -1) : h(hh), cls(c), s(ss) {
     if (h.profiling) {
+      char nm[48];
+      if (level >= 0) snprintf(nm, sizeof nm, "%s L%d", kclass_name[cls], level);
+      else snprintf(nm, sizeof nm, "%s", kclass_name[cls]);
+      nvtxRangePushA(nm);
       cudaEvent_t a = next_event(h);
       b = next_event(h);
       cudaEventRecord(a, s);
@@ -301,7 +309,10 @@ struct ProfScope {
     }
   }
   ~ProfScope() {
-    if (h.profiling) cudaEventRecord(b, s);
+    if (h.profiling) {
+      cudaEventRecord(b, s);
+      nvtxRangePop();
+    }
   }
 };
 
