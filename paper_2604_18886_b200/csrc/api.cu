@@ -262,6 +262,12 @@ octmg_status build_schedule(Group& g) {
       OCTMG_CUDA(cudaDeviceSynchronize());
       if (p->cd_K >= p->sub_K) p->sub_K = p->cd_K;
       else p->cd_K = -1;
+      // level 2 too, in a thread-block cluster, when it is a replicated complete level
+      if (p->cd_K == 1 && (p->nranks == 1 || p->lg > 2)) {
+        OCTMG_TRY(build_coarse_cluster(*p, nullptr));
+        OCTMG_CUDA(cudaDeviceSynchronize());
+        if (p->cc_K == 2) p->sub_K = 2;
+      }
     }
   }
   Hier& h = *g.parts[0];
@@ -353,6 +359,11 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
                                        T.ic, h.bar, s);
     if (e != cudaSuccess) set_error(std::string("k_coarse_grid launch: ") + cudaGetErrorString(e));
+    return;
+  }
+  if (op.kind == 4 && h.cc_K == 2 && l == 2) {
+    ProfScope ps(h, KC_SUBCYCLE, s, 0.0, op.level);
+    launch_coarse_cluster(h, op.stage, h.uinA, h.binner, s);
     return;
   }
   if (op.kind == 4 && h.cd_K >= 0) {

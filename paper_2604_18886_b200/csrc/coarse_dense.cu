@@ -28,7 +28,11 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "octmg_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace octmg {
 
@@ -220,6 +224,45 @@ __device__ __forceinline__ void cd_prolong(const CDArgs& A, const CDMem& M, int 
   __syncthreads();
 }
 
+// Alg. 4 from level `top` down, iteratively (explicit per-level count of the mu coarse calls);
+// fas_first: the first of the mu calls from level top + 1 (forms the FAS rhs of level top)
+template <int NT>
+__device__ void cd_cycle(const CDArgs& A, const CDMem& M, int top, bool fas_first) {
+  int done[CD_MAXL + 1];
+  int l = top;
+  bool ff = fas_first;
+  bool entering = true;
+  while (true) {
+    if (entering) {
+      if (ff && !A.std_form) cd_fasrhs<NT>(A, M, l);
+      if (l == 0) {
+        const int h1 = A.nu_coarsest / 2;
+        cd_passes<NT>(A, M, 0, h1, true);
+        cd_passes<NT>(A, M, 0, A.nu_coarsest - h1, false);
+      } else {
+        cd_passes<NT>(A, M, l, A.nu_pre, true);
+        cd_restrict<NT>(A, M, l);
+        done[l] = 0;
+        l -= 1;
+        ff = true;
+        continue;
+      }
+      entering = false;
+    }
+    if (l == top) break;
+    const int p = l + 1;
+    if (++done[p] < A.mu) {  // the next coarse call starts from the previous one's u^l
+      l = p - 1;
+      ff = false;
+      entering = true;
+      continue;
+    }
+    cd_prolong<NT>(A, M, p);
+    cd_passes<NT>(A, M, p, A.nu_post, false);
+    l = p;
+  }
+}
+
 template <int NT>
 __global__ __launch_bounds__(NT, 1) void k_coarse_dense(const __grid_constant__ CDArgs A) {
   extern __shared__ __align__(16) float smem[];
@@ -270,40 +313,7 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_dense(const __grid_constant__ 
     }
   }
   __syncthreads();
-  // Alg. 4 from level K down, iteratively (explicit per-level count of the mu coarse calls)
-  int done[CD_MAXL + 1];
-  int l = A.K;
-  bool ff = A.fas_first != 0;
-  bool entering = true;
-  while (true) {
-    if (entering) {
-      if (ff && !A.std_form) cd_fasrhs<NT>(A, M, l);
-      if (l == 0) {
-        const int h1 = A.nu_coarsest / 2;
-        cd_passes<NT>(A, M, 0, h1, true);
-        cd_passes<NT>(A, M, 0, A.nu_coarsest - h1, false);
-      } else {
-        cd_passes<NT>(A, M, l, A.nu_pre, true);
-        cd_restrict<NT>(A, M, l);
-        done[l] = 0;
-        l -= 1;
-        ff = true;
-        continue;
-      }
-      entering = false;
-    }
-    if (l == A.K) break;
-    const int p = l + 1;
-    if (++done[p] < A.mu) {  // the next coarse call starts from the previous one's u^l
-      l = p - 1;
-      ff = false;
-      entering = true;
-      continue;
-    }
-    cd_prolong<NT>(A, M, p);
-    cd_passes<NT>(A, M, p, A.nu_post, false);
-    l = p;
-  }
+  cd_cycle<NT>(A, M, A.K, A.fas_first != 0);
   // copy out u^K and b^K (the FAS rhs persists across the mu calls from level K+1)
   const CDLevel& L = A.lv[A.K];
   for (int g = threadIdx.x; g < L.n; g += NT) {
@@ -337,6 +347,251 @@ int shift_of(int v) {  // log2(v) for a power of two, else -1
   return -1;
 }
 
+
+// ------------------------------------------------------------------------------------
+// Levels 0..2 in one thread-block cluster (ext = (1,1,1)): level 2 (32^3 cells) is cut into
+// CC z-slabs of 32 x 32 x SLZ cells, one per CTA of the cluster, each a dense colour-split
+// grid in its CTA's shared memory (the colour of a cell is (x + y + z_local) & 1 since the
+// slab origin is even); the z-neighbours across a slab boundary are read from the adjacent
+// CTA's shared memory (distributed shared memory), and every level-2 phase ends with a
+// cluster barrier (release/acquire at cluster scope).  Levels 0-1 live in CTA 0 as in
+// k_coarse_dense and run there between two cluster barriers; the level-2 restriction writes
+// the level-1 parents (slab c -> level-1 plane c) and the prolongation reads them through
+// distributed shared memory.  One launch per level-2 visit replaces ~11 per-level launches
+// and the level-1 dense launches of the W-cycle.
+// ------------------------------------------------------------------------------------
+constexpr int CC = 16;        // CTAs per cluster (non-portable cluster size)
+constexpr int SLZ = 2;        // level-2 planes per CTA (32 / CC)
+
+struct CCArgs {
+  CDArgs A;                   // levels 0..1 (CTA 0), K = 1
+  int nx, ny;                 // level-2 plane (32 x 32)
+  const float* dcoef2;        // [CC][NP][nS] slab coefficient planes
+  const int* tmap2;           // level-2 tile map [tz][ty][tx] (4 x 4 x 4)
+  int fas_first;              // form the FAS rhs of level 2 first
+  int tK0;                    // (unused: level-2 tiles via tmap2)
+};
+
+struct Slab {
+  int nx, ny, n, hx, hxy;     // n = nx * ny * SLZ, hx = nx / 2, hxy = hx * ny
+  int c;                      // cluster rank = slab index
+  float* coef;                // NP planes of n
+  float* u;
+  float* b;
+  float* scr;
+  const float* u_lo;          // u of the slab below (rank c - 1; null at the bottom wall)
+  const float* cz_hi;         // c_z- plane of the slab above (rank c + 1; null at the top wall)
+  const float* u_hi;
+};
+
+__device__ __forceinline__ void slab_cell(const Slab& S, int c, int k, int& x, int& y, int& z) {
+  // k-th cell of colour c: row = k / hx (power-of-two dims)
+  const int row = k / S.hx;
+  y = row % S.ny;
+  z = row / S.ny;
+  x = 2 * (k - row * S.hx) + ((c + y + z) & 1);
+}
+__device__ __forceinline__ int slab_idx(const Slab& S, int x, int y, int z) {
+  return (((x + y + z) & 1) * (S.n >> 1)) + (z * S.ny + y) * S.hx + (x >> 1);
+}
+
+// face sum of slab cell (x, y, z) (index i), order x-, x+, y-, y+, z-, z+, from s0
+__device__ __forceinline__ float slab_face_sum(const Slab& S, int x, int y, int z, int i, float s0) {
+  const float* cx = S.coef + S.n;
+  const float* cy = cx + S.n;
+  const float* cz = cy + S.n;
+  const float* u = S.u;
+  const int j = i < (S.n >> 1) ? i + (S.n >> 1) : i - (S.n >> 1);
+  const int p = x & 1;
+  const bool xl = x > 0, xh = x < S.nx - 1, yl = y > 0, yh = y < S.ny - 1;
+  float s = s0;
+  s = fmaf(cx[i], xl ? u[j - 1 + p] : 0.0f, s);
+  s = fmaf(xh ? cx[j + p] : 0.0f, xh ? u[j + p] : 0.0f, s);
+  s = fmaf(cy[i], yl ? u[j - S.hx] : 0.0f, s);
+  s = fmaf(yh ? cy[j + S.hx] : 0.0f, yh ? u[j + S.hx] : 0.0f, s);
+  // z-: the plane below (in this slab, or the top plane of the slab below)
+  float vzm = 0.0f;
+  if (z > 0) vzm = u[j - S.hxy];
+  else if (S.u_lo) vzm = S.u_lo[j + S.hxy];
+  s = fmaf(cz[i], vzm, s);
+  float vzp = 0.0f, czp = 0.0f;
+  if (z < SLZ - 1) { vzp = u[j + S.hxy]; czp = cz[j + S.hxy]; }
+  else if (S.u_hi) { vzp = S.u_hi[j - S.hxy]; czp = S.cz_hi[j - S.hxy]; }
+  s = fmaf(czp, vzp, s);
+  return s;
+}
+
+template <int NT>
+__device__ __forceinline__ void slab_pass(const Slab& S, int colour, cg::cluster_group& cl) {
+  const int nh = S.n >> 1;
+  for (int k = threadIdx.x; k < nh; k += NT) {
+    int x, y, z;
+    slab_cell(S, colour, k, x, y, z);
+    const int i = colour * nh + k;
+    S.u[i] = (S.b[i] - slab_face_sum(S, x, y, z, i, 0.0f)) * S.coef[4 * S.n + i];
+  }
+  cl.sync();
+}
+
+template <int NT>
+__global__ __launch_bounds__(NT, 1) void k_coarse_cluster(const __grid_constant__ CCArgs C) {
+  extern __shared__ __align__(16) float smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const CDArgs& A = C.A;
+  // shared memory: levels 0-1 (used by CTA 0) | level-2 slab
+  CDMem M;
+  M.coef = smem;
+  M.u = M.coef + NP * A.total;
+  M.b = M.u + A.total;
+  M.us = M.b + A.total;
+  M.scr = M.us + A.total;
+  Slab S;
+  S.nx = C.nx;
+  S.ny = C.ny;
+  S.n = C.nx * C.ny * SLZ;
+  S.hx = C.nx >> 1;
+  S.hxy = S.hx * C.ny;
+  S.c = rank;
+  S.coef = M.scr + A.lv[1].n;
+  S.u = S.coef + NP * S.n;
+  S.b = S.u + S.n;
+  S.scr = M.scr;  // the level-1 residual scratch is idle while level 2 runs
+  S.u_lo = rank > 0 ? cl.map_shared_rank(S.u, rank - 1) : nullptr;
+  S.u_hi = rank < CC - 1 ? cl.map_shared_rank(S.u, rank + 1) : nullptr;
+  S.cz_hi = rank < CC - 1 ? cl.map_shared_rank(S.coef + 3 * S.n, rank + 1) : nullptr;
+  // level-1 fields of CTA 0 (written by the restriction, read by the prolongation)
+  const CDLevel& L1 = A.lv[1];
+  float* u1 = cl.map_shared_rank(M.u + L1.off, 0);
+  float* us1 = cl.map_shared_rank(M.us + L1.off, 0);
+  float* b1 = cl.map_shared_rank(M.b + L1.off, 0);
+  // copy in: the slab's coefficients, its u^2 and b^2 (tile layout); CTA 0 also levels 0-1
+  {
+    const float4* src = reinterpret_cast<const float4*>(C.dcoef2 + (size_t)rank * NP * S.n);
+    float4* dst = reinterpret_cast<float4*>(S.coef);
+    for (int i = threadIdx.x; i < NP * S.n / 4; i += NT) dst[i] = __ldg(src + i);
+    if (rank == 0) {
+      const float4* s0 = reinterpret_cast<const float4*>(A.dcoef);
+      float4* d0 = reinterpret_cast<float4*>(M.coef);
+      for (int i = threadIdx.x; i < NP * A.total / 4; i += NT) d0[i] = __ldg(s0 + i);
+    }
+    for (int i = threadIdx.x; i < S.n; i += NT) {
+      const int c = i >= (S.n >> 1);
+      int x, y, z;
+      slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
+      const int zg = SLZ * rank + z;
+      const int t = __ldg(C.tmap2 + ((zg >> 3) * (C.ny >> 3) + (y >> 3)) * (C.nx >> 3) + (x >> 3));
+      const size_t gi = (size_t)(t - A.NL) * TB3 + cslot(x & 7, y & 7, zg & 7);
+      S.u[i] = A.u_inner[gi];
+      S.b[i] = A.b_inner[gi];
+    }
+  }
+  cl.sync();
+  if (C.fas_first && !A.std_form) {  // b^2 += A^2 u* (u^2 = u* on entry)
+    for (int i = threadIdx.x; i < S.n; i += NT) {
+      const int c = i >= (S.n >> 1);
+      int x, y, z;
+      slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
+      const float cc = S.coef[i];
+      S.scr[i] = cc != 0.0f ? S.b[i] + slab_face_sum(S, x, y, z, i, cc * S.u[i]) : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < S.n; i += NT) S.b[i] = S.scr[i];
+    cl.sync();  // the neighbours' reads of u done before the passes write it
+  }
+  // pre-smoothing (R, B) x nu_pre
+  for (int k = 0; k < A.nu_pre; ++k) {
+    slab_pass<NT>(S, 0, cl);
+    slab_pass<NT>(S, 1, cl);
+  }
+  // residual, then the level-1 parents of this slab (plane `rank`) into CTA 0
+  for (int i = threadIdx.x; i < S.n; i += NT) {
+    const int c = i >= (S.n >> 1);
+    int x, y, z;
+    slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
+    const float cc = S.coef[i];
+    S.scr[i] = cc != 0.0f ? S.b[i] - slab_face_sum(S, x, y, z, i, cc * S.u[i]) : 0.0f;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < (S.nx >> 1) * (S.ny >> 1); q += NT) {
+    const int X = q % (S.nx >> 1), Y = q / (S.nx >> 1);
+    float rs[2][2], us[2][2];
+    int na = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 2; ++dy) {
+        float r2 = 0.0f, u2 = 0.0f;
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const int ci = slab_idx(S, 2 * X + dx, 2 * Y + dy, dz);
+          const bool act = S.coef[ci] != 0.0f;
+          const float uv = act ? S.u[ci] : 0.0f;
+          r2 = dx ? r2 + S.scr[ci] : S.scr[ci];
+          u2 = dx ? u2 + uv : uv;
+          na += act;
+        }
+        rs[dz][dy] = r2;
+        us[dz][dy] = u2;
+      }
+    const float rsum = (rs[0][0] + rs[0][1]) + (rs[1][0] + rs[1][1]);
+    const float usum = (us[0][0] + us[0][1]) + (us[1][0] + us[1][1]);
+    const float mP = na ? usum / (float)na : 0.0f;
+    const int pi = didx(L1, X, Y, rank);
+    u1[pi] = A.std_form ? 0.0f : mP;
+    us1[pi] = A.std_form ? 0.0f : mP;
+    b1[pi] = A.beta * (rsum / A.alpha);
+  }
+  cl.sync();
+  // the mu coarse calls at levels 1..0 in CTA 0 (shared memory, CTA barriers)
+  if (rank == 0)
+    for (int k = 0; k < A.mu; ++k) cd_cycle<NT>(A, M, 1, k == 0);
+  cl.sync();
+  // prolongation u^2 += pro_scale (u^1 - u*) from CTA 0, then post-smoothing (B, R) x nu_post
+  for (int i = threadIdx.x; i < S.n; i += NT) {
+    if (S.coef[i] == 0.0f) continue;
+    const int c = i >= (S.n >> 1);
+    int x, y, z;
+    slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
+    const int pi = didx(L1, x >> 1, y >> 1, rank);
+    S.u[i] += A.pro_scale * (u1[pi] - us1[pi]);
+  }
+  cl.sync();
+  for (int k = 0; k < A.nu_post; ++k) {
+    slab_pass<NT>(S, 1, cl);
+    slab_pass<NT>(S, 0, cl);
+  }
+  // copy out u^2 (and the FAS rhs b^2 of the first mu call)
+  for (int i = threadIdx.x; i < S.n; i += NT) {
+    const int c = i >= (S.n >> 1);
+    int x, y, z;
+    slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
+    const int zg = SLZ * rank + z;
+    const int t = __ldg(C.tmap2 + ((zg >> 3) * (C.ny >> 3) + (y >> 3)) * (C.nx >> 3) + (x >> 3));
+    const size_t gi = (size_t)(t - A.NL) * TB3 + cslot(x & 7, y & 7, zg & 7);
+    A.u_inner[gi] = S.u[i];
+    if (C.fas_first) A.b_inner[gi] = S.b[i];
+  }
+}
+
+// setup: level-2 coefficient records -> the slab planes [CC][NP][nS]
+__global__ void k_slab_coef(const float* coef, const int* tmap2, int nx, int ny, float* dst) {
+  const int nS = nx * ny * SLZ;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nS * CC) return;
+  const int rank = g / nS, i = g % nS;
+  Slab S;
+  S.nx = nx; S.ny = ny; S.n = nS; S.hx = nx >> 1; S.hxy = S.hx * ny;
+  const int c = i >= (nS >> 1);
+  int x, y, z;
+  slab_cell(S, c, i - c * (nS >> 1), x, y, z);
+  const int zg = SLZ * rank + z;
+  const int t = tmap2[((zg >> 3) * (ny >> 3) + (y >> 3)) * (nx >> 3) + (x >> 3)];
+  const float* p = coef + ((size_t)t << 11) + cslot(x & 7, y & 7, zg & 7);
+  float* d = dst + (size_t)rank * NP * nS;
+  for (int k = 0; k < 4; ++k) d[(size_t)k * nS + i] = p[k * 512];
+  d[(size_t)4 * nS + i] = p[0] != 0.0f ? 1.0f / p[0] : 0.0f;
+}
 }  // namespace
 
 size_t coarse_dense_smem(int total_cells, int nK) { return sizeof(float) * ((size_t)(NP + 3) * total_cells + nK); }
@@ -464,6 +719,130 @@ void launch_coarse_dense(const Hier& h, int K, int fas_first, float* u_inner, fl
     case 512: k_coarse_dense<512><<<1, 512, sm, s>>>(A); break;
     default: k_coarse_dense<1024><<<1, 1024, sm, s>>>(A); break;
   }
+}
+
+}  // namespace octmg
+
+namespace octmg {
+
+// Levels 0..2 in one cluster of CC CTAs (k_coarse_cluster): needs the dense levels 0-1
+// (cd_K == 1), a complete inner level 2 of a unit-cube domain, and a device that can host a
+// cluster of CC CTAs with this much shared memory each.  Sets h.cc_K = 2 on success.
+octmg_status build_coarse_cluster(Hier& h, cudaStream_t s) {
+  const Tree& T = *h.tree;
+  h.cc_K = -1;
+  const char* e = getenv("OCTMG_COARSE_CLUSTER");
+  if (e && atoi(e) == 0) return OCTMG_OK;
+  if (h.cd_K != 1 || T.L < 3 || T.ext[0] != 1 || T.ext[1] != 1 || T.ext[2] != 1) return OCTMG_OK;
+  if (T.lc[2] != 0 || T.ic[2] != 64) return OCTMG_OK;
+  const int nx = 32, ny = 32, nS = nx * ny * SLZ;
+  // level-2 tile map
+  std::vector<int4> tile(T.T);
+  OCTMG_CUDA(cudaMemcpy(tile.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
+  std::vector<int> map(64, -1);
+  for (int t = T.ib[2]; t < T.ib[2] + T.ic[2]; ++t) {
+    const int4 v = tile[t];
+    if (v.x != 2 || v.y < 0 || v.y > 3 || v.z < 0 || v.z > 3 || v.w < 0 || v.w > 3) return OCTMG_OK;
+    map[(v.w * 4 + v.z) * 4 + v.y] = t;
+  }
+  for (int v : map)
+    if (v < 0) return OCTMG_OK;
+  const size_t smem = coarse_dense_smem(h.cd_total, T.ic[1] * TB3) + sizeof(float) * (size_t)(NP + 2) * nS;
+  const int NTc = 512;
+  if (cudaFuncSetAttribute(k_coarse_cluster<NTc>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+      cudaFuncSetAttribute(k_coarse_cluster<NTc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return OCTMG_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CC);
+  cfg.blockDim = dim3(NTc);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, k_coarse_cluster<NTc>, &cfg) != cudaSuccess || nclusters < 1) {
+    cudaGetLastError();
+    return OCTMG_OK;
+  }
+  int* dmap = (int*)dev_malloc(sizeof(int) * 64);
+  float* dc2 = (float*)dev_malloc(sizeof(float) * (size_t)CC * NP * nS);
+  if (!dmap || !dc2) {
+    set_error("device allocation failed (cluster coarse levels)");
+    return OCTMG_E_OOM;
+  }
+  h.allocs.push_back(dmap);
+  h.allocs.push_back(dc2);
+  OCTMG_CUDA(cudaMemcpy(dmap, map.data(), sizeof(int) * 64, cudaMemcpyHostToDevice));
+  k_slab_coef<<<(nS * CC + 255) / 256, 256, 0, s>>>(h.coef, dmap, nx, ny, dc2);
+  OCTMG_CUDA(cudaGetLastError());
+  h.cc_map = dmap;
+  h.cc_coef = dc2;
+  h.cc_smem = smem;
+  h.cc_K = 2;
+  return OCTMG_OK;
+}
+
+void launch_coarse_cluster(const Hier& h, int fas_first, float* u_inner, float* b_inner, cudaStream_t s) {
+  const Tree& T = *h.tree;
+  CCArgs C;
+  CDArgs& A = C.A;
+  for (int l = 0; l <= CD_MAXL; ++l) {
+    CDLevel& L = A.lv[l];
+    if (l <= 1) {
+      L.nx = h.cd_lv[l][0]; L.ny = h.cd_lv[l][1]; L.nz = h.cd_lv[l][2];
+      L.n = L.nx * L.ny * L.nz;
+      L.off = h.cd_lv[l][3];
+      L.ntx = T.ext[0] << l;
+      L.nty = T.ext[1] << l;
+      L.tmap = h.cd_map + h.cd_moff[l];
+      L.shx = shift_of(L.nx >> 1);
+      L.shy = shift_of(L.ny);
+    } else {
+      L = CDLevel{0, 0, 0, 0, -1, -1, 0, 0, 0, nullptr};
+    }
+  }
+  A.K = 1;
+  A.fas_first = 0;
+  A.mu = h.prm.mu;
+  A.nu_pre = h.prm.nu_pre;
+  A.nu_post = h.prm.nu_post;
+  A.nu_coarsest = h.prm.nu_coarsest;
+  A.std_form = h.prm.form == 1;
+  A.alpha = h.prm.alpha;
+  A.beta = A.std_form ? 1.0f : h.prm.beta_overshoot;
+  A.pro_scale = A.std_form ? h.prm.beta_overshoot : 1.0f;
+  A.dcoef = h.cd_coef;
+  A.u_inner = u_inner;
+  A.b_inner = b_inner;
+  A.tile = T.tile;
+  A.tK0 = T.ib[1];
+  A.NL = T.NL;
+  A.total = A.lv[0].n + A.lv[1].n;
+  C.nx = 32;
+  C.ny = 32;
+  C.dcoef2 = h.cc_coef;
+  C.tmap2 = h.cc_map;
+  C.fas_first = fas_first;
+  C.tK0 = T.ib[2];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CC);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = h.cc_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_coarse_cluster<512>, C);
 }
 
 }  // namespace octmg

@@ -235,6 +235,8 @@ void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const 
 constexpr int CD_MAXL = 3;
 octmg_status build_coarse_dense(Hier& h, int Kmax, cudaStream_t s);  // sets h.cd_K (-1: not applicable)
 void launch_coarse_dense(const Hier& h, int K, int fas_first, float* u_inner, float* b_inner, cudaStream_t s);
+octmg_status build_coarse_cluster(Hier& h, cudaStream_t s);  // sets h.cc_K = 2 (levels 0-2 in a cluster) or -1
+void launch_coarse_cluster(const Hier& h, int fas_first, float* u_inner, float* b_inner, cudaStream_t s);
 
 // direct coarsest solve (coarsest.cu)
 constexpr int C0_MAX_CELLS = 4096;
@@ -324,6 +326,10 @@ struct Hier {
   std::vector<int> cd_moff;      // per level: offset of its tile map
   float* cd_coef = nullptr;      // dense coefficient planes
   int cd_threads = 512;          // threads of its CTA
+  int cc_K = -1;                 // 2: levels 0..2 in one thread-block cluster (k_coarse_cluster), else -1
+  int* cc_map = nullptr;         // its level-2 tile map
+  float* cc_coef = nullptr;      // its level-2 slab coefficient planes
+  size_t cc_smem = 0;            // its dynamic shared memory per CTA
   int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
   int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
   float* c0M = nullptr;          // direct coarsest solve: M0 [c0n][c0n] (coarsest = 1)

@@ -255,9 +255,9 @@ def test_full_size_cfg2_parity(om):
                                  {"OCTMG_SUBCYCLE_CTAS": "8", "OCTMG_SUBCYCLE_LD": "2"},
                                  {"OCTMG_GRID": "1", "OCTMG_GRID_TILES": "64"}, {"OCTMG_PASS_BIG": "1"},
                                  {"OCTMG_PASS_V": "2"}, {"OCTMG_PASS_GHOST": "inline"}, {"OCTMG_PASS_GHOST": "call"},
-                                 {"OCTMG_COARSE_DENSE": "0"},
+                                 {"OCTMG_COARSE_DENSE": "0"}, {"OCTMG_COARSE_CLUSTER": "0"},
                                  {"OCTMG_APPLY_IRR": "inline"}])
-@pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64"])
+@pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64", "sphere_35"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -302,7 +302,7 @@ def test_apply_smooth_input_matches_oracle(om, name):
 @pytest.mark.parametrize("gather", [0, 1])
 @pytest.mark.parametrize("parts", [2, 3, 4])
 @pytest.mark.parametrize("name", ["uniform64", "sphere_small", "tank_small", "sphere_small_dir", "sphere_35"])
-def test_loopback_partition_matches_single(om, name, parts, gather):
+def test_loopback_partition_matches_single(om, name, parts, gather, monkeypatch):
     """P parts of a Morton-range partition in one process (loopback transport: the halo
     exchanges, the gather of the restricted parents into the replicated levels below the
     partition level and the scalar allreduces are device copies), with the default
@@ -313,12 +313,15 @@ def test_loopback_partition_matches_single(om, name, parts, gather):
     tree = om.Tree(cfg["tiles"], cfg["ext"], cfg["wall_bc"])
     kind = torch.from_numpy(cfg["kind"]).to(DEV)
     frac = None if cfg["w"] is None else torch.from_numpy(np.ascontiguousarray(cfg["w"])).to(DEV)
-    h1 = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
-    hp = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"], loopback_parts=parts, gather_below_cells=gather)
     lcnt = tree.leaf_count + tree.inner_count
     lmin = int(np.flatnonzero(tree.leaf_count)[0])
     cand = [l for l in range(lmin + 1) if lcnt[l] >= 8 * parts and lcnt[l] * 512 >= (gather or (1 << 21))]
-    assert hp.partition(0)[0] == (cand[0] if cand else lmin)
+    lg = cand[0] if cand else lmin
+    if lg <= 2:  # level 2 partitioned: its per-level kernels, not the cluster one, in both runs
+        monkeypatch.setenv("OCTMG_COARSE_CLUSTER", "0")
+    h1 = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"])
+    hp = om.Hierarchy(tree, kind, face_frac=frac, mu=cfg["mu"], loopback_parts=parts, gather_below_cells=gather)
+    assert hp.partition(0)[0] == lg
     # ownership: every leaf tile owned by exactly one part
     owned = np.zeros(tree.NL, dtype=np.int64)
     for p in range(parts):
