@@ -219,6 +219,8 @@ void read_env(Hier& h) {
   const char* rv = getenv("OCTMG_RESTRICT_V");
   // 6 / 8: k_restrict_v2 at >= 6 / 8 CTAs/SM; 1: staged k_restrict_direct
   h.restrict_v2 = !rv ? 6 : (std::string(rv) == "1" ? 0 : (std::string(rv) == "8" ? 8 : 6));
+  const char* rw = getenv("OCTMG_RESTRICT_ROW");
+  h.restrict_row = rw ? (atoi(rw) != 0 ? 1 : 0) : -1;
   const Tree& T = *h.tree;
   const char* gv = getenv("OCTMG_GRID");
   const bool grid = gv && std::string(gv) == "1";
@@ -402,7 +404,13 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
   ProfScope ps(h, cls, s, bytes, op.level);
   if (mode == SM_RESTRICT) {
-    launch_restrict_direct(a, s, h.restrict_v2);
+    // levels with T-junction tiles: the row-form restriction (its ghost path in the row);
+    // OCTMG_RESTRICT_ROW=0 keeps k_restrict_v2 everywhere, =1 takes the row form everywhere
+    // (measured: faster on config 3's 85696-tile level 7 — 3.86 vs 4.13 ms per solve — slower on
+    // config 4's smaller ghost levels, so only on ghost levels of >= 32768 tiles)
+    const bool big_ghost = h.lvl_ghost[l] && T.lc[l] + T.ic[l] >= 32768;
+    const int rr = h.restrict_row < 0 ? (big_ghost ? 64 : 0) : (h.restrict_row ? 64 : 0);
+    launch_restrict_direct(a, s, h.restrict_v2 ? (h.restrict_v2 | rr) : 0);
   } else {
     // kernel chosen by the level's total tile count, so every part of a partitioned solve runs
     // the same per-tile arithmetic as the single-part solve
@@ -565,7 +573,7 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_TRY(halloc(h.allocs, &h.p0, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.p1, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.q, NLc));
-  h.n_partial = std::max<size_t>((size_t)T.NL, 2 * (size_t)vec_grid()) + 16;
+  h.n_partial = std::max<size_t>(4 * (size_t)T.NL + 512, 2 * (size_t)vec_grid()) + 16;  // apply: 4 warp partials per leaf tile + chunk sums
   OCTMG_TRY(halloc(h.allocs, &h.partial, h.n_partial));
   OCTMG_TRY(halloc(h.allocs, &h.counter, 16));
   OCTMG_TRY(halloc(h.allocs, &h.bar, 1));
@@ -1092,7 +1100,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
-    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (5 + (ns ? 1 : 0) + (g.comm ? 1 : 0)) + 1);
+    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 + (ns ? 1 : 0) + (g.comm ? 1 : 0)) + 1);
     hist_lim = LOOP_HCAP;
     if (report && report->history) {
       const int nh = std::min(kk, std::min((int)report->history_cap, LOOP_HCAP));
@@ -1131,7 +1139,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
         launch_apply(a, s);
       }
     }
-    g.launches += 2 * np;
+    g.launches += 3 * np;  // apply, chunk sums, finish
     OCTMG_TRY(allreduce(g, SF_PQ, 1, s));
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r

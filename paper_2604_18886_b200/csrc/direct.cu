@@ -365,6 +365,73 @@ __global__ __launch_bounds__(NT, MINB) void k_restrict_v2(SmoothArgs a) {
   }
 }
 
+// Residual + restriction + Avg (Alg. 4 lines 8-10) in the row layout of k_apply_v6, for the
+// levels that have T-junction (ghost) tiles: thread j of a 128-thread tile CTA owns row
+// j >> 1 of colour j & 1.  r = b - A^l u per cell with the Eq. 12 ghosts substituted in the
+// row (rowk::row_ghosts; m_P by shuffles), then per 2x2x2 block the residual sum r_own +
+// r_oth (lane j^1), + the row y^1 (j^2), + the row z^1 (j^16) — k_restrict_v2's order — and
+// the active-u mean m_P.  The rows with z even write the four parent cells of their block
+// row, one each ((y & 1) * 2 + colour).  On ghost-free levels k_restrict_v2 (pairs of cells
+// per thread) is faster (config 2: 0.94 vs 1.04 ms per solve); on ghost levels this one
+// (config 3: 3.80 vs 4.18 ms) — the per-cell general ghost path is the slow part there.
+template <bool GHOST>
+__device__ __forceinline__ void restrict_row_body(const SmoothArgs& a, int t, const int (&nb)[6]) {
+  using namespace rowk;
+  const int4 tv = __ldg(a.tile + t);
+  const int P = __ldg(a.parent + t);
+  const RowGeo g = row_geo(threadIdx.x & 1, threadIdx.x >> 1);
+  const float* ut = tptr(a.u, t, a.NL);
+  const float* ct = a.coef + ((size_t)t << 11);
+  const float4 q0 = ld4(ct + g.own), qx = ld4(ct + 512 + g.own), qy = ld4(ct + 1024 + g.own),
+               qz = ld4(ct + 1536 + g.own);
+  const float4 uu = ld4(ut + g.own);
+  const float4 bb = ld4(tptr(a.b, t, a.NL) + g.own);
+  const float4 co = ld4(ct + g.oth);
+  const Fld uf = a.u;
+  const int NL = a.NL;
+  auto tu = [uf, NL](int n) -> const float* { return tptr(uf, n, NL); };
+  RowSt s;
+  row_load(s, tu, a.coef, t, nb, g);
+  const float4 mP = row_block_mean<2, 16>(msk4(uu, q0), q0, msk4(s.ox, co), co);
+  if (GHOST) {
+    const Fld ucf = a.uc;
+    auto uc_of = [ucf, NL](int C) -> const float* { return tptr(ucf, C, NL); };
+    row_ghosts<false>(s, g, t, nb, tv, a.coef, a.glayer_val, a.glayer, uc_of, uu, mP);
+  }
+  const float4 f = row_sums(s, g, qx, qy, qz, make_float4(q0.x * uu.x, q0.y * uu.y, q0.z * uu.z, q0.w * uu.w));
+  const unsigned FULL = 0xffffffffu;
+  float rs[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const float c = e4(q0, m);
+    float v = c != 0.0f ? e4(bb, m) - e4(f, m) : 0.0f;
+    v += __shfl_xor_sync(FULL, v, 1);
+    v += __shfl_xor_sync(FULL, v, 2);
+    v += __shfl_xor_sync(FULL, v, 16);
+    rs[m] = v;
+  }
+  if ((g.z & 1) == 0) {
+    const int m = 2 * (g.y & 1) + (threadIdx.x & 1);
+    const int pc = cslot(((tv.y & 1) << 2) + m, ((tv.z & 1) << 2) + (g.y >> 1), ((tv.w & 1) << 2) + (g.z >> 1));
+    const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
+    const float mm = e4(mP, m);
+    a.u.inner[pi] = a.std_form ? 0.0f : mm;  // Alg. 2: zero coarse guess, u* = 0
+    a.ustar_w[pi] = a.std_form ? 0.0f : mm;
+    a.b.inner[pi] = a.beta * ((m == 0 ? rs[0] : m == 1 ? rs[1] : m == 2 ? rs[2] : rs[3]) / a.alpha);
+  }
+}
+
+__global__ __launch_bounds__(128, 6) void k_restrict_row(const __grid_constant__ SmoothArgs a) {
+  const int t = a.order[blockIdx.x];
+  int nb[6];
+  rowk::load_nb(a.nbr, t, nb);
+  bool ghost = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
+  if (ghost) restrict_row_body<true>(a, t, nb);  // CTA-uniform
+  else restrict_row_body<false>(a, t, nb);
+}
+
 // Prolongation of the coarse update, in place: u_i += u^{l-1}_P - u*_P for every active
 // cell (Alg. 4 line 15; no beta).  4 cells per thread (float4).
 __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
@@ -486,6 +553,10 @@ void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt) {
 
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2) {
   if (!a.n) return;
+  if (v2 & 64) {  // a level with ghost tiles: the row form
+    k_restrict_row<<<a.n, 128, 0, s>>>(a);
+    return;
+  }
   if (v2 == 8) k_restrict_v2<8><<<a.n, NT, 0, s>>>(a);
   else if (v2) k_restrict_v2<6><<<a.n, NT, 0, s>>>(a);
   else k_restrict_direct<<<a.n, NT, 0, s>>>(a);

@@ -3,6 +3,8 @@
 // colour row of 4 cells per thread (rowtile.cuh); the operator is evaluated in flux form
 // with the exact row sums of setup.cu (k_leaf_rowsum); the +face coupling comes from the
 // neighbour record or the ghost layer.
+#include <algorithm>
+
 #include "octmg_internal.cuh"
 #include "rowtile.cuh"
 
@@ -88,10 +90,12 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
                                c0.w != 0.0f ? f.w : 0.0f);
   *reinterpret_cast<float4*>(a.q + ((size_t)t << 9) + g.own) = r;
   if (DOT) {
-    const double dd = (double)pv.x * (double)r.x + (double)pv.y * (double)r.y + (double)pv.z * (double)r.z +
-                      (double)pv.w * (double)r.w;
-    double bs = block_reduce_d(dd, sred);
-    if (threadIdx.x == 0) a.partial[blockIdx.x] = bs;
+    // fp64 partial per warp (4 per tile, no CTA barrier: the warps of an irregular tile finish
+    // independently); k_finish_sigma sums them in tile order (deterministic)
+    double dd = (double)pv.x * (double)r.x + (double)pv.y * (double)r.y + (double)pv.z * (double)r.z +
+                (double)pv.w * (double)r.w;
+    for (int o = 16; o; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+    if ((threadIdx.x & 31) == 0) a.partial[4 * (size_t)blockIdx.x + (threadIdx.x >> 5)] = dd;
   }
 }
 
@@ -121,7 +125,23 @@ __global__ __launch_bounds__(128, INL ? 6 : 8) void k_apply_v6(const __grid_cons
   apply_row_body<DOT, false>(a, t, nb, sred);
 }
 
-// sigma = p.q from the per-tile partials (fixed order => deterministic)
+// first stage of the p.q sum: block b adds the contiguous chunk b of the per-warp partials
+// in a fixed order (deterministic), so the final single-CTA stage reads a few hundred values
+__global__ __launch_bounds__(256) void k_chunk_sums(const double* partial, int64_t n, int64_t chunk, double* out) {
+  __shared__ double sred[8];
+  const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  double s0 = 0.0, s1 = 0.0;
+  int64_t k = lo + threadIdx.x;
+  for (; k + 256 < hi; k += 512) {
+    s0 += partial[k];
+    s1 += partial[k + 256];
+  }
+  for (; k < hi; k += 256) s0 += partial[k];
+  const double bs = block_reduce_d(s0 + s1, sred);
+  if (threadIdx.x == 0) out[blockIdx.x] = bs;
+}
+
+// sigma = p.q from the partials (fixed order => deterministic)
 __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, int n, Scalars* sc) {
   __shared__ double sred[32];
   // four independent accumulators per thread keep several loads in flight (fixed order)
@@ -380,7 +400,12 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   if (a.partial) {
     if (inl) k_apply_v6<true, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<true, false><<<a.ntiles, 128, 0, s>>>(a);
-    k_finish_sigma<<<1, 1024, 0, s>>>(a.partial, a.ntiles, a.sc);
+    // 4 warp partials per tile, summed in two fixed-order stages
+    const int64_t n = 4 * (int64_t)a.ntiles;
+    const int G = (int)std::min<int64_t>(296, (n + 4095) / 4096);
+    const int64_t chunk = (n + G - 1) / G;
+    k_chunk_sums<<<G, 256, 0, s>>>(a.partial, n, chunk, a.partial + n);
+    k_finish_sigma<<<1, 1024, 0, s>>>(a.partial + n, G, a.sc);
   } else {
     if (inl) k_apply_v6<false, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<false, false><<<a.ntiles, 128, 0, s>>>(a);
