@@ -227,10 +227,10 @@ __device__ __noinline__ void pass_row_ghost(const SmoothArgs& a, int t, int n0, 
   pass_row_body<MODE, true>(a, t, nb);
 }
 
-// INL: the ghost body inlined, at 12 CTAs/SM (80 registers: no spills on either path)
+// INL: the ghost body inlined (1: at 12 CTAs/SM, 80 registers; 2: at 14 CTAs/SM, 72 registers)
 // instead of out of line at 16 (the regular path's occupancy; the ghost body spills)
-template <int MODE, bool INL>
-__global__ __launch_bounds__(64, INL ? 12 : 16) void k_pass_v3(const __grid_constant__ SmoothArgs a) {
+template <int MODE, int INL>  // INL: 0 out of line (16 CTAs/SM), 1 inline at 12, 2 inline at 14
+__global__ __launch_bounds__(64, INL == 1 ? 12 : (INL == 2 ? 14 : 16)) void k_pass_v3(const __grid_constant__ SmoothArgs a) {
   const int t = a.order[blockIdx.x];
   int nb[6];
   rowk::load_nb(a.nbr, t, nb);
@@ -238,7 +238,7 @@ __global__ __launch_bounds__(64, INL ? 12 : 16) void k_pass_v3(const __grid_cons
 #pragma unroll
   for (int f = 0; f < 6; ++f) ghost |= nb[f] <= -2;
   if (MODE != SM_ZERO1 && ghost) {  // CTA-uniform
-    if (INL) pass_row_body<MODE, true>(a, t, nb);
+    if (INL != 0) pass_row_body<MODE, true>(a, t, nb);
     else pass_row_ghost<MODE>(a, t, nb[0], nb[1], nb[2], nb[3], nb[4], nb[5]);
     return;
   }
@@ -496,6 +496,18 @@ static bool pass_ghost_inline(bool level_has_ghosts) {
   return mode == 1 || (mode == 0 && level_has_ghosts);
 }
 
+// the inlined ghost body at 14 CTAs/SM (72 registers, 16 B of spills; measured config 3
+// 10.19 -> 9.58 ms and config 4 21.4 -> 20.0 ms of passes per solve against 12 CTAs/SM at 80
+// registers); OCTMG_PASS_GHOST_MINB=12 for the latter
+static int pass_ghost_minb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OCTMG_PASS_GHOST_MINB");
+    v = e ? atoi(e) : 14;
+  }
+  return v;
+}
+
 // OCTMG_PASS_V=2: the scalar k_pass_v2 on big levels instead of the 128-bit k_pass_v3
 static bool pass_v3_enabled() {
   static int on = -1;
@@ -515,14 +527,16 @@ static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool 
   const int grid = a.n;
   if (CPT == 4 && v2 && pass_v3_enabled()) {  // 128-bit row form (CPT 4 = 64 threads per tile)
     switch (mode) {
-      case SM_ZERO1: k_pass_v3<SM_ZERO1, false><<<grid, 64, 0, s>>>(a); break;
+      case SM_ZERO1: k_pass_v3<SM_ZERO1, 0><<<grid, 64, 0, s>>>(a); break;
       case SM_ZERO2:
-        if (pass_ghost_inline(ghosts)) k_pass_v3<SM_ZERO2, true><<<grid, 64, 0, s>>>(a);
-        else k_pass_v3<SM_ZERO2, false><<<grid, 64, 0, s>>>(a);
+        if (!pass_ghost_inline(ghosts)) k_pass_v3<SM_ZERO2, 0><<<grid, 64, 0, s>>>(a);
+        else if (pass_ghost_minb() == 14) k_pass_v3<SM_ZERO2, 2><<<grid, 64, 0, s>>>(a);
+        else k_pass_v3<SM_ZERO2, 1><<<grid, 64, 0, s>>>(a);
         break;
       default:
-        if (pass_ghost_inline(ghosts)) k_pass_v3<SM_PLAIN, true><<<grid, 64, 0, s>>>(a);
-        else k_pass_v3<SM_PLAIN, false><<<grid, 64, 0, s>>>(a);
+        if (!pass_ghost_inline(ghosts)) k_pass_v3<SM_PLAIN, 0><<<grid, 64, 0, s>>>(a);
+        else if (pass_ghost_minb() == 14) k_pass_v3<SM_PLAIN, 2><<<grid, 64, 0, s>>>(a);
+        else k_pass_v3<SM_PLAIN, 1><<<grid, 64, 0, s>>>(a);
         break;
     }
     return;
