@@ -126,6 +126,23 @@ octmg_status build_orders(Hier& h) {
     for (int t = 0; t < T.T; ++t)
       for (int f = 0; f < 6; ++f)
         if (nbr[6 * (size_t)t + f] <= -2) h.lvl_ghost[tile[t].x] = true;
+    // the face layers of inner tiles that are same-level neighbours of this part's leaf
+    // tiles: the apply reads their active-children means from pbar (k_inner_face_means)
+    if (!h.ifaces) {
+      std::vector<int2> fl;
+      for (int l = 0; l <= T.L; ++l)
+        for (int t = h.own_lb[l]; t < h.own_lb[l] + h.own_lc[l]; ++t)
+          for (int f = 0; f < 6; ++f) {
+            const int n = nbr[6 * (size_t)t + f];
+            if (n >= T.NL) fl.push_back(make_int2(n, f ^ 1));
+          }
+      h.n_ifaces = (int)fl.size();
+      OCTMG_TRY(halloc(h.allocs, &h.ifaces, std::max<size_t>(fl.size(), 1)));
+      if (!fl.empty()) {
+        OCTMG_CUDA(cudaMemcpy(h.ifaces, fl.data(), sizeof(int2) * fl.size(), cudaMemcpyHostToDevice));
+        OCTMG_TRY(halloc(h.allocs, &h.pbar, (size_t)T.NI * TB3));
+      }
+    }
   }
   auto m2 = [](uint32_t x, uint32_t y) {
     uint64_t m = 0;
@@ -278,6 +295,13 @@ octmg_status build_schedule(Group& g) {
   Builder b{g, h};
   b.fas(T.L, false);
   return OCTMG_OK;
+}
+
+// parts whose apply first forms the inner-face children means (one more kernel per apply)
+int inner_mean_kernels(const Group& g) {
+  int n = 0;
+  for (const Hier* h : g.parts) n += h->n_ifaces > 0;
+  return n;
 }
 
 int64_t schedule_kernels(const Group& g) {
@@ -732,6 +756,7 @@ ApplyArgs apply_args(const Hier& h) {
   if (h.nranks == 1 && h.n_apply_tiles == h.tree->NL) a.tiles = nullptr;  // identity: skip the indirection
   a.tile = T.tile; a.nbr = T.nbr; a.child = T.child; a.coef = h.coef; a.glayer_val = h.glayer_val;
   a.glayer = T.glayer; a.dtile = h.dtile; a.dval = h.dval; a.z = nullptr; a.q = nullptr;
+  a.pbar = h.pbar; a.ifaces = h.ifaces; a.n_ifaces = h.n_ifaces;
   a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL;
   return a;
 }
@@ -1100,7 +1125,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
-    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 + (ns ? 1 : 0) + (g.comm ? 1 : 0)) + 1);
+    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 + (ns ? 1 : 0) + (g.comm ? 1 : 0)) + 1 + inner_mean_kernels(g));
     hist_lim = LOOP_HCAP;
     if (report && report->history) {
       const int nh = std::min(kk, std::min((int)report->history_cap, LOOP_HCAP));
@@ -1139,7 +1164,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
         launch_apply(a, s);
       }
     }
-    g.launches += 3 * np;  // apply, chunk sums, finish
+    g.launches += 3 * np + inner_mean_kernels(g);  // (inner-face means,) apply, chunk sums, finish
     OCTMG_TRY(allreduce(g, SF_PQ, 1, s));
     for (Hier* h : g.parts) {
       ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r

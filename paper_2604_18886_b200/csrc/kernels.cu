@@ -69,9 +69,12 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
   const float4 c0 = ld4(ct + g.own), cxm = ld4(ct + 512 + g.own), cym = ld4(ct + 1024 + g.own),
                czm = ld4(ct + 1536 + g.own);
   const int NL = a.NL;
-  // leaf values of tile n; an inner neighbour's entries are replaced below (row_inner), so
-  // its unconditional row load reads the own tile instead
-  auto tu = [pz, NL, t](int n) -> const float* { return pz + ((size_t)(n < NL ? n : t) << 9); };
+  // values of tile n: a leaf's p, or for a same-level inner neighbour the means of its
+  // active children precomputed on the face layer the row reads (k_inner_face_means)
+  const float* pb = a.pbar;
+  auto tu = [pz, pb, NL](int n) -> const float* {
+    return n < NL ? pz + ((size_t)n << 9) : pb + ((size_t)(n - NL) << 9);
+  };
   RowSt s;
   row_load<decltype(tu), true>(s, tu, a.coef, t, nb, g);
   const float4 d = dk >= 0 ? ld4(a.dval + ((size_t)dk << 9) + g.own) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -82,8 +85,6 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
     const float4 mP = row_block_mean<2, 16>(pv, c0, msk4(s.ox, co), co);
     row_ghosts<false, decltype(tu), true>(s, g, t, nb, __ldg(a.tile + t), a.coef, a.glayer_val, a.glayer, tu, pv,
                                           mP, &rp);
-    auto pvf = [pz](int tt, int sl) { return __ldg(pz + ((size_t)tt << 9) + sl); };
-    row_inner<decltype(pvf), true>(s, g, nb, NL, a.child, a.coef, pvf, pv, &rp);
   }
   const float4 f = row_sums_flux(s, g, rp, cxm, cym, czm, pv, d);
   const float4 r = make_float4(c0.x != 0.0f ? f.x : 0.0f, c0.y != 0.0f ? f.y : 0.0f, c0.z != 0.0f ? f.z : 0.0f,
@@ -116,13 +117,40 @@ __global__ __launch_bounds__(128, INL ? 6 : 8) void k_apply_v6(const __grid_cons
   rowk::load_nb(a.nbr, t, nb);
   bool irr = false;
 #pragma unroll
-  for (int f = 0; f < 6; ++f) irr |= nb[f] <= -2 || nb[f] >= a.NL;
+  for (int f = 0; f < 6; ++f) irr |= nb[f] <= -2;  // ghost faces (inner neighbours read pbar)
   if (irr) {  // CTA-uniform
     if (INL) apply_row_body<DOT, true>(a, t, nb, sred);
     else apply_row_irr<DOT>(a, t, nb[0], nb[1], nb[2], nb[3], nb[4], nb[5], sred);
     return;
   }
   apply_row_body<DOT, false>(a, t, nb, sred);
+}
+
+// The composite operator's value across a face toward a same-level inner tile is the mean of
+// the active children of the neighbour cell.  One CTA of 64 threads per listed
+// (inner tile, face) layer: each thread one cell of the layer, its 8 children (octant
+// dx + 2dy + 4dz, activity and value loaded together) — all loads independent, unlike the
+// same computation inside the apply's rows.  p is zero on inactive cells.
+__global__ __launch_bounds__(64) void k_inner_face_means(const int2* ifaces, const int* child, const float* coef,
+                                                        const float* p, float* pbar, int NL) {
+  const int2 it = __ldg(ifaces + blockIdx.x);
+  const int n = it.x, f = it.y, ax = f >> 1;
+  const int c2 = threadIdx.x;
+  int c[3];
+  c[ax] = (f & 1) ? 7 : 0;
+  c[ax == 0 ? 1 : 0] = c2 & 7;
+  c[ax == 2 ? 1 : 2] = c2 >> 3;
+  const int ct = __ldg(child + 8 * (size_t)(n - NL) + (c[0] >> 2) + 2 * (c[1] >> 2) + 4 * (c[2] >> 2));
+  float sm = 0.0f;
+  int k = 0;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const int sl = cslot((2 * c[0] + (d & 1)) & 7, (2 * c[1] + ((d >> 1) & 1)) & 7, (2 * c[2] + (d >> 2)) & 7);
+    const float cc = __ldg(coef + ((size_t)ct << 11) + sl);
+    const float v = __ldg(p + ((size_t)ct << 9) + sl);
+    if (cc != 0.0f) { sm += v; k++; }
+  }
+  pbar[((size_t)(n - NL) << 9) + cslot(c[0], c[1], c[2])] = k ? sm / (float)k : 0.0f;
 }
 
 // first stage of the p.q sum: block b adds the contiguous chunk b of the per-warp partials
@@ -388,6 +416,7 @@ __global__ void k_build_mask(const float* coef, int64_t nwords, uint32_t* act) {
 }  // namespace
 
 void launch_apply(const ApplyArgs& a, cudaStream_t s) {
+  if (a.n_ifaces > 0) k_inner_face_means<<<a.n_ifaces, 64, 0, s>>>(a.ifaces, a.child, a.coef, a.z, a.pbar, a.NL);
   if (a.ntiles == 0) {
     if (a.partial) cudaMemsetAsync(&a.sc->sum_pq, 0, sizeof(double), s);
     return;

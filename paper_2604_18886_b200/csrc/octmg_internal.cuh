@@ -160,6 +160,9 @@ struct ApplyArgs {
   const int* dtile;     // leaf row sums (flux form): tile -> row of dval, -1 = all zero
   const float* dval;
   const float* z;       // p (user x for octmg_apply), zero on inactive cells
+  float* pbar;          // inner-tile field: the active-children means of p on the listed face layers
+  const int2* ifaces;   // (inner tile, face) layers neighbouring this part's leaf tiles
+  int n_ifaces;
   float* q;             // A p
   double* partial;      // per-tile fp64 partial of p.q (nullptr: no dot)
   unsigned* counter;
@@ -288,6 +291,9 @@ struct Hier {
   float* coef = nullptr;         // [T*2048] SoA per tile: c, cxm, cym, czm planes (cidx)
   uint32_t* act = nullptr;       // [NL*512/32] activity bitmask of the leaf cells
   float* glayer_val = nullptr;   // [n_glayers*64]
+  int2* ifaces = nullptr;        // (inner tile, face) layers the composite apply reads as children means
+  int n_ifaces = 0;
+  float* pbar = nullptr;         // [NI*512] those means (only the listed face layers are written)
   int* dtile = nullptr;          // [NL] leaf row sums d (flux-form apply): tile's row in dval, or -1 (all d = 0)
   float* dval = nullptr;         // [n_dtiles*512] d of those tiles (slot order)
   int n_dtiles = 0;
