@@ -236,6 +236,8 @@ void read_env(Hier& h) {
   const char* rv = getenv("OCTMG_RESTRICT_V");
   // 6 / 8: k_restrict_v2 at >= 6 / 8 CTAs/SM; 1: staged k_restrict_direct
   h.restrict_v2 = !rv ? 6 : (std::string(rv) == "1" ? 0 : (std::string(rv) == "8" ? 8 : 6));
+  const char* rd = getenv("OCTMG_RESTRICT_RED");
+  h.restrict_red = !(rd && atoi(rd) == 0);
   const char* rw = getenv("OCTMG_RESTRICT_ROW");
   h.restrict_row = rw ? (atoi(rw) != 0 ? 1 : 0) : -1;
   const Tree& T = *h.tree;
@@ -433,7 +435,10 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     // (measured: faster on config 3's 85696-tile level 7 — 3.86 vs 4.13 ms per solve — slower on
     // config 4's smaller ghost levels, so only on ghost levels of >= 32768 tiles)
     const bool big_ghost = h.lvl_ghost[l] && T.lc[l] + T.ic[l] >= 32768;
-    const int rr = h.restrict_row < 0 ? (big_ghost ? 64 : 0) : (h.restrict_row ? 64 : 0);
+    int rr = h.restrict_row < 0 ? (big_ghost ? 64 : 0) : (h.restrict_row ? 64 : 0);
+    // ghost-free levels: the red-row restriction (the black residual is zero after the black
+    // pass that ends the pre-smoothing); OCTMG_RESTRICT_RED=0 keeps k_restrict_v2
+    if (!rr && !h.lvl_ghost[l] && h.restrict_red) rr = 128;
     launch_restrict_direct(a, s, h.restrict_v2 ? (h.restrict_v2 | rr) : 0);
   } else {
     // kernel chosen by the level's total tile count, so every part of a partitioned solve runs

@@ -432,6 +432,62 @@ __global__ __launch_bounds__(128, 6) void k_restrict_row(const __grid_constant__
   else restrict_row_body<false>(a, t, nb);
 }
 
+// Residual + restriction + Avg on a level without T-junction tiles, right after the
+// pre-smoothing's last pass (black): that pass set every black cell to u_B = (b_B - sum_f
+// c_f u_f) / c_B from its red neighbours, which have not changed since, so r_B = b_B - c_B u_B
+// - sum_f c_f u_f = 0 (in exact arithmetic; in fp32 a recomputation would only add the
+// cancellation noise of b - c u - sum).  Only the red rows are computed: thread j of a
+// 64-thread tile CTA owns red row (y, z) = (j & 7, j >> 3) — the colour pass's layout and
+// loads, plus the black c plane for the Avg activity — and the block sums are the red
+// residuals of the rows y, y^1 (lane j^1) and z^1 (lane j^8) (k_restrict_v2's pair / y / z
+// order with a zero black term).  The rows with z even write the block row's four parents,
+// two each.  22 B per cell instead of 25.5, and one stencil per two cells.
+__global__ __launch_bounds__(64, 14) void k_restrict_red(const __grid_constant__ SmoothArgs a) {
+  using namespace rowk;
+  const int t = a.order[blockIdx.x];
+  int nb[6];
+  load_nb(a.nbr, t, nb);
+  const int4 tv = __ldg(a.tile + t);
+  const int P = __ldg(a.parent + t);
+  const RowGeo g = row_geo(0, threadIdx.x);
+  const float* ut = tptr(a.u, t, a.NL);
+  const float* ct = a.coef + ((size_t)t << 11);
+  const float4 q0 = ld4(ct + g.own), qx = ld4(ct + 512 + g.own), qy = ld4(ct + 1024 + g.own),
+               qz = ld4(ct + 1536 + g.own);
+  const float4 uu = ld4(ut + g.own);
+  const float4 bb = ld4(tptr(a.b, t, a.NL) + g.own);
+  const float4 co = ld4(ct + g.oth);
+  const Fld uf = a.u;
+  const int NL = a.NL;
+  auto tu = [uf, NL](int n) -> const float* { return tptr(uf, n, NL); };
+  RowSt s;
+  row_load(s, tu, a.coef, t, nb, g);
+  const float4 mP = row_block_mean<1, 8>(msk4(uu, q0), q0, msk4(s.ox, co), co);
+  const float4 f = row_sums(s, g, qx, qy, qz, make_float4(q0.x * uu.x, q0.y * uu.y, q0.z * uu.z, q0.w * uu.w));
+  const unsigned FULL = 0xffffffffu;
+  float rs[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const float c = e4(q0, m);
+    float v = c != 0.0f ? e4(bb, m) - e4(f, m) : 0.0f;
+    v += __shfl_xor_sync(FULL, v, 1);
+    v += __shfl_xor_sync(FULL, v, 8);
+    rs[m] = v;
+  }
+  if ((g.z & 1) == 0) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int m = 2 * (g.y & 1) + k;
+      const int pc = cslot(((tv.y & 1) << 2) + m, ((tv.z & 1) << 2) + (g.y >> 1), ((tv.w & 1) << 2) + (g.z >> 1));
+      const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
+      const float mm = e4(mP, m);
+      a.u.inner[pi] = a.std_form ? 0.0f : mm;  // Alg. 2: zero coarse guess, u* = 0
+      a.ustar_w[pi] = a.std_form ? 0.0f : mm;
+      a.b.inner[pi] = a.beta * ((m == 0 ? rs[0] : m == 1 ? rs[1] : m == 2 ? rs[2] : rs[3]) / a.alpha);
+    }
+  }
+}
+
 // Prolongation of the coarse update, in place: u_i += u^{l-1}_P - u*_P for every active
 // cell (Alg. 4 line 15; no beta).  4 cells per thread (float4).
 __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
@@ -569,6 +625,10 @@ void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2) {
   if (!a.n) return;
   if (v2 & 64) {  // a level with ghost tiles: the row form
     k_restrict_row<<<a.n, 128, 0, s>>>(a);
+    return;
+  }
+  if (v2 & 128) {  // a ghost-free level after a black pass: red rows only
+    k_restrict_red<<<a.n, 64, 0, s>>>(a);
     return;
   }
   if (v2 == 8) k_restrict_v2<8><<<a.n, NT, 0, s>>>(a);

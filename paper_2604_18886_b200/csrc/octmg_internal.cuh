@@ -323,6 +323,7 @@ struct Hier {
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
+  bool restrict_red = true;      // red-row restriction on ghost-free levels (OCTMG_RESTRICT_RED=0: off)
   int restrict_row = -1;         // row-form restriction: -1 on levels with ghost tiles, 0 never, 1 always (OCTMG_RESTRICT_ROW)
   int restrict_v2 = 6;           // k_restrict_v2 (vectorised regular tiles) at >= 6 (8: OCTMG_RESTRICT_V=8) CTAs/SM; 0: staged k_restrict_direct (OCTMG_RESTRICT_V=1)
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
