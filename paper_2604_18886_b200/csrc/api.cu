@@ -118,10 +118,10 @@ octmg_status build_orders(Hier& h) {
   const Tree& T = *h.tree;
   std::vector<int4> tile(T.T);
   OCTMG_CUDA(cudaMemcpy(tile.data(), T.tile, sizeof(int4) * T.T, cudaMemcpyDeviceToHost));
+  std::vector<int> nbr((size_t)T.T * 6);
+  OCTMG_CUDA(cudaMemcpy(nbr.data(), T.nbr, sizeof(int) * nbr.size(), cudaMemcpyDeviceToHost));
   {
     // levels with a T-junction (ghost) face anywhere (all parts decide alike)
-    std::vector<int> nbr((size_t)T.T * 6);
-    OCTMG_CUDA(cudaMemcpy(nbr.data(), T.nbr, sizeof(int) * nbr.size(), cudaMemcpyDeviceToHost));
     for (int l = 0; l <= MAXL; ++l) h.lvl_ghost[l] = false;
     for (int t = 0; t < T.T; ++t)
       for (int f = 0; f < 6; ++f)
@@ -159,6 +159,15 @@ octmg_status build_orders(Hier& h) {
       if (tile[a].w != tile[b].w) return tile[a].w < tile[b].w;
       return m2(tile[a].y, tile[a].z) < m2(tile[b].y, tile[b].z);
     });
+    // tiles without a ghost face first (each group keeps that order): kernels with a
+    // ghost-free fast path can be launched on the two groups separately
+    auto regular = [&](int t) {
+      for (int f = 0; f < 6; ++f)
+        if (nbr[6 * (size_t)t + f] <= -2) return false;
+      return true;
+    };
+    const auto mid = std::stable_partition(ts.begin(), ts.end(), regular);
+    h.lvl_nreg[l] = (int)(mid - ts.begin());
     h.lvl_order_off[l] = (int)order.size();
     h.lvl_n[l] = (int)ts.size();
     order.insert(order.end(), ts.begin(), ts.end());
@@ -306,10 +315,38 @@ int inner_mean_kernels(const Group& g) {
   return n;
 }
 
+// restrictions launched as two kernels (big ghost level: ghost-free tiles + ghost tiles)
+bool split_restrict(const Hier& h, int l) {
+  const Tree& T = *h.tree;
+  const bool big_ghost = h.lvl_ghost[l] && T.lc[l] + T.ic[l] >= 32768;
+  const bool row = h.restrict_row < 0 ? big_ghost : h.restrict_row == 1;
+  return row && h.restrict_red && h.restrict_v2 && h.lvl_nreg[l] > 0 && h.lvl_nreg[l] < h.lvl_n[l];
+}
+
+// colour passes launched as two kernels on big ghost levels (OCTMG_PASS_SPLIT=1; measured
+// slower than one launch with the inlined ghost body: config 3 10.28 vs 10.02 ms, config 5
+// level 9 111.7 vs 108.7 ms of passes per solve — the second launch's ramp and tail)
+bool split_pass(const Hier& h, int l, int mode) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("OCTMG_PASS_SPLIT");
+    on = e && atoi(e) == 1;
+  }
+  const Tree& T = *h.tree;
+  return on && mode != SM_ZERO1 && h.pass_v2 && h.pass_cpt == 4 && h.lvl_ghost[l] &&
+         T.lc[l] + T.ic[l] >= std::max(32768, h.pass_big) && h.lvl_nreg[l] > 0 && h.lvl_nreg[l] < h.lvl_n[l];
+}
+
 int64_t schedule_kernels(const Group& g) {
   int64_t n = 0;
-  for (const Op& op : g.ops) n += op.kind != 2 && op.kind != 7 && op.kind != 8;
-  return n * (int64_t)g.parts.size();
+  for (const Hier* h : g.parts)
+    for (const Op& op : g.ops) {
+      if (op.kind == 2 || op.kind == 7 || op.kind == 8) continue;
+      n += 1;
+      if (op.kind == 0 && (op.stage >> 1) == SM_RESTRICT && split_restrict(*h, op.level)) n += 1;
+      if (op.kind == 0 && (op.stage >> 1) != SM_RESTRICT && split_pass(*h, op.level, op.stage >> 1)) n += 1;
+    }
+  return n;
 }
 
 Fld ubuf(const Hier& h) { return Fld{h.z, h.uinA}; }
@@ -439,13 +476,35 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     // ghost-free levels: the red-row restriction (the black residual is zero after the black
     // pass that ends the pre-smoothing); OCTMG_RESTRICT_RED=0 keeps k_restrict_v2
     if (!rr && !h.lvl_ghost[l] && h.restrict_red) rr = 128;
-    launch_restrict_direct(a, s, h.restrict_v2 ? (h.restrict_v2 | rr) : 0);
+    if (rr == 64 && split_restrict(h, l)) {
+      // big ghost level: the ghost-free tiles (first in the order) with the red-row kernel,
+      // the ghost tiles with the row form
+      SmoothArgs ar = a, ag = a;
+      ar.n = h.lvl_nreg[l];
+      ag.order = a.order + h.lvl_nreg[l];
+      ag.n = a.n - h.lvl_nreg[l];
+      launch_restrict_direct(ar, s, h.restrict_v2 | 128);
+      launch_restrict_direct(ag, s, h.restrict_v2 | 64);
+    } else {
+      launch_restrict_direct(a, s, h.restrict_v2 ? (h.restrict_v2 | rr) : 0);
+    }
   } else {
     // kernel chosen by the level's total tile count, so every part of a partitioned solve runs
     // the same per-tile arithmetic as the single-part solve
     const int level_tiles = T.lc[l] + T.ic[l];
-    launch_pass_direct(a, s, (level_tiles >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0) |
-                                 (h.lvl_ghost[l] ? 32 : 0));
+    const int cpt = (level_tiles >= h.pass_big ? h.pass_cpt : 1) | (h.pass_v2 ? 16 : 0);
+    if (split_pass(h, l, mode)) {
+      // big ghost level: the ghost-free tiles (first in the order) with the regular-path
+      // kernel at 16 CTAs/SM, the ghost tiles with the inlined ghost body
+      SmoothArgs ar = a, ag = a;
+      ar.n = h.lvl_nreg[l];
+      ag.order = a.order + h.lvl_nreg[l];
+      ag.n = a.n - h.lvl_nreg[l];
+      launch_pass_direct(ar, s, cpt);
+      launch_pass_direct(ag, s, cpt | 32);
+    } else {
+      launch_pass_direct(a, s, cpt | (h.lvl_ghost[l] ? 32 : 0));
+    }
   }
 }
 

@@ -319,7 +319,8 @@ struct Hier {
   int* order = nullptr;          // [T] per level: tiles in rank order (segment at lvl_order_off)
   int lvl_order_off[MAXL + 1] = {};
   int lvl_n[MAXL + 1] = {};
-  bool lvl_ghost[MAXL + 1] = {};  // the level has T-junction (ghost) tiles (anywhere, all parts)
+  bool lvl_ghost[MAXL + 1] = {};
+  int lvl_nreg[MAXL + 1] = {};    // tiles of the level without a ghost face (first in its order segment)  // the level has T-junction (ghost) tiles (anywhere, all parts)
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)

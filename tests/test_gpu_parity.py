@@ -257,7 +257,7 @@ def test_full_size_cfg2_parity(om):
                                  {"OCTMG_GRID": "1", "OCTMG_GRID_TILES": "64"}, {"OCTMG_PASS_BIG": "1"},
                                  {"OCTMG_PASS_V": "2"}, {"OCTMG_PASS_GHOST": "inline"}, {"OCTMG_PASS_GHOST": "call"},
                                  {"OCTMG_COARSE_DENSE": "0"}, {"OCTMG_COARSE_CLUSTER": "0"},
-                                 {"OCTMG_RESTRICT_ROW": "1"}, {"OCTMG_RESTRICT_ROW": "0"}, {"OCTMG_PASS_GHOST_MINB": "12"}, {"OCTMG_RESTRICT_RED": "0"},
+                                 {"OCTMG_RESTRICT_ROW": "1"}, {"OCTMG_RESTRICT_ROW": "0"}, {"OCTMG_PASS_GHOST_MINB": "12"}, {"OCTMG_RESTRICT_RED": "0"}, {"OCTMG_PASS_SPLIT": "1"},
                                  {"OCTMG_APPLY_IRR": "inline"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64", "sphere_35"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
