@@ -316,11 +316,18 @@ int inner_mean_kernels(const Group& g) {
 }
 
 // restrictions launched as two kernels (big ghost level: ghost-free tiles + ghost tiles)
+// (every ghost level with ghost-free tiles: they take the red-row kernel; OCTMG_RESTRICT_SPLIT=
+// big: only levels of >= 32768 tiles)
 bool split_restrict(const Hier& h, int l) {
+  static int all = -1;
+  if (all < 0) {
+    const char* e = getenv("OCTMG_RESTRICT_SPLIT");
+    all = !(e && std::string(e) == "big");
+  }
   const Tree& T = *h.tree;
   const bool big_ghost = h.lvl_ghost[l] && T.lc[l] + T.ic[l] >= 32768;
-  const bool row = h.restrict_row < 0 ? big_ghost : h.restrict_row == 1;
-  return row && h.restrict_red && h.restrict_v2 && h.lvl_nreg[l] > 0 && h.lvl_nreg[l] < h.lvl_n[l];
+  const bool ok = all ? h.lvl_ghost[l] : big_ghost;
+  return ok && h.restrict_red && h.restrict_v2 && h.restrict_row != 0 && h.lvl_nreg[l] > 0 && h.lvl_nreg[l] < h.lvl_n[l];
 }
 
 // colour passes launched as two kernels on big ghost levels (OCTMG_PASS_SPLIT=1; measured
@@ -476,15 +483,15 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     // ghost-free levels: the red-row restriction (the black residual is zero after the black
     // pass that ends the pre-smoothing); OCTMG_RESTRICT_RED=0 keeps k_restrict_v2
     if (!rr && !h.lvl_ghost[l] && h.restrict_red) rr = 128;
-    if (rr == 64 && split_restrict(h, l)) {
-      // big ghost level: the ghost-free tiles (first in the order) with the red-row kernel,
-      // the ghost tiles with the row form
+    if (split_restrict(h, l)) {
+      // ghost level: the ghost-free tiles (first in the order) with the red-row kernel, the
+      // ghost tiles with the row form (big levels) or k_restrict_v2
       SmoothArgs ar = a, ag = a;
       ar.n = h.lvl_nreg[l];
       ag.order = a.order + h.lvl_nreg[l];
       ag.n = a.n - h.lvl_nreg[l];
       launch_restrict_direct(ar, s, h.restrict_v2 | 128);
-      launch_restrict_direct(ag, s, h.restrict_v2 | 64);
+      launch_restrict_direct(ag, s, h.restrict_v2 | rr);
     } else {
       launch_restrict_direct(a, s, h.restrict_v2 ? (h.restrict_v2 | rr) : 0);
     }
