@@ -194,6 +194,12 @@ __device__ __forceinline__ void pass_row_body(const SmoothArgs& a, int t, const 
     *reinterpret_cast<float4*>(ut + g.own) = r;
     return;
   }
+  int4 tv;
+  int3 gl;
+  if (GHOST) {  // the ghost path's tile origin and ghost-layer indices, issued first
+    tv = __ldg(a.tile + t);
+    gl = load_gl(a.glayer, t);
+  }
   const float4 qx = ld4(ct + 512 + g.own), qy = ld4(ct + 1024 + g.own), qz = ld4(ct + 1536 + g.own);
   const Fld uf = a.u;
   const int NL = a.NL;
@@ -207,7 +213,7 @@ __device__ __forceinline__ void pass_row_body(const SmoothArgs& a, int t, const 
     const float4 mP = row_block_mean<1, 8>(msk4(ui, q0), q0, msk4(s.ox, co), co);
     const Fld ucf = a.uc;
     auto uc_of = [ucf, NL](int C) -> const float* { return tptr(ucf, C, NL); };
-    row_ghosts<MODE == SM_ZERO2>(s, g, t, nb, __ldg(a.tile + t), a.coef, a.glayer_val, a.glayer, uc_of, ui, mP);
+    row_ghosts<MODE == SM_ZERO2>(s, g, t, nb, tv, a.coef, a.glayer_val, gl, uc_of, ui, mP);
   }
   const float4 f = row_sums(s, g, qx, qy, qz, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
   float4 r;
@@ -379,6 +385,8 @@ __device__ __forceinline__ void restrict_row_body(const SmoothArgs& a, int t, co
   using namespace rowk;
   const int4 tv = __ldg(a.tile + t);
   const int P = __ldg(a.parent + t);
+  int3 gl;
+  if (GHOST) gl = load_gl(a.glayer, t);
   const RowGeo g = row_geo(threadIdx.x & 1, threadIdx.x >> 1);
   const float* ut = tptr(a.u, t, a.NL);
   const float* ct = a.coef + ((size_t)t << 11);
@@ -396,7 +404,7 @@ __device__ __forceinline__ void restrict_row_body(const SmoothArgs& a, int t, co
   if (GHOST) {
     const Fld ucf = a.uc;
     auto uc_of = [ucf, NL](int C) -> const float* { return tptr(ucf, C, NL); };
-    row_ghosts<false>(s, g, t, nb, tv, a.coef, a.glayer_val, a.glayer, uc_of, uu, mP);
+    row_ghosts<false>(s, g, t, nb, tv, a.coef, a.glayer_val, gl, uc_of, uu, mP);
   }
   const float4 f = row_sums(s, g, qx, qy, qz, make_float4(q0.x * uu.x, q0.y * uu.y, q0.z * uu.z, q0.w * uu.w));
   const unsigned FULL = 0xffffffffu;

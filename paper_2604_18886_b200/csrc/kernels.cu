@@ -83,8 +83,10 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
   if (IRR) {
     const float4 co = ld4(ct + g.oth);
     const float4 mP = row_block_mean<2, 16>(pv, c0, msk4(s.ox, co), co);
-    row_ghosts<false, decltype(tu), true>(s, g, t, nb, __ldg(a.tile + t), a.coef, a.glayer_val, a.glayer, tu, pv,
-                                          mP, &rp);
+    // (the tile origin and ghost-layer indices loaded here, not up front: measured better for
+    // the out-of-line irregular body, whose registers are short)
+    row_ghosts<false, decltype(tu), true>(s, g, t, nb, __ldg(a.tile + t), a.coef, a.glayer_val,
+                                          rowk::load_gl(a.glayer, t), tu, pv, mP, &rp);
   }
   const float4 f = row_sums_flux(s, g, rp, cxm, cym, czm, pv, d);
   const float4 r = make_float4(c0.x != 0.0f ? f.x : 0.0f, c0.y != 0.0f ? f.y : 0.0f, c0.z != 0.0f ? f.z : 0.0f,

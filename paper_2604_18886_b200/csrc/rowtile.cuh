@@ -181,7 +181,7 @@ __device__ __forceinline__ float4 row_block_mean(const float4& own_m, const floa
 // and rp records them.
 template <bool ZERO_UC, class UC, bool FLUX = false>
 __device__ __forceinline__ void row_ghosts(RowSt& s, const RowGeo& g, int t, const int (&nb)[6], const int4& tv,
-                                           const float* coef, const float* glayer_val, const int* glayer,
+                                           const float* coef, const float* glayer_val, const int3& gl,
                                            const UC& uc_of, const float4& ui, const float4& mP,
                                            RowRep* rp = nullptr) {
   auto gval = [&](int m, int f) {
@@ -195,8 +195,8 @@ __device__ __forceinline__ void row_ghosts(RowSt& s, const RowGeo& g, int t, con
     if (FLUX) return cC != 0.0f ? 0.5f * (uc - e4(mP, m)) : -e4(ui, m);
     return cC != 0.0f ? e4(ui, m) + 0.5f * (uc - e4(mP, m)) : 0.0f;
   };
-  auto glv = [&](int ax, int x) {
-    return __ldg(glayer_val + (size_t)__ldg(glayer + 3 * t + ax) * 64 +
+  auto glv = [&](int ax, int x) {  // gl: the tile's +x / +y / +z ghost-layer indices
+    return __ldg(glayer_val + (size_t)(ax == 0 ? gl.x : (ax == 1 ? gl.y : gl.z)) * 64 +
                  (ax == 0 ? g.y + 8 * g.z : (ax == 1 ? x + 8 * g.z : x + 8 * g.y)));
   };
   const bool gx = (g.p == 0 && nb[0] <= -2) || (g.p == 1 && nb[1] <= -2);
@@ -259,6 +259,12 @@ __device__ __forceinline__ void row_inner(RowSt& s, const RowGeo& g, const int (
   if (FLUX) {
     rp->xs |= ix; rp->ym |= iym; rp->yp |= iyp; rp->zm |= izm; rp->zp |= izp;
   }
+}
+
+// the tile's +x / +y / +z ghost-layer indices (loaded early, with the tile origin, so the
+// ghost couplings are one dependent load away instead of two)
+__device__ __forceinline__ int3 load_gl(const int* glayer, int t) {
+  return make_int3(__ldg(glayer + 3 * t), __ldg(glayer + 3 * t + 1), __ldg(glayer + 3 * t + 2));
 }
 
 __device__ __forceinline__ void load_nb(const int* nbr, int t, int (&nb)[6]) {
