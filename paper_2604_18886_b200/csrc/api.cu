@@ -204,10 +204,6 @@ struct Builder {
   // Alg. 4 at level l; fas_first: first of the mu calls from level l+1 (forms the FAS rhs)
   void fas(int l, bool fas_first) {
     const Tree& T = *h.tree;
-    if (l <= h.grid_K) {  // the rest of the cycle in one cooperative grid launch
-      push(Op{9, l, fas_first ? 1 : 0});
-      return;
-    }
     if (l <= h.sub_K) {  // the rest of the cycle runs on chip in one CTA
       push(Op{4, l, fas_first ? 1 : 0});
       return;
@@ -240,22 +236,15 @@ void read_env(Hier& h) {
   h.pass_cpt = pc ? (atoi(pc) >= 4 ? 4 : std::max(1, std::min(2, atoi(pc)))) : 4;
   const char* pb = getenv("OCTMG_PASS_BIG");
   h.pass_big = pb ? std::max(1, atoi(pb)) : 1024;  // levels with >= this many tiles take pass_cpt
-  const char* pv = getenv("OCTMG_PASS_V");
-  h.pass_v2 = !(pv && std::string(pv) == "1");
-  const char* rv = getenv("OCTMG_RESTRICT_V");
-  // 6 / 8: k_restrict_v2 at >= 6 / 8 CTAs/SM; 1: staged k_restrict_direct
-  h.restrict_v2 = !rv ? 6 : (std::string(rv) == "1" ? 0 : (std::string(rv) == "8" ? 8 : 6));
+  h.pass_v2 = true;
+  h.restrict_v2 = 6;  // k_restrict_v2 at >= 6 CTAs/SM
   const char* rd = getenv("OCTMG_RESTRICT_RED");
   h.restrict_red = !(rd && atoi(rd) == 0);
   const char* rw = getenv("OCTMG_RESTRICT_ROW");
   h.restrict_row = rw ? (atoi(rw) != 0 ? 1 : 0) : -1;
   const Tree& T = *h.tree;
-  const char* gv = getenv("OCTMG_GRID");
-  const bool grid = gv && std::string(gv) == "1";
   const char* sc = getenv("OCTMG_SUBCYCLE");
-  // the grid kernel's CTA-0 tail is the one-CTA sub-cycle, so then its levels must fit one CTA
-  h.sub_ctas = grid ? 1 : subcycle_ctas();
-  const int sub_cap = subcycle_max_tiles(h.sub_ctas);
+  const int sub_cap = subcycle_max_tiles();
   h.sub_K = -1;
   if (!(sc && std::string(sc) == "0"))
     for (int l = 0; l <= std::min(T.L, subcycle_max_level()); ++l) {
@@ -263,21 +252,6 @@ void read_env(Hier& h) {
       if (h.nranks > 1 && l >= h.lg) break;  // only replicated levels run on chip
       h.sub_K = l;
     }
-  // cooperative coarse-cycle kernel (opt-in, OCTMG_GRID=1; measured slower than the
-  // per-level launches on config 2): every level below the finest from grid_K down fits it
-  // (OCTMG_GRID_TILES caps the tiles per level)
-  h.grid_K = -1;
-  const int nb = grid ? coarse_grid_blocks() : 0;
-  if (nb > 0) {
-    const char* gt = getenv("OCTMG_GRID_TILES");
-    const int cap = std::min(coarse_grid_max_tiles(nb), gt ? atoi(gt) : 1 << 30);
-    for (int l = 0; l < T.L && l <= coarse_grid_max_level(); ++l) {
-      if (h.lvl_n[l] > cap) break;
-      if (h.nranks > 1 && l >= h.lg) break;  // only replicated levels
-      h.grid_K = l;
-    }
-    if (h.grid_K <= h.sub_K) h.grid_K = -1;  // nothing above the one-CTA sub-cycle
-  }
 }
 
 octmg_status build_schedule(Group& g) {
@@ -287,7 +261,7 @@ octmg_status build_schedule(Group& g) {
     read_env(*p);
     // the on-chip sub-cycle levels as dense shared-memory grids when they are complete
     // inner levels (coarse_dense.cu); otherwise the tile-layout k_subcycle
-    if (p->sub_K >= 0 && p->grid_K < 0 && p->c0n == 0) {
+    if (p->sub_K >= 0 && p->c0n == 0) {
       OCTMG_TRY(build_coarse_dense(*p, p->nranks > 1 ? p->lg - 1 : MAXL, nullptr));
       OCTMG_CUDA(cudaDeviceSynchronize());
       if (p->cd_K >= p->sub_K) p->sub_K = p->cd_K;
@@ -426,13 +400,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
     launch_coarse_direct(a, s);
     return;
   }
-  if (op.kind == 9) {
-    ProfScope ps(h, KC_COARSE_GRID, s, 0.0, op.level);
-    cudaError_t e = launch_coarse_grid(a, T.L, l, h.sub_K, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib,
-                                       T.ic, h.bar, s);
-    if (e != cudaSuccess) set_error(std::string("k_coarse_grid launch: ") + cudaGetErrorString(e));
-    return;
-  }
+
   if (op.kind == 4 && h.cc_K == 2 && l == 2) {
     ProfScope ps(h, KC_SUBCYCLE, s, 0.0, op.level);
     launch_coarse_cluster(h, op.stage, h.uinA, h.binner, s);
@@ -445,7 +413,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   }
   if (op.kind == 4) {
     ProfScope ps(h, KC_SUBCYCLE, s, 0.0, op.level);
-    launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, h.sub_ctas, s);
+    launch_subcycle(a, T.L, l, op.stage, h.prm, h.order, h.lvl_order_off, h.lvl_n, T.ib, T.ic, s);
     return;
   }
   if (op.kind == 3) {
@@ -671,7 +639,6 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   h.n_partial = std::max<size_t>(4 * (size_t)T.NL + 512, 2 * (size_t)vec_grid()) + 16;  // apply: 4 warp partials per leaf tile + chunk sums
   OCTMG_TRY(halloc(h.allocs, &h.partial, h.n_partial));
   OCTMG_TRY(halloc(h.allocs, &h.counter, 16));
-  OCTMG_TRY(halloc(h.allocs, &h.bar, 1));
   OCTMG_TRY(halloc(h.allocs, &h.sc, 1));
   if (cudaMallocHost(&h.sc_host, sizeof(Scalars)) != cudaSuccess) {
     cudaGetLastError();

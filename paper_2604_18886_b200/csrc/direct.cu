@@ -18,50 +18,6 @@ namespace {
 
 constexpr int NT = 256;
 
-// RBGS colour pass, in place.  MODE: PLAIN, ZERO1 (first pass of the cycle:
-// all values zero), ZERO2 (second pass: own-colour cells still zero).  CPT colour cells per
-// thread (CPT = 2: the second cell is 4 z-layers up), NT/CPT threads per tile CTA.
-template <int MODE, int CPT>
-__global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_direct(SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
-  const int colour = a.stage[0] & 1;
-  const int j = threadIdx.x;
-  const int y = (j >> 2) & 7, z0 = j >> 5;
-  float* ut = tptr(a.u, t, a.NL);
-  const float* bt = tptr(a.b, t, a.NL);
-  const bool ghost = MODE != SM_ZERO1 && has_ghost(a, t);
-  float unew[CPT];
-  bool act[CPT];
-  int offs[CPT];
-#pragma unroll
-  for (int k = 0; k < CPT; ++k) {
-    const int z = z0 + k * (8 / CPT);
-    const int x = 2 * (j & 3) + ((colour + y + z) & 1);
-    const int off = loff(x, y, z);
-    offs[k] = off;
-    const float4 q = ldcoef(a.coef, (size_t)t * TB3 + off);
-    const float b = __ldg(bt + off);
-    act[k] = q.x != 0.0f;
-    unew[k] = 0.0f;
-    if (act[k]) {
-      if (MODE == SM_ZERO1) {
-        unew[k] = b / q.x;
-      } else {
-        float ui = 0.0f, mP = 0.0f;
-        if (ghost) {
-          ui = MODE == SM_ZERO2 ? 0.0f : __ldg(ut + off);
-          mP = block_mean<MODE == SM_ZERO2>(a, t, x, y, z, colour);
-        }
-        unew[k] = (b - face_sum<MODE == SM_ZERO2>(a, t, x, y, z, q, ui, mP, colour, 0.0f)) / q.x;
-      }
-    }
-  }
-  __syncthreads();  // every pass-start read of this tile precedes the in-place writes
-#pragma unroll
-  for (int k = 0; k < CPT; ++k)
-    if (act[k] || MODE == SM_ZERO1 || MODE == SM_ZERO2) ut[offs[k]] = unew[k];
-}
-
 // Regular-tile stencil context: the tile's and its six neighbours' value pointers and the
 // +face coupling planes, set up once per thread and shared by its colour cells.  In the
 // colour-split slot order all six neighbours of a cell sit in the other colour's half at
@@ -254,55 +210,10 @@ __global__ __launch_bounds__(64, INL == 1 ? 12 : (INL == 2 ? 14 : 16)) void k_pa
 // Residual r = b - A^l u and, per parent (inner, level l-1): u* = mean of the active
 // children (Avg, Alg. 4 line 9), u^{l-1} := u*, b^{l-1} := beta * (R r), R = P^T / alpha
 // (Alg. 4 lines 8-10; "residual computation and restriction step are fused").
-// Thread layout: lanes of one 2x2x2 block are 4 apart in a warp (bits 2,3 = y&1, z&1), so
-// block sums are two xor-shuffles.
-__global__ __launch_bounds__(NT, 8) void k_restrict_direct(SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
-  const int j = threadIdx.x;
-  const int x2 = j & 3;
-  const int y = ((j >> 2) & 1) | (((j >> 4) & 3) << 1);
-  const int z = ((j >> 3) & 1) | ((j >> 6) << 1);
-  const int x0 = 2 * x2;
-  const size_t base = (size_t)t * TB3;
-  const int off0 = loff(x0, y, z), off1 = off0 ^ 256;  // the x-pair: same q, opposite colours
-  const float4 q0 = ldcoef(a.coef, base + off0), q1 = ldcoef(a.coef, base + off1);
-  const float2 uu = ldpair(tptr(a.u, t, a.NL), off0);
-  const float2 bb = ldpair(tptr(a.b, t, a.NL), off0);
-  __shared__ float su_t[TB3];
-  __shared__ float scm[3][TB3];
-  su_t[off0] = uu.x;
-  su_t[off1] = uu.y;
-  scm[0][off0] = q0.y; scm[1][off0] = q0.z; scm[2][off0] = q0.w;
-  scm[0][off1] = q1.y; scm[1][off1] = q1.z; scm[2][off1] = q1.w;
-  // active u sum / count of the block (also the ghost m_P of its cells)
-  float su = (q0.x != 0.0f ? uu.x : 0.0f) + (q1.x != 0.0f ? uu.y : 0.0f);
-  int na = (q0.x != 0.0f) + (q1.x != 0.0f);
-  su += __shfl_xor_sync(0xffffffffu, su, 4);
-  na += __shfl_xor_sync(0xffffffffu, na, 4);
-  su += __shfl_xor_sync(0xffffffffu, su, 8);
-  na += __shfl_xor_sync(0xffffffffu, na, 8);
-  const float mP = na ? su / (float)na : 0.0f;
-  __syncthreads();
-  float r0 = 0.0f, r1 = 0.0f;
-  if (q0.x != 0.0f) r0 = bb.x - face_sum<false>(a, t, x0, y, z, q0, uu.x, mP, 0, q0.x * uu.x, su_t, scm);
-  if (q1.x != 0.0f) r1 = bb.y - face_sum<false>(a, t, x0 + 1, y, z, q1, uu.y, mP, 0, q1.x * uu.y, su_t, scm);
-  float rs = r0 + r1;
-  rs += __shfl_xor_sync(0xffffffffu, rs, 4);
-  rs += __shfl_xor_sync(0xffffffffu, rs, 8);
-  if (((j >> 2) & 3) == 0) {
-    const int4 tv = __ldg(a.tile + t);
-    const int P = __ldg(a.parent + t);
-    const int pc = pcell_of(tv, x0, y, z);
-    const size_t pi = (size_t)(P - a.NL) * TB3 + pc;
-    a.u.inner[pi] = a.std_form ? 0.0f : mP;  // Alg. 2: zero coarse guess, u* = 0
-    a.ustar_w[pi] = a.std_form ? 0.0f : mP;
-    a.b.inner[pi] = a.beta * (rs / a.alpha);
-  }
-}
-
-// Residual + restriction + Avg with the neighbour entries prefetched and, on tiles without a
-// ghost face, the branch-free face sum (every load in flight at once, in-tile neighbours
-// from L1).  Same thread layout and outputs as k_restrict_direct.
+// Thread j of a 256-thread tile CTA owns the x-pair (2 (j & 3), y, z); the lanes of one
+// 2x2x2 block are 4 apart in a warp (bits 2, 3 = y & 1, z & 1), so block sums are two
+// xor-shuffles.  Neighbour entries prefetched; on tiles without a ghost face the
+// branch-free face sum (every load in flight at once, in-tile neighbours from L1).
 template <int MINB>
 __global__ __launch_bounds__(NT, MINB) void k_restrict_v2(SmoothArgs a) {
   const int t = a.order[blockIdx.x];
@@ -605,18 +516,10 @@ static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool 
     }
     return;
   }
-  if (v2) {
-    switch (mode) {
-      case SM_ZERO1: k_pass_v2<SM_ZERO1, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
-      case SM_ZERO2: k_pass_v2<SM_ZERO2, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
-      default: k_pass_v2<SM_PLAIN, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
-    }
-    return;
-  }
   switch (mode) {
-    case SM_ZERO1: k_pass_direct<SM_ZERO1, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
-    case SM_ZERO2: k_pass_direct<SM_ZERO2, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
-    default: k_pass_direct<SM_PLAIN, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+    case SM_ZERO1: k_pass_v2<SM_ZERO1, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+    case SM_ZERO2: k_pass_v2<SM_ZERO2, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
+    default: k_pass_v2<SM_PLAIN, CPT><<<grid, NT / CPT, 0, s>>>(a); break;
   }
 }
 
@@ -639,9 +542,7 @@ void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2) {
     k_restrict_red<<<a.n, 64, 0, s>>>(a);
     return;
   }
-  if (v2 == 8) k_restrict_v2<8><<<a.n, NT, 0, s>>>(a);
-  else if (v2) k_restrict_v2<6><<<a.n, NT, 0, s>>>(a);
-  else k_restrict_direct<<<a.n, NT, 0, s>>>(a);
+  k_restrict_v2<6><<<a.n, NT, 0, s>>>(a);
 }
 
 void launch_prolong(const SmoothArgs& a, cudaStream_t s) {

@@ -221,18 +221,11 @@ void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2);  // 0 staged, 6 / 8: k_restrict_v2 min CTAs/SM
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
-int subcycle_ctas();
-int subcycle_max_tiles(int ctas);
+int subcycle_max_tiles();
 int subcycle_max_level();
-int coarse_grid_max_level();
-int coarse_grid_max_tiles(int nblocks);
-int coarse_grid_blocks();  // co-resident CTAs of k_coarse_grid (one per SM), 0 if it cannot run
-cudaError_t launch_coarse_grid(const SmoothArgs& base, int L, int K, int sK, int fas_first,
-                               const octmg_mg_params& prm, const int* order_all, const int* lvl_off,
-                               const int* lvl_n, const int* ib, const int* ic, unsigned* bar, cudaStream_t s);
 void launch_subcycle(const SmoothArgs& base, int L, int K, int fas_first, const octmg_mg_params& prm,
                      const int* order_all, const int* lvl_off, const int* lvl_n, const int* ib, const int* ic,
-                     int ctas, cudaStream_t s);
+                     cudaStream_t s);
 
 // the coarsest complete levels as dense grids in shared memory (coarse_dense.cu)
 constexpr int CD_MAXL = 3;
@@ -279,7 +272,7 @@ struct Op {
   int kind;    // 0 smoother stage, 1 FAS rhs, 2 zero coarse leaves, 3 prolongation, 4 sub-cycle,
                // (5, 6: retired fused-RB kinds), 7 halo exchange of level
                // `level` of u, 8 broadcast of the restricted partition-parent level,
-               // 9 cooperative coarse cycle from `level` down (k_coarse_grid)
+               // (9: the retired cooperative coarse grid)
   int level;
   int stage;   // bit0 colour, bits1.. mode (SM_*)
   int in_buf = 0, out_buf = 0;
@@ -322,11 +315,11 @@ struct Hier {
   bool lvl_ghost[MAXL + 1] = {};
   int lvl_nreg[MAXL + 1] = {};    // tiles of the level without a ghost face (first in its order segment)  // the level has T-junction (ghost) tiles (anywhere, all parts)
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
-  bool pass_v2 = true;           // k_pass_v2 / k_apply_v2: prefetched neighbour entries (OCTMG_PASS_V=1: old)
+  bool pass_v2 = true;           // k_pass_v2 on the small levels (the round-1 k_pass_direct is retired)
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
   bool restrict_red = true;      // red-row restriction on ghost-free levels (OCTMG_RESTRICT_RED=0: off)
   int restrict_row = -1;         // row-form restriction: -1 on levels with ghost tiles, 0 never, 1 always (OCTMG_RESTRICT_ROW)
-  int restrict_v2 = 6;           // k_restrict_v2 (vectorised regular tiles) at >= 6 (8: OCTMG_RESTRICT_V=8) CTAs/SM; 0: staged k_restrict_direct (OCTMG_RESTRICT_V=1)
+  int restrict_v2 = 6;           // k_restrict_v2 (x-pairs) at >= 6 CTAs/SM
   int sub_K = -1;                // top level of the on-chip coarse sub-cycle (-1: none)
   int cd_K = -1;                 // top level of the dense shared-memory coarse cycle (coarse_dense.cu; -1: none)
   int cd_total = 0;              // its cells (levels 0..cd_K)
@@ -339,12 +332,9 @@ struct Hier {
   int* cc_map = nullptr;         // its level-2 tile map
   float* cc_coef = nullptr;      // its level-2 slab coefficient planes
   size_t cc_smem = 0;            // its dynamic shared memory per CTA
-  int sub_ctas = 1;              // its CTAs: 1, or one cluster (OCTMG_SUBCYCLE_CTAS)
-  int grid_K = -1;               // top level of the cooperative coarse-cycle kernel (-1: none)
   float* c0M = nullptr;          // direct coarsest solve: M0 [c0n][c0n] (coarsest = 1)
   int* c0tile = nullptr;         // its level-0 tiles
   int c0n = 0;
-  unsigned* bar = nullptr;       // its grid barrier counter
   // profiling
   bool profiling = false;
   struct Ev { int cls; double bytes; cudaEvent_t a, b; int level; };

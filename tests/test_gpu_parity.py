@@ -249,16 +249,14 @@ def test_full_size_cfg2_parity(om):
 # ---------------------------------------------------------------------------------------
 # alternative schedules selected at setup (same semantics, must match the oracle too)
 # ---------------------------------------------------------------------------------------
-@pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"},
-                                 {"OCTMG_GRID": "1"}, {"OCTMG_GRID": "1", "OCTMG_SUBCYCLE": "0"},
-                                 {"OCTMG_SUBCYCLE_CTAS": "8"}, {"OCTMG_GRAPH_LOOP": "0"}, {"OCTMG_RESTRICT_V": "8"},
-                                 {"OCTMG_RESTRICT_V": "1"}, {"OCTMG_PASS_V": "1"},
-                                 {"OCTMG_SUBCYCLE_CTAS": "8", "OCTMG_SUBCYCLE_LD": "2"},
-                                 {"OCTMG_GRID": "1", "OCTMG_GRID_TILES": "64"}, {"OCTMG_PASS_BIG": "1"},
-                                 {"OCTMG_PASS_V": "2"}, {"OCTMG_PASS_GHOST": "inline"}, {"OCTMG_PASS_GHOST": "call"},
+@pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"}, {"OCTMG_GRAPH_LOOP": "0"},
+                                 {"OCTMG_PASS_BIG": "1"}, {"OCTMG_PASS_V": "2"}, {"OCTMG_PASS_GHOST": "inline"},
+                                 {"OCTMG_PASS_GHOST": "call"}, {"OCTMG_PASS_GHOST_MINB": "12"}, {"OCTMG_PASS_SPLIT": "1"},
                                  {"OCTMG_COARSE_DENSE": "0"}, {"OCTMG_COARSE_CLUSTER": "0"},
-                                 {"OCTMG_RESTRICT_ROW": "1"}, {"OCTMG_RESTRICT_ROW": "0"}, {"OCTMG_PASS_GHOST_MINB": "12"}, {"OCTMG_RESTRICT_RED": "0"}, {"OCTMG_PASS_SPLIT": "1"},
-                                 {"OCTMG_APPLY_IRR": "inline"}])
+                                 {"OCTMG_COARSE_DENSE": "0", "OCTMG_SUBCYCLE": "0"},
+                                 {"OCTMG_RESTRICT_ROW": "1"}, {"OCTMG_RESTRICT_ROW": "0"}, {"OCTMG_RESTRICT_RED": "0"},
+                                 {"OCTMG_RESTRICT_SPLIT": "big"}, {"OCTMG_APPLY_IRR": "inline"},
+                                 {"OCTMG_CD_THREADS": "1024"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64", "sphere_35"])
 def test_schedule_variants_match_oracle(om, env, name, monkeypatch):
     for k, v in env.items():
