@@ -238,6 +238,8 @@ void read_env(Hier& h) {
   h.pass_big = pb ? std::max(1, atoi(pb)) : 1024;  // levels with >= this many tiles take pass_cpt
   h.pass_v2 = true;
   h.restrict_v2 = 6;  // k_restrict_v2 at >= 6 CTAs/SM
+  const char* to = getenv("OCTMG_TILE_ORDER");  // slab: the slab-major order array
+  h.direct_order = !(to && std::string(to) == "slab");
   const char* rd = getenv("OCTMG_RESTRICT_RED");
   h.restrict_red = !(rd && atoi(rd) == 0);
   const char* rw = getenv("OCTMG_RESTRICT_ROW");
@@ -388,6 +390,10 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.beta = a.std_form ? 1.0f : h.prm.beta_overshoot;
   a.pro_scale = a.std_form ? h.prm.beta_overshoot : 1.0f;
   a.order = h.order + h.lvl_order_off[l];
+  a.ord_leaf0 = h.own_lb[l];
+  a.ord_nleaf = h.own_lc[l];
+  a.ord_inner0 = h.own_ib[l];
+  if (h.direct_order) a.order = nullptr;  // tiles by index (Morton within leaves, inners)
   a.n = h.lvl_n[l];
   a.first_tile = T.ib[l];
   a.stage[0] = op.stage;
@@ -455,8 +461,9 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
       // ghost level: the ghost-free tiles (first in the order) with the red-row kernel, the
       // ghost tiles with the row form (big levels) or k_restrict_v2
       SmoothArgs ar = a, ag = a;
+      ar.order = h.order + h.lvl_order_off[l];
       ar.n = h.lvl_nreg[l];
-      ag.order = a.order + h.lvl_nreg[l];
+      ag.order = ar.order + h.lvl_nreg[l];
       ag.n = a.n - h.lvl_nreg[l];
       launch_restrict_direct(ar, s, h.restrict_v2 | 128);
       launch_restrict_direct(ag, s, h.restrict_v2 | rr);
@@ -472,8 +479,9 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
       // big ghost level: the ghost-free tiles (first in the order) with the regular-path
       // kernel at 16 CTAs/SM, the ghost tiles with the inlined ghost body
       SmoothArgs ar = a, ag = a;
+      ar.order = h.order + h.lvl_order_off[l];
       ar.n = h.lvl_nreg[l];
-      ag.order = a.order + h.lvl_nreg[l];
+      ag.order = ar.order + h.lvl_nreg[l];
       ag.n = a.n - h.lvl_nreg[l];
       launch_pass_direct(ar, s, cpt);
       launch_pass_direct(ag, s, cpt | 32);

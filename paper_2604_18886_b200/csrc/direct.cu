@@ -73,7 +73,7 @@ __device__ __forceinline__ float face_sum_regular(const RegCtx& c, const float* 
 // are the contiguous slots colour*256 + j + k*256/CPT.
 template <int MODE, int CPT>
 __global__ __launch_bounds__(NT / CPT, 7 * CPT) void k_pass_v2(SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
+  const int t = level_tile(a, blockIdx.x);
   int nb[6];
   {
     const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
@@ -193,7 +193,7 @@ __device__ __noinline__ void pass_row_ghost(const SmoothArgs& a, int t, int n0, 
 // instead of out of line at 16 (the regular path's occupancy; the ghost body spills)
 template <int MODE, int INL>  // INL: 0 out of line (16 CTAs/SM), 1 inline at 12, 2 inline at 14
 __global__ __launch_bounds__(64, INL == 1 ? 12 : (INL == 2 ? 14 : 16)) void k_pass_v3(const __grid_constant__ SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
+  const int t = level_tile(a, blockIdx.x);
   int nb[6];
   rowk::load_nb(a.nbr, t, nb);
   bool ghost = false;
@@ -216,7 +216,7 @@ __global__ __launch_bounds__(64, INL == 1 ? 12 : (INL == 2 ? 14 : 16)) void k_pa
 // branch-free face sum (every load in flight at once, in-tile neighbours from L1).
 template <int MINB>
 __global__ __launch_bounds__(NT, MINB) void k_restrict_v2(SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
+  const int t = level_tile(a, blockIdx.x);
   int nb[6];
   {
     const int2* np = reinterpret_cast<const int2*>(a.nbr + 6 * (size_t)t);
@@ -341,7 +341,7 @@ __device__ __forceinline__ void restrict_row_body(const SmoothArgs& a, int t, co
 }
 
 __global__ __launch_bounds__(128, 6) void k_restrict_row(const __grid_constant__ SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
+  const int t = level_tile(a, blockIdx.x);
   int nb[6];
   rowk::load_nb(a.nbr, t, nb);
   bool ghost = false;
@@ -363,7 +363,7 @@ __global__ __launch_bounds__(128, 6) void k_restrict_row(const __grid_constant__
 // two each.  22 B per cell instead of 25.5, and one stencil per two cells.
 __global__ __launch_bounds__(64, 14) void k_restrict_red(const __grid_constant__ SmoothArgs a) {
   using namespace rowk;
-  const int t = a.order[blockIdx.x];
+  const int t = level_tile(a, blockIdx.x);
   int nb[6];
   load_nb(a.nbr, t, nb);
   const int4 tv = __ldg(a.tile + t);
@@ -410,7 +410,7 @@ __global__ __launch_bounds__(64, 14) void k_restrict_red(const __grid_constant__
 // Prolongation of the coarse update, in place: u_i += u^{l-1}_P - u*_P for every active
 // cell (Alg. 4 line 15; no beta).  4 cells per thread (float4).
 __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
-  const int t = a.order[blockIdx.x];
+  const int t = level_tile(a, blockIdx.x);
   // thread j: the 4 same-q cells at slots j, j + 128 (red) and j + 256, j + 384 (black):
   // every access is a coalesced scalar per warp
   const int4 tv = __ldg(a.tile + t);

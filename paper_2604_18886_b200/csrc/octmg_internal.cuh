@@ -92,6 +92,7 @@ struct Fld {
   float* inner;
 };
 
+struct SmoothArgs;
 __device__ __forceinline__ float* tptr(const Fld& f, int t, int NL) {
   return t < NL ? f.leaf + (size_t)t * TB3 : f.inner + (size_t)(t - NL) * TB3;
 }
@@ -207,7 +208,9 @@ struct SmoothArgs {
   int std_form;         // Alg. 2: u^{l-1} := 0 and u* := 0 at restriction (no Avg, no FAS rhs)
   float pro_scale;      // prolongation: u += pro_scale (u^{l-1} - u*) (Alg. 2: beta; Alg. 4: 1)
   int NL;
-  const int* order;     // tiles of the level in rank order (slab-major)
+  const int* order;     // tiles of the level in rank order (slab-major), or nullptr: the level's
+                        // tiles by index, ord_nleaf leaves from ord_leaf0 then inners from ord_inner0
+  int ord_leaf0, ord_nleaf, ord_inner0;
   int n;                // tiles in the level
   int first_tile;       // k_fasrhs: first inner tile of the level
   int stage[1];         // bit0 colour, bits1.. mode
@@ -317,6 +320,7 @@ struct Hier {
   int pass_cpt = 4;              // colour cells per thread of the direct pass (OCTMG_PASS_CPT)
   bool pass_v2 = true;           // k_pass_v2 on the small levels (the round-1 k_pass_direct is retired)
   int pass_big = 1024;           // levels with >= pass_big tiles run pass_cpt cells/thread, smaller ones 1 (OCTMG_PASS_BIG)
+  bool direct_order = true;      // level kernels take tiles by index (OCTMG_TILE_ORDER=slab: the order array)
   bool restrict_red = true;      // red-row restriction on ghost-free levels (OCTMG_RESTRICT_RED=0: off)
   int restrict_row = -1;         // row-form restriction: -1 on levels with ghost tiles, 0 never, 1 always (OCTMG_RESTRICT_ROW)
   int restrict_v2 = 6;           // k_restrict_v2 (x-pairs) at >= 6 CTAs/SM

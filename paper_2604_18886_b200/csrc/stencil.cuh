@@ -11,6 +11,13 @@ namespace octmg {
 
 enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
 
+// the i-th tile of a level launch: from the order array, or computed (no dependent load
+// before the tile's own loads can issue)
+__device__ __forceinline__ int level_tile(const SmoothArgs& a, int i) {
+  if (a.order) return __ldg(a.order + i);
+  return i < a.ord_nleaf ? a.ord_leaf0 + i : a.ord_inner0 + (i - a.ord_nleaf);
+}
+
 // NC: 1 = read-only path (__ldg), 2 = L2 only (__ldcg; data written by other CTAs earlier
 // in the same launch, across a grid barrier), 0 = plain load (same-CTA data)
 template <int NC>
