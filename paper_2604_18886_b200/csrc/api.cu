@@ -648,7 +648,11 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_TRY(halloc(h.allocs, &h.partial, h.n_partial));
   OCTMG_TRY(halloc(h.allocs, &h.counter, 16));
   OCTMG_TRY(halloc(h.allocs, &h.sc, 1));
-  if (cudaMallocHost(&h.sc_host, sizeof(Scalars)) != cudaSuccess) {
+  // mapped pinned memory: the solve reads its scalars through a kernel that writes them
+  // there, not through a device-to-host copy, which would queue behind a caller's large
+  // copies on the copy engine (a serving loop downloads the previous solution meanwhile)
+  if (cudaHostAlloc(&h.sc_host, sizeof(Scalars), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void**)&h.sc_host_dev, h.sc_host, 0) != cudaSuccess) {
     cudaGetLastError();
     set_error("pinned allocation failed");
     return OCTMG_E_OOM;
@@ -1002,7 +1006,8 @@ octmg_status build_loop_graph(Group& g, bool ns) {
   if (!g.loop) {
     g.loop = (LoopState*)dev_malloc(sizeof(LoopState));
     if (!g.loop) { set_error("device allocation failed (PCG loop state)"); return OCTMG_E_OOM; }
-    OCTMG_CUDA(cudaMallocHost(&g.loop_host, sizeof(LoopState)));
+    OCTMG_CUDA(cudaHostAlloc(&g.loop_host, sizeof(LoopState), cudaHostAllocMapped));
+    OCTMG_CUDA(cudaHostGetDevicePointer((void**)&g.loop_host_dev, g.loop_host, 0));
   }
   if (g.loop_graph) {
     cudaGraphExecDestroy(g.loop_graph);
@@ -1100,8 +1105,8 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     }
     return st;
   };
-  auto fetch = [&]() -> octmg_status {
-    OCTMG_CUDA(cudaMemcpyAsync(hs, h0.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  auto fetch = [&]() -> octmg_status {  // the scalars into mapped host memory by a kernel
+    launch_copy_words(h0.sc, h0.sc_host_dev, sizeof(Scalars), s);
     OCTMG_CUDA(cudaStreamSynchronize(s));
     return OCTMG_OK;
   };
@@ -1159,15 +1164,14 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     L->max_iters = prm.max_iters;
     L->status = 0;
     L->converged = 0;
-    OCTMG_CUDA(cudaMemcpyAsync(g.loop, L, offsetof(LoopState, hist), cudaMemcpyHostToDevice, s));
+    launch_copy_words(g.loop_host_dev, g.loop, offsetof(LoopState, hist), s);  // read over PCIe by a kernel
     // beta = 0 on the first iteration: rho = inf, p = 0
-    static const double inf = INFINITY;
     for (Hier* h : g.parts) {
-      OCTMG_CUDA(cudaMemcpyAsync(&h->sc->rho, &inf, sizeof(double), cudaMemcpyHostToDevice, s));
+      launch_set_rho_inf(h->sc, s);
       OCTMG_CUDA(cudaMemsetAsync(h->p0, 0, sizeof(float) * (size_t)h->tree->NL * TB3, s));
     }
     OCTMG_CUDA(cudaGraphLaunch(g.loop_graph, s));
-    OCTMG_CUDA(cudaMemcpyAsync(L, g.loop, sizeof(LoopState), cudaMemcpyDeviceToHost, s));
+    launch_copy_words(g.loop, g.loop_host_dev, sizeof(LoopState), s);
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
@@ -1267,8 +1271,8 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
     }
     return st;
   };
-  auto fetch = [&]() -> octmg_status {
-    OCTMG_CUDA(cudaMemcpyAsync(hs, h0.sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  auto fetch = [&]() -> octmg_status {  // the scalars into mapped host memory by a kernel
+    launch_copy_words(h0.sc, h0.sc_host_dev, sizeof(Scalars), s);
     OCTMG_CUDA(cudaStreamSynchronize(s));
     return OCTMG_OK;
   };

@@ -459,6 +459,14 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
                    cudaStream_t s, int grid) {
   k_dot_rz<<<grid, 256, 0, s>>>(r, z, R, partial, counter, sc);
 }
+__global__ void k_set_rho_inf(Scalars* sc) { sc->rho = INFINITY; }
+__global__ void k_copy_words(const unsigned* src, unsigned* dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+void launch_set_rho_inf(Scalars* sc, cudaStream_t s) { k_set_rho_inf<<<1, 1, 0, s>>>(sc); }
+void launch_copy_words(const void* src, void* dst, size_t nbytes, cudaStream_t s) {
+  k_copy_words<<<1, 256, 0, s>>>((const unsigned*)src, (unsigned*)dst, (int)(nbytes / 4));
+}
 void launch_set_beta(Scalars* sc, cudaStream_t s) { k_set_beta<<<1, 1, 0, s>>>(sc); }
 void launch_pcg_check(Scalars* sc, LoopState* ls, unsigned long long handle, cudaStream_t s) {
   k_pcg_check<<<1, 1, 0, s>>>(sc, ls, (cudaGraphConditionalHandle)handle);

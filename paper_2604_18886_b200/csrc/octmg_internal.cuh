@@ -183,6 +183,10 @@ void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* part
                    Scalars* sc, cudaStream_t s, int grid);
 void launch_copy_ranges(const float* src, float* dst, const Ranges& R, cudaStream_t s);
 void launch_set_beta(Scalars* sc, cudaStream_t s);  // beta_f from the (all-part) sums
+void launch_set_rho_inf(Scalars* sc, cudaStream_t s);  // rho = inf (beta = 0 on the first iteration)
+// copy nbytes (a multiple of 4) between device and mapped host memory by a kernel (no copy
+// engine: small transfers never queue behind a caller's large copies)
+void launch_copy_words(const void* src, void* dst, size_t nbytes, cudaStream_t s);
 void launch_pupdate(const float* z, float* p, const Ranges& R, const Scalars* sc, bool use_beta, cudaStream_t s,
                     int grid);  // p = z + beta p in place
 void launch_mask_copy(const float* src, const uint32_t* act, float* dst, int64_t n, cudaStream_t s);  // nat -> slots
@@ -308,7 +312,8 @@ struct Hier {
   size_t n_partial = 0;
   unsigned* counter = nullptr;   // last-block counters (one per reduction slot)
   Scalars* sc = nullptr;         // device scalars
-  Scalars* sc_host = nullptr;    // pinned mirror
+  Scalars* sc_host = nullptr;    // mapped pinned mirror (host pointer)
+  Scalars* sc_host_dev = nullptr;  // its device pointer (written by launch_copy_words)
   double n_active = 0;
   int any_dirichlet = 0;
   // per-level tile orders (this part's tiles at partitioned levels)
@@ -389,7 +394,8 @@ struct Group {
   cudaStream_t graph_stream = nullptr;
   cudaGraphExec_t loop_graph = nullptr;  // the whole PCG loop as a conditional-while graph
   LoopState* loop = nullptr;             // device
-  LoopState* loop_host = nullptr;        // pinned
+  LoopState* loop_host = nullptr;        // mapped pinned (host pointer)
+  LoopState* loop_host_dev = nullptr;    // its device pointer
   int loop_ns = -1;                      // null-space flag the loop graph was built with
   bool loop_unavailable = false;         // building the loop graph failed: host-driven loop
   int64_t launches = 0;
