@@ -1089,10 +1089,13 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
   const int np = (int)g.parts.size();
   Scalars* hs = h0.sc_host;
   int hist_lim = 1 << 30;  // the device-side loop records LOOP_HCAP entries at most
+  bool x_copied = false;  // the device loop issues the copy-out with its state read-back
   auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
     // the iterate (slot order) -> the caller's x (natural order), owned cells of each part
-    for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
-    cudaStreamSynchronize(s);
+    if (!x_copied) {
+      for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
+      cudaStreamSynchronize(s);
+    }
     if (report) {
       report->iters = iters;
       report->converged = conv ? 1 : 0;
@@ -1172,6 +1175,8 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     }
     OCTMG_CUDA(cudaGraphLaunch(g.loop_graph, s));
     launch_copy_words(g.loop, g.loop_host_dev, sizeof(LoopState), s);
+    for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);  // the result, same sync
+    x_copied = true;
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
@@ -1255,10 +1260,13 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
   const int64_t launches0 = g.launches;
   const int np = (int)g.parts.size();
   Scalars* hs = h0.sc_host;
+  bool x_copied = false;  // the device loop issues the copy-out with its state read-back
   auto fill = [&](octmg_status st, int iters, bool conv, double rel, double bn) {
     // the iterate (slot order) -> the caller's x (natural order), owned cells of each part
-    for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
-    cudaStreamSynchronize(s);
+    if (!x_copied) {
+      for (Hier* h : g.parts) launch_copy_to_nat(h->xs, x, h->own_cells, s);
+      cudaStreamSynchronize(s);
+    }
     if (report) {
       report->iters = iters;
       report->converged = conv ? 1 : 0;
