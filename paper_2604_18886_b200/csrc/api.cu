@@ -808,6 +808,8 @@ ApplyArgs apply_args(const Hier& h) {
   a.glayer = T.glayer; a.dtile = h.dtile; a.dval = h.dval; a.z = nullptr; a.q = nullptr;
   a.pbar = h.pbar; a.ifaces = h.ifaces; a.n_ifaces = h.n_ifaces;
   a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL;
+  a.irr_inline = 0;
+  for (int l = 0; l <= T.L; ++l) a.irr_inline |= h.lvl_ghost[l] ? 1 : 0;
   return a;
 }
 

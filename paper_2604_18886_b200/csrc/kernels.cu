@@ -111,6 +111,7 @@ __device__ __noinline__ void apply_row_irr(const ApplyArgs& a, int t, int n0, in
 }
 
 // INL: the irregular body inlined, at 6 CTAs/SM (80 registers) instead of out of line at 8
+// (measured on configs 3 / 5: inlined at 7 or 8 CTAs/SM, 72 / 64 registers with spills, slower)
 template <bool DOT, bool INL>
 __global__ __launch_bounds__(128, INL ? 6 : 8) void k_apply_v6(const __grid_constant__ ApplyArgs a) {
   __shared__ double sred[4];
@@ -423,11 +424,16 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
     if (a.partial) cudaMemsetAsync(&a.sc->sum_pq, 0, sizeof(double), s);
     return;
   }
-  static int inl = -1;  // OCTMG_APPLY_IRR=inline: the irregular body inlined
-  if (inl < 0) {
+  // the irregular (T-junction) body inlined at 6 CTAs/SM (80 registers) on trees with
+  // T-junction tiles; out of line at 8 CTAs/SM otherwise (its call frame spills to local
+  // memory: 100M L2 sectors of local traffic per config-3 apply under ncu, config 5 apply
+  // 45.2 -> 38.6 ms per solve inlined); OCTMG_APPLY_IRR=inline / call forces one form
+  static int env = -2;
+  if (env == -2) {
     const char* e = getenv("OCTMG_APPLY_IRR");
-    inl = e && e[0] == 'i';
+    env = !e ? -1 : (e[0] == 'i' ? 1 : 0);
   }
+  const bool inl = env >= 0 ? env == 1 : a.irr_inline != 0;
   if (a.partial) {
     if (inl) k_apply_v6<true, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<true, false><<<a.ntiles, 128, 0, s>>>(a);

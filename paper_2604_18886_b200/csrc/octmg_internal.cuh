@@ -169,6 +169,7 @@ struct ApplyArgs {
   unsigned* counter;
   Scalars* sc;          // sum_pq written by the finish kernel
   int NL;
+  int irr_inline;       // the irregular-tile body inlined (trees with T-junction tiles)
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 

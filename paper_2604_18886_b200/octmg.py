@@ -75,9 +75,10 @@ def lib():
     """Load liboctmg.so (built by __graft_entry__.build()); raise if it is absent."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise ImportError(f"{LIB} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
-        L = C.CDLL(LIB)
+        path = os.environ.get("OCTMG_LIB_AB") or LIB  # (tools/: A/B of two builds of the library)
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(path)
         P, I32, I64 = C.c_void_p, C.c_int32, C.c_int64
         L.octmg_last_error.restype = C.c_char_p
         L.octmg_version.restype = C.c_char_p
