@@ -295,7 +295,7 @@ int inner_mean_kernels(const Group& g) {
 // (every ghost level with ghost-free tiles: they take the red-row kernel; OCTMG_RESTRICT_SPLIT=
 // big: only levels of >= 32768 tiles)
 bool split_restrict(const Hier& h, int l) {
-  static int all = -1;
+  int all = -1;  // (read per call: the variant tests switch it within one process)
   if (all < 0) {
     const char* e = getenv("OCTMG_RESTRICT_SPLIT");
     all = !(e && std::string(e) == "big");
@@ -310,7 +310,7 @@ bool split_restrict(const Hier& h, int l) {
 // slower than one launch with the inlined ghost body: config 3 10.28 vs 10.02 ms, config 5
 // level 9 111.7 vs 108.7 ms of passes per solve — the second launch's ramp and tail)
 bool split_pass(const Hier& h, int l, int mode) {
-  static int on = -1;
+  int on = -1;
   if (on < 0) {
     const char* e = getenv("OCTMG_PASS_SPLIT");
     on = e && atoi(e) == 1;

@@ -456,6 +456,33 @@ __global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
   bt[off1] = q1.x != 0.0f ? b1 + face_sum<false>(a, t, x0 + 1, y, z, q1, 0.0f, 0.0f, 0, q1.x * uu.y) : 0.0f;
 }
 
+// The FAS right-hand side in the row layout (thread j of a 128-thread tile CTA owns row j >> 1 of
+// colour j & 1, rowtile.cuh): b_I += (A^{l-1} u*)_I summed as c*u, then faces x-, x+, y-, y+,
+// z-, z+ (k_fasrhs's order, so bit-identical) from one float4 row of each neighbour instead
+// of k_fasrhs's per-cell general path (config 2 level 4: 28 us -> ~8 us per visit, L2-resident)
+__global__ __launch_bounds__(128, 8) void k_fasrhs_row(const __grid_constant__ SmoothArgs a) {
+  using namespace rowk;
+  const int t = a.first_tile + blockIdx.x;
+  int nb[6];
+  load_nb(a.nbr, t, nb);
+  const RowGeo g = row_geo(threadIdx.x & 1, threadIdx.x >> 1);
+  const float* ct = a.coef + ((size_t)t << 11);
+  const float4 q0 = ld4(ct + g.own), qx = ld4(ct + 512 + g.own), qy = ld4(ct + 1024 + g.own),
+               qz = ld4(ct + 1536 + g.own);
+  const float4 uu = ld4(tptr(a.u, t, a.NL) + g.own);
+  float* bt = a.b.inner + (size_t)(t - a.NL) * TB3 + g.own;
+  const float4 bb = *reinterpret_cast<const float4*>(bt);
+  const Fld uf = a.u;
+  const int NL = a.NL;
+  auto tu = [uf, NL](int n) -> const float* { return tptr(uf, n, NL); };
+  RowSt st;
+  row_load(st, tu, a.coef, t, nb, g);  // inner tiles never border a ghost (grading)
+  const float4 f = row_sums(st, g, qx, qy, qz, make_float4(q0.x * uu.x, q0.y * uu.y, q0.z * uu.z, q0.w * uu.w));
+  *reinterpret_cast<float4*>(bt) =
+      make_float4(q0.x != 0.0f ? bb.x + f.x : 0.0f, q0.y != 0.0f ? bb.y + f.y : 0.0f,
+                  q0.z != 0.0f ? bb.z + f.z : 0.0f, q0.w != 0.0f ? bb.w + f.w : 0.0f);
+}
+
 }  // namespace
 
 // k_pass_v3's ghost body: inlined (80 registers, 12 CTAs/SM) on levels with ghost tiles,
@@ -463,7 +490,7 @@ __global__ __launch_bounds__(NT, 8) void k_fasrhs(SmoothArgs a) {
 // forces one form on every level (measured: inline 10.2 vs 11.3 ms of passes per config-3
 // solve; out of line 2.72 vs 3.15 ms on config 2, which has no ghost tile)
 static bool pass_ghost_inline(bool level_has_ghosts) {
-  static int mode = -1;
+  int mode = -1;  // (env read per call: the variant tests switch it within one process)
   if (mode < 0) {
     const char* e = getenv("OCTMG_PASS_GHOST");
     mode = !e ? 0 : (std::string(e) == "inline" ? 1 : (std::string(e) == "call" ? 2 : 0));
@@ -475,7 +502,7 @@ static bool pass_ghost_inline(bool level_has_ghosts) {
 // 10.19 -> 9.58 ms and config 4 21.4 -> 20.0 ms of passes per solve against 12 CTAs/SM at 80
 // registers); OCTMG_PASS_GHOST_MINB=12 for the latter
 static int pass_ghost_minb() {
-  static int v = -1;
+  int v = -1;
   if (v < 0) {
     const char* e = getenv("OCTMG_PASS_GHOST_MINB");
     v = e ? atoi(e) : 14;
@@ -485,7 +512,7 @@ static int pass_ghost_minb() {
 
 // OCTMG_PASS_V=2: the scalar k_pass_v2 on big levels instead of the 128-bit k_pass_v3
 static bool pass_v3_enabled() {
-  static int on = -1;
+  int on = -1;
   if (on < 0) {
     const char* e = getenv("OCTMG_PASS_V");
     on = !(e && (std::string(e) == "2" || std::string(e) == "1"));
@@ -493,8 +520,16 @@ static bool pass_v3_enabled() {
   return on == 1;
 }
 
+// OCTMG_FASRHS=cell: the per-cell k_fasrhs instead of the row form
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s) {
-  if (ninner > 0) k_fasrhs<<<ninner, NT, 0, s>>>(a);
+  int cell = -1;
+  if (cell < 0) {
+    const char* e = getenv("OCTMG_FASRHS");
+    cell = e && std::string(e) == "cell";
+  }
+  if (ninner <= 0) return;
+  if (cell) k_fasrhs<<<ninner, NT, 0, s>>>(a);
+  else k_fasrhs_row<<<ninner, 128, 0, s>>>(a);
 }
 
 template <int CPT>

@@ -428,7 +428,7 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   // T-junction tiles; out of line at 8 CTAs/SM otherwise (its call frame spills to local
   // memory: 100M L2 sectors of local traffic per config-3 apply under ncu, config 5 apply
   // 45.2 -> 38.6 ms per solve inlined); OCTMG_APPLY_IRR=inline / call forces one form
-  static int env = -2;
+  int env = -2;  // (read per call: the variant tests switch it within one process)
   if (env == -2) {
     const char* e = getenv("OCTMG_APPLY_IRR");
     env = !e ? -1 : (e[0] == 'i' ? 1 : 0);
