@@ -101,6 +101,10 @@ struct Oracle {
   // indices, leaf segment then inner segment) and the dense solution operator M0 (row-major)
   std::vector<size_t> c0_cells;
   std::vector<double> M0;
+  // GMG comparison mode (setup_gmg): the cycle's records, = c / cm on the leaf cells and the
+  // grid-assembled records on the inner cells; the preconditioner swaps them in for its cycle
+  bool gmg = false;
+  std::vector<double> gmg_c, gmg_cm[3];
 
   int levels() const { return L + 1; }
   int tlev(int t) const { return tile[t][0]; }
@@ -903,8 +907,85 @@ void mucycle_std(Oracle& o, int l, const MG& p, std::vector<double>& r) {
   smooth(o, l, p.nu_post, false);
 }
 
+// GMG comparison mode: the coarse operators of the cycle "obtained directly
+// from the grid, without explicit reference to the fine-level operator": every inner
+// cell's record by Eq. 3 (kinds P:L318-335) at its own level, from its own kind
+// and face weights and those of its same-level neighbours (an inner cell never borders a
+// ghost, SURVEY c-1), instead of Alg. 3.  In fluid-only regions this equals the Galerkin
+// record; next to solid cells it does not ("the terms related to i will
+// vanish from A_II^{l-1}" under Galerkin, not here).  The leaf records — and so the composite
+// operator the PCG solves — are unchanged; only the preconditioner's cycle uses these.
+// kind_inner / w_inner: the inner cells' inputs (inner-tile order, natural cell order;
+// w_inner [6][NI*B3] or NULL = 1).
+int setup_gmg(Oracle& o, const uint8_t* kind_inner, const float* w_inner) {
+  if (!o.setup) { g_err = "setup_gmg needs setup first"; return S_INVALID; }
+  const size_t NL3 = (size_t)o.NL * o.B3, NI3 = (size_t)o.NI * o.B3;
+  for (size_t i = 0; i < NI3; ++i)
+    if (kind_inner[i] > 2) { g_err = "bad cell kind"; return S_INVALID; }
+  o.gmg_c = o.c;
+  for (int a = 0; a < 3; ++a) o.gmg_cm[a] = o.cm[a];
+  auto kind_of = [&](size_t j) -> int { return j < NL3 ? o.kind[j] : kind_inner[j - NL3]; };
+  auto w_of = [&](int f, size_t j) -> double {
+    if (j < NL3) return o.wf(f, j);
+    return w_inner ? (double)w_inner[(size_t)f * NI3 + (j - NL3)] : 1.0;
+  };
+  int err = S_OK;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int t = o.NL; t < o.T; ++t) {
+    const int l = o.tlev(t);
+    const double h = o.hcell(l);
+    for (int off = 0; off < o.B3; ++off) {
+      const size_t i = o.idx(t, off);
+      const int k = kind_of(i);
+      int64_t X, Y, Z;
+      o.coords(t, off, &X, &Y, &Z);
+      double c = 0.0, cm[3] = {0.0, 0.0, 0.0};
+      if (k != K_NEUMANN) {
+        for (int f = 0; f < 6; ++f) {
+          const int a = f / 2, sg = (f & 1) ? 1 : -1;
+          int64_t q[3] = {X, Y, Z};
+          q[a] += sg;
+          const Loc n = o.locate(l, q[0], q[1], q[2]);
+          if (n.what == L_WALL) {
+            if (k == K_FLUID && o.wall[f] == 1) c += w_of(f, i) * h;
+          } else if (n.what == L_CELL) {
+            const size_t j = o.idx(n.tile, n.off);
+            if (kind_of(j) != K_NEUMANN) {
+              if (k == K_FLUID) c += (sg < 0 ? w_of(f, i) : w_of(f ^ 1, j)) * h;
+              if (sg < 0) cm[a] = -w_of(f, i) * h;
+            }
+          } else {
+#pragma omp critical(orc_gmg_err)
+            { err = S_NOT_GRADED; g_err = "inner cell next to a ghost or an uncovered position"; }
+          }
+        }
+      }
+      o.gmg_c[i] = c;  // a fluid cell with c == 0 is isolated and therefore inactive
+      for (int a = 0; a < 3; ++a) o.gmg_cm[a][i] = cm[a];
+    }
+  }
+  if (err) return err;
+  o.gmg = true;
+  o.M0.clear();
+  o.c0_cells.clear();
+  return S_OK;
+}
+
+// the cycle's coefficient set in place of c / cm for the duration of a preconditioner call
+struct CycleCoefs {
+  Oracle& o;
+  explicit CycleCoefs(Oracle& oo) : o(oo) { swap(); }
+  ~CycleCoefs() { swap(); }
+  void swap() {
+    if (!o.gmg) return;
+    std::swap(o.c, o.gmg_c);
+    for (int a = 0; a < 3; ++a) std::swap(o.cm[a], o.gmg_cm[a]);
+  }
+};
+
 // M(r): u^l := 0 for all l; b^l[leaf(l)] := r; cycle from the finest level; z := u[leaves]
 void precond(Oracle& o, const MG& p, const double* rin, double* z, bool fas_form) {
+  CycleCoefs cyc(o);  // GMG mode: the grid-assembled coarse records (same leaf records)
   size_t NC = (size_t)o.T * o.B3, N = (size_t)o.NL * o.B3;
   std::fill(o.u.begin(), o.u.end(), 0.0);
   std::fill(o.b.begin(), o.b.end(), 0.0);
@@ -1284,6 +1365,22 @@ int32_t orc_setup(void* h, const uint8_t* kind, const float* w, double alpha, in
 // out: T*B3*4 doubles (c, cxm, cym, czm) per cell in all-tile order
 void orc_coefs(void* h, double* out) {
   auto* o = (Oracle*)h;
+  size_t NC = (size_t)o->T * o->B3;
+  for (size_t i = 0; i < NC; ++i) {
+    out[4 * i] = o->c[i];
+    for (int a = 0; a < 3; ++a) out[4 * i + 1 + a] = o->cm[a][i];
+  }
+}
+
+// GMG comparison mode: the inner cells' records assembled from their own kinds / weights
+int32_t orc_setup_gmg(void* h, const uint8_t* kind_inner, const float* w_inner) {
+  return setup_gmg(*(Oracle*)h, kind_inner, w_inner);
+}
+
+// the cycle's records (= orc_coefs unless GMG mode), same layout as orc_coefs
+void orc_coefs_cycle(void* h, double* out) {
+  auto* o = (Oracle*)h;
+  CycleCoefs cyc(*o);
   size_t NC = (size_t)o->T * o->B3;
   for (size_t i = 0; i < NC; ++i) {
     out[4 * i] = o->c[i];

@@ -45,6 +45,9 @@ def lib():
         _lib.orc_setup.restype = I32
         _lib.orc_setup.argtypes = [P, P, P, D, I32]
         _lib.orc_coefs.argtypes = [P, P]
+        _lib.orc_setup_gmg.restype = I32
+        _lib.orc_setup_gmg.argtypes = [P, P, P]
+        _lib.orc_coefs_cycle.argtypes = [P, P]
         _lib.orc_ghost_coef.restype = I32
         _lib.orc_ghost_coef.argtypes = [P, I32, I64, I64, I64, P]
         _lib.orc_apply.argtypes = [P, P, P]
@@ -162,9 +165,31 @@ class Oracle:
         self.alpha = alpha
         return self
 
+    def setup_gmg(self, kind_inner=None, w_inner=None):
+        """GMG comparison mode: the cycle's inner-cell records assembled
+        by Eq. 3 from the inner cells' own kinds / face weights (inner-tile order; None = all fluid,
+        w = 1) instead of Alg. 3; the composite operator is unchanged.  Call after setup()."""
+        NI3 = self.NI * self.B3
+        k = np.zeros(NI3, dtype=np.uint8) if kind_inner is None else np.ascontiguousarray(kind_inner, dtype=np.uint8)
+        assert k.size == NI3
+        if w_inner is not None:
+            wv = np.ascontiguousarray(np.asarray(w_inner, dtype=np.float32).reshape(6, NI3))
+            st = lib().orc_setup_gmg(self._h, _p(k), _p(wv))
+        else:
+            st = lib().orc_setup_gmg(self._h, _p(k), None)
+        if st:
+            raise OracleError(st, lib().orc_last_error().decode())
+        return self
+
     def coefs(self):
         out = np.zeros((self.T * self.B3, 4), dtype=np.float64)
         lib().orc_coefs(self._h, _p(out))
+        return out
+
+    def coefs_cycle(self):
+        """The records the cycle uses (= coefs() unless GMG mode)."""
+        out = np.zeros((self.T * self.B3, 4), dtype=np.float64)
+        lib().orc_coefs_cycle(self._h, _p(out))
         return out
 
     def coefs_diag_leaf(self):
