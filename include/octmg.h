@@ -170,6 +170,28 @@ octmg_status octmg_setup_hierarchy_loopback(octmg_tree* tree, int32_t nparts, co
                                             const octmg_mg_params* params, octmg_stream stream,
                                             octmg_hier** out);
 
+/*
+ * GMG comparison mode (Fig. 12): the
+ * cycle's coarse operators "given directly by the grid discretization" instead of
+ * Alg. 3 — every inner cell's record (c, c_x-, c_y-, c_z-) assembled by Eq. 3 (P:L303-316,
+ * kinds P:L318-335) at its own level from its own kind and face weights and those of its
+ * same-level neighbours (leaf inputs for leaf cells).  Only the preconditioner changes: the
+ * leaf records, and so the composite operator octmg_apply / octmg_pcg_solve solve with, are
+ * those of octmg_setup_hierarchy (a T-junction face keeps its Alg. 3 coupling there).  In
+ * fluid-only domains both constructions coincide; next to solid cells the grid
+ * records ignore the sub-cell structure, which is what makes GMG stall on cut cells (Fig. 12).
+ *  kind, face_beta, face_frac: as octmg_setup_hierarchy (leaf cells).
+ *  kind_inner:      device u8[NI*512], the inner cells' kinds (inner tiles in canonical order,
+ *                   cells x + 8y + 64z) — e.g. octmg_tank_fields_inner.
+ *  face_beta_inner, face_frac_inner: device f32[6][NI*512] or NULL (= 1).
+ * Single-part hierarchies only (OCTMG_E_INVALID for a multi-rank tree).  Inputs are read
+ * during the call only.  Costs a second coefficient store (the cycle's).
+ */
+octmg_status octmg_setup_hierarchy_gmg(octmg_tree* tree, const uint8_t* kind, const float* face_beta,
+                                       const float* face_frac, const uint8_t* kind_inner,
+                                       const float* face_beta_inner, const float* face_frac_inner,
+                                       const octmg_mg_params* params, octmg_stream stream, octmg_hier** out);
+
 /* Partition of part `part` (0 for an NCCL rank): partition level lg (levels < lg are
  * replicated), rank, nranks, and per level the owned leaf tiles [begin, begin+count). */
 octmg_status octmg_partition_info(const octmg_hier* h, int32_t part, int32_t* lg, int32_t* rank,
@@ -230,6 +252,12 @@ octmg_status octmg_band_tiles(const int32_t* ext3, int32_t l0, int32_t extra, co
 octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind,
                                float* face_frac, float* b, octmg_stream stream);
 
+/* The same tank geometry on the inner cells (each at its own level): kinds and face
+ * fractions for octmg_setup_hierarchy_gmg.  kind_inner: device u8[NI*512], face_frac_inner:
+ * device f32[6][NI*512] (inner tiles in canonical order, cells x + 8y + 64z; caller-owned). */
+octmg_status octmg_tank_fields_inner(const octmg_tree* tree, const double* centre3, double radius,
+                                     uint8_t* kind_inner, float* face_frac_inner, octmg_stream stream);
+
 /*
  * Projection operators on the composite octree (after the pressure solve
  * "apply the pressure gradient to project the velocity field and measure the divergence";
@@ -288,6 +316,9 @@ octmg_status octmg_set_allocator(octmg_alloc_fn alloc, octmg_free_fn release, vo
  * in tile order, cells x + 8y + 64z within a tile (the library's internal colour-split,
  * structure-of-arrays layout is converted).  Synchronises `stream` of the last call. */
 octmg_status octmg_hier_export_coefs(const octmg_hier* h, float* host_dst, size_t bytes);
+/* The same export of the records the cycle uses (differs from the above only for a GMG
+ * comparison-mode hierarchy, octmg_setup_hierarchy_gmg: its inner records). */
+octmg_status octmg_hier_export_cycle_coefs(const octmg_hier* h, float* host_dst, size_t bytes);
 
 /* y = A x, the composite operator over all leaf cells (T-junction ghosts, Eq. 12,
  * P:L661-665; inner neighbour value = mean of its active children).  x, y are

@@ -867,6 +867,10 @@ void fas(Oracle& o, int l, const MG& p, std::vector<double>& r) {
       size_t ch[8];
       children_of(o, lc, t, off, ch);
       size_t I = o.idx(t, off);
+      // an inactive coarse cell carries no correction (DESIGN reading 20: it is not a DOF; with
+      // Alg. 3 it has no active child and u = u* = 0, in the GMG comparison mode a solid
+      // coarse cell can have fluid children and a nonzero u*)
+      if (o.c[I] == 0.0) continue;
       double corr = o.u[I] - o.ustar[I];
       for (int d = 0; d < 8; ++d)
         if (o.c[ch[d]] != 0.0) o.u[ch[d]] += corr;

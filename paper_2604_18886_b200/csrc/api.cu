@@ -263,7 +263,9 @@ octmg_status build_schedule(Group& g) {
     read_env(*p);
     // the on-chip sub-cycle levels as dense shared-memory grids when they are complete
     // inner levels (coarse_dense.cu); otherwise the tile-layout k_subcycle
-    if (p->sub_K >= 0 && p->c0n == 0) {
+    // (not in the GMG comparison mode: its prolongation skips inactive parents, which the
+    // dense and cluster kernels do not test)
+    if (p->sub_K >= 0 && p->c0n == 0 && p->ccoef == p->coef) {
       OCTMG_TRY(build_coarse_dense(*p, p->nranks > 1 ? p->lg - 1 : MAXL, nullptr));
       OCTMG_CUDA(cudaDeviceSynchronize());
       if (p->cd_K >= p->sub_K) p->sub_K = p->cd_K;
@@ -380,7 +382,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   }
   const int l = op.level;
   SmoothArgs a;
-  a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.coef; a.glayer_val = h.glayer_val;
+  a.tile = T.tile; a.nbr = T.nbr; a.parent = T.parent; a.coef = h.ccoef; a.glayer_val = h.glayer_val;
   a.glayer = T.glayer; a.u = ubuf(h); a.uc = ubuf(h); a.ustar = h.ustar; a.ustar_w = h.ustar;
   a.b = Fld{h.r, h.binner};
   a.alpha = h.prm.alpha; a.NL = T.NL;
@@ -389,6 +391,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   a.std_form = h.prm.form == 1;
   a.beta = a.std_form ? 1.0f : h.prm.beta_overshoot;
   a.pro_scale = a.std_form ? h.prm.beta_overshoot : 1.0f;
+  a.pro_active_only = h.ccoef != h.coef;  // GMG comparison mode (reading 20)
   a.order = h.order + h.lvl_order_off[l];
   a.ord_leaf0 = h.own_lb[l];
   a.ord_nleaf = h.own_lc[l];
@@ -745,7 +748,8 @@ bool valid_params(const octmg_mg_params& prm) {
 // a Group of `nparts` parts (1 = single GPU / one NCCL rank; >1 = loopback partition)
 octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void* nccl_comm, const uint8_t* kind,
                         const float* fbeta, const float* ffrac, const octmg_mg_params* params, cudaStream_t s,
-                        octmg_hier** out) {
+                        octmg_hier** out, const uint8_t* gmg_kind = nullptr, const float* gmg_beta = nullptr,
+                        const float* gmg_frac = nullptr) {
   octmg_mg_params prm{2.0f, 2.0f, 1, 2, 2, 10, 0, 0, 0, 0, 0};
   if (params) prm = *params;
   if (!valid_params(prm)) {
@@ -766,7 +770,12 @@ octmg_status make_group(octmg_tree* tree, int nparts, int rank, int nranks, void
     g.parts.push_back(h);
     h->rank = nparts > 1 ? p : rank;
     h->nranks = nranks;
+    h->gmg_kind = gmg_kind;
+    h->gmg_beta = gmg_beta;
+    h->gmg_frac = gmg_frac;
     octmg_status st = setup_part(*h, &tree->t, kind, fbeta, ffrac, prm, s);
+    h->gmg_kind = nullptr;
+    h->gmg_beta = h->gmg_frac = nullptr;
     if (st) return fail(st);
   }
   const PartPlan* P = nullptr;
@@ -826,6 +835,18 @@ octmg_status octmg_setup_hierarchy(octmg_tree* tree, const uint8_t* kind, const 
   const Tree& T = tree->t;
   return make_group(tree, 1, T.rank, T.nranks, T.nccl_comm, kind, face_beta, face_frac, params, (cudaStream_t)stream,
                     out);
+}
+
+octmg_status octmg_setup_hierarchy_gmg(octmg_tree* tree, const uint8_t* kind, const float* face_beta,
+                                       const float* face_frac, const uint8_t* kind_inner,
+                                       const float* face_beta_inner, const float* face_frac_inner,
+                                       const octmg_mg_params* params, octmg_stream stream, octmg_hier** out) {
+  if (!tree || !kind || !kind_inner || !out) { set_error("null argument"); return OCTMG_E_INVALID; }
+  *out = nullptr;
+  const Tree& T = tree->t;
+  if (T.nranks > 1) { set_error("the GMG comparison mode is single-part only"); return OCTMG_E_INVALID; }
+  return make_group(tree, 1, 0, 1, nullptr, kind, face_beta, face_frac, params, (cudaStream_t)stream, out,
+                    kind_inner, face_beta_inner, face_frac_inner);
 }
 
 octmg_status octmg_setup_hierarchy_loopback(octmg_tree* tree, int32_t nparts, const uint8_t* kind,
@@ -938,14 +959,21 @@ octmg_status octmg_tank_fields(const octmg_tree* tree, const double* centre3, do
   return tank_fields(tree->t, centre3, radius, kind, face_frac, b, (cudaStream_t)stream);
 }
 
-octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size_t bytes) {
+octmg_status octmg_tank_fields_inner(const octmg_tree* tree, const double* centre3, double radius, uint8_t* kind_inner,
+                                     float* face_frac_inner, octmg_stream stream) {
+  if (!tree || !centre3 || !kind_inner || !face_frac_inner) { set_error("null argument"); return OCTMG_E_INVALID; }
+  return tank_fields_inner(tree->t, centre3, radius, kind_inner, face_frac_inner, (cudaStream_t)stream);
+}
+
+static octmg_status export_store(const octmg_hier* hh, float* host_dst, size_t bytes, bool cycle) {
   if (!hh || !host_dst) { set_error("null argument"); return OCTMG_E_INVALID; }
   const Hier& h = *hh->g.parts[0];
+  const float* src = cycle ? h.ccoef : h.coef;
   size_t need = (size_t)h.tree->T * TB3 * sizeof(float4);
   if (bytes != need) { set_error("export buffer size mismatch"); return OCTMG_E_INVALID; }
   OCTMG_CUDA(cudaDeviceSynchronize());
   std::vector<float> soa((size_t)h.tree->T * TB3 * 4);
-  OCTMG_CUDA(cudaMemcpy(soa.data(), h.coef, need, cudaMemcpyDeviceToHost));
+  OCTMG_CUDA(cudaMemcpy(soa.data(), src, need, cudaMemcpyDeviceToHost));
   // SoA planes per tile in slot order -> the ABI's record order (c, c_x-, c_y-, c_z-) per
   // cell in natural order
   for (size_t t = 0; t < (size_t)h.tree->T; ++t)
@@ -954,6 +982,14 @@ octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size
       for (int k = 0; k < 4; ++k) host_dst[4 * o + k] = soa[cidx(i, k)];
     }
   return OCTMG_OK;
+}
+
+octmg_status octmg_hier_export_coefs(const octmg_hier* hh, float* host_dst, size_t bytes) {
+  return export_store(hh, host_dst, bytes, false);
+}
+
+octmg_status octmg_hier_export_cycle_coefs(const octmg_hier* hh, float* host_dst, size_t bytes) {
+  return export_store(hh, host_dst, bytes, true);
 }
 
 octmg_status octmg_apply(octmg_hier* hh, const float* x, float* y, octmg_stream stream) {

@@ -657,7 +657,7 @@ octmg_status build_coarse_dense(Hier& h, int Kmax, cudaStream_t s) {
     L.tmap = dmap + moff[l];
     L.shx = shift_of(L.nx >> 1);
     L.shy = shift_of(L.ny);
-    k_dense_coef<<<(L.n + 255) / 256, 256, 0, s>>>(h.coef, L, T.NL, dcoef + NP * (size_t)off);
+    k_dense_coef<<<(L.n + 255) / 256, 256, 0, s>>>(h.ccoef, L, T.NL, dcoef + NP * (size_t)off);
     h.cd_lv[l][0] = L.nx; h.cd_lv[l][1] = L.ny; h.cd_lv[l][2] = L.nz; h.cd_lv[l][3] = off;
     off += L.n;
   }
@@ -779,7 +779,7 @@ octmg_status build_coarse_cluster(Hier& h, cudaStream_t s) {
   h.allocs.push_back(dmap);
   h.allocs.push_back(dc2);
   OCTMG_CUDA(cudaMemcpy(dmap, map.data(), sizeof(int) * 64, cudaMemcpyHostToDevice));
-  k_slab_coef<<<(nS * CC + 255) / 256, 256, 0, s>>>(h.coef, dmap, nx, ny, dc2);
+  k_slab_coef<<<(nS * CC + 255) / 256, 256, 0, s>>>(h.ccoef, dmap, nx, ny, dc2);
   OCTMG_CUDA(cudaGetLastError());
   h.cc_map = dmap;
   h.cc_coef = dc2;

@@ -276,7 +276,7 @@ octmg_status build_coarse_direct(Hier& h, cudaStream_t s) {
   int* floating = csize + n;
   C0Map m{h.c0tile, T.lb[0], T.lc[0], T.ib[0]};
   cudaMemsetAsync(A, 0, sizeof(double) * nn, s);
-  k_c0_assemble<<<(n + 127) / 128, 128, 0, s>>>(h.coef, T.nbr, m, n, A, nb6);
+  k_c0_assemble<<<(n + 127) / 128, 128, 0, s>>>(h.ccoef, T.nbr, m, n, A, nb6);
   k_c0_components<<<1, 1024, 0, s>>>(A, nb6, n, comp, csize, csum, floating);
   k_c0_regularize<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(A, comp, csize, csum, floating, n, R);
   const unsigned eg = (unsigned)((2 * nn + 255) / 256);

@@ -434,7 +434,8 @@ __global__ __launch_bounds__(128) void k_prolong(SmoothArgs a) {
     int x, y, z;
     slot_xyz(sl, x, y, z);
     const int pc = pcell_of(tv, x, y, z);
-    const float c = a.pro_scale * (__ldg(uc + pc) - __ldg(us + pc));
+    float c = a.pro_scale * (__ldg(uc + pc) - __ldg(us + pc));
+    if (a.pro_active_only && __ldg(a.coef + ((size_t)P << 11) + pc) == 0.0f) c = 0.0f;
     if (cv[k] != 0.0f) ut[sl] = uo[k] + c;
   }
 }

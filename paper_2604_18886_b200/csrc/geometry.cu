@@ -11,7 +11,7 @@ namespace octmg {
 namespace {
 
 struct TankArgs {
-  const int4* tile;
+  const int4* tile;     // the tiles the fields cover (leaf tiles, or the inner tiles)
   int NL;
   double ext[3];
   double c[3];
@@ -105,7 +105,7 @@ __global__ __launch_bounds__(512) void k_tank_fields(TankArgs A) {
     A.frac[(size_t)f * A.N + i] = ff;
     if (a == 1) wy[side] = (double)ff;
   }
-  A.b[i] = solid ? 0.0f : (float)(h * h * (wy[1] - wy[0]));
+  if (A.b) A.b[i] = solid ? 0.0f : (float)(h * h * (wy[1] - wy[0]));
 }
 
 }  // namespace
@@ -126,6 +126,28 @@ octmg_status tank_fields(const Tree& T, const double* centre, double radius, uin
   A.b = b;
   A.N = (int64_t)T.NL * TB3;
   k_tank_fields<<<T.NL, TB3, 0, s>>>(A);
+  OCTMG_CUDA(cudaGetLastError());
+  return OCTMG_OK;
+}
+
+// the same scene on the inner tiles (kinds and face fractions of the coarse cells, for the
+// GMG comparison mode's grid-assembled coarse operators)
+octmg_status tank_fields_inner(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac,
+                               cudaStream_t s) {
+  if (T.NI == 0) return OCTMG_OK;
+  TankArgs A;
+  A.tile = T.tile + T.NL;
+  A.NL = T.NI;
+  for (int k = 0; k < 3; ++k) {
+    A.ext[k] = (double)T.ext[k];
+    A.c[k] = centre[k];
+  }
+  A.r = radius;
+  A.kind = kind;
+  A.frac = frac;
+  A.b = nullptr;
+  A.N = (int64_t)T.NI * TB3;
+  k_tank_fields<<<T.NI, TB3, 0, s>>>(A);
   OCTMG_CUDA(cudaGetLastError());
   return OCTMG_OK;
 }

@@ -212,6 +212,8 @@ struct SmoothArgs {
   float beta, alpha;    // restriction: b^{l-1} = beta R r, R = P^T / alpha
   int std_form;         // Alg. 2: u^{l-1} := 0 and u* := 0 at restriction (no Avg, no FAS rhs)
   float pro_scale;      // prolongation: u += pro_scale (u^{l-1} - u*) (Alg. 2: beta; Alg. 4: 1)
+  int pro_active_only;  // prolong only from active parents (GMG comparison mode: a solid coarse
+                        // cell can have fluid children and a nonzero u*; DESIGN reading 20)
   int NL;
   const int* order;     // tiles of the level in rank order (slab-major), or nullptr: the level's
                         // tiles by index, ord_nleaf leaves from ord_leaf0 then inners from ord_inner0
@@ -261,6 +263,8 @@ octmg_status subtract_gradient(const Hier& h, const uint8_t* kind, const float* 
 // cut-cell geometry of the tank scene (geometry.cu)
 octmg_status tank_fields(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac, float* b,
                          cudaStream_t s);
+octmg_status tank_fields_inner(const Tree& T, const double* centre, double radius, uint8_t* kind, float* frac,
+                               cudaStream_t s);  // the same geometry on the inner tiles (GMG mode)
 
 // narrow-band refinement of the sphere-surface test grids on the device (band.cu)
 octmg_status band_tiles(const int32_t* ext, int l0, int extra, const double* centre, double radius, int repair,
@@ -290,6 +294,12 @@ struct Hier {
   Tree* tree = nullptr;
   octmg_mg_params prm{};
   float* coef = nullptr;         // [T*2048] SoA per tile: c, cxm, cym, czm planes (cidx)
+  float* ccoef = nullptr;        // the records the cycle uses: = coef, or (GMG comparison mode) a
+                                 // copy with the inner tiles' records assembled from the grid
+  // GMG comparison mode inputs (octmg_setup_hierarchy_gmg; read during setup only)
+  const uint8_t* gmg_kind = nullptr;   // [NI*512] inner cells' kinds (natural cell order)
+  const float* gmg_beta = nullptr;     // [6][NI*512] or null (= 1)
+  const float* gmg_frac = nullptr;     // [6][NI*512] or null (= 1)
   uint32_t* act = nullptr;       // [NL*512/32] activity bitmask of the leaf cells
   float* glayer_val = nullptr;   // [n_glayers*64]
   int2* ifaces = nullptr;        // (inner tile, face) layers the composite apply reads as children means

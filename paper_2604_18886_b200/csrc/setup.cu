@@ -233,6 +233,54 @@ __global__ void k_any_dirichlet(const uint8_t* kind, int64_t n, int* flag) {
     if (kind[i] == KD) { *flag = 1; return; }
 }
 
+// GMG comparison mode: the cycle's coarse records "given directly by the grid
+// discretization" — Eq. 3 (kinds P:L318-335) on every inner cell at its
+// own level, from its own kind / face weights and those of its same-level neighbours (an
+// inner tile never borders a ghost), in place of Alg. 3.  Written into the cycle's copy of
+// the store; the leaf records (the composite operator) are untouched.  Same fp32 terms and
+// order as k_assemble_diag / offdiag.
+struct GmgArgs {
+  const int4* tile;
+  const int* nbr;
+  const uint8_t* kind;    // leaf cells (slot order)
+  WIn w;
+  const uint8_t* kind_i;  // inner cells (slot order)
+  WIn wi;
+  float* coef;            // the cycle's store
+  int NL;
+  uint8_t wall[6];
+};
+__global__ __launch_bounds__(256) void k_gmg_inner(GmgArgs a) {
+  const int t = a.NL + blockIdx.x;
+  const int4 tv = a.tile[t];
+  const float h = ldexpf(1.0f, -tv.x) * 0.125f;
+  const size_t NL3 = (size_t)a.NL * TB3;
+  auto kind_of = [&](size_t j) -> int { return j < NL3 ? a.kind[j] : a.kind_i[j - NL3]; };
+  auto w_of = [&](int f, size_t j) -> float { return j < NL3 ? a.w.w(f, j) : a.wi.w(f, j - NL3); };
+  for (int off = threadIdx.x; off < TB3; off += blockDim.x) {
+    int x, y, z;
+    slot_xyz(off, x, y, z);
+    const size_t i = (size_t)t * TB3 + off;
+    const int k = kind_of(i);
+    float c = 0.0f, cm[3] = {0.0f, 0.0f, 0.0f};
+    if (k != KN) {
+      for (int f = 0; f < 6; ++f) {
+        const NbRef nb = nb_ref(a.nbr, tv, t, a.NL, x, y, z, f);
+        if (nb.what == NB_WALL) {
+          if (k == KF && a.wall[f]) c += w_of(f, i) * h;
+        } else if (nb.what == NB_LEAF || nb.what == NB_INNER) {
+          const size_t j = (size_t)nb.tile * TB3 + nb.off;
+          if (kind_of(j) != KN) {
+            if (k == KF) c += ((f & 1) ? w_of(f ^ 1, j) : w_of(f, i)) * h;
+            if (!(f & 1)) cm[f >> 1] = -w_of(f, i) * h;
+          }
+        }
+      }
+    }
+    stcoef(a.coef, i, make_float4(c, cm[0], cm[1], cm[2]));
+  }
+}
+
 }  // namespace
 
 octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbeta, const float* ffrac,
@@ -298,6 +346,43 @@ octmg_status assemble_leaf_coefs(Hier& h, const uint8_t* kind, const float* fbet
     OCTMG_CUDA(cudaGetLastError());
     OCTMG_CUDA(cudaFreeAsync(dfull, s));
     OCTMG_CUDA(cudaFreeAsync(dflag, s));
+  }
+  h.ccoef = h.coef;
+  if (h.gmg_kind && T.NI > 0) {
+    // GMG comparison mode: the cycle's own store, inner records from the grid
+    const int64_t Ni = (int64_t)T.NI * TB3;
+    float* cc = (float*)dev_malloc(sizeof(float) * (size_t)T.T * TB3 * 4);
+    if (!cc) { set_error("device allocation failed (GMG cycle coefficients)"); return OCTMG_E_OOM; }
+    h.allocs.push_back(cc);
+    OCTMG_CUDA(cudaMemcpyAsync(cc, h.coef, sizeof(float) * (size_t)T.T * TB3 * 4, cudaMemcpyDeviceToDevice, s));
+    uint8_t* ki = nullptr;
+    float *bi = nullptr, *fi = nullptr;
+    OCTMG_CUDA(cudaMallocAsync(&ki, Ni, s));
+    launch_permute_u8(h.gmg_kind, ki, Ni, true, s);
+    if (h.gmg_beta) {
+      OCTMG_CUDA(cudaMallocAsync(&bi, sizeof(float) * 6 * Ni, s));
+      launch_permute_f32(h.gmg_beta, bi, Ni, 6, true, s);
+    }
+    if (h.gmg_frac) {
+      OCTMG_CUDA(cudaMallocAsync(&fi, sizeof(float) * 6 * Ni, s));
+      launch_permute_f32(h.gmg_frac, fi, Ni, 6, true, s);
+    }
+    GmgArgs g;
+    g.tile = T.tile;
+    g.nbr = T.nbr;
+    g.kind = kind;
+    g.w = a.w;
+    g.kind_i = ki;
+    g.wi = WIn{bi, fi, (size_t)Ni};
+    g.coef = cc;
+    g.NL = T.NL;
+    for (int f = 0; f < 6; ++f) g.wall[f] = T.wall[f];
+    k_gmg_inner<<<T.NI, 256, 0, s>>>(g);
+    OCTMG_CUDA(cudaGetLastError());
+    OCTMG_CUDA(cudaFreeAsync(ki, s));
+    if (bi) OCTMG_CUDA(cudaFreeAsync(bi, s));
+    if (fi) OCTMG_CUDA(cudaFreeAsync(fi, s));
+    h.ccoef = cc;
   }
   // active leaf-cell count and whether any Dirichlet kind exists (null-space auto)
   unsigned long long* d_cnt;

@@ -228,6 +228,7 @@ __device__ __noinline__ void sc_prolong(const SubArgs& A, int l, unsigned& epoch
     slot_xyz(off, ox, oy, oz);
     const int pc = pcell_of(tv, ox, oy, oz);
     float* up = tptr(a.u, t, a.NL) + off;
+    if (a.pro_active_only && __ldg(a.coef + ((size_t)P << 11) + pc) == 0.0f) continue;  // (GMG mode)
     *up = ldv<M>(up) + a.pro_scale * (ldv<M>(tptr(a.uc, P, a.NL) + pc) - ldv<M>(a.ustar + (size_t)(P - a.NL) * TB3 + pc));
   }
   __syncthreads();

@@ -66,7 +66,8 @@ ABI_SYMBOLS = ["octmg_last_error", "octmg_version", "octmg_build_tree", "octmg_t
                "octmg_hier_destroy", "octmg_tree_destroy", "octmg_mg_solve", "octmg_tank_fields",
                "octmg_divergence", "octmg_subtract_gradient",
                "octmg_grade_repair_host", "octmg_set_allocator", "octmg_profile_read_level",
-               "octmg_band_tiles"]
+               "octmg_band_tiles", "octmg_setup_hierarchy_gmg", "octmg_tank_fields_inner",
+               "octmg_hier_export_cycle_coefs"]
 
 _lib = None
 
@@ -117,6 +118,12 @@ def lib():
         L.octmg_hier_destroy.argtypes = [P]
         L.octmg_tree_destroy.argtypes = [P]
         L.octmg_partition_plan_host.argtypes = [P, P, P, P, I32, I32, I32, P, I32, P, P, P, P, I64, I64]
+        L.octmg_setup_hierarchy_gmg.argtypes = [P, P, P, P, P, P, P, C.POINTER(MGParams), P, C.POINTER(P)]
+        L.octmg_setup_hierarchy_gmg.restype = C.c_int
+        L.octmg_tank_fields_inner.argtypes = [P, P, C.c_double, P, P, P]
+        L.octmg_tank_fields_inner.restype = C.c_int
+        L.octmg_hier_export_cycle_coefs.argtypes = [P, P, C.c_size_t]
+        L.octmg_hier_export_cycle_coefs.restype = C.c_int
         for name in ABI_SYMBOLS[2:16] + ["octmg_partition_plan_host"]:
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -240,17 +247,36 @@ def tank_fields(tree, centre=(0.5, 0.5, 0.5), radius=0.3, stream=None):
     return kind, frac, b
 
 
+def tank_fields_inner(tree, centre=(0.5, 0.5, 0.5), radius=0.3, stream=None):
+    """octmg_tank_fields_inner: the inner cells' (kind u8[NI*512], face_frac f32[6][NI*512])."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = tree.NI * 512
+    kind = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    frac = torch.empty((6, max(n, 1)), dtype=torch.float32, device=dev)
+    c = (C.c_double * 3)(*centre)
+    _check(lib().octmg_tank_fields_inner(tree._h, C.cast(c, C.c_void_p), float(radius), _ptr(kind), _ptr(frac),
+                                         _stream(stream)))
+    return kind[:n], frac[:, :n]
+
+
 class Hierarchy:
-    """octmg_setup_hierarchy + the solver calls.  Device tensors (torch, cuda) in and out."""
+    """octmg_setup_hierarchy + the solver calls.  Device tensors (torch, cuda) in and out.
+    gmg=(kind_inner, face_beta_inner, face_frac_inner): the GMG comparison mode
+    (octmg_setup_hierarchy_gmg; the beta / frac entries may be None)."""
 
     def __init__(self, tree: Tree, kind, face_beta=None, face_frac=None, alpha=2.0, beta=2.0, mu=1,
                  nu_pre=2, nu_post=2, nu_coarsest=10, stream=None, loopback_parts: int = 0, form="fas",
-                 coarsen_literal=False, coarsest="smooth", gather_below_cells=0):
+                 coarsen_literal=False, coarsest="smooth", gather_below_cells=0, gmg=None):
         self.tree = tree
         p = MGParams(alpha, beta, mu, nu_pre, nu_post, nu_coarsest, {"fas": 0, "alg2": 1}[form],
                      int(coarsen_literal), {"smooth": 0, "direct": 1}[coarsest], 0, int(gather_below_cells))
         h = C.c_void_p()
-        if loopback_parts:
+        if gmg is not None:
+            ki, bi, fi = gmg
+            _check(lib().octmg_setup_hierarchy_gmg(tree._h, _ptr(kind), _ptr(face_beta), _ptr(face_frac), _ptr(ki),
+                                                   _ptr(bi), _ptr(fi), C.byref(p), _stream(stream), C.byref(h)))
+        elif loopback_parts:
             _check(lib().octmg_setup_hierarchy_loopback(tree._h, loopback_parts, _ptr(kind), _ptr(face_beta),
                                                         _ptr(face_frac), C.byref(p), _stream(stream), C.byref(h)))
         else:
@@ -313,6 +339,11 @@ class Hierarchy:
     def export_coefs(self):
         out = np.zeros((self.tree.T * 512, 4), dtype=np.float32)
         _check(lib().octmg_hier_export_coefs(self._h, out.ctypes.data_as(C.c_void_p), out.nbytes))
+        return out
+
+    def export_cycle_coefs(self):
+        out = np.zeros((self.tree.T * 512, 4), dtype=np.float32)
+        _check(lib().octmg_hier_export_cycle_coefs(self._h, out.ctypes.data_as(C.c_void_p), out.nbytes))
         return out
 
     def profile(self, on: bool):
