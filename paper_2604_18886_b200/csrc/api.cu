@@ -647,7 +647,8 @@ octmg_status setup_part(Hier& h, Tree* tree, const uint8_t* kind, const float* f
   OCTMG_TRY(halloc(h.allocs, &h.p0, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.p1, NLc));
   OCTMG_TRY(halloc(h.allocs, &h.q, NLc));
-  h.n_partial = std::max<size_t>(4 * (size_t)T.NL + 512, 2 * (size_t)vec_grid()) + 16;  // apply: 4 warp partials per leaf tile + chunk sums
+  // apply: 4 warp partials per leaf tile of p.q and of sum q + their chunk sums
+  h.n_partial = std::max<size_t>(8 * (size_t)T.NL + 1024, 2 * (size_t)vec_grid()) + 16;
   OCTMG_TRY(halloc(h.allocs, &h.partial, h.n_partial));
   OCTMG_TRY(halloc(h.allocs, &h.counter, 16));
   OCTMG_TRY(halloc(h.allocs, &h.sc, 1));
@@ -1086,13 +1087,12 @@ octmg_status build_loop_graph(Group& g, bool ns) {
       a.counter = p->counter + 3;
       launch_apply(a, cs);  // q = A p, p.q
     }
-    OCTMG_TRY(allreduce(g, SF_PQ, 1, cs));
-    for (Hier* p : g.parts) launch_update(p->xs, p->r, p->p0, p->q, p->own_cells, p->partial, p->counter + 4, p->sc, cs, G);
+    OCTMG_TRY(allreduce(g, SF_PQ, 2, cs));  // p.q and sum q
+    // x, r update with the null-space projection of r fused in (k_update)
+    for (Hier* p : g.parts)
+      launch_update(p->xs, p->r, p->p0, p->q, p->own_cells, p->partial, p->counter + 4, p->sc, cs, G, 0.0f,
+                    ns ? p->act : nullptr);
     OCTMG_TRY(allreduce(g, SF_RR, 2, cs));
-    if (ns) {
-      for (Hier* p : g.parts) launch_project(p->r, p->act, p->own_cells, p->partial, p->counter + 1, p->sc, cs, G);
-      OCTMG_TRY(allreduce(g, SF_RR, 1, cs));
-    }
     launch_pcg_check(h.sc, g.loop, (unsigned long long)hd, cs);  // the allreduced sums of part 0
     return OCTMG_OK;
   };
@@ -1157,7 +1157,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       launch_project(h->r, h->act, h->own_cells, h->partial, h->counter + 1, h->sc, s, G);
     }
     g.launches += np;
-    return allreduce(g, SF_RR, 1, s);
+    return allreduce(g, SF_RR, 2, s);  // ||r||^2 and sum r of the projected r
   };
   auto dot_rz = [&]() -> octmg_status {
     for (Hier* h : g.parts) {
@@ -1218,7 +1218,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
-    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 + (ns ? 1 : 0) + (g.comm ? 1 : 0)) + 1 + inner_mean_kernels(g));
+    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 + (g.comm ? 1 : 0)) + 1 + inner_mean_kernels(g));
     hist_lim = LOOP_HCAP;
     if (report && report->history) {
       const int nh = std::min(kk, std::min((int)report->history_cap, LOOP_HCAP));
@@ -1258,14 +1258,15 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       }
     }
     g.launches += 3 * np + inner_mean_kernels(g);  // (inner-face means,) apply, chunk sums, finish
-    OCTMG_TRY(allreduce(g, SF_PQ, 1, s));
+    OCTMG_TRY(allreduce(g, SF_PQ, 2, s));  // p.q and sum q
     for (Hier* h : g.parts) {
-      ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * 24.0);  // read x, r, p, q; write x, r
-      launch_update(h->xs, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G);
+      // read x, r, p, q (+ the activity bits with the fused projection); write x, r
+      ProfScope ps(*h, KC_UPDATE, s, (double)h->n_apply_tiles * TB3 * (ns ? 24.125 : 24.0));
+      launch_update(h->xs, h->r, h->p0, h->q, h->own_cells, h->partial, h->counter + 4, h->sc, s, G, 0.0f,
+                    ns ? h->act : nullptr);
     }
     g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RR, 2, s));
-    if (ns) OCTMG_TRY(project());
     OCTMG_CUDA(cudaGetLastError());
     OCTMG_TRY(fetch());
     if (hs->flags & 1) {
@@ -1328,7 +1329,7 @@ octmg_status octmg_mg_solve(octmg_hier* hh, const float* b, float* x, const octm
       launch_project(h->r, h->act, h->own_cells, h->partial, h->counter + 1, h->sc, s, G);
     }
     g.launches += np;
-    return allreduce(g, SF_RR, 1, s);
+    return allreduce(g, SF_RR, 2, s);  // ||r||^2 and sum r
   };
   for (Hier* h : g.parts) {
     ProfScope ps(*h, KC_INIT, s, (double)h->n_apply_tiles * TB3 * 12.125);

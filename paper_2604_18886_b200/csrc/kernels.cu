@@ -93,12 +93,21 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
                                c0.w != 0.0f ? f.w : 0.0f);
   *reinterpret_cast<float4*>(a.q + ((size_t)t << 9) + g.own) = r;
   if (DOT) {
-    // fp64 partial per warp (4 per tile, no CTA barrier: the warps of an irregular tile finish
-    // independently); k_finish_sigma sums them in tile order (deterministic)
+    // fp64 partials per warp (4 per tile, no CTA barrier: the warps of an irregular tile finish
+    // independently) of p.q and of sum q (the null-space projection's mean shift, fused into
+    // k_update); k_chunk_sums / k_finish_sigma sum them in tile order (deterministic)
     double dd = (double)pv.x * (double)r.x + (double)pv.y * (double)r.y + (double)pv.z * (double)r.z +
                 (double)pv.w * (double)r.w;
-    for (int o = 16; o; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
-    if ((threadIdx.x & 31) == 0) a.partial[4 * (size_t)blockIdx.x + (threadIdx.x >> 5)] = dd;
+    double dq = ((double)r.x + (double)r.y) + ((double)r.z + (double)r.w);
+    for (int o = 16; o; o >>= 1) {
+      dd += __shfl_down_sync(0xffffffffu, dd, o);
+      dq += __shfl_down_sync(0xffffffffu, dq, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      const size_t w = 4 * (size_t)blockIdx.x + (threadIdx.x >> 5);
+      a.partial[w] = dd;
+      a.partial[4 * (size_t)gridDim.x + w] = dq;
+    }
   }
 }
 
@@ -160,6 +169,8 @@ __global__ __launch_bounds__(64) void k_inner_face_means(const int2* ifaces, con
 // in a fixed order (deterministic), so the final single-CTA stage reads a few hundred values
 __global__ __launch_bounds__(256) void k_chunk_sums(const double* partial, int64_t n, int64_t chunk, double* out) {
   __shared__ double sred[8];
+  partial += blockIdx.y * n;  // y = 0: the p.q partials, 1: the sum-q partials
+  out += blockIdx.y * gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   double s0 = 0.0, s1 = 0.0;
   int64_t k = lo + threadIdx.x;
@@ -172,9 +183,11 @@ __global__ __launch_bounds__(256) void k_chunk_sums(const double* partial, int64
   if (threadIdx.x == 0) out[blockIdx.x] = bs;
 }
 
-// sigma = p.q from the partials (fixed order => deterministic)
+// sigma = p.q and sum q from the partials (fixed order => deterministic): block 0 the first
+// n values (p.q chunks) into sum_pq, block 1 the next n (q chunks) into sum_q
 __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, int n, Scalars* sc) {
   __shared__ double sred[32];
+  partial += (size_t)blockIdx.x * n;
   // four independent accumulators per thread keep several loads in flight (fixed order)
   const int bd = blockDim.x;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -193,7 +206,8 @@ __global__ __launch_bounds__(1024) void k_finish_sigma(const double* partial, in
   if (threadIdx.x == 0) {
     double tot = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sred[w];
-    sc->sum_pq = tot;
+    if (blockIdx.x == 0) sc->sum_pq = tot;
+    else sc->sum_q = tot;
   }
 }
 
@@ -256,13 +270,19 @@ __global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* ac
 // x += alpha p, r -= alpha q with alpha = (r,z)/(p,Ap) (Alg. 1 lines 9-11); sums ||r||^2,
 // sum r.  The last block flags a breakdown and records rho = (r, z) for the next beta.
 // alpha_fixed != 0: that step length instead (standalone multigrid: x += z, r -= A z)
+// act (PCG with the null-space projection): the projection of the new r fused in,
+// r -= m on the active cells with m = mean_active(r - alpha q) = (sum r - alpha sum q) / n
+// formed from the sums of the projected r (previous update / initial projection) and of q
+// (the apply) — the k_project pass and its 8 B/leaf are gone from the loop
 __global__ __launch_bounds__(256) void k_update(float* __restrict__ x, float* __restrict__ r,
                                                 const float* __restrict__ p, const float* __restrict__ q, Ranges R,
-                                                double* partial, unsigned* counter, Scalars* sc, float alpha_fixed) {
+                                                double* partial, unsigned* counter, Scalars* sc, float alpha_fixed,
+                                                const uint32_t* __restrict__ act) {
   __shared__ double sred[8];
   const double pq = sc->sum_pq, rz = sc->sum_rz;
   const bool ok = alpha_fixed != 0.0f || (pq > 0.0 && isfinite(pq) && isfinite(rz));
   const float alpha = alpha_fixed != 0.0f ? alpha_fixed : (ok ? (float)(rz / pq) : 0.0f);
+  const float m = act ? (float)((sc->sum_r - (double)alpha * sc->sum_q) / sc->n_active) : 0.0f;
   double s2 = 0.0, s1 = 0.0;
   FOR_RANGES(R, i) {
     float4 xv = reinterpret_cast<float4*>(x)[i];
@@ -273,6 +293,13 @@ __global__ __launch_bounds__(256) void k_update(float* __restrict__ x, float* __
     xv.z = fmaf(alpha, pv.z, xv.z); xv.w = fmaf(alpha, pv.w, xv.w);
     rv.x = fmaf(-alpha, qv.x, rv.x); rv.y = fmaf(-alpha, qv.y, rv.y);
     rv.z = fmaf(-alpha, qv.z, rv.z); rv.w = fmaf(-alpha, qv.w, rv.w);
+    if (act) {
+      const unsigned am = act4(act, i);
+      if (am & 1u) rv.x -= m;
+      if (am & 2u) rv.y -= m;
+      if (am & 4u) rv.z -= m;
+      if (am & 8u) rv.w -= m;
+    }
     reinterpret_cast<float4*>(x)[i] = xv;
     reinterpret_cast<float4*>(r)[i] = rv;
     s2 += (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
@@ -299,7 +326,7 @@ __global__ __launch_bounds__(256) void k_project(float* __restrict__ r, const ui
                                                  unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   const float m = (float)(sc->sum_r / sc->n_active);
-  double s2 = 0.0;
+  double s2 = 0.0, s1 = 0.0;
   FOR_RANGES(R, i) {
     float4 v = reinterpret_cast<float4*>(r)[i];
     float e[4] = {v.x, v.y, v.z, v.w};
@@ -307,12 +334,12 @@ __global__ __launch_bounds__(256) void k_project(float* __restrict__ r, const ui
     for (int k = 0; k < 4; ++k) {
       if ((am >> k) & 1u) e[k] -= m;
       s2 += (double)e[k] * e[k];
+      s1 += (double)e[k];
     }
     reinterpret_cast<float4*>(r)[i] = make_float4(e[0], e[1], e[2], e[3]);
   }
-  double b2 = block_reduce_d(s2, sred);
-  double tot;
-  if (last_block_sum(b2, partial, counter, gridDim.x, &tot, sred)) sc->sum_rr = tot;
+  // ||r||^2 and the sum of the projected r (the next fused projection's starting mean)
+  reduce2(s2, s1, partial, counter, sc, SF_RR, SF_R, sred);
 }
 
 // (r, z) (Alg. 1 line 12)
@@ -437,12 +464,12 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   if (a.partial) {
     if (inl) k_apply_v6<true, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<true, false><<<a.ntiles, 128, 0, s>>>(a);
-    // 4 warp partials per tile, summed in two fixed-order stages
+    // 4 warp partials per tile of p.q, then of sum q; summed in two fixed-order stages
     const int64_t n = 4 * (int64_t)a.ntiles;
     const int G = (int)std::min<int64_t>(296, (n + 4095) / 4096);
     const int64_t chunk = (n + G - 1) / G;
-    k_chunk_sums<<<G, 256, 0, s>>>(a.partial, n, chunk, a.partial + n);
-    k_finish_sigma<<<1, 1024, 0, s>>>(a.partial + n, G, a.sc);
+    k_chunk_sums<<<dim3(G, 2), 256, 0, s>>>(a.partial, n, chunk, a.partial + 2 * n);
+    k_finish_sigma<<<2, 1024, 0, s>>>(a.partial + 2 * n, G, a.sc);
   } else {
     if (inl) k_apply_v6<false, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<false, false><<<a.ntiles, 128, 0, s>>>(a);
@@ -454,8 +481,9 @@ void launch_init(const float* b, const uint32_t* act, float* r, float* x, const 
   k_init<<<grid, 256, 0, s>>>(b, act, r, x, R, partial, counter, sc);
 }
 void launch_update(float* x, float* r, const float* p, const float* q, const Ranges& R, double* partial,
-                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid, float alpha_fixed) {
-  k_update<<<grid, 256, 0, s>>>(x, r, p, q, R, partial, counter, sc, alpha_fixed);
+                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid, float alpha_fixed,
+                   const uint32_t* act_proj) {
+  k_update<<<grid, 256, 0, s>>>(x, r, p, q, R, partial, counter, sc, alpha_fixed, act_proj);
 }
 void launch_project(float* r, const uint32_t* act, const Ranges& R, double* partial, unsigned* counter, Scalars* sc,
                     cudaStream_t s, int grid) {

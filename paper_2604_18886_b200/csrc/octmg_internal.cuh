@@ -124,13 +124,14 @@ struct Scalars {
   double sum_r;    // sum of r over active cells (null-space projection)
   double sum_rz;   // (r, z) of the current iteration
   double sum_pq;   // (p, A p)
+  double sum_q;    // sum of A p over active cells (the projected update's mean)
   double rho;      // (r, z) of the previous iteration (beta = sum_rz / rho)
   double n_active; // number of active leaf cells (all parts)
   int flags;       // bit0: breakdown (sigma <= 0 or non-finite)
   float beta_f;    // beta = sum_rz / rho of Alg. 1 line 12 in fp32, set once per iteration
 };
 // offsets (in doubles) of the reduced fields, for the cross-part sums
-enum { SF_RR = 0, SF_R = 1, SF_RZ = 2, SF_PQ = 3 };
+enum { SF_RR = 0, SF_R = 1, SF_RZ = 2, SF_PQ = 3, SF_Q = 4 };
 
 // owned leaf cells as float4 index ranges (one per level at most)
 struct Ranges {
@@ -177,7 +178,8 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s);
 void launch_init(const float* b, const uint32_t* act, float* r, float* x, const Ranges& R, double* partial,
                  unsigned* counter, Scalars* sc, cudaStream_t s, int grid);
 void launch_update(float* x, float* r, const float* p, const float* q, const Ranges& R, double* partial,
-                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid, float alpha_fixed = 0.0f);
+                   unsigned* counter, Scalars* sc, cudaStream_t s, int grid, float alpha_fixed = 0.0f,
+                   const uint32_t* act_proj = nullptr);  // act_proj: also project r (null-space, fused)
 void launch_project(float* r, const uint32_t* act, const Ranges& R, double* partial, unsigned* counter,
                     Scalars* sc, cudaStream_t s, int grid);
 void launch_dot_rz(const float* r, const float* z, const Ranges& R, double* partial, unsigned* counter,
