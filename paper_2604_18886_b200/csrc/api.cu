@@ -820,6 +820,8 @@ ApplyArgs apply_args(const Hier& h) {
   a.partial = nullptr; a.counter = nullptr; a.sc = h.sc; a.NL = T.NL;
   a.irr_inline = 0;
   for (int l = 0; l <= T.L; ++l) a.irr_inline |= h.lvl_ghost[l] ? 1 : 0;
+  a.lean = h.n_dtiles == 0 ? 1 : 0;
+  a.sumq = 0;
   return a;
 }
 
@@ -1085,6 +1087,7 @@ octmg_status build_loop_graph(Group& g, bool ns) {
       a.q = p->q;
       a.partial = p->partial;
       a.counter = p->counter + 3;
+      a.sumq = ns ? 1 : 0;
       launch_apply(a, cs);  // q = A p, p.q
     }
     OCTMG_TRY(allreduce(g, SF_PQ, 2, cs));  // p.q and sum q
@@ -1251,6 +1254,7 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
       a.q = h->q;
       a.partial = h->partial;
       a.counter = h->counter + 3;
+      a.sumq = ns ? 1 : 0;
       {
         // read p, record; write q
         ProfScope ps(*h, KC_APPLY, s, (double)h->n_apply_tiles * TB3 * 24.0);

@@ -191,6 +191,8 @@ __device__ __noinline__ void pass_row_ghost(const SmoothArgs& a, int t, int n0, 
 
 // INL: the ghost body inlined (1: at 12 CTAs/SM, 80 registers; 2: at 14 CTAs/SM, 72 registers)
 // instead of out of line at 16 (the regular path's occupancy; the ghost body spills)
+// (an instance without the ghost path for ghost-free levels — 61 registers, no call frame —
+// measured slower: config 2 level-5 passes 2.77 vs 2.63 ms per solve; not kept)
 template <int MODE, int INL>  // INL: 0 out of line (16 CTAs/SM), 1 inline at 12, 2 inline at 14
 __global__ __launch_bounds__(64, INL == 1 ? 12 : (INL == 2 ? 14 : 16)) void k_pass_v3(const __grid_constant__ SmoothArgs a) {
   const int t = level_tile(a, blockIdx.x);

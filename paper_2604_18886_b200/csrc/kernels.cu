@@ -58,13 +58,15 @@ __device__ __forceinline__ bool last_block_sum(double mine, double* partial, uns
 // row sums d (setup.cu k_leaf_rowsum, rowk::row_sums_flux); the ghost and inner entries are
 // formed directly as differences.  Algorithmic bytes: read p and the 4 record planes, write
 // q = 24 B per leaf cell (+4 B on tiles with a nonzero row sum).
-template <bool DOT, bool IRR>
+// LEAN: a hierarchy without same-level inner neighbours of leaf tiles and without nonzero row
+// sums (every uniform tree): no pbar select per neighbour pointer, no row-sum load
+template <bool DOT, bool IRR, bool LEAN = false>
 __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const int (&nb)[6], double* sred) {
   using namespace rowk;
   const RowGeo g = row_geo(threadIdx.x & 1, threadIdx.x >> 1);
   const float* pz = a.z;
   const float* ct = a.coef + ((size_t)t << 11);
-  const int dk = __ldg(a.dtile + t);
+  const int dk = LEAN ? -1 : __ldg(a.dtile + t);
   const float4 pc = ld4(pz + ((size_t)t << 9) + g.own);
   const float4 c0 = ld4(ct + g.own), cxm = ld4(ct + 512 + g.own), cym = ld4(ct + 1024 + g.own),
                czm = ld4(ct + 1536 + g.own);
@@ -73,7 +75,7 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
   // active children precomputed on the face layer the row reads (k_inner_face_means)
   const float* pb = a.pbar;
   auto tu = [pz, pb, NL](int n) -> const float* {
-    return n < NL ? pz + ((size_t)n << 9) : pb + ((size_t)(n - NL) << 9);
+    return (LEAN || n < NL) ? pz + ((size_t)n << 9) : pb + ((size_t)(n - NL) << 9);
   };
   RowSt s;
   row_load<decltype(tu), true>(s, tu, a.coef, t, nb, g);
@@ -98,15 +100,13 @@ __device__ __forceinline__ void apply_row_body(const ApplyArgs& a, int t, const 
     // k_update); k_chunk_sums / k_finish_sigma sum them in tile order (deterministic)
     double dd = (double)pv.x * (double)r.x + (double)pv.y * (double)r.y + (double)pv.z * (double)r.z +
                 (double)pv.w * (double)r.w;
-    double dq = ((double)r.x + (double)r.y) + ((double)r.z + (double)r.w);
-    for (int o = 16; o; o >>= 1) {
-      dd += __shfl_down_sync(0xffffffffu, dd, o);
-      dq += __shfl_down_sync(0xffffffffu, dq, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      const size_t w = 4 * (size_t)blockIdx.x + (threadIdx.x >> 5);
-      a.partial[w] = dd;
-      a.partial[4 * (size_t)gridDim.x + w] = dq;
+    for (int o = 16; o; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+    const size_t w = 4 * (size_t)blockIdx.x + (threadIdx.x >> 5);
+    if ((threadIdx.x & 31) == 0) a.partial[w] = dd;
+    if (a.sumq) {  // (uniform: PCG with the null-space projection)
+      double dq = ((double)r.x + (double)r.y) + ((double)r.z + (double)r.w);
+      for (int o = 16; o; o >>= 1) dq += __shfl_down_sync(0xffffffffu, dq, o);
+      if ((threadIdx.x & 31) == 0) a.partial[4 * (size_t)gridDim.x + w] = dq;
     }
   }
 }
@@ -121,12 +121,16 @@ __device__ __noinline__ void apply_row_irr(const ApplyArgs& a, int t, int n0, in
 
 // INL: the irregular body inlined, at 6 CTAs/SM (80 registers) instead of out of line at 8
 // (measured on configs 3 / 5: inlined at 7 or 8 CTAs/SM, 72 / 64 registers with spills, slower)
-template <bool DOT, bool INL>
+template <bool DOT, bool INL, bool LEAN = false>
 __global__ __launch_bounds__(128, INL ? 6 : 8) void k_apply_v6(const __grid_constant__ ApplyArgs a) {
   __shared__ double sred[4];
   const int t = a.tiles ? a.tiles[blockIdx.x] : (int)blockIdx.x;
   int nb[6];
   rowk::load_nb(a.nbr, t, nb);
+  if (LEAN) {  // (a tree without T-junction tiles: no irregular body, no call frame)
+    apply_row_body<DOT, false, true>(a, t, nb, sred);
+    return;
+  }
   bool irr = false;
 #pragma unroll
   for (int f = 0; f < 6; ++f) irr |= nb[f] <= -2;  // ghost faces (inner neighbours read pbar)
@@ -461,17 +465,25 @@ void launch_apply(const ApplyArgs& a, cudaStream_t s) {
     env = !e ? -1 : (e[0] == 'i' ? 1 : 0);
   }
   const bool inl = env >= 0 ? env == 1 : a.irr_inline != 0;
+  // trees without T-junction tiles, inner neighbours of leaf tiles or row sums: the lean body
+  // (no pbar select, no row-sum load, no out-of-line call frame; 62 registers: config 2
+  // apply 0.76 -> 0.67 ms per solve)
+  const char* le = getenv("OCTMG_APPLY_LEAN");  // 0: the general body everywhere
+  const bool lean = !inl && !a.irr_inline && a.n_ifaces == 0 && a.lean && !(le && le[0] == '0');
   if (a.partial) {
     if (inl) k_apply_v6<true, true><<<a.ntiles, 128, 0, s>>>(a);
+    else if (lean) k_apply_v6<true, false, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<true, false><<<a.ntiles, 128, 0, s>>>(a);
     // 4 warp partials per tile of p.q, then of sum q; summed in two fixed-order stages
     const int64_t n = 4 * (int64_t)a.ntiles;
     const int G = (int)std::min<int64_t>(296, (n + 4095) / 4096);
     const int64_t chunk = (n + G - 1) / G;
-    k_chunk_sums<<<dim3(G, 2), 256, 0, s>>>(a.partial, n, chunk, a.partial + 2 * n);
-    k_finish_sigma<<<2, 1024, 0, s>>>(a.partial + 2 * n, G, a.sc);
+    const int ny = a.sumq ? 2 : 1;
+    k_chunk_sums<<<dim3(G, ny), 256, 0, s>>>(a.partial, n, chunk, a.partial + 2 * n);
+    k_finish_sigma<<<ny, 1024, 0, s>>>(a.partial + 2 * n, G, a.sc);
   } else {
     if (inl) k_apply_v6<false, true><<<a.ntiles, 128, 0, s>>>(a);
+    else if (lean) k_apply_v6<false, false, true><<<a.ntiles, 128, 0, s>>>(a);
     else k_apply_v6<false, false><<<a.ntiles, 128, 0, s>>>(a);
   }
 }

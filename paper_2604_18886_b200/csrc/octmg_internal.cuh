@@ -171,6 +171,8 @@ struct ApplyArgs {
   Scalars* sc;          // sum_pq written by the finish kernel
   int NL;
   int irr_inline;       // the irregular-tile body inlined (trees with T-junction tiles)
+  int lean;             // no nonzero leaf row sums (the lean body skips the row-sum load)
+  int sumq;             // also sum q into Scalars::sum_q (PCG with the null-space projection)
 };
 void launch_apply(const ApplyArgs& a, cudaStream_t s);
 
