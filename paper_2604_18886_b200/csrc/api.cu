@@ -108,7 +108,7 @@ Group::~Group() {
 // ------------------------------------------------------------------------------------
 namespace {
 
-enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
+enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5, SM_PLAIN_RZ = 6 };
 
 inline int stage_desc(int colour, int mode) { return colour | (mode << 1); }
 
@@ -256,6 +256,8 @@ void read_env(Hier& h) {
     }
 }
 
+bool split_pass(const Hier& h, int l, int mode);
+
 octmg_status build_schedule(Group& g) {
   g.ops.clear();
   for (Hier* p : g.parts) {
@@ -283,6 +285,21 @@ octmg_status build_schedule(Group& g) {
   if (T.NL > T.lc[T.L]) g.ops.push_back(Op{2, 0, 0});  // coarse leaves start the cycle at 0
   Builder b{g, h};
   b.fas(T.L, false);
+  // (r, z) fused into the last pass of M when every leaf is at the finest level and that level
+  // runs the 128-bit row pass (OCTMG_RZ_FUSED=0: the separate k_dot_rz pass)
+  g.rz_fused = false;
+  const char* rf = getenv("OCTMG_RZ_FUSED");
+  const int lt = T.lc[T.L] + T.ic[T.L];
+  if (!(rf && atoi(rf) == 0) && T.NL == T.lc[T.L] && T.L > h.sub_K && lt >= h.pass_big && h.pass_cpt == 4 &&
+      h.pass_v2 && pass_v3_on() && !h.lvl_ghost[T.L] && h.prm.form == 0)
+    for (auto it = g.ops.rbegin(); it != g.ops.rend(); ++it)
+      if (it->kind == 0 && it->level == T.L) {
+        if ((it->stage >> 1) == SM_PLAIN && !split_pass(h, T.L, SM_PLAIN)) {
+          it->stage = stage_desc(it->stage & 1, SM_PLAIN_RZ);
+          g.rz_fused = true;
+        }
+        break;
+      }
   return OCTMG_OK;
 }
 
@@ -328,6 +345,7 @@ int64_t schedule_kernels(const Group& g) {
     for (const Op& op : g.ops) {
       if (op.kind == 2 || op.kind == 7 || op.kind == 8) continue;
       n += 1;
+      if (op.kind == 0 && (op.stage >> 1) == SM_PLAIN_RZ) n += 2;  // + the (r, z) chunk sums and finish
       if (op.kind == 0 && (op.stage >> 1) == SM_RESTRICT && split_restrict(*h, op.level)) n += 1;
       if (op.kind == 0 && (op.stage >> 1) != SM_RESTRICT && split_pass(*h, op.level, op.stage >> 1)) n += 1;
     }
@@ -446,6 +464,7 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
   // parents' u, u*, b (1.5 B); prolongation-fused passes read the parents' u, u* (+1 B)
   const double cells = (double)a.n * TB3;
   double bytes = cells * (mode == SM_RESTRICT ? 25.5 : (mode == SM_ZERO1 ? 6.0 : 20.0));
+  if (mode == SM_PLAIN_RZ) bytes += 2.0 * cells;  // the other colour's r
   if (mode == SM_PRO1 || mode == SM_PRO2) bytes += cells;
   int cls = mode == SM_RESTRICT ? KC_RESTRICT
           : (l == 0 ? KC_COARSEST : (l < T.L ? KC_SMOOTH_COARSE : KC_PASS));
@@ -489,7 +508,9 @@ void launch_op(Hier& h, const Op& op, cudaStream_t s) {
       launch_pass_direct(ar, s, cpt);
       launch_pass_direct(ag, s, cpt | 32);
     } else {
+      a.rz_partial = h.partial;
       launch_pass_direct(a, s, cpt | (h.lvl_ghost[l] ? 32 : 0));
+      if (mode == SM_PLAIN_RZ) launch_rz_finish(h.partial, 2 * (int64_t)a.n, h.partial + 2 * (size_t)a.n, h.sc, s);
     }
   }
 }
@@ -1070,8 +1091,9 @@ octmg_status build_loop_graph(Group& g, bool ns) {
   const int G = vec_grid();
   OCTMG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
   auto seq = [&]() -> octmg_status {
-    OCTMG_TRY(launch_ops(g, cs));  // z = M r
-    for (Hier* p : g.parts) launch_dot_rz(p->r, p->z, p->own_cells, p->partial, p->counter + 2, p->sc, cs, G);
+    OCTMG_TRY(launch_ops(g, cs));  // z = M r (with (r, z) when fused into its last pass)
+    if (!g.rz_fused)
+      for (Hier* p : g.parts) launch_dot_rz(p->r, p->z, p->own_cells, p->partial, p->counter + 2, p->sc, cs, G);
     OCTMG_TRY(allreduce(g, SF_RZ, 1, cs));  // (r, z)
     if (g.comm)
       for (Hier* p : g.parts) launch_set_beta(p->sc, cs);  // beta from the summed (r, z)
@@ -1163,11 +1185,13 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     return allreduce(g, SF_RR, 2, s);  // ||r||^2 and sum r of the projected r
   };
   auto dot_rz = [&]() -> octmg_status {
-    for (Hier* h : g.parts) {
-      ProfScope ps(*h, KC_DOT, s, (double)h->n_apply_tiles * TB3 * 8.0);
-      launch_dot_rz(h->r, h->z, h->own_cells, h->partial, h->counter + 2, h->sc, s, G);
+    if (!g.rz_fused) {  // (else summed by the last pass of M)
+      for (Hier* h : g.parts) {
+        ProfScope ps(*h, KC_DOT, s, (double)h->n_apply_tiles * TB3 * 8.0);
+        launch_dot_rz(h->r, h->z, h->own_cells, h->partial, h->counter + 2, h->sc, s, G);
+      }
+      g.launches += np;
     }
-    g.launches += np;
     OCTMG_TRY(allreduce(g, SF_RZ, 1, s));
     if (g.comm) {  // beta from the summed (r, z)
       for (Hier* h : g.parts) launch_set_beta(h->sc, s);
@@ -1221,7 +1245,8 @@ octmg_status octmg_pcg_solve(octmg_hier* hh, const float* b, float* x, const oct
     OCTMG_CUDA(cudaStreamSynchronize(s));
     const int kk = L->k;
     // per iteration: the cycle, dot_rz, p update, apply + finish, x/r update, projection, check
-    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 + (g.comm ? 1 : 0)) + 1 + inner_mean_kernels(g));
+    g.launches += (int64_t)kk * (schedule_kernels(g) + np * (6 - (g.rz_fused ? 1 : 0) + (g.comm ? 1 : 0)) + 1 +
+                                 inner_mean_kernels(g));
     hist_lim = LOOP_HCAP;
     if (report && report->history) {
       const int nh = std::min(kk, std::min((int)report->history_cap, LOOP_HCAP));

@@ -178,6 +178,19 @@ __device__ __forceinline__ void pass_row_body(const SmoothArgs& a, int t, const 
   r.z = q0.z != 0.0f ? (bb.z - f.z) / q0.z : 0.0f;
   r.w = q0.w != 0.0f ? (bb.w - f.w) / q0.w : 0.0f;
   *reinterpret_cast<float4*>(ut + g.own) = r;
+  if (MODE == SM_PLAIN_RZ) {
+    // the last pass of M on a uniform tree (every leaf at this level): z is final here — this
+    // colour's row just computed, the other colour's row (s.ox) untouched since the previous
+    // pass — so (r, z) of Alg. 1 line 12 is summed here (r = the leaf b) instead of in a pass
+    // of its own; one fp64 partial per warp (2 per tile), summed in fixed order afterwards
+    const float4 bo = ld4(tptr(a.b, t, a.NL) + g.oth);
+    double dd = (double)bb.x * (double)r.x + (double)bb.y * (double)r.y + (double)bb.z * (double)r.z +
+                (double)bb.w * (double)r.w;
+    dd += (double)bo.x * (double)s.ox.x + (double)bo.y * (double)s.ox.y + (double)bo.z * (double)s.ox.z +
+          (double)bo.w * (double)s.ox.w;
+    for (int o = 16; o; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+    if ((threadIdx.x & 31) == 0) a.rz_partial[2 * (size_t)blockIdx.x + (threadIdx.x >> 5)] = dd;
+  }
 }
 
 // the ghost-tile body out of line: its extra registers (spilled to L1-resident local memory
@@ -514,7 +527,9 @@ static int pass_ghost_minb() {
 }
 
 // OCTMG_PASS_V=2: the scalar k_pass_v2 on big levels instead of the 128-bit k_pass_v3
-static bool pass_v3_enabled() {
+bool pass_v3_on();
+static bool pass_v3_enabled() { return pass_v3_on(); }
+bool pass_v3_on() {
   int on = -1;
   if (on < 0) {
     const char* e = getenv("OCTMG_PASS_V");
@@ -546,6 +561,7 @@ static void launch_pass_cpt(const SmoothArgs& a, int mode, cudaStream_t s, bool 
         else if (pass_ghost_minb() == 14) k_pass_v3<SM_ZERO2, 2><<<grid, 64, 0, s>>>(a);
         else k_pass_v3<SM_ZERO2, 1><<<grid, 64, 0, s>>>(a);
         break;
+      case SM_PLAIN_RZ: k_pass_v3<SM_PLAIN_RZ, 0><<<grid, 64, 0, s>>>(a); break;  // (ghost-free levels only)
       default:
         if (!pass_ghost_inline(ghosts)) k_pass_v3<SM_PLAIN, 0><<<grid, 64, 0, s>>>(a);
         else if (pass_ghost_minb() == 14) k_pass_v3<SM_PLAIN, 2><<<grid, 64, 0, s>>>(a);

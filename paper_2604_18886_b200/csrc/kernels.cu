@@ -449,6 +449,38 @@ __global__ void k_build_mask(const float* coef, int64_t nwords, uint32_t* act) {
 
 }  // namespace
 
+// (r, z) from the fused last pass's partials (2 per tile) and beta = (r, z) / rho
+__global__ __launch_bounds__(1024) void k_finish_rz(const double* partial, int n, Scalars* sc) {
+  __shared__ double sred[32];
+  const int bd = blockDim.x;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = threadIdx.x;
+  for (; k + 3 * bd < n; k += 4 * bd) {
+    s0 += partial[k];
+    s1 += partial[k + bd];
+    s2 += partial[k + 2 * bd];
+    s3 += partial[k + 3 * bd];
+  }
+  for (; k < n; k += bd) s0 += partial[k];
+  double s = (s0 + s1) + (s2 + s3);
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sred[w];
+    sc->sum_rz = tot;
+    sc->beta_f = (float)(tot / sc->rho);  // (multi-part jobs recompute it after the allreduce)
+  }
+}
+
+void launch_rz_finish(const double* partial, int64_t n, double* scratch, Scalars* sc, cudaStream_t s) {
+  const int G = (int)std::min<int64_t>(296, (n + 4095) / 4096);
+  const int64_t chunk = (n + G - 1) / G;
+  k_chunk_sums<<<G, 256, 0, s>>>(partial, n, chunk, scratch);
+  k_finish_rz<<<1, 1024, 0, s>>>(scratch, G, sc);
+}
+
 void launch_apply(const ApplyArgs& a, cudaStream_t s) {
   if (a.n_ifaces > 0) k_inner_face_means<<<a.n_ifaces, 64, 0, s>>>(a.ifaces, a.child, a.coef, a.z, a.pbar, a.NL);
   if (a.ntiles == 0) {

@@ -230,9 +230,14 @@ struct SmoothArgs {
   const float* c0M;
   const int* c0tile;
   int c0n;
+  double* rz_partial;   // SM_PLAIN_RZ (the last pass of M on a uniform tree): per-warp fp64
+                        // partials of (r, z) over the tile's cells (PCG Alg. 1 line 12)
 };
 void launch_fasrhs(const SmoothArgs& a, int ninner, cudaStream_t s);
 void launch_pass_direct(const SmoothArgs& a, cudaStream_t s, int cpt);
+bool pass_v3_on();  // the 128-bit row pass on big levels (not OCTMG_PASS_V=2)
+// (r, z) and beta from the SM_PLAIN_RZ pass's 2 partials per tile (fixed order)
+void launch_rz_finish(const double* partial, int64_t n, double* scratch, Scalars* sc, cudaStream_t s);
 void launch_restrict_direct(const SmoothArgs& a, cudaStream_t s, int v2);  // 0 staged, 6 / 8: k_restrict_v2 min CTAs/SM
 void launch_prolong(const SmoothArgs& a, cudaStream_t s);
 int subcycle_max_tiles();
@@ -412,6 +417,7 @@ struct Group {
   LoopState* loop_host = nullptr;        // mapped pinned (host pointer)
   LoopState* loop_host_dev = nullptr;    // its device pointer
   int loop_ns = -1;                      // null-space flag the loop graph was built with
+  bool rz_fused = false;                 // (r, z) summed by the last pass of M (build_schedule)
   bool loop_unavailable = false;         // building the loop graph failed: host-driven loop
   int64_t launches = 0;
   ~Group();

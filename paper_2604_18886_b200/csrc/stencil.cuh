@@ -9,7 +9,7 @@
 
 namespace octmg {
 
-enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5 };
+enum { SM_PLAIN = 0, SM_ZERO1 = 1, SM_ZERO2 = 2, SM_PRO1 = 3, SM_PRO2 = 4, SM_RESTRICT = 5, SM_PLAIN_RZ = 6 };
 
 // the i-th tile of a level launch: from the order array, or computed (no dependent load
 // before the tile's own loads can issue)

@@ -256,7 +256,7 @@ def test_full_size_cfg2_parity(om):
                                  {"OCTMG_COARSE_DENSE": "0", "OCTMG_SUBCYCLE": "0"},
                                  {"OCTMG_RESTRICT_ROW": "1"}, {"OCTMG_RESTRICT_ROW": "0"}, {"OCTMG_RESTRICT_RED": "0"},
                                  {"OCTMG_RESTRICT_SPLIT": "big"}, {"OCTMG_APPLY_IRR": "inline"},
-                                 {"OCTMG_APPLY_IRR": "call"}, {"OCTMG_FASRHS": "cell"},
+                                 {"OCTMG_APPLY_IRR": "call"}, {"OCTMG_FASRHS": "cell"}, {"OCTMG_RZ_FUSED": "0"},
                                  {"OCTMG_APPLY_LEAN": "0"},
                                  {"OCTMG_CD_THREADS": "1024"}, {"OCTMG_TILE_ORDER": "slab"}])
 @pytest.mark.parametrize("name", ["sphere_small", "tank_small", "uniform64", "sphere_35"])
