@@ -120,18 +120,81 @@ __device__ __forceinline__ float dface_sum(const CDLevel& L, const CDMem& M, int
   return s;
 }
 
-// RBGS colour pass at level l, in place (reads only the other colour)
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float g4(const float4& v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; }
+
+// One colour row segment of 4 cells (x = 2m + p, m = 4 seg .. 4 seg + 3) of a dense colour-split
+// grid: the face sums of the 4 cells from 128-bit shared-memory loads of the other colour's
+// rows (same / y-+1 / z-+1) and coupling planes plus the one x-neighbour outside the segment
+// — the row form of the tile kernels (rowtile.cuh) on shared memory, same sum order as
+// dface_sum (x-, x+, y-, y+, z-, z+ from 0; walls 0), ~16 loads per 4 cells instead of ~14
+// per cell and the index arithmetic once per segment.  vzm/vzp, czp: the z-neighbour rows
+// (given by the caller: in the level, or across a slab boundary through distributed smem).
+struct RowNb {
+  float4 ox, ym, yp, zm, zp, cxo, cyp, czp;
+  float xs, xsc;
+};
+__device__ __forceinline__ float4 row_face4(const RowNb& r, int p, const float4& qx, const float4& qy,
+                                            const float4& qz) {
+  float o[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const float vxm = p ? g4(r.ox, m) : (m == 0 ? r.xs : g4(r.ox, m - 1));
+    const float vxp = p ? (m == 3 ? r.xs : g4(r.ox, m + 1)) : g4(r.ox, m);
+    const float cxp = p ? (m == 3 ? r.xsc : g4(r.cxo, m + 1)) : g4(r.cxo, m);
+    float sm = 0.0f;
+    sm = fmaf(g4(qx, m), vxm, sm);
+    sm = fmaf(cxp, vxp, sm);
+    sm = fmaf(g4(qy, m), g4(r.ym, m), sm);
+    sm = fmaf(g4(r.cyp, m), g4(r.yp, m), sm);
+    sm = fmaf(g4(qz, m), g4(r.zm, m), sm);
+    sm = fmaf(g4(r.czp, m), g4(r.zp, m), sm);
+    o[m] = sm;
+  }
+  return make_float4(o[0], o[1], o[2], o[3]);
+}
+
+// the in-plane part of a segment's neighbours (x, y) from the other colour's row at `oth`
+__device__ __forceinline__ void row_nb_xy(RowNb& r, const float* u, const float* cx, const float* cy, int oth,
+                                          int p, int seg, int nseg, int hx, int y, int ny) {
+  const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  r.ox = lds4(u + oth);
+  r.cxo = lds4(cx + oth);
+  const bool xin = p ? seg < nseg - 1 : seg > 0;  // the x-neighbour outside the segment exists
+  const int xo = p ? oth + 4 : oth - 1;
+  r.xs = xin ? u[xo] : 0.0f;
+  r.xsc = (p && xin) ? cx[xo] : 0.0f;
+  r.ym = y > 0 ? lds4(u + oth - hx) : Z4;
+  r.yp = y < ny - 1 ? lds4(u + oth + hx) : Z4;
+  r.cyp = y < ny - 1 ? lds4(cy + oth + hx) : Z4;
+}
+
+// RBGS colour pass at level l, in place (reads only the other colour), row segments of 4
 template <int NT>
 __device__ __forceinline__ void cd_pass(const CDArgs& A, const CDMem& M, int l, int colour) {
   const CDLevel& L = A.lv[l];
-  const int nh = L.n >> 1;
-#pragma unroll 4
-  for (int k = threadIdx.x; k < nh; k += NT) {
-    int x, y, z;
-    dcell(L, colour, k, x, y, z);
-    const int i = colour * nh + k;
+  const int nh = L.n >> 1, hx = L.nx >> 1, nseg = hx >> 2, hxy = hx * L.ny;
+  const float* u = M.u + L.off;
+  const float* cc = M.coef + NP * L.off;
+  const float *cx = cc + L.n, *cy = cx + L.n, *cz = cy + L.n, *inv = cz + L.n;
+  const float* b = M.b + L.off;
+  const int nw = (L.n >> 3);  // rows x segments of one colour (nh / 4)
+  const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  for (int w = threadIdx.x; w < nw; w += NT) {
+    const int seg = w % nseg, row = w / nseg;
+    const int y = row % L.ny, z = row / L.ny;
+    const int p = (colour + y + z) & 1;
+    const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
+    RowNb r;
+    row_nb_xy(r, u, cx, cy, oth, p, seg, nseg, hx, y, L.ny);
+    r.zm = z > 0 ? lds4(u + oth - hxy) : Z4;
+    r.zp = z < L.nz - 1 ? lds4(u + oth + hxy) : Z4;
+    r.czp = z < L.nz - 1 ? lds4(cz + oth + hxy) : Z4;
+    const float4 f = row_face4(r, p, lds4(cx + own), lds4(cy + own), lds4(cz + own));
+    const float4 bb = lds4(b + own), iv = lds4(inv + own);
     // u = (b - sum) / c with the precomputed 1/c (0 on inactive cells: u = 0 there)
-    M.u[L.off + i] = (M.b[L.off + i] - dface_sum(L, M, x, y, z, i, 0.0f)) * M.coef[NP * L.off + 4 * L.n + i];
+    *reinterpret_cast<float4*>(M.u + L.off + own) =
+        make_float4((bb.x - f.x) * iv.x, (bb.y - f.y) * iv.y, (bb.z - f.z) * iv.z, (bb.w - f.w) * iv.w);
   }
   __syncthreads();
 }
@@ -421,14 +484,38 @@ __device__ __forceinline__ float slab_face_sum(const Slab& S, int x, int y, int 
   return s;
 }
 
+// the slab colour pass in row segments of 4 (cd_pass's form; the z-neighbour rows across the
+// slab boundary from the adjacent CTAs' shared memory, 128-bit distributed-smem loads)
 template <int NT>
 __device__ __forceinline__ void slab_pass(const Slab& S, int colour, cg::cluster_group& cl) {
-  const int nh = S.n >> 1;
-  for (int k = threadIdx.x; k < nh; k += NT) {
-    int x, y, z;
-    slab_cell(S, colour, k, x, y, z);
-    const int i = colour * nh + k;
-    S.u[i] = (S.b[i] - slab_face_sum(S, x, y, z, i, 0.0f)) * S.coef[4 * S.n + i];
+  const int nh = S.n >> 1, hx = S.hx, nseg = hx >> 2, hxy = S.hxy;
+  const float* u = S.u;
+  const float *cx = S.coef + S.n, *cy = cx + S.n, *cz = cy + S.n, *inv = cz + S.n;
+  const int nw = S.n >> 3;
+  const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  for (int w = threadIdx.x; w < nw; w += NT) {
+    const int seg = w % nseg, row = w / nseg;
+    const int y = row % S.ny, z = row / S.ny;
+    const int p = (colour + y + z) & 1;
+    const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
+    RowNb r;
+    row_nb_xy(r, u, cx, cy, oth, p, seg, nseg, hx, y, S.ny);
+    if (z > 0) r.zm = lds4(u + oth - hxy);
+    else r.zm = S.u_lo ? lds4(S.u_lo + oth + hxy) : Z4;
+    if (z < SLZ - 1) {
+      r.zp = lds4(u + oth + hxy);
+      r.czp = lds4(cz + oth + hxy);
+    } else if (S.u_hi) {
+      r.zp = lds4(S.u_hi + oth - hxy);
+      r.czp = lds4(S.cz_hi + oth - hxy);
+    } else {
+      r.zp = Z4;
+      r.czp = Z4;
+    }
+    const float4 f = row_face4(r, p, lds4(cx + own), lds4(cy + own), lds4(cz + own));
+    const float4 bb = lds4(S.b + own), iv = lds4(inv + own);
+    *reinterpret_cast<float4*>(S.u + own) =
+        make_float4((bb.x - f.x) * iv.x, (bb.y - f.y) * iv.y, (bb.z - f.z) * iv.z, (bb.w - f.w) * iv.w);
   }
   cl.sync();
 }
