@@ -97,37 +97,14 @@ __device__ __forceinline__ void dcell(const CDLevel& L, int c, int k, int& x, in
   x = 2 * (k - row * hx) + ((c + y + z) & 1);
 }
 
-// 7-point face sum of cell (x, y, z) (dense index i) at level L starting from s0, in the
-// order x-, x+, y-, y+, z-, z+ (walls: value 0)
-__device__ __forceinline__ float dface_sum(const CDLevel& L, const CDMem& M, int x, int y, int z, int i, float s0) {
-  const int o = L.off;
-  const float* u = M.u + o;
-  const float* cx = M.coef + NP * o + L.n;
-  const float* cy = cx + L.n;
-  const float* cz = cy + L.n;
-  const int hx = L.nx >> 1, hxy = hx * L.ny;
-  const int j = i < (L.n >> 1) ? i + (L.n >> 1) : i - (L.n >> 1);  // same (x>>1, y, z) in the other half
-  const int p = x & 1;
-  float s = s0;
-  // x-: cell x-1 at j - 1 + p; x+: x+1 at j + p
-  const bool xl = x > 0, xh = x < L.nx - 1, yl = y > 0, yh = y < L.ny - 1, zl = z > 0, zh = z < L.nz - 1;
-  s = fmaf(cx[i], xl ? u[j - 1 + p] : 0.0f, s);
-  s = fmaf(xh ? cx[j + p] : 0.0f, xh ? u[j + p] : 0.0f, s);
-  s = fmaf(cy[i], yl ? u[j - hx] : 0.0f, s);
-  s = fmaf(yh ? cy[j + hx] : 0.0f, yh ? u[j + hx] : 0.0f, s);
-  s = fmaf(cz[i], zl ? u[j - hxy] : 0.0f, s);
-  s = fmaf(zh ? cz[j + hxy] : 0.0f, zh ? u[j + hxy] : 0.0f, s);
-  return s;
-}
-
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ float g4(const float4& v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; }
 
 // One colour row segment of 4 cells (x = 2m + p, m = 4 seg .. 4 seg + 3) of a dense colour-split
 // grid: the face sums of the 4 cells from 128-bit shared-memory loads of the other colour's
 // rows (same / y-+1 / z-+1) and coupling planes plus the one x-neighbour outside the segment
-// — the row form of the tile kernels (rowtile.cuh) on shared memory, same sum order as
-// dface_sum (x-, x+, y-, y+, z-, z+ from 0; walls 0), ~16 loads per 4 cells instead of ~14
+// — the row form of the tile kernels (rowtile.cuh) on shared memory, sum order x-, x+,
+// y-, y+, z-, z+ from 0 or c u (the tile kernels'; walls 0), ~16 loads per 4 cells instead of ~14
 // per cell and the index arithmetic once per segment.  vzm/vzp, czp: the z-neighbour rows
 // (given by the caller: in the level, or across a slab boundary through distributed smem).
 struct RowNb {
@@ -135,14 +112,14 @@ struct RowNb {
   float xs, xsc;
 };
 __device__ __forceinline__ float4 row_face4(const RowNb& r, int p, const float4& qx, const float4& qy,
-                                            const float4& qz) {
+                                            const float4& qz, const float4& s0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f)) {
   float o[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
     const float vxm = p ? g4(r.ox, m) : (m == 0 ? r.xs : g4(r.ox, m - 1));
     const float vxp = p ? (m == 3 ? r.xs : g4(r.ox, m + 1)) : g4(r.ox, m);
     const float cxp = p ? (m == 3 ? r.xsc : g4(r.cxo, m + 1)) : g4(r.cxo, m);
-    float sm = 0.0f;
+    float sm = g4(s0, m);
     sm = fmaf(g4(qx, m), vxm, sm);
     sm = fmaf(cxp, vxp, sm);
     sm = fmaf(g4(qy, m), g4(r.ym, m), sm);
@@ -199,6 +176,33 @@ __device__ __forceinline__ void cd_pass(const CDArgs& A, const CDMem& M, int l, 
   __syncthreads();
 }
 
+// every row segment of both colours of a dense level: op(own, c, b, A u) with (A u) = c u +
+// the face sums (row_face4's order from c u) — the residual and FAS-rhs phases in row form
+template <int NT, class Op>
+__device__ __forceinline__ void cd_rows_au(const CDLevel& L, const CDMem& M, const Op& op) {
+  const int nh = L.n >> 1, hx = L.nx >> 1, nseg = hx >> 2, hxy = hx * L.ny, nw = L.n >> 3;
+  const float* u = M.u + L.off;
+  const float* cc = M.coef + NP * L.off;
+  const float *cx = cc + L.n, *cy = cx + L.n, *cz = cy + L.n;
+  const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  for (int w = threadIdx.x; w < 2 * nw; w += NT) {
+    const int colour = w >= nw, ww = w - colour * nw;
+    const int seg = ww % nseg, row = ww / nseg;
+    const int y = row % L.ny, z = row / L.ny;
+    const int p = (colour + y + z) & 1;
+    const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
+    RowNb r;
+    row_nb_xy(r, u, cx, cy, oth, p, seg, nseg, hx, y, L.ny);
+    r.zm = z > 0 ? lds4(u + oth - hxy) : Z4;
+    r.zp = z < L.nz - 1 ? lds4(u + oth + hxy) : Z4;
+    r.czp = z < L.nz - 1 ? lds4(cz + oth + hxy) : Z4;
+    const float4 c4 = lds4(cc + own), u4 = lds4(u + own);
+    const float4 f = row_face4(r, p, lds4(cx + own), lds4(cy + own), lds4(cz + own),
+                               make_float4(c4.x * u4.x, c4.y * u4.y, c4.z * u4.z, c4.w * u4.w));
+    op(own, c4, f);
+  }
+}
+
 template <int NT>
 __device__ __forceinline__ void cd_passes(const CDArgs& A, const CDMem& M, int l, int iters, bool red_first) {
   for (int k = 0; k < iters; ++k) {
@@ -213,14 +217,14 @@ template <int NT>
 __device__ __forceinline__ void cd_restrict(const CDArgs& A, const CDMem& M, int l) {
   const CDLevel& L = A.lv[l];
   const CDLevel& P = A.lv[l - 1];
-  for (int i = threadIdx.x; i < L.n; i += NT) {
-    const int c = i >= (L.n >> 1);
-    int x, y, z;
-    dcell(L, c, i - c * (L.n >> 1), x, y, z);
-    const float cc = M.coef[NP * L.off + i];
-    const float u = M.u[L.off + i];
-    M.scr[i] = cc != 0.0f ? M.b[L.off + i] - dface_sum(L, M, x, y, z, i, cc * u) : 0.0f;
-  }
+  const float* bl = M.b + L.off;
+  float* scr = M.scr;
+  cd_rows_au<NT>(L, M, [&](int own, const float4& c4, const float4& f) {
+    const float4 bb = lds4(bl + own);
+    *reinterpret_cast<float4*>(scr + own) =
+        make_float4(c4.x != 0.0f ? bb.x - f.x : 0.0f, c4.y != 0.0f ? bb.y - f.y : 0.0f,
+                    c4.z != 0.0f ? bb.z - f.z : 0.0f, c4.w != 0.0f ? bb.w - f.w : 0.0f);
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < P.n; i += NT) {
     const int c = i >= (P.n >> 1);
@@ -259,15 +263,14 @@ __device__ __forceinline__ void cd_restrict(const CDArgs& A, const CDMem& M, int
 template <int NT>
 __device__ __forceinline__ void cd_fasrhs(const CDArgs& A, const CDMem& M, int l) {
   const CDLevel& L = A.lv[l];
-  for (int i = threadIdx.x; i < L.n; i += NT) {
-    const int c = i >= (L.n >> 1);
-    int x, y, z;
-    dcell(L, c, i - c * (L.n >> 1), x, y, z);
-    const float cc = M.coef[NP * L.off + i];
-    const float u = M.u[L.off + i];
-    // each thread reads and writes only its own b (the stencil reads u)
-    M.b[L.off + i] = cc != 0.0f ? M.b[L.off + i] + dface_sum(L, M, x, y, z, i, cc * u) : 0.0f;
-  }
+  float* bl = M.b + L.off;
+  // each thread reads and writes only its own b (the stencil reads u)
+  cd_rows_au<NT>(L, M, [&](int own, const float4& c4, const float4& f) {
+    const float4 bb = lds4(bl + own);
+    *reinterpret_cast<float4*>(bl + own) =
+        make_float4(c4.x != 0.0f ? bb.x + f.x : 0.0f, c4.y != 0.0f ? bb.y + f.y : 0.0f,
+                    c4.z != 0.0f ? bb.z + f.z : 0.0f, c4.w != 0.0f ? bb.w + f.w : 0.0f);
+  });
   __syncthreads();
 }
 
@@ -458,30 +461,39 @@ __device__ __forceinline__ int slab_idx(const Slab& S, int x, int y, int z) {
   return (((x + y + z) & 1) * (S.n >> 1)) + (z * S.ny + y) * S.hx + (x >> 1);
 }
 
-// face sum of slab cell (x, y, z) (index i), order x-, x+, y-, y+, z-, z+, from s0
-__device__ __forceinline__ float slab_face_sum(const Slab& S, int x, int y, int z, int i, float s0) {
-  const float* cx = S.coef + S.n;
-  const float* cy = cx + S.n;
-  const float* cz = cy + S.n;
+// every row segment of both colours of the slab: op(own, c, A u) (cd_rows_au's form, the
+// z-neighbour rows across the slab boundary from the adjacent CTAs' shared memory)
+template <int NT, class Op>
+__device__ __forceinline__ void slab_rows_au(const Slab& S, const Op& op) {
+  const int nh = S.n >> 1, hx = S.hx, nseg = hx >> 2, hxy = S.hxy, nw = S.n >> 3;
   const float* u = S.u;
-  const int j = i < (S.n >> 1) ? i + (S.n >> 1) : i - (S.n >> 1);
-  const int p = x & 1;
-  const bool xl = x > 0, xh = x < S.nx - 1, yl = y > 0, yh = y < S.ny - 1;
-  float s = s0;
-  s = fmaf(cx[i], xl ? u[j - 1 + p] : 0.0f, s);
-  s = fmaf(xh ? cx[j + p] : 0.0f, xh ? u[j + p] : 0.0f, s);
-  s = fmaf(cy[i], yl ? u[j - S.hx] : 0.0f, s);
-  s = fmaf(yh ? cy[j + S.hx] : 0.0f, yh ? u[j + S.hx] : 0.0f, s);
-  // z-: the plane below (in this slab, or the top plane of the slab below)
-  float vzm = 0.0f;
-  if (z > 0) vzm = u[j - S.hxy];
-  else if (S.u_lo) vzm = S.u_lo[j + S.hxy];
-  s = fmaf(cz[i], vzm, s);
-  float vzp = 0.0f, czp = 0.0f;
-  if (z < SLZ - 1) { vzp = u[j + S.hxy]; czp = cz[j + S.hxy]; }
-  else if (S.u_hi) { vzp = S.u_hi[j - S.hxy]; czp = S.cz_hi[j - S.hxy]; }
-  s = fmaf(czp, vzp, s);
-  return s;
+  const float *cx = S.coef + S.n, *cy = cx + S.n, *cz = cy + S.n;
+  const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  for (int w = threadIdx.x; w < 2 * nw; w += NT) {
+    const int colour = w >= nw, ww = w - colour * nw;
+    const int seg = ww % nseg, row = ww / nseg;
+    const int y = row % S.ny, z = row / S.ny;
+    const int p = (colour + y + z) & 1;
+    const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
+    RowNb r;
+    row_nb_xy(r, u, cx, cy, oth, p, seg, nseg, hx, y, S.ny);
+    if (z > 0) r.zm = lds4(u + oth - hxy);
+    else r.zm = S.u_lo ? lds4(S.u_lo + oth + hxy) : Z4;
+    if (z < SLZ - 1) {
+      r.zp = lds4(u + oth + hxy);
+      r.czp = lds4(cz + oth + hxy);
+    } else if (S.u_hi) {
+      r.zp = lds4(S.u_hi + oth - hxy);
+      r.czp = lds4(S.cz_hi + oth - hxy);
+    } else {
+      r.zp = Z4;
+      r.czp = Z4;
+    }
+    const float4 c4 = lds4(S.coef + own), u4 = lds4(u + own);
+    const float4 f = row_face4(r, p, lds4(cx + own), lds4(cy + own), lds4(cz + own),
+                               make_float4(c4.x * u4.x, c4.y * u4.y, c4.z * u4.z, c4.w * u4.w));
+    op(own, c4, f);
+  }
 }
 
 // the slab colour pass in row segments of 4 (cd_pass's form; the z-neighbour rows across the
@@ -574,16 +586,13 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_cluster(const __grid_constant_
     }
   }
   cl.sync();
-  if (C.fas_first && !A.std_form) {  // b^2 += A^2 u* (u^2 = u* on entry)
-    for (int i = threadIdx.x; i < S.n; i += NT) {
-      const int c = i >= (S.n >> 1);
-      int x, y, z;
-      slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
-      const float cc = S.coef[i];
-      S.scr[i] = cc != 0.0f ? S.b[i] + slab_face_sum(S, x, y, z, i, cc * S.u[i]) : 0.0f;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < S.n; i += NT) S.b[i] = S.scr[i];
+  if (C.fas_first && !A.std_form) {  // b^2 += A^2 u* (u^2 = u* on entry; the stencil reads u only)
+    slab_rows_au<NT>(S, [&](int own, const float4& c4, const float4& f) {
+      const float4 bb = lds4(S.b + own);
+      *reinterpret_cast<float4*>(S.b + own) =
+          make_float4(c4.x != 0.0f ? bb.x + f.x : 0.0f, c4.y != 0.0f ? bb.y + f.y : 0.0f,
+                      c4.z != 0.0f ? bb.z + f.z : 0.0f, c4.w != 0.0f ? bb.w + f.w : 0.0f);
+    });
     cl.sync();  // the neighbours' reads of u done before the passes write it
   }
   // pre-smoothing (R, B) x nu_pre
@@ -592,13 +601,12 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_cluster(const __grid_constant_
     slab_pass<NT>(S, 1, cl);
   }
   // residual, then the level-1 parents of this slab (plane `rank`) into CTA 0
-  for (int i = threadIdx.x; i < S.n; i += NT) {
-    const int c = i >= (S.n >> 1);
-    int x, y, z;
-    slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
-    const float cc = S.coef[i];
-    S.scr[i] = cc != 0.0f ? S.b[i] - slab_face_sum(S, x, y, z, i, cc * S.u[i]) : 0.0f;
-  }
+  slab_rows_au<NT>(S, [&](int own, const float4& c4, const float4& f) {
+    const float4 bb = lds4(S.b + own);
+    *reinterpret_cast<float4*>(S.scr + own) =
+        make_float4(c4.x != 0.0f ? bb.x - f.x : 0.0f, c4.y != 0.0f ? bb.y - f.y : 0.0f,
+                    c4.z != 0.0f ? bb.z - f.z : 0.0f, c4.w != 0.0f ? bb.w - f.w : 0.0f);
+  });
   __syncthreads();
   for (int q = threadIdx.x; q < (S.nx >> 1) * (S.ny >> 1); q += NT) {
     const int X = q % (S.nx >> 1), Y = q / (S.nx >> 1);
