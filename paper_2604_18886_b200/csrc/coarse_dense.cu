@@ -107,6 +107,23 @@ __device__ __forceinline__ float g4(const float4& v, int m) { return m == 0 ? v.
 // y-, y+, z-, z+ from 0 or c u (the tile kernels'; walls 0), ~16 loads per 4 cells instead of ~14
 // per cell and the index arithmetic once per segment.  vzm/vzp, czp: the z-neighbour rows
 // (given by the caller: in the level, or across a slab boundary through distributed smem).
+// (segment, row, y, z) of row-segment work item w of a dense level: shifts when the dims are
+// powers of two (every unit-cube level), divisions otherwise
+__device__ __forceinline__ void seg_rc(const CDLevel& L, int w, int nseg, int& seg, int& y, int& z) {
+  int row;
+  if (L.shx >= 2 && L.shy >= 0) {
+    seg = w & (nseg - 1);
+    row = w >> (L.shx - 2);
+    y = row & (L.ny - 1);
+    z = row >> L.shy;
+  } else {
+    seg = w % nseg;
+    row = w / nseg;
+    y = row % L.ny;
+    z = row / L.ny;
+  }
+}
+
 struct RowNb {
   float4 ox, ym, yp, zm, zp, cxo, cyp, czp;
   float xs, xsc;
@@ -158,8 +175,9 @@ __device__ __forceinline__ void cd_pass(const CDArgs& A, const CDMem& M, int l, 
   const int nw = (L.n >> 3);  // rows x segments of one colour (nh / 4)
   const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   for (int w = threadIdx.x; w < nw; w += NT) {
-    const int seg = w % nseg, row = w / nseg;
-    const int y = row % L.ny, z = row / L.ny;
+    int seg, y, z;
+    seg_rc(L, w, nseg, seg, y, z);
+    const int row = z * L.ny + y;
     const int p = (colour + y + z) & 1;
     const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
     RowNb r;
@@ -187,8 +205,9 @@ __device__ __forceinline__ void cd_rows_au(const CDLevel& L, const CDMem& M, con
   const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   for (int w = threadIdx.x; w < 2 * nw; w += NT) {
     const int colour = w >= nw, ww = w - colour * nw;
-    const int seg = ww % nseg, row = ww / nseg;
-    const int y = row % L.ny, z = row / L.ny;
+    int seg, y, z;
+    seg_rc(L, ww, nseg, seg, y, z);
+    const int row = z * L.ny + y;
     const int p = (colour + y + z) & 1;
     const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
     RowNb r;
@@ -440,6 +459,7 @@ struct CCArgs {
 
 struct Slab {
   int nx, ny, n, hx, hxy;     // n = nx * ny * SLZ, hx = nx / 2, hxy = hx * ny
+  int shseg, shy;             // log2(hx / 4), log2(ny) (powers of two: the unit cube's level 2)
   int c;                      // cluster rank = slab index
   float* coef;                // NP planes of n
   float* u;
@@ -471,8 +491,8 @@ __device__ __forceinline__ void slab_rows_au(const Slab& S, const Op& op) {
   const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   for (int w = threadIdx.x; w < 2 * nw; w += NT) {
     const int colour = w >= nw, ww = w - colour * nw;
-    const int seg = ww % nseg, row = ww / nseg;
-    const int y = row % S.ny, z = row / S.ny;
+    const int seg = ww & (nseg - 1), row = ww >> S.shseg;  // (slab dims are powers of two)
+    const int y = row & (S.ny - 1), z = row >> S.shy;
     const int p = (colour + y + z) & 1;
     const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
     RowNb r;
@@ -506,8 +526,8 @@ __device__ __forceinline__ void slab_pass(const Slab& S, int colour, cg::cluster
   const int nw = S.n >> 3;
   const float4 Z4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   for (int w = threadIdx.x; w < nw; w += NT) {
-    const int seg = w % nseg, row = w / nseg;
-    const int y = row % S.ny, z = row / S.ny;
+    const int seg = w & (nseg - 1), row = w >> S.shseg;
+    const int y = row & (S.ny - 1), z = row >> S.shy;
     const int p = (colour + y + z) & 1;
     const int own = colour * nh + row * hx + 4 * seg, oth = own + (colour ? -nh : nh);
     RowNb r;
@@ -551,6 +571,8 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_cluster(const __grid_constant_
   S.n = C.nx * C.ny * SLZ;
   S.hx = C.nx >> 1;
   S.hxy = S.hx * C.ny;
+  S.shseg = 31 - __clz(S.hx >> 2);
+  S.shy = 31 - __clz(C.ny);
   S.c = rank;
   S.coef = M.scr + A.lv[1].n;
   S.u = S.coef + NP * S.n;
