@@ -298,13 +298,30 @@ template <int NT>
 __device__ __forceinline__ void cd_prolong(const CDArgs& A, const CDMem& M, int l) {
   const CDLevel& L = A.lv[l];
   const CDLevel& P = A.lv[l - 1];
-  for (int i = threadIdx.x; i < L.n; i += NT) {
-    if (M.coef[NP * L.off + i] == 0.0f) continue;
-    const int c = i >= (L.n >> 1);
-    int x, y, z;
-    dcell(L, c, i - c * (L.n >> 1), x, y, z);
-    const int pi = didx(P, x >> 1, y >> 1, z >> 1);
-    M.u[L.off + i] += A.pro_scale * (M.u[P.off + pi] - M.us[P.off + pi]);
+  // row segments of 4 cells (x = 2m + p, m = 4 seg + k): their parents X = m (both colours)
+  const int nh = L.n >> 1, hx = L.nx >> 1, nseg = hx >> 2, nw = L.n >> 3, phx = P.nx >> 1, pnh = P.n >> 1;
+  const float* pu = M.u + P.off;
+  const float* ps = M.us + P.off;
+  for (int w = threadIdx.x; w < 2 * nw; w += NT) {
+    const int colour = w >= nw, ww = w - colour * nw;
+    int seg, y, z;
+    seg_rc(L, ww, nseg, seg, y, z);
+    const int own = colour * nh + (z * L.ny + y) * hx + 4 * seg;
+    const int Y = y >> 1, Z = z >> 1, pb = (Z * P.ny + Y) * phx;
+    float4 u4 = lds4(M.u + L.off + own);
+    const float4 c4 = lds4(M.coef + NP * L.off + own);
+    float d[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int X = 4 * seg + m;
+      const int pi = ((X + Y + Z) & 1) * pnh + pb + (X >> 1);
+      d[m] = A.pro_scale * (pu[pi] - ps[pi]);
+    }
+    if (c4.x != 0.0f) u4.x += d[0];
+    if (c4.y != 0.0f) u4.y += d[1];
+    if (c4.z != 0.0f) u4.z += d[2];
+    if (c4.w != 0.0f) u4.w += d[3];
+    *reinterpret_cast<float4*>(M.u + L.off + own) = u4;
   }
   __syncthreads();
 }
@@ -372,44 +389,33 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_dense(const __grid_constant__ 
       for (int k = 0; k < 8; ++k)
         if (i0 + k * NT < nv) dst[i0 + k * NT] = v[k];
     }
+    // u^K, b^K: a tile's colour row (4 slots, one 128-bit run) is 4 consecutive dense cells
     const CDLevel& L = A.lv[A.K];
-    for (int g0 = threadIdx.x; g0 < L.n; g0 += 4 * NT) {
-      float uv[4], bv[4];
-      int di[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int g = g0 + k * NT;
-        if (g >= L.n) break;
-        const int t = A.tK0 + (g >> 9), sl = g & 511;
-        const int4 tv = __ldg(A.tile + t);
-        int x, y, z;
-        slot_xyz(sl, x, y, z);
-        di[k] = didx(L, tv.y * 8 + x, tv.z * 8 + y, tv.w * 8 + z);
-        const size_t gi = (size_t)(t - A.NL) * TB3 + sl;
-        uv[k] = A.u_inner[gi];
-        bv[k] = A.b_inner[gi];
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (g0 + k * NT >= L.n) break;
-        M.u[L.off + di[k]] = uv[k];
-        M.b[L.off + di[k]] = bv[k];
-      }
+    const int nrow = (L.n >> 9) * 128;  // tiles x 2 colours x 64 rows
+    for (int w = threadIdx.x; w < nrow; w += NT) {
+      const int t = A.tK0 + (w >> 7), rc = w & 127;
+      const int4 tv = __ldg(A.tile + t);
+      const int sl = 4 * rc;  // colour (rc >> 6) half, row (y, z) = (rc & 7, (rc >> 3) & 7)
+      const int di = ((rc >> 6) * (L.n >> 1)) + ((tv.w * 8 + ((rc >> 3) & 7)) * L.ny + tv.z * 8 + (rc & 7)) * (L.nx >> 1) +
+                     4 * tv.y;
+      const size_t gi = (size_t)(t - A.NL) * TB3 + sl;
+      *reinterpret_cast<float4*>(M.u + L.off + di) = __ldg(reinterpret_cast<const float4*>(A.u_inner + gi));
+      *reinterpret_cast<float4*>(M.b + L.off + di) = __ldg(reinterpret_cast<const float4*>(A.b_inner + gi));
     }
   }
   __syncthreads();
   cd_cycle<NT>(A, M, A.K, A.fas_first != 0);
-  // copy out u^K and b^K (the FAS rhs persists across the mu calls from level K+1)
+  // copy out u^K and b^K (the FAS rhs persists across the mu calls from level K+1), tile rows
   const CDLevel& L = A.lv[A.K];
-  for (int g = threadIdx.x; g < L.n; g += NT) {
-    const int t = A.tK0 + (g >> 9), sl = g & 511;
+  const int nrow = (L.n >> 9) * 128;
+  for (int w = threadIdx.x; w < nrow; w += NT) {
+    const int t = A.tK0 + (w >> 7), rc = w & 127;
     const int4 tv = __ldg(A.tile + t);
-    int x, y, z;
-    slot_xyz(sl, x, y, z);
-    const int di = didx(L, tv.y * 8 + x, tv.z * 8 + y, tv.w * 8 + z);
-    const size_t gi = (size_t)(t - A.NL) * TB3 + sl;
-    A.u_inner[gi] = M.u[L.off + di];
-    if (A.fas_first) A.b_inner[gi] = M.b[L.off + di];
+    const int di = ((rc >> 6) * (L.n >> 1)) + ((tv.w * 8 + ((rc >> 3) & 7)) * L.ny + tv.z * 8 + (rc & 7)) * (L.nx >> 1) +
+                   4 * tv.y;
+    const size_t gi = (size_t)(t - A.NL) * TB3 + 4 * rc;
+    *reinterpret_cast<float4*>(A.u_inner + gi) = lds4(M.u + L.off + di);
+    if (A.fas_first) *reinterpret_cast<float4*>(A.b_inner + gi) = lds4(M.b + L.off + di);
   }
 }
 
@@ -596,15 +602,19 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_cluster(const __grid_constant_
       float4* d0 = reinterpret_cast<float4*>(M.coef);
       for (int i = threadIdx.x; i < NP * A.total / 4; i += NT) d0[i] = __ldg(s0 + i);
     }
-    for (int i = threadIdx.x; i < S.n; i += NT) {
-      const int c = i >= (S.n >> 1);
-      int x, y, z;
-      slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
+    // u^2, b^2: a row segment of 4 same-colour cells (x = 2(4 seg + k) + p) is one 128-bit run of
+    // 4 slots of tile x >> 3 = seg (the tile's colour = the slab's: the slab origin is even)
+    const int nseg = S.hx >> 2, nw = S.n >> 3, nh = S.n >> 1;
+    for (int w = threadIdx.x; w < 2 * nw; w += NT) {
+      const int colour = w >= nw, ww = w - colour * nw;
+      const int seg = ww & (nseg - 1), row = ww >> S.shseg;
+      const int y = row & (S.ny - 1), z = row >> S.shy;
       const int zg = SLZ * rank + z;
-      const int t = __ldg(C.tmap2 + ((zg >> 3) * (C.ny >> 3) + (y >> 3)) * (C.nx >> 3) + (x >> 3));
-      const size_t gi = (size_t)(t - A.NL) * TB3 + cslot(x & 7, y & 7, zg & 7);
-      S.u[i] = A.u_inner[gi];
-      S.b[i] = A.b_inner[gi];
+      const int t = __ldg(C.tmap2 + ((zg >> 3) * (C.ny >> 3) + (y >> 3)) * (C.nx >> 3) + seg);
+      const size_t gi = (size_t)(t - A.NL) * TB3 + (colour << 8) + 4 * (y & 7) + 32 * (zg & 7);
+      const int own = colour * nh + row * S.hx + 4 * seg;
+      *reinterpret_cast<float4*>(S.u + own) = __ldg(reinterpret_cast<const float4*>(A.u_inner + gi));
+      *reinterpret_cast<float4*>(S.b + own) = __ldg(reinterpret_cast<const float4*>(A.b_inner + gi));
     }
   }
   cl.sync();
@@ -665,29 +675,51 @@ __global__ __launch_bounds__(NT, 1) void k_coarse_cluster(const __grid_constant_
     for (int k = 0; k < A.mu; ++k) cd_cycle<NT>(A, M, 1, k == 0);
   cl.sync();
   // prolongation u^2 += pro_scale (u^1 - u*) from CTA 0, then post-smoothing (B, R) x nu_post
-  for (int i = threadIdx.x; i < S.n; i += NT) {
-    if (S.coef[i] == 0.0f) continue;
-    const int c = i >= (S.n >> 1);
-    int x, y, z;
-    slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
-    const int pi = didx(L1, x >> 1, y >> 1, rank);
-    S.u[i] += A.pro_scale * (u1[pi] - us1[pi]);
+  {
+    // row segments of 4 cells: their parents X = 4 seg + k in plane `rank` of level 1 (CTA 0)
+    const int nseg = S.hx >> 2, nw = S.n >> 3, nh = S.n >> 1, phx = L1.nx >> 1, pnh = L1.n >> 1;
+    for (int w = threadIdx.x; w < 2 * nw; w += NT) {
+      const int colour = w >= nw, ww = w - colour * nw;
+      const int seg = ww & (nseg - 1), row = ww >> S.shseg;
+      const int y = row & (S.ny - 1), z = row >> S.shy;
+      const int own = colour * nh + row * S.hx + 4 * seg;
+      const int Y = y >> 1, Z = rank, pb = (Z * L1.ny + Y) * phx;
+      float4 u4 = lds4(S.u + own);
+      const float4 c4 = lds4(S.coef + own);
+      float d[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int X = 4 * seg + m;
+        const int pi = ((X + Y + Z) & 1) * pnh + pb + (X >> 1);
+        d[m] = A.pro_scale * (u1[pi] - us1[pi]);
+      }
+      (void)z;
+      if (c4.x != 0.0f) u4.x += d[0];
+      if (c4.y != 0.0f) u4.y += d[1];
+      if (c4.z != 0.0f) u4.z += d[2];
+      if (c4.w != 0.0f) u4.w += d[3];
+      *reinterpret_cast<float4*>(S.u + own) = u4;
+    }
   }
   cl.sync();
   for (int k = 0; k < A.nu_post; ++k) {
     slab_pass<NT>(S, 1, cl);
     slab_pass<NT>(S, 0, cl);
   }
-  // copy out u^2 (and the FAS rhs b^2 of the first mu call)
-  for (int i = threadIdx.x; i < S.n; i += NT) {
-    const int c = i >= (S.n >> 1);
-    int x, y, z;
-    slab_cell(S, c, i - c * (S.n >> 1), x, y, z);
-    const int zg = SLZ * rank + z;
-    const int t = __ldg(C.tmap2 + ((zg >> 3) * (C.ny >> 3) + (y >> 3)) * (C.nx >> 3) + (x >> 3));
-    const size_t gi = (size_t)(t - A.NL) * TB3 + cslot(x & 7, y & 7, zg & 7);
-    A.u_inner[gi] = S.u[i];
-    if (C.fas_first) A.b_inner[gi] = S.b[i];
+  // copy out u^2 (and the FAS rhs b^2 of the first mu call), row segments as the copy-in
+  {
+    const int nseg = S.hx >> 2, nw = S.n >> 3, nh = S.n >> 1;
+    for (int w = threadIdx.x; w < 2 * nw; w += NT) {
+      const int colour = w >= nw, ww = w - colour * nw;
+      const int seg = ww & (nseg - 1), row = ww >> S.shseg;
+      const int y = row & (S.ny - 1), z = row >> S.shy;
+      const int zg = SLZ * rank + z;
+      const int t = __ldg(C.tmap2 + ((zg >> 3) * (C.ny >> 3) + (y >> 3)) * (C.nx >> 3) + seg);
+      const size_t gi = (size_t)(t - A.NL) * TB3 + (colour << 8) + 4 * (y & 7) + 32 * (zg & 7);
+      const int own = colour * nh + row * S.hx + 4 * seg;
+      *reinterpret_cast<float4*>(A.u_inner + gi) = lds4(S.u + own);
+      if (C.fas_first) *reinterpret_cast<float4*>(A.b_inner + gi) = lds4(S.b + own);
+    }
   }
 }
 
