@@ -514,14 +514,15 @@ static bool pass_ghost_inline(bool level_has_ghosts) {
   return mode == 1 || (mode == 0 && level_has_ghosts);
 }
 
-// the inlined ghost body at 14 CTAs/SM (72 registers, 16 B of spills; measured config 3
-// 10.19 -> 9.58 ms and config 4 21.4 -> 20.0 ms of passes per solve against 12 CTAs/SM at 80
-// registers); OCTMG_PASS_GHOST_MINB=12 for the latter
+// the inlined ghost body at 12 CTAs/SM (80 registers, no spills); OCTMG_PASS_GHOST_MINB=14 for
+// 72 registers with 24 B of spills (measured late in round 2, after the ghost-row changes: 12
+// is faster on configs 3 / 4 / 5 — 24.85 vs 25.49, 102.3 vs 104.1, 468.7 vs 479.7 ms per solve;
+// earlier in the round 14 had measured better on config 3)
 static int pass_ghost_minb() {
   int v = -1;
   if (v < 0) {
     const char* e = getenv("OCTMG_PASS_GHOST_MINB");
-    v = e ? atoi(e) : 14;
+    v = e ? atoi(e) : 12;
   }
   return v;
 }

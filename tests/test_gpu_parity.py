@@ -251,7 +251,7 @@ def test_full_size_cfg2_parity(om):
 # ---------------------------------------------------------------------------------------
 @pytest.mark.parametrize("env", [{"OCTMG_SUBCYCLE": "0"}, {"OCTMG_PASS_CPT": "1"}, {"OCTMG_GRAPH_LOOP": "0"},
                                  {"OCTMG_PASS_BIG": "1"}, {"OCTMG_PASS_V": "2"}, {"OCTMG_PASS_GHOST": "inline"},
-                                 {"OCTMG_PASS_GHOST": "call"}, {"OCTMG_PASS_GHOST_MINB": "12"}, {"OCTMG_PASS_SPLIT": "1"},
+                                 {"OCTMG_PASS_GHOST": "call"}, {"OCTMG_PASS_GHOST_MINB": "14"}, {"OCTMG_PASS_SPLIT": "1"},
                                  {"OCTMG_COARSE_DENSE": "0"}, {"OCTMG_COARSE_CLUSTER": "0"},
                                  {"OCTMG_COARSE_DENSE": "0", "OCTMG_SUBCYCLE": "0"},
                                  {"OCTMG_RESTRICT_ROW": "1"}, {"OCTMG_RESTRICT_ROW": "0"}, {"OCTMG_RESTRICT_RED": "0"},
