@@ -358,7 +358,10 @@ typedef struct {
  * the device: one host synchronisation per solve; a partitioned hierarchy captures its
  * transport's halo exchanges and fp64 scalar allreduces into the same body.  Environment
  * OCTMG_GRAPH_LOOP=0, profiling, or a transport / driver that cannot be captured: the
- * host-driven loop (the same kernels, one scalar read per iteration).
+ * host-driven loop (the same kernels, one scalar read per iteration).  The null-space
+ * projection of the updated r is fused into the x / r update (its mean from the projected r's
+ * sum and the apply's sum of A p, the same projection up to rounding); on trees whose leaves
+ * all lie on the finest level (r, z) is summed by the last colour pass of M.
  * b (read-only) and x (overwritten) are device f32[N].  Synchronises `stream` before
  * returning.  report may be NULL.
  */
