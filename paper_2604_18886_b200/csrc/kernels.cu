@@ -230,6 +230,15 @@ __device__ __forceinline__ unsigned act4(const uint32_t* act, int64_t i) { retur
     for (int64_t i = (R).begin[rr_] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;             \
          i < (R).begin[rr_] + (R).len[rr_]; i += (int64_t)gridDim.x * blockDim.x)
 
+// natural-order rows (8 cells x + 8y + 64z of one tile row) of the ranges: q-th row of range rr
+// starts at cell 4 begin + 8 q; its red / black halves are the slot-order float4s at
+// tile + 4 row and tile + 256 + 4 row (row = y + 8z); cell x = 2m + p of the red half
+// (p = (y + z) & 1) is natural x, of the black half 2m + 1 - p
+#define FOR_ROWS(R, c0)                                                                           \
+  for (int rr_ = 0; rr_ < (R).n; ++rr_)                                                           \
+    for (int64_t q_ = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, c0 = 0;                     \
+         q_ < (R).len[rr_] / 2 && ((c0 = 4 * (R).begin[rr_] + 8 * q_), true); q_ += (int64_t)gridDim.x * blockDim.x)
+
 // two ordered sums (s2, s1) over the grid; the last block stores them at sc fields f2, f1
 __device__ __forceinline__ void reduce2(double s2, double s1, double* partial, unsigned* counter, Scalars* sc,
                                         int f2, int f1, double* sred) {
@@ -252,20 +261,29 @@ __global__ __launch_bounds__(256) void k_init(const float* b, const uint32_t* ac
                                               double* partial, unsigned* counter, Scalars* sc) {
   __shared__ double sred[8];
   double s2 = 0.0, s1 = 0.0;
-  FOR_RANGES(R, i) {
-    // b is in the caller's natural cell order: gather the 4 slots' cells
-    const int64_t c0 = 4 * i, tb = c0 & ~(int64_t)511;
-    const int s0 = (int)(c0 & 511);
-    float m[4];
-    for (int k = 0; k < 4; ++k) m[k] = __ldg(b + tb + slot_nat(s0 + k));
-    const unsigned am = act4(act, i);
-    for (int k = 0; k < 4; ++k) {
-      if (!((am >> k) & 1u)) m[k] = 0.0f;
-      s2 += (double)m[k] * m[k];
-      s1 += (double)m[k];
+  FOR_ROWS(R, c0) {
+    // b is in the caller's natural cell order: one natural row (two 128-bit loads) gives the
+    // red and the black colour row of the slot order
+    const int64_t tb = c0 & ~(int64_t)511;
+    const int row = (int)((c0 & 511) >> 3), y = row & 7, z = row >> 3, p = (y + z) & 1;
+    const float4 n0 = __ldg(reinterpret_cast<const float4*>(b + c0)), n1 = __ldg(reinterpret_cast<const float4*>(b + c0 + 4));
+    const float nv[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int64_t i = (tb + (c << 8) + 4 * row) >> 2;  // float4 index of the colour row
+      const int pc = c ? 1 - p : p;
+      float m[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) m[k] = nv[2 * k + pc];
+      const unsigned am = act4(act, i);
+      for (int k = 0; k < 4; ++k) {
+        if (!((am >> k) & 1u)) m[k] = 0.0f;
+        s2 += (double)m[k] * m[k];
+        s1 += (double)m[k];
+      }
+      reinterpret_cast<float4*>(r)[i] = make_float4(m[0], m[1], m[2], m[3]);
+      reinterpret_cast<float4*>(x)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    reinterpret_cast<float4*>(r)[i] = make_float4(m[0], m[1], m[2], m[3]);
-    reinterpret_cast<float4*>(x)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) sc->flags = 0;
   reduce2(s2, s1, partial, counter, sc, SF_RR, SF_R, sred);
@@ -413,16 +431,19 @@ __global__ void k_mask_copy(const float* src, const uint32_t* act, float* dst, i
     dst[i] = ((act[i >> 5] >> (i & 31)) & 1u) ? src[(i & ~(int64_t)511) + slot_nat((int)(i & 511))] : 0.0f;
 }
 
-// dst (caller's natural order) = src (slot order) on the cells of the ranges
+// dst (caller's natural order) = src (slot order) on the cells of the ranges: per natural row,
+// the red and black colour rows interleaved into two 128-bit stores
 __global__ void k_copy_to_nat(const float* src, float* dst, Ranges R) {
-  FOR_RANGES(R, i) {
-    const float4 v = reinterpret_cast<const float4*>(src)[i];
-    const int64_t c0 = 4 * i, tb = c0 & ~(int64_t)511;
-    const int s0 = (int)(c0 & 511);
-    dst[tb + slot_nat(s0)] = v.x;
-    dst[tb + slot_nat(s0 + 1)] = v.y;
-    dst[tb + slot_nat(s0 + 2)] = v.z;
-    dst[tb + slot_nat(s0 + 3)] = v.w;
+  FOR_ROWS(R, c0) {
+    const int64_t tb = c0 & ~(int64_t)511;
+    const int row = (int)((c0 & 511) >> 3), y = row & 7, z = row >> 3, p = (y + z) & 1;
+    const float4 vr = reinterpret_cast<const float4*>(src)[(tb + 4 * row) >> 2];
+    const float4 vb = reinterpret_cast<const float4*>(src)[(tb + 256 + 4 * row) >> 2];
+    // natural x = 2m + p holds red m, 2m + 1 - p black m
+    const float4 a = p ? make_float4(vb.x, vr.x, vb.y, vr.y) : make_float4(vr.x, vb.x, vr.y, vb.y);
+    const float4 c = p ? make_float4(vb.z, vr.z, vb.w, vr.w) : make_float4(vr.z, vb.z, vr.w, vb.w);
+    *reinterpret_cast<float4*>(dst + c0) = a;
+    *reinterpret_cast<float4*>(dst + c0 + 4) = c;
   }
 }
 
